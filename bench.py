@@ -1,0 +1,383 @@
+#!/usr/bin/env python3
+"""Benchmark of the SPGM hot path (BASELINE.json metric: A-entry evals/s, fwd+adj,
+and SPGM iterations/s, as a fraction of the FP32+SFU roofline).
+
+One step = one SPGM iteration on the chosen workload (default: BASELINE 'Large',
+|B| = 4096 flat minibatch, complex64): device sampler → batch prepare → fused
+forward → [NCCL all-reduce of the 2·|B| partial sums over voxel slabs] → fused
+adjoint + soft-threshold prox + termination statistics. Entries per step = 2·|B|·N.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload large|medium|small]
+    python bench.py --impl reference ...   # the reference algorithm on the host CPU
+
+N > 1 runs under torchrun (one process per GPU, voxel-slab sharding, strong scaling).
+Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "A-entry evals/sec (fwd+adj) & SPGM iters/sec; % of FP32+SFU roofline, 1/2/4/8 GPU"
+UNIT = "entries/s"
+# SFU roofline: 2 MUFU (sin, cos) per entry, 16 MUFU/clk/SM, 148 SMs
+ENTRIES_PER_CLK_SM = 8.0
+N_SM = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="large", choices=["large", "medium", "small"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle port)
+
+
+def cpu_baseline(workload: str, steps: int, budget_s: float, rank_sample_seed: int = 0):
+    """The reference's CPU algorithm (phasor tables + BLAS dots, forward.py:183-336),
+    restated in oracle/ and run with all host threads on a voxel sample of the same
+    workload: the first n voxels (flat order) of the grid, the same |B| and flat sampling."""
+    from oracle import nfmimo_oracle as O
+    from paper_2509_00774_b200 import configs
+
+    w = configs.WORKLOADS[workload]()
+    geo_full = O.geom_from_scenario(w.scenario) if w.scenario.n_voxels <= 1 << 17 else None
+    if geo_full is None:
+        v = w.scenario.voxels
+        n_sample = 4096
+        cen = O.centers_of(v.corner.as_array(), v.spacing, v.dims, (0, 1))[:n_sample]
+        freqs = w.scenario.frequencies.values()
+        geo = O.Geom(w.scenario.array.tx_positions(), w.scenario.array.rx_positions(), freqs,
+                     w.scenario.pulse.evaluate(freqs), cen, w.scenario.c)
+        sample = f"first {n_sample} voxels (of {w.scenario.n_voxels}) of the {workload} grid, all M channels"
+    else:
+        geo = geo_full
+        sample = f"full {workload} grid ({geo.N} voxels)"
+    threads = O.host_threads()
+    t0 = time.perf_counter()
+    op = O.TableOperator(geo)
+    build_s = time.perf_counter() - t0
+    rng = np.random.default_rng(0)
+    y = rng.standard_normal(geo.M) + 1j * rng.standard_normal(geo.M)
+    s = np.zeros(geo.N, dtype=np.complex128)
+    seq_rng = np.random.default_rng(configs.SEEDS["minibatch"])
+    done, t_iter = 0, 0.0
+    times = []
+    while done < max(steps, 1) and (t_iter < budget_s or done < 2):
+        idx = np.sort(seq_rng.choice(geo.M, w.batch, replace=False))
+        t1 = time.perf_counter()
+        resid = op.forward(s, idx, threads) - y[idx]
+        g = op.adjoint(resid, idx, threads) / idx.size
+        s = O.soft_threshold(s - 1e-3 * g, 1e-6)
+        dt = time.perf_counter() - t1
+        times.append(dt)
+        t_iter += dt
+        done += 1
+    per = float(np.mean(times[1:] if len(times) > 2 else times))
+    entries = 2.0 * w.batch * geo.N
+    return {
+        "value": entries / per, "unit": UNIT, "cores": threads, "kind": "port",
+        "sample": f"{sample}; |B|={w.batch} flat; {done} SPGM iterations of the oracle's table restatement "
+                  f"of the reference algorithm (forward.py:183-336); table build {build_s:.1f}s excluded",
+        "iters_timed": done, "s_per_iter": per, "table_build_s": build_s,
+        "table_bytes": O.TableOperator.table_bytes(geo),
+    }
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    cb = cpu_baseline(args.workload, args.steps, args.cpu_seconds * max(1, args.steps) / 30.0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": cb["iters_timed"], "warmup": 1, "ms_per_step": cb["s_per_iter"] * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": args.workload, "sample": cb["sample"]},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+
+
+def slab(nz: int, rank: int, world: int):
+    from paper_2509_00774_b200.sharding import slab_range
+
+    return slab_range(nz, rank, world)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_00774_b200 import configs
+    from paper_2509_00774_b200.plan import DevicePlan
+    from paper_2509_00774_b200.sharding import ShardedSetup
+    from paper_2509_00774_b200.solver import SPGMEngine
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    w = configs.WORKLOADS[args.workload]()
+    scn = w.scenario
+    B, N, M = w.batch, scn.n_voxels, scn.n_channels
+    nz = scn.voxels.dims[2]
+    zr = slab(nz, rank, world)
+
+    t_setup = time.perf_counter()
+    setup = ShardedSetup(scn, dtype=w.dtype, device=dev, z_range=zr, process_group=pg)
+    s_true = configs.make_scene(w)
+    clean = setup.forward_full(s_true)
+    y = configs.add_noise(clean, configs.noise_sigma(clean, w.snr_db))
+    L = setup.lipschitz(n_iters=20, rng_seed=configs.SEEDS["power"])
+    lam = 1e-3 * setup.max_abs_adjoint(y) / M
+    eta, alpha = 1.0 / L, lam / L
+    setup.release()
+    plan = DevicePlan(scn, dtype=w.dtype, device=dev, z_range=zr, max_batch=B)
+    eng = SPGMEngine(plan, y, eta, alpha, process_group=pg)
+    setup_s = time.perf_counter() - t_setup
+    seed = configs.SEEDS["minibatch"]
+
+    def step(k):
+        eng.sample_device(seed, k, B)
+        eng.step_staged()
+
+    def barrier():
+        if pg is not None:
+            dist.barrier(device_ids=[local])
+
+    launches0 = plan.info()["launches"]
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    launches_warm = plan.info()["launches"]
+    barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        for k in range(args.steps):
+            step(args.warmup + k)
+        e1.record(st)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches_timed = plan.info()["launches"] - launches_warm
+    if pg is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    change = eng.magnitude_change()
+    ms_step = ms / args.steps
+    entries_step = 2.0 * B * N
+    value = entries_step / (ms_step * 1e-3)
+
+    # per-kernel timing of the two fused kernels (same stream, CUDA events, steady state)
+    kt = kernel_times(eng, plan, seed, args.warmup + args.steps, reps=max(5, min(args.steps, 20)))
+    if pg is not None:
+        t = torch.tensor([kt["fwd_ms"], kt["adj_ms"]], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        kt["fwd_ms"], kt["adj_ms"] = (float(v) for v in t.tolist())
+
+    # e2e: public-API semantics, host buffers: host-sampled indices (numpy, as the reference)
+    # H2D each step, the termination statistic D2H each step
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(eng, scn, B, N, args, pg, local)
+
+    clocks = clk.summary()
+    local_entries = 2.0 * B * plan.n_local
+    peak = N_SM * ENTRIES_PER_CLK_SM * 1.965e9
+    dom = "adjoint_prox" if kt["adj_ms"] >= kt["fwd_ms"] else "forward"
+    dom_ms = max(kt["adj_ms"], kt["fwd_ms"])
+    achieved = (B * plan.n_local) / (dom_ms * 1e-3)
+    roof = {
+        "bound": "fp32+sfu", "kernel": dom, "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gentry/s",
+        "frac": achieved / peak,
+        "peak_source": "nominal SFU roof: 148 SM x 16 MUFU/clk / 2 MUFU per entry x 1.965 GHz (MEASURED_PEAKS.json "
+                       "has no SFU figure)",
+        "frac_at_observed_clock": (achieved / (N_SM * ENTRIES_PER_CLK_SM * clocks["sm_mhz"] * 1e6)
+                                   if clocks.get("sm_mhz") else None),
+        "fwd_ms": kt["fwd_ms"], "adj_ms": kt["adj_ms"], "entries_per_launch": B * plan.n_local,
+        "traffic": None,
+    }
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c64" if w.dtype == "c64" else "c128", "data": "synthetic",
+            "iters_per_s": 1e3 / ms_step,
+            "config": {"workload": args.workload, "M": M, "N": N, "batch": B, "sampler": "device flat (Feistel)",
+                       "parallelism": f"voxel-slab x{world}", "l2": "inputs larger than L2 (distance table "
+                       f"{plan.info()['device_bytes'] / 2**30:.2f} GiB streamed per kernel)",
+                       "eta": eta, "alpha": alpha, "setup_s": setup_s},
+            "roofline": roof, "clocks": clocks, "gpu_launches": launches_timed,
+            "final_change": change,
+        }
+        if e2e is not None:
+            out["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_baseline(args.workload, 30, args.cpu_seconds)
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(out), flush=True)
+    if pg is not None:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    del launches0
+    return 0
+
+
+def kernel_times(eng, plan, seed, k0, reps):
+    import torch
+
+    st = torch.cuda.current_stream()
+    B = plan.B
+    f_ms, a_ms = [], []
+    for i in range(reps):
+        eng.sample_device(seed, k0 + i, B)
+        yb = eng.ybuf[:B]
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        c = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        plan.forward(eng.s, out=yb)
+        b.record(st)
+        if eng.pg is not None:
+            torch.distributed.all_reduce(torch.view_as_real(yb), group=eng.pg)
+        c0 = torch.cuda.Event(enable_timing=True)
+        c0.record(st)
+        plan.adjoint_prox(yb, eng.y, eng.s, eng.s_next, eng.eta / B, eng.alpha, eng.stats)
+        c.record(st)
+        eng.s, eng.s_next = eng.s_next, eng.s
+        torch.cuda.synchronize()
+        f_ms.append(a.elapsed_time(b))
+        a_ms.append(c0.elapsed_time(c))
+    return {"fwd_ms": float(np.median(f_ms)), "adj_ms": float(np.median(a_ms))}
+
+
+def e2e_run(eng, scn, B, N, args, pg, local):
+    import torch
+    import torch.distributed as dist
+
+    rng = np.random.default_rng(1234)
+    M = scn.n_channels
+    steps = args.steps
+    host_idx = torch.empty(B, dtype=torch.int32).pin_memory()
+    for _ in range(2):
+        host_idx.copy_(torch.from_numpy(np.sort(rng.choice(M, B, replace=False)).astype(np.int32)))
+        eng.stage(host_idx)
+        eng.step_staged()
+        eng.magnitude_change()
+    if pg is not None:
+        dist.barrier(device_ids=[local])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        host_idx.copy_(torch.from_numpy(np.sort(rng.choice(M, B, replace=False)).astype(np.int32)))
+        eng.stage(host_idx)
+        eng.step_staged()
+        eng.magnitude_change()  # D2H of the 4-double stats vector (+ all-reduce when sharded)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if pg is not None:
+        t = torch.tensor([dt], device=eng.plan.device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": 2.0 * B * N * steps / dt, "unit": UNIT, "h2d_bytes_per_step": 4 * B,
+            "d2h_bytes_per_step": 32, "ms_per_step": dt / steps * 1e3,
+            "how": "wall clock around spgm steps with host numpy flat sampling (sorted choice without "
+                   "replacement, as the reference), pinned H2D of the index list, D2H of the termination stats"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

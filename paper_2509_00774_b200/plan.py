@@ -1,0 +1,201 @@
+"""Device-level wrapper around one ``nf_plan`` (include/nfgpu.h).
+
+A :class:`DevicePlan` is the GPU replacement of the reference's cached
+``_OperatorPlan`` (pkg/src/nfmimo/forward.py:183-211). It owns a frequency-free
+per-(antenna, voxel) distance table for one voxel z-slab on one CUDA device.
+Its methods take and return *device* torch tensors and enqueue work on the
+current torch stream. Only the stream handle and raw pointers cross into the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import functools
+
+import numpy as np
+import torch
+
+from . import _lib
+from .geometry import ImagingScenario
+
+DTYPES = {"c64": (_lib.NF_C64, torch.complex64), "c128": (_lib.NF_C128, torch.complex128)}
+
+
+def _dptr(x: np.ndarray):
+    return x.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(device: torch.device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def require_cuda(device=None) -> torch.device:
+    """The GPU path is the only path: fail loudly without a CUDA device."""
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_2509_00774_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback"
+        )
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.type != "cuda":
+        raise RuntimeError(f"device must be a CUDA device, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+class DevicePlan:
+    """One voxel slab [z_begin, z_end) of a scenario on one GPU."""
+
+    def __init__(
+        self,
+        scenario: ImagingScenario,
+        dtype: str = "c128",
+        device=None,
+        z_range: tuple[int, int] | None = None,
+        max_batch: int | None = None,
+    ):
+        if dtype not in DTYPES:
+            raise ValueError(f"dtype must be one of {sorted(DTYPES)}, got {dtype!r}")
+        self.lib = _lib.load()
+        self.device = require_cuda(device)
+        self.scenario = scenario
+        self.dtype_name = dtype
+        self.nf_dtype, self.torch_dtype = DTYPES[dtype]
+        self.real_dtype = torch.float32 if dtype == "c64" else torch.float64
+        nx, ny, nz = scenario.voxels.dims
+        z0, z1 = (0, nz) if z_range is None else (int(z_range[0]), int(z_range[1]))
+        self.z_range = (z0, z1)
+        self.n_local = nx * ny * (z1 - z0)
+        self.vox_offset = nx * ny * z0
+        self.M = scenario.n_channels
+        self.max_batch = self.M if max_batch is None else int(max_batch)
+
+        tx = np.ascontiguousarray(scenario.array.tx_positions(), dtype=np.float64)
+        rx = np.ascontiguousarray(scenario.array.rx_positions(), dtype=np.float64)
+        freqs = np.ascontiguousarray(scenario.frequencies.values(), dtype=np.float64)
+        pulse = scenario.pulse.evaluate(freqs).astype(np.complex128)
+        pulse_ri = np.ascontiguousarray(np.stack([pulse.real, pulse.imag], axis=1).reshape(-1))
+        corner = np.array(scenario.voxels.corner.as_array(), dtype=np.float64)
+        spacing = np.array(scenario.voxels.spacing, dtype=np.float64)
+        dims = (ctypes.c_int * 3)(nx, ny, nz)
+        out = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            rc = self.lib.nf_plan_create(
+                _dptr(tx), tx.shape[0], _dptr(rx), rx.shape[0], _dptr(freqs), _dptr(pulse_ri),
+                freqs.size, float(scenario.c), _dptr(corner), _dptr(spacing), dims, z0, z1,
+                self.nf_dtype, self.max_batch, ctypes.byref(out),
+            )
+        _lib.check(rc, "nf_plan_create")
+        self._h = out
+        self.B = 0
+        self._idx = None  # keeps the staged index tensor alive
+
+    # ---------------------------------------------------------------- lifecycle
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.nf_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def info(self) -> dict:
+        buf = (ctypes.c_int64 * 8)()
+        _lib.check(self.lib.nf_plan_info(self._h, buf), "nf_plan_info")
+        keys = ("n_local", "M", "tiles", "tx_group", "device_bytes", "fwd_ctas", "dtype", "launches")
+        return dict(zip(keys, list(buf)))
+
+    @property
+    def launches(self) -> int:
+        return self.info()["launches"]
+
+    # ---------------------------------------------------------------- helpers
+    def vec(self, n: int) -> torch.Tensor:
+        return torch.empty(n, dtype=self.torch_dtype, device=self.device)
+
+    def _as_dev(self, x, n: int, name: str) -> torch.Tensor:
+        if isinstance(x, torch.Tensor):
+            t = x.to(device=self.device, dtype=self.torch_dtype)
+        else:
+            t = torch.as_tensor(np.asarray(x), device=self.device).to(self.torch_dtype)
+        t = t.contiguous()
+        if t.shape != (n,):
+            raise ValueError(f"{name}: expected shape ({n},), got {tuple(t.shape)}")
+        return t
+
+    # ---------------------------------------------------------------- operator
+    def prepare(self, idx: torch.Tensor) -> None:
+        """Stage channel subset ``idx`` (int32 device tensor, validated by the caller)."""
+        if idx.dtype != torch.int32 or idx.device != self.device or not idx.is_contiguous():
+            idx = idx.to(device=self.device, dtype=torch.int32).contiguous()
+        B = int(idx.numel())
+        _lib.check(self.lib.nf_batch_prepare(self._h, _ptr(idx), B, _stream(self.device)), "nf_batch_prepare")
+        self.B = B
+        self._idx = idx
+
+    def forward(self, s: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """out[k] = Σ_{n in slab} A[m_k, n] s[n] (subset order)."""
+        if out is None:
+            out = self.vec(self.B)
+        _lib.check(self.lib.nf_forward(self._h, _ptr(s), _ptr(out), _stream(self.device)), "nf_forward")
+        return out
+
+    def adjoint(self, r: torch.Tensor, out: torch.Tensor | None = None, ymeas: torch.Tensor | None = None,
+                scale: float = 1.0) -> torch.Tensor:
+        """out[n] = scale Σ_k conj(A[m_k, n]) (r[k] - ymeas[m_k])."""
+        if out is None:
+            out = self.vec(self.n_local)
+        _lib.check(
+            self.lib.nf_adjoint(self._h, _ptr(r), _ptr(ymeas), _ptr(out), float(scale), _stream(self.device)),
+            "nf_adjoint",
+        )
+        return out
+
+    def adjoint_prox(self, r, ymeas, s_in, s_out, eta_over_b: float, alpha: float, stats: torch.Tensor):
+        _lib.check(
+            self.lib.nf_adjoint_prox(
+                self._h, _ptr(r), _ptr(ymeas), _ptr(s_in), _ptr(s_out), float(eta_over_b), float(alpha),
+                _ptr(stats), _stream(self.device),
+            ),
+            "nf_adjoint_prox",
+        )
+
+    def sample_flat(self, seed: int, it: int, batch: int, out: torch.Tensor) -> torch.Tensor:
+        _lib.check(
+            self.lib.nf_sample_flat(self._h, int(seed) & (2**64 - 1), int(it), int(batch), _ptr(out),
+                                    _stream(self.device)),
+            "nf_sample_flat",
+        )
+        return out
+
+
+def soft_threshold_dev(v: torch.Tensor, alpha: float, out: torch.Tensor | None = None) -> torch.Tensor:
+    lib = _lib.load()
+    nf = _lib.NF_C64 if v.dtype == torch.complex64 else _lib.NF_C128
+    v = v.contiguous()
+    out = torch.empty_like(v) if out is None else out
+    _lib.check(lib.nf_soft_threshold(nf, _ptr(v), _ptr(out), v.numel(), float(alpha), _stream(v.device)),
+               "nf_soft_threshold")
+    return out
+
+
+def magnitude_change_dev(a: torch.Tensor, b: torch.Tensor, stats: torch.Tensor | None = None) -> torch.Tensor:
+    lib = _lib.load()
+    nf = _lib.NF_C64 if a.dtype == torch.complex64 else _lib.NF_C128
+    a, b = a.contiguous(), b.contiguous()
+    if stats is None:
+        stats = torch.empty(2, dtype=torch.float64, device=a.device)
+    _lib.check(lib.nf_magnitude_change(nf, _ptr(a), _ptr(b), a.numel(), _ptr(stats), _stream(a.device)),
+               "nf_magnitude_change")
+    return stats
+
+
+@functools.lru_cache(maxsize=4)
+def cached_plan(scenario: ImagingScenario, dtype: str, device_index: int) -> DevicePlan:
+    """Per-scenario plan cache, the analogue of the reference's lru_cache'd _plan (forward.py:190)."""
+    return DevicePlan(scenario, dtype=dtype, device=torch.device("cuda", device_index))

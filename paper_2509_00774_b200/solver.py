@@ -1,0 +1,464 @@
+"""ℓ1-regularized PGM / SPGM reconstruction — public API of the reference's
+``nfmimo.solver`` (pkg/src/nfmimo/solver.py), with the iterate resident on the GPU.
+
+One SPGM iteration (solver.py:281-310) maps to four device steps on one stream:
+
+    sample idx     host numpy, same RNG call sequence as the reference  (solver.py:206-225, 274, 284)
+                   or the device Feistel sampler (sampler="device")
+    nf_batch_prepare      sort the batch into kernel work order
+    nf_forward            y_B = A_B s                                  (solver.py:182)
+    nf_adjoint_prox       s⁺ = soft(s − η/B · A_B^H (y_B − y[idx]), α),  plus termination stats
+                                                                        (solver.py:183, 288-289)
+
+The only host↔device traffic per iteration is the index list (B int32) and the
+four-double stats vector. The stats vector carries the relative magnitude change
+the termination test needs (solver.py:302).
+
+Sampling modes (SolverConfig.sampler):
+  "host"   (default) composition → structured Cartesian product via the reference
+           algorithm; flat_batch → np.sort(rng.choice(M, B, replace=False)).
+           Identical index sequence to a reference run with the same seed.
+  "device" flat batches drawn on the GPU (keyed Feistel bijection; no host work).
+  "table"  an explicit [iters, B] index table (parity runs).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .forward import (
+    ChannelSubset,
+    MeasurementSet,
+    ReflectivityVolume,
+    _subset_indices,
+    adjoint_values,
+    default_dtype,
+    forward_values,
+    get_plan,
+)
+from .geometry import ImagingScenario
+from .plan import DevicePlan, magnitude_change_dev, require_cuda, soft_threshold_dev
+
+__all__ = [
+    "MinibatchComposition",
+    "SolverConfig",
+    "IterationRecord",
+    "SolveReport",
+    "data_fidelity",
+    "full_gradient",
+    "minibatch_gradient",
+    "sample_minibatch",
+    "soft_threshold",
+    "relative_magnitude_change",
+    "check_termination",
+    "pgm_solve",
+    "spgm_solve",
+    "lipschitz_estimate",
+    "SPGMEngine",
+]
+
+TERMINATION_TOLERANCE = "tolerance_reached"
+TERMINATION_MAX_ITERS = "max_iters"
+TERMINATION_TIME_BUDGET = "time_budget"
+_ZERO_NORM_GUARD = 1e-12
+
+
+@dataclass(frozen=True)
+class MinibatchComposition:
+    """(#frequencies, #transmitters, #receivers) drawn per iteration (solver.py:61-95)."""
+
+    n_f: int
+    n_tx: int
+    n_rx: int
+
+    def __post_init__(self):
+        for k in ("n_f", "n_tx", "n_rx"):
+            v = int(getattr(self, k))
+            if v < 1:
+                raise ValueError(f"{k} must be >= 1, got {v}")
+            object.__setattr__(self, k, v)
+
+    @property
+    def batch_size(self) -> int:
+        return self.n_f * self.n_tx * self.n_rx
+
+    def validate_for(self, scenario: ImagingScenario) -> None:
+        caps = (scenario.frequencies.count, scenario.array.n_tx, scenario.array.n_rx)
+        for k, v, cap in zip(("n_f", "n_tx", "n_rx"), (self.n_f, self.n_tx, self.n_rx), caps):
+            if v > cap:
+                raise ValueError(f"{k}={v} exceeds the scenario axis size {cap}")
+
+    def is_full_for(self, scenario: ImagingScenario) -> bool:
+        return (self.n_f, self.n_tx, self.n_rx) == (
+            scenario.frequencies.count,
+            scenario.array.n_tx,
+            scenario.array.n_rx,
+        )
+
+
+@dataclass
+class SolverConfig:
+    """Reference fields (solver.py:98-128) plus the GPU controls.
+
+    dtype       "c128" (default, parity) or "c64" (performance).
+    flat_batch  B for flat uniform sampling without replacement (BASELINE configs);
+                mutually exclusive with ``composition``.
+    sampler     "host" | "device" | "table" (see module docstring).
+    index_table [iters, B] int array for sampler="table".
+    check_every read the termination stats back every k iterations (1 = reference semantics).
+    """
+
+    eta: float = 1e-3
+    alpha: float = 4e-5
+    max_iters: int = 1000
+    tol: float = 1e-3
+    rng_seed: int = 0
+    composition: MinibatchComposition | None = None
+    time_budget_s: float | None = None
+    threads: int = 1
+    dtype: str | None = None
+    flat_batch: int | None = None
+    sampler: str = "host"
+    index_table: np.ndarray | None = None
+    check_every: int = 1
+
+    def __post_init__(self):
+        if not (math.isfinite(self.eta) and self.eta > 0):
+            raise ValueError(f"eta must be > 0, got {self.eta}")
+        if not (math.isfinite(self.alpha) and self.alpha >= 0):
+            raise ValueError(f"alpha must be >= 0, got {self.alpha}")
+        if int(self.max_iters) < 1:
+            raise ValueError(f"max_iters must be >= 1, got {self.max_iters}")
+        self.max_iters = int(self.max_iters)
+        if not (math.isfinite(self.tol) and self.tol > 0):
+            raise ValueError(f"tol must be > 0, got {self.tol}")
+        if self.time_budget_s is not None and not self.time_budget_s > 0:
+            raise ValueError(f"time_budget_s must be > 0, got {self.time_budget_s}")
+        if int(self.threads) < 1:
+            raise ValueError("threads must be >= 1")
+        if self.sampler not in ("host", "device", "table"):
+            raise ValueError(f"sampler must be host/device/table, got {self.sampler!r}")
+        if self.flat_batch is not None:
+            if int(self.flat_batch) < 1:
+                raise ValueError("flat_batch must be >= 1")
+            if self.composition is not None:
+                raise ValueError("give either composition or flat_batch, not both")
+            self.flat_batch = int(self.flat_batch)
+        if int(self.check_every) < 1:
+            raise ValueError("check_every must be >= 1")
+
+
+@dataclass
+class IterationRecord:
+    iter: int
+    magnitude_change: float
+    elapsed_seconds: float
+    batch_size: int
+
+
+@dataclass
+class SolveReport:
+    volume: ReflectivityVolume
+    iterations: int
+    wall_time_s: float
+    per_iteration: list = field(default_factory=list)
+    termination: str = TERMINATION_MAX_ITERS
+
+
+# ------------------------------------------------------------------ helpers
+
+
+def _measurement_values(y, scenario: ImagingScenario) -> np.ndarray:
+    if isinstance(y, MeasurementSet):
+        if not y.matches(scenario):
+            raise ValueError(
+                "measurement fingerprint does not match the scenario (wrong scenario or stale measurement file)"
+            )
+        return y.values
+    v = np.asarray(y, dtype=np.complex128)
+    if v.shape != (scenario.n_channels,):
+        raise ValueError(f"expected {scenario.n_channels} measurements, got shape {v.shape}")
+    return v
+
+
+def _subset_or_all(subset, scenario: ImagingScenario) -> np.ndarray:
+    if subset is None:
+        return np.arange(scenario.n_channels, dtype=np.int64)
+    if isinstance(subset, ChannelSubset):
+        return subset.indices
+    return ChannelSubset(np.asarray(subset)).indices
+
+
+def _volume_like(s, scenario: ImagingScenario) -> np.ndarray:
+    if isinstance(s, ReflectivityVolume):
+        if s.grid != scenario.voxels:
+            raise ValueError("initial volume grid does not match the scenario")
+        return s.values
+    v = np.asarray(s, dtype=np.complex128)
+    if v.shape != (scenario.n_voxels,):
+        raise ValueError(f"expected {scenario.n_voxels} initial values")
+    return v
+
+
+def _gradient(s, yv, scenario, idx, dtype=None) -> np.ndarray:
+    plan = get_plan(scenario, dtype)
+    _subset_indices(idx, scenario)
+    pred = forward_values(plan, np.asarray(s, dtype=np.complex128), idx)
+    return adjoint_values(plan, pred - yv[idx], idx) / idx.size
+
+
+# ------------------------------------------------------------------ public functions
+
+
+def data_fidelity(s, y, scenario: ImagingScenario, subset=None, threads: int = 1, *, dtype=None) -> float:
+    """(1/B) Σ ½|A_sub s − y_sub|² (solver.py:172-178)."""
+    from .forward import _volume_values
+
+    yv = _measurement_values(y, scenario)
+    idx = _subset_or_all(subset, scenario)
+    _subset_indices(idx, scenario)
+    resid = forward_values(get_plan(scenario, dtype), _volume_values(s, scenario), idx) - yv[idx]
+    return 0.5 * float(np.mean(np.abs(resid) ** 2))
+
+
+def full_gradient(s, y, scenario: ImagingScenario, threads: int = 1, *, dtype=None) -> np.ndarray:
+    """(1/M) A^H (A s − y) (solver.py:186-190)."""
+    yv = _measurement_values(y, scenario)
+    return _gradient(s, yv, scenario, np.arange(scenario.n_channels, dtype=np.int64), dtype)
+
+
+def minibatch_gradient(s, y, scenario: ImagingScenario, subset, threads: int = 1, *, dtype=None) -> np.ndarray:
+    """(1/B) A_sub^H (A_sub s − y_sub); the full subset is bitwise full_gradient (solver.py:193-203)."""
+    if subset is None:
+        raise ValueError("minibatch_gradient requires a non-empty channel subset")
+    yv = _measurement_values(y, scenario)
+    return _gradient(s, yv, scenario, _subset_or_all(subset, scenario), dtype)
+
+
+def sample_minibatch(composition: MinibatchComposition, scenario: ImagingScenario, rng) -> ChannelSubset:
+    """Structured Cartesian minibatch; same RNG call sequence as solver.py:206-225."""
+    composition.validate_for(scenario)
+    if not isinstance(rng, np.random.Generator):
+        rng = np.random.default_rng(rng)
+    T, R = scenario.array.n_tx, scenario.array.n_rx
+    fs = np.sort(rng.choice(scenario.frequencies.count, composition.n_f, replace=False))
+    ts = np.sort(rng.choice(T, composition.n_tx, replace=False))
+    rs = np.sort(rng.choice(R, composition.n_rx, replace=False))
+    return ChannelSubset((rs[None, None, :] + R * (ts[None, :, None] + T * fs[:, None, None])).reshape(-1))
+
+
+def sample_flat(scenario: ImagingScenario, batch: int, rng) -> np.ndarray:
+    """Flat uniform minibatch without replacement, ascending (BASELINE sampling)."""
+    return np.sort(rng.choice(scenario.n_channels, batch, replace=False)).astype(np.int64)
+
+
+def _device_or_default():
+    return require_cuda(None)
+
+
+def soft_threshold(v, alpha: float) -> np.ndarray:
+    """v·max(|v|−α, 0)/|v|; magnitudes ≤ α map to exactly 0 (solver.py:228-241)."""
+    if not (math.isfinite(alpha) and alpha >= 0):
+        raise ValueError(f"alpha must be >= 0, got {alpha}")
+    arr = np.asarray(v, dtype=np.complex128)
+    dev = _device_or_default()
+    out = soft_threshold_dev(torch.from_numpy(np.ascontiguousarray(arr).ravel()).to(dev), alpha)
+    return out.cpu().numpy().reshape(arr.shape)
+
+
+def relative_magnitude_change(s_prev, s_next) -> float:
+    """‖|s⁺| − |s|‖₂ / max(‖|s|‖₂, 1e-12) (solver.py:244-251)."""
+    a = np.asarray(s_prev)
+    b = np.asarray(s_next)
+    if a.shape != b.shape:
+        raise ValueError(f"iterate shapes differ: {a.shape} vs {b.shape}")
+    dev = _device_or_default()
+    ta = torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128).ravel()).to(dev)
+    tb = torch.from_numpy(np.ascontiguousarray(b, dtype=np.complex128).ravel()).to(dev)
+    st = magnitude_change_dev(ta, tb).cpu().numpy()
+    return float(math.sqrt(st[1])) / max(float(math.sqrt(st[0])), _ZERO_NORM_GUARD)
+
+
+def check_termination(s_prev, s_next, tol: float) -> bool:
+    return relative_magnitude_change(s_prev, s_next) < tol
+
+
+# ------------------------------------------------------------------ device SPGM engine
+
+
+class SPGMEngine:
+    """GPU-resident SPGM state for one voxel slab.
+
+    ``step(idx)`` enqueues one full iteration without synchronising. With a
+    process group the forward partial sums over voxel slabs are all-reduced
+    (one NCCL all-reduce of 2·B reals) before the adjoint.
+    """
+
+    def __init__(self, plan: DevicePlan, y: np.ndarray | torch.Tensor, eta: float, alpha: float,
+                 initial: np.ndarray | torch.Tensor | None = None, process_group=None):
+        self.plan = plan
+        self.eta = float(eta)
+        self.alpha = float(alpha)
+        self.pg = process_group
+        dev = plan.device
+        self.y = plan._as_dev(y, plan.M, "y")
+        self.s = torch.zeros(plan.n_local, dtype=plan.torch_dtype, device=dev)
+        if initial is not None:
+            self.s.copy_(plan._as_dev(initial, plan.n_local, "initial"))
+        self.s_next = torch.empty_like(self.s)
+        self.ybuf = torch.empty(plan.max_batch, dtype=plan.torch_dtype, device=dev)
+        self.stats = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.idx_dev = torch.empty(plan.max_batch, dtype=torch.int32, device=dev)
+
+    def stage(self, idx) -> int:
+        """Stage a host (numpy) or device index list; returns B."""
+        if isinstance(idx, torch.Tensor) and idx.device == self.plan.device:
+            t = idx.to(torch.int32)
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(np.asarray(idx, dtype=np.int32)))
+            t = t.pin_memory() if not t.is_pinned() else t
+            B = t.numel()
+            self.idx_dev[:B].copy_(t, non_blocking=True)
+            t = self.idx_dev[:B]
+        self.plan.prepare(t)
+        return int(t.numel())
+
+    def sample_device(self, seed: int, it: int, batch: int) -> None:
+        self.plan.sample_flat(seed, it, batch, self.idx_dev)
+        self.plan.prepare(self.idx_dev[:batch])
+
+    def step_staged(self) -> None:
+        """One iteration on the staged batch: forward, [allreduce], adjoint+prox, swap."""
+        B = self.plan.B
+        yb = self.ybuf[:B]
+        self.plan.forward(self.s, out=yb)
+        if self.pg is not None:
+            torch.distributed.all_reduce(torch.view_as_real(yb), group=self.pg)
+        self.plan.adjoint_prox(yb, self.y, self.s, self.s_next, self.eta / B, self.alpha, self.stats)
+        self.s, self.s_next = self.s_next, self.s
+
+    def magnitude_change(self) -> float:
+        st = self.stats
+        if self.pg is not None:
+            st = st.clone()
+            torch.distributed.all_reduce(st, group=self.pg)
+        st = st.cpu().numpy()
+        return float(math.sqrt(st[1])) / max(float(math.sqrt(st[0])), _ZERO_NORM_GUARD)
+
+    def volume(self) -> np.ndarray:
+        return self.s.to(torch.complex128).cpu().numpy()
+
+
+def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress, stochastic: bool) -> SolveReport:
+    yv = _measurement_values(y, scenario)
+    m = scenario.n_channels
+    s0 = None if initial is None else np.array(_volume_like(initial, scenario), dtype=np.complex128)
+    dtype = config.dtype or default_dtype()
+    plan = get_plan(scenario, dtype)
+    eng = SPGMEngine(plan, yv, config.eta, config.alpha, initial=s0)
+    rng = np.random.default_rng(config.rng_seed)
+    full_idx = np.arange(m, dtype=np.int64)
+    records: list[IterationRecord] = []
+    termination = TERMINATION_MAX_ITERS
+    iterations = 0
+    staged_full = False
+    pending: list[tuple[int, float, int]] = []
+
+    t_start = time.perf_counter()
+    for k in range(1, config.max_iters + 1):
+        t_iter = time.perf_counter()
+        if not stochastic:
+            if not staged_full:
+                eng.stage(full_idx)
+                staged_full = True
+            B = m
+        elif config.sampler == "device":
+            B = config.flat_batch or (config.composition.batch_size if config.composition else m)
+            eng.sample_device(config.rng_seed, k, B)
+        elif config.sampler == "table":
+            B = eng.stage(np.asarray(config.index_table[k - 1]))
+        elif config.flat_batch is not None:
+            B = eng.stage(sample_flat(scenario, config.flat_batch, rng))
+        else:
+            B = eng.stage(sample_minibatch(config.composition, scenario, rng).indices)
+        eng.step_staged()
+        iterations = k
+        check_now = (k % config.check_every == 0) or k == config.max_iters or progress is not None
+        if check_now:
+            change = eng.magnitude_change()
+            records.append(IterationRecord(k, change, time.perf_counter() - t_iter, B))
+        else:
+            records.append(IterationRecord(k, float("nan"), time.perf_counter() - t_iter, B))
+        if progress is not None:
+            progress(k, eng.volume())
+        if check_now and change < config.tol:
+            termination = TERMINATION_TOLERANCE
+            break
+        if config.time_budget_s is not None and time.perf_counter() - t_start > config.time_budget_s:
+            termination = TERMINATION_TIME_BUDGET
+            break
+    del pending
+    vol = eng.volume()
+    wall = time.perf_counter() - t_start
+    return SolveReport(
+        volume=ReflectivityVolume(vol, scenario.voxels),
+        iterations=iterations,
+        wall_time_s=wall,
+        per_iteration=records,
+        termination=termination,
+    )
+
+
+def pgm_solve(y, scenario: ImagingScenario, config: SolverConfig | None = None, initial=None,
+              progress=None) -> SolveReport:
+    """Full-batch proximal gradient from s⁰ = 0 (solver.py:332-346)."""
+    config = config or SolverConfig()
+    if config.composition is not None and not config.composition.is_full_for(scenario):
+        raise ValueError("pgm_solve needs a full-batch config; use spgm_solve for minibatches")
+    return _solve(y, scenario, config, initial, progress, stochastic=False)
+
+
+def spgm_solve(y, scenario: ImagingScenario, config: SolverConfig | None = None, initial=None,
+               progress=None) -> SolveReport:
+    """Stochastic PGM, fresh minibatch per iteration (solver.py:349-365)."""
+    config = config or SolverConfig()
+    if config.composition is None and config.flat_batch is None and config.sampler != "table":
+        raise ValueError("spgm_solve requires config.composition")
+    if config.composition is not None:
+        config.composition.validate_for(scenario)
+    if config.flat_batch is not None and config.flat_batch > scenario.n_channels:
+        raise ValueError(f"flat_batch={config.flat_batch} exceeds M={scenario.n_channels}")
+    return _solve(y, scenario, config, initial, progress, stochastic=True)
+
+
+def lipschitz_estimate(scenario: ImagingScenario, n_iters: int = 50, rng_seed: int = 0, tol: float = 1e-9,
+                       threads: int = 1, *, dtype=None) -> float:
+    """λ_max((1/M) A^H A) by power iteration from the reference's start vector (solver.py:368-397)."""
+    plan = get_plan(scenario, dtype)
+    rng = np.random.default_rng(rng_seed)
+    n, m = scenario.n_voxels, scenario.n_channels
+    x0 = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    x0 /= np.linalg.norm(x0)
+    x = plan._as_dev(x0, n, "x")
+    plan.prepare(torch.arange(m, dtype=torch.int32, device=plan.device))
+    y = plan.vec(m)
+    z = plan.vec(n)
+    lam = 0.0
+    for _ in range(n_iters):
+        plan.forward(x, out=y)
+        plan.adjoint(y, out=z, scale=1.0 / m)
+        lam_new = float(torch.vdot(x, z).real)
+        nz = float(torch.linalg.vector_norm(z))
+        if nz == 0.0:
+            return 0.0
+        x = z / nz
+        if lam > 0 and abs(lam_new - lam) <= tol * lam:
+            lam = lam_new
+            break
+        lam = lam_new
+    return lam

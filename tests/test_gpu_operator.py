@@ -1,0 +1,243 @@
+"""GPU parity of the operator (forward / adjoint) against the reference's outputs
+(tests/golden) and the oracle, through the C ABI. Tolerances are the north star's:
+relative L2 ≤ 1e-10 in complex128 and ≤ 1e-5 in complex64. Subset restriction
+must be bit-exact."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden, rc, rel_l2, small, tiny
+from oracle import nfmimo_oracle as O
+from paper_2509_00774_b200 import (
+    ArrayGeometry,
+    ChannelSubset,
+    FrequencyGrid,
+    ImagingScenario,
+    ReflectivityVolume,
+    Vec3,
+    VoxelGrid,
+    adjoint_apply,
+    configs,
+    forward_apply,
+    materialize_dense,
+    matrix_element,
+    simulate_measurements,
+)
+from paper_2509_00774_b200.plan import DevicePlan
+
+pytestmark = pytest.mark.gpu
+TOL = {"c128": 1e-10, "c64": 1e-5}
+DTYPES = ("c128", "c64")
+
+
+def one_voxel(tx, rx, vox, f):
+    return ImagingScenario(
+        array=ArrayGeometry((Vec3(*tx),), (Vec3(*rx),)),
+        frequencies=FrequencyGrid(f, f, 1),
+        voxels=VoxelGrid(center=Vec3(*vox), extent=(0, 0, 0), dims=(1, 1, 1)),
+    )
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_known_answers(dtype):
+    ka = golden("known_answers")
+    c = 299_792_458.0
+    rel = 1e-12 if dtype == "c128" else 1e-6
+    val = matrix_element(0, 0, one_voxel((0.1, 0, 0), (-0.1, 0, 0), (0, 0, 0.4), 10e9), dtype=dtype)
+    assert val == pytest.approx(complex(ka["golden_element"]), rel=rel)
+    assert val == pytest.approx(-0.4677243613935091 + 0.018818304865202827j, rel=rel)
+    assert matrix_element(0, 0, one_voxel((0, 0, 0), (0, 0, 0), (0, 0, 0.5), c), dtype=dtype) == pytest.approx(
+        1 / np.pi, rel=rel)
+    assert matrix_element(0, 0, one_voxel((0, 0, 0), (0, 0, 0), (0, 0, 0.5), c / 4), dtype=dtype) == pytest.approx(
+        -1j / np.pi, rel=rel)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("name,builder", [("tiny", tiny), ("small", small)])
+def test_reference_fixture_scenarios(name, builder, dtype):
+    g = golden("unit_scenarios")
+    scn = builder()
+    tol = TOL[dtype]
+    assert rel_l2(materialize_dense(scn, dtype=dtype), g[f"{name}_dense"]) <= tol
+    s, r, sub = g[f"{name}_s"], g[f"{name}_r"], g[f"{name}_sub"]
+    assert rel_l2(forward_apply(s, scn, dtype=dtype), g[f"{name}_fwd"]) <= tol
+    assert rel_l2(forward_apply(s, scn, subset=sub, dtype=dtype), g[f"{name}_fwd_sub"]) <= tol
+    assert rel_l2(adjoint_apply(r, scn, dtype=dtype), g[f"{name}_adj"]) <= tol
+    assert rel_l2(adjoint_apply(r[: sub.size], scn, subset=sub, dtype=dtype), g[f"{name}_adj_sub"]) <= tol
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_subset_restriction_bit_exact(dtype, rng):
+    scn = configs.small_scenario()
+    s = rc(rng, scn.n_voxels)
+    full = forward_apply(s, scn, dtype=dtype)
+    for _ in range(6):
+        size = int(rng.integers(1, scn.n_channels + 1))
+        sub = rng.choice(scn.n_channels, size=size, replace=False)
+        assert np.array_equal(forward_apply(s, scn, subset=sub, dtype=dtype), full[sub])
+    # order of the subset is the order of the output
+    sub = ChannelSubset(np.array([5, 1, 3]))
+    assert np.array_equal(forward_apply(s, scn, subset=sub, dtype=dtype), full[[5, 1, 3]])
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_adjoint_identity_over_random_subsets(dtype, rng):
+    scn = small()
+    m_count = scn.n_channels
+    for _ in range(50):
+        size = int(rng.integers(1, m_count + 1))
+        sub = rng.choice(m_count, size=size, replace=False)
+        s = rc(rng, scn.n_voxels)
+        r = rc(rng, size)
+        as_ = forward_apply(s, scn, subset=sub, dtype=dtype)
+        ahr = adjoint_apply(r, scn, subset=sub, dtype=dtype)
+        bound = (1e-10 if dtype == "c128" else 1e-5) * (
+            np.linalg.norm(as_) * np.linalg.norm(r) + np.linalg.norm(s) * np.linalg.norm(ahr))
+        assert abs(np.vdot(r, as_) - np.vdot(ahr, s)) <= bound
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_linearity_zero_and_unit_vectors(dtype, small_scenario, rng):
+    scn = small_scenario
+    assert np.array_equal(forward_apply(np.zeros(scn.n_voxels), scn, dtype=dtype), np.zeros(scn.n_channels))
+    assert np.array_equal(adjoint_apply(np.zeros(scn.n_channels), scn, dtype=dtype), np.zeros(scn.n_voxels))
+    s1, s2 = rc(rng, scn.n_voxels), rc(rng, scn.n_voxels)
+    a, b = 0.7 - 0.2j, -1.3 + 0.4j
+    lhs = forward_apply(a * s1 + b * s2, scn, dtype=dtype)
+    rhs = a * forward_apply(s1, scn, dtype=dtype) + b * forward_apply(s2, scn, dtype=dtype)
+    assert rel_l2(lhs, rhs) <= (1e-12 if dtype == "c128" else 1e-5)
+    dense = golden("unit_scenarios")["small_dense"]
+    e = np.zeros(scn.n_voxels, complex)
+    e[5] = 1.0
+    assert rel_l2(forward_apply(e, scn, dtype=dtype), dense[:, 5]) <= TOL[dtype]
+    r = np.zeros(scn.n_channels, complex)
+    r[7] = 1.0
+    assert rel_l2(adjoint_apply(r, scn, dtype=dtype), np.conj(dense[7])) <= TOL[dtype]
+
+
+def test_validation_errors(small_scenario, tiny_scenario):
+    scn = small_scenario
+    with pytest.raises(ValueError, match="grid"):
+        forward_apply(ReflectivityVolume.zeros(tiny_scenario.voxels), scn)
+    with pytest.raises(ValueError, match="voxel values"):
+        forward_apply(np.zeros(3), scn)
+    with pytest.raises(ValueError, match="residual"):
+        adjoint_apply(np.zeros(3), scn, subset=np.array([0, 1]))
+    with pytest.raises(IndexError):
+        forward_apply(np.zeros(scn.n_voxels), scn, subset=np.array([scn.n_channels]))
+    with pytest.raises(ValueError):
+        forward_apply(np.zeros(scn.n_voxels), scn, subset=np.array([], dtype=int))
+    with pytest.raises(IndexError):
+        matrix_element(0, scn.n_voxels, scn)
+    with pytest.raises(IndexError):
+        matrix_element(scn.n_channels, 0, scn)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_baseline_small_probe(dtype):
+    b = golden("baseline_small")
+    scn = configs.small_scenario()
+    assert rel_l2(forward_apply(b["probe_s"], scn, subset=b["probe_idx"], dtype=dtype), b["probe_fwd"]) <= TOL[dtype]
+    assert rel_l2(adjoint_apply(b["probe_r"], scn, subset=b["probe_idx"], dtype=dtype), b["probe_adj"]) <= TOL[dtype]
+    assert rel_l2(forward_apply(b["s_true"], scn, dtype=dtype), b["clean"]) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_medium_against_reference_outputs(dtype):
+    """BASELINE config 1 geometry: the reference's cached-table results (tests/golden/medium_ops.npz)."""
+    m = golden("medium_ops")
+    scn = configs.medium_scenario()
+    s = rc(np.random.default_rng(int(m["s_seed"])), scn.n_voxels)
+    r = rc(np.random.default_rng(int(m["r_seed"])), m["idx"].size)
+    assert rel_l2(forward_apply(s, scn, subset=m["idx"], dtype=dtype), m["fwd"]) <= TOL[dtype]
+    adj = adjoint_apply(r, scn, subset=m["idx"], dtype=dtype)
+    assert rel_l2(adj[m["adj_probe_voxels"]], m["adj_probe"]) <= TOL[dtype]
+    assert np.linalg.norm(adj) == pytest.approx(float(m["adj_norm"]), rel=TOL[dtype])
+
+
+def test_large_spot_check_against_direct_formula():
+    """BASELINE config 2 (Large, c64): the reference's tables (206 GB) cannot be built, so sampled
+    output rows (forward) and sampled voxels (adjoint) are checked against the table-free oracle."""
+    scn = configs.large_scenario()
+    geo = O.geom_from_scenario(scn)
+    rng = np.random.default_rng(5)
+    s = rc(rng, scn.n_voxels).astype(np.complex64).astype(np.complex128)
+    idx = np.sort(rng.choice(scn.n_channels, 4096, replace=False))
+    y = forward_apply(s, scn, subset=idx, dtype="c64")
+    rows = rng.choice(idx.size, 24, replace=False)
+    assert rel_l2(y[rows], O.direct_forward(geo, s, idx[rows], chunk=65536)) <= 1e-5
+    r = rc(rng, idx.size).astype(np.complex64).astype(np.complex128)
+    g = adjoint_apply(r, scn, subset=idx, dtype="c64")
+    vox = rng.choice(scn.n_voxels, 2048, replace=False)
+    assert rel_l2(g[vox], O.direct_adjoint(geo, r, idx, voxels=vox)) <= 1e-5
+
+
+@pytest.mark.parametrize("dims", [(5, 3, 2), (1, 1, 7), (9, 1, 1), (17, 6, 5)])
+def test_ragged_grids_match_oracle(dims, rng):
+    """Grids that do not fill the 8×4×4 warp tiles (masked lanes)."""
+    ext = tuple(0.0 if d == 1 else 0.05 * d / 4 for d in dims)
+    scn = ImagingScenario(
+        array=ArrayGeometry(((0.03, 0.01, 0.0), (-0.02, 0.04, 0.0), (0.0, -0.05, 0.0)),
+                            ((0.01, 0.0, 0.0), (-0.04, -0.01, 0.0))),
+        frequencies=FrequencyGrid(20e9, 30e9, 5),
+        voxels=VoxelGrid(center=Vec3(0.0, 0.0, 0.3), extent=ext, dims=dims),
+    )
+    geo = O.geom_from_scenario(scn)
+    s, r = rc(rng, scn.n_voxels), rc(rng, scn.n_channels)
+    for dtype in DTYPES:
+        assert rel_l2(forward_apply(s, scn, dtype=dtype), O.direct_forward(geo, s, np.arange(geo.M))) <= TOL[dtype]
+        assert rel_l2(adjoint_apply(r, scn, dtype=dtype), O.direct_adjoint(geo, r, np.arange(geo.M))) <= TOL[dtype]
+
+
+def test_many_transmitters_several_tx_groups(rng):
+    """T=30 (3 shared-memory tx groups in c64, 5 in c128), single-channel and full batches."""
+    tx = tuple((0.01 * i - 0.15, 0.07 * ((i % 3) - 1), 0.0) for i in range(30))
+    rx = tuple((0.05 * ((i % 2) * 2 - 1), 0.013 * i - 0.05, 0.0) for i in range(9))
+    scn = ImagingScenario(array=ArrayGeometry(tx, rx), frequencies=FrequencyGrid(30e9, 32e9, 3),
+                          voxels=VoxelGrid(center=Vec3(0, 0, 0.25), extent=(0.05, 0.04, 0.03), dims=(12, 9, 6)))
+    geo = O.geom_from_scenario(scn)
+    s = rc(rng, scn.n_voxels)
+    full = np.arange(geo.M)
+    ref_f = O.direct_forward(geo, s, full)
+    for dtype in DTYPES:
+        assert rel_l2(forward_apply(s, scn, dtype=dtype), ref_f) <= TOL[dtype]
+        one = forward_apply(s, scn, subset=[437], dtype=dtype)
+        assert abs(one[0] - ref_f[437]) <= TOL[dtype] * 10 * abs(ref_f[437])
+        r = rc(rng, 7)
+        sub = rng.choice(geo.M, 7, replace=False)
+        assert rel_l2(adjoint_apply(r, scn, subset=sub, dtype=dtype), O.direct_adjoint(geo, r, sub)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_slab_plans_sum_to_full(dtype, rng):
+    """Voxel-slab sharding: per-slab forward partials sum to the full forward;
+    per-slab adjoints are the slices of the full adjoint."""
+    scn = configs.small_scenario()
+    s = rc(rng, scn.n_voxels)
+    idx = torch.from_numpy(np.sort(rng.choice(scn.n_channels, 40, replace=False)).astype(np.int32)).cuda()
+    full = DevicePlan(scn, dtype=dtype)
+    full.prepare(idx)
+    st = full._as_dev(s, scn.n_voxels, "s")
+    y_full = full.forward(st).cpu().numpy()
+    r = full._as_dev(rc(rng, 40), 40, "r")
+    g_full = full.adjoint(r).cpu().numpy()
+    nxy = 16 * 16
+    acc = np.zeros_like(y_full)
+    for z0, z1 in ((0, 3), (3, 8)):
+        p = DevicePlan(scn, dtype=dtype, z_range=(z0, z1))
+        p.prepare(idx)
+        acc += p.forward(st[z0 * nxy:z1 * nxy].contiguous()).cpu().numpy()
+        assert rel_l2(p.adjoint(r).cpu().numpy(), g_full[z0 * nxy:z1 * nxy]) <= TOL[dtype]
+    assert rel_l2(acc, y_full) <= TOL[dtype]
+
+
+def test_simulate_measurements_noise_convention(small_scenario, rng):
+    s = rc(rng, small_scenario.n_voxels)
+    a = simulate_measurements(s, small_scenario, noise_sigma=0.0)
+    assert np.array_equal(a.values, forward_apply(s, small_scenario)) and a.matches(small_scenario)
+    b = simulate_measurements(s, small_scenario, noise_sigma=0.5, rng_seed=9)
+    c = simulate_measurements(s, small_scenario, noise_sigma=0.5, rng_seed=9)
+    assert np.array_equal(b.values, c.values)
