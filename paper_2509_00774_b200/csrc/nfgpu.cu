@@ -2,49 +2,57 @@
 // near-field MIMO imaging reference `nfmimo` (arXiv 2509.00774).
 //
 // The reference (pkg/src/nfmimo/forward.py:183-336) caches F×(T+R)×N complex128
-// phasor tables. Each forward/adjoint is then elementwise products plus BLAS dots.
-// Here nothing frequency-dependent is stored. Every operator entry
+// phasor tables and turns each forward/adjoint into elementwise products plus
+// BLAS dots. Nothing frequency-dependent is stored here. Every operator entry
 //     A[m,n] = p_f exp(-j 2π f (dT+dR)/c) / (4π dT dR)            (forward.py:142-155)
-// is regenerated in registers from a frequency-free per-(antenna, voxel)
+// is regenerated in registers. The inputs are a frequency-free per-(antenna, voxel)
 // distance table (8 B per pair in c64) and two MUFU ops (sin, cos).
 //
 // Work decomposition:
 //   * voxels are cut into warp tiles of 8×4×4 = 128 voxels. Lane L owns 4 voxels
-//     that are consecutive in x (coalesced s loads, conflict-free smem rows).
-//   * each tile has an fp64 anchor (its centre). The table stores
-//     δ = d − D0(tile, antenna) in fp32, plus 1/d. The per-(channel, tile) phase
-//     offset frac(f/c·(D0_T+D0_R)) is computed once in fp64. Per entry the
-//     phase is x = base + (f/c)·(δT+δR) with |x| <~ 8 rev. It is reduced to
-//     [-½,½] and fed to __sincosf. This keeps ~1e-6 rad accuracy at phases of ~2e3 rad.
-//   * the channel batch is sorted on the device by (tx-group, rx, tx, f).
-//     A warp keeps the rx-side table entries for the current rx run in registers.
-//     The tx-side entries of the current tx group sit in shared memory, so each
-//     entry costs one conflict-free 16-byte shared load per 4 voxels.
+//     that are consecutive in x, stored as two fp32x2 pairs so the per-entry
+//     arithmetic runs on packed FADD2/FFMA2/FMUL2 (sm_100a).
+//   * each tile has an fp64 anchor (its centre). The table stores δ = d − D0(tile, antenna)
+//     in fp32, plus 1/d. The per-(channel, tile) phase offset frac(f/c·(D0_T + D0_R))
+//     is computed once per channel and tile in fp64. Per entry the phase in
+//     revolutions is x = base + (f/c)·(δT+δR), |x| ≲ 8. It is reduced exactly to
+//     [-½, ½] before MUFU.SIN/COS. That holds the phase error to ~1e-6 rad at
+//     phases of ~2e3 rad.
+//   * the channel batch is sorted on the device by (tx-group, rx, tx, f). Per rx
+//     run, a warp keeps the rx-side table entries of its voxels in registers
+//     (prefetched one run ahead). Per tx group, the tx-side entries sit in the warp's
+//     shared memory. Each entry then costs one conflict-free 16-byte shared load per 4 voxels.
+//   * adjoint (+prox): a warp owns (tile, channel chunk). Chunks of a tile are
+//     combined in fixed order by the last-arriving warp, which also applies the
+//     complex soft-threshold prox (solver.py:228-241) and writes the termination
+//     statistics (solver.py:244-251). The result is deterministic, with no float atomics.
 //   * forward: per-channel lane partials → warp transpose-reduce through smem →
-//     CTA combine → deterministic cross-CTA column reduce (fp64) in a second kernel.
-//   * adjoint: a warp owns its tile for the whole batch (no reduction across warps).
-//     The complex soft-threshold prox (solver.py:228-241) and the termination
-//     statistics (solver.py:244-251) run in the epilogue.
+//     CTA combine → two-level deterministic fp64 column reduce.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/nfgpu.h"
 
 namespace {
 
-constexpr int V = 4;            // voxels per lane
+constexpr int V = 4;  // voxels per lane
 constexpr int TILE_X = 8, TILE_Y = 4, TILE_Z = 4;
 constexpr int TILE = TILE_X * TILE_Y * TILE_Z;  // 128 = 32 lanes × V
+constexpr int TABW = 2 * TILE;                  // Reals per (tile, antenna): δ block + 1/d block
 constexpr int FWD_WARPS = 4;
 constexpr int ADJ_WARPS = 4;
-constexpr int TG_MAX_F = 12;    // tx per smem group (c64): 12 KB smem per warp
-constexpr int TG_MAX_D = 6;     // tx per smem group (c128): 12 KB smem per warp
+constexpr int TG_MAX = 6;      // tx per shared-memory group
+constexpr int A_MAX = 256;     // antennas (T + R) per plan
+constexpr int RED_THREADS = 300000;
+constexpr unsigned FULL = 0xffffffffu;
 constexpr double PI = 3.14159265358979323846;
 
 thread_local std::string g_err;
@@ -61,42 +69,176 @@ int fail(int code, const std::string& msg) {
       return fail(NF_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-// ------------------------------------------------------------------ phasor
-// cos/sin(2π·rev) of rev = base + k·dsum with the revolution count reduced to [-½, ½]
-// before the MUFU (magic-number round-to-nearest, exact for |x| < 2^22).
-__device__ __forceinline__ void phasor(float k, float base, float dsum, float& c, float& s) {
-  float x = fmaf(k, dsum, base);
-  float u = x + 12582912.0f;
-  float r = u - 12582912.0f;
-  float fr = x - r;
-  __sincosf(fr * 6.28318530717958647692f, &s, &c);
+// ------------------------------------------------------------------ packed fp32x2 (sm_100a)
+__device__ __forceinline__ uint64_t as_u64(float2 v) { return *reinterpret_cast<uint64_t*>(&v); }
+__device__ __forceinline__ float2 as_f2(uint64_t v) { return *reinterpret_cast<float2*>(&v); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)));
+  return as_f2(d);
 }
-__device__ __forceinline__ void phasor(double k, double base, double dsum, double& c, double& s) {
-  double x = fma(k, dsum, base);
-  double fr = x - rint(x);
-  sincospi(2.0 * fr, &s, &c);
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)));
+  return as_f2(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)));
+  return as_f2(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)), "l"(as_u64(c)));
+  return as_f2(d);
+}
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
+
+// ------------------------------------------------------------------ 4-voxel lane vectors
+struct F4 {  // voxels (0,1) and (2,3) of a lane as fp32 pairs
+  float2 a, b;
+};
+struct D4 {
+  double v[4];
+};
+template <typename Real>
+using Q4 = typename std::conditional<std::is_same<Real, float>::value, F4, D4>::type;
+
+__device__ __forceinline__ F4 ld4(const float* p) {
+  const float4 q = *reinterpret_cast<const float4*>(p);
+  return F4{make_float2(q.x, q.y), make_float2(q.z, q.w)};
+}
+__device__ __forceinline__ D4 ld4(const double* p) {
+  const double2 q0 = reinterpret_cast<const double2*>(p)[0];
+  const double2 q1 = reinterpret_cast<const double2*>(p)[1];
+  return D4{{q0.x, q0.y, q1.x, q1.y}};
+}
+__device__ __forceinline__ float get(const F4& q, int v) { return v == 0 ? q.a.x : v == 1 ? q.a.y : v == 2 ? q.b.x : q.b.y; }
+__device__ __forceinline__ double get(const D4& q, int v) { return q.v[v]; }
+__device__ __forceinline__ void zero(F4& q) { q.a = q.b = make_float2(0.f, 0.f); }
+__device__ __forceinline__ void zero(D4& q) { q.v[0] = q.v[1] = q.v[2] = q.v[3] = 0.0; }
+
+// cos/sin(2π·x_v), x_v = base + k·(dT_v + dR_v), reduced exactly to [-½, ½] revolutions
+// (magic-number round-to-nearest, exact for |x| < 2^22) before MUFU.SIN/COS.
+__device__ __forceinline__ void phasor4(float k, float base, const F4& dT, const F4& dR, F4& c, F4& s) {
+  const float2 M2 = bc(12582912.0f);
+  const float2 x0 = fma2(bc(k), add2(dT.a, dR.a), bc(base));
+  const float2 x1 = fma2(bc(k), add2(dT.b, dR.b), bc(base));
+  const float2 f0 = sub2(x0, sub2(add2(x0, M2), M2));
+  const float2 f1 = sub2(x1, sub2(add2(x1, M2), M2));
+  const float2 r0 = mul2(f0, bc(6.28318530717958647692f));
+  const float2 r1 = mul2(f1, bc(6.28318530717958647692f));
+  __sincosf(r0.x, &s.a.x, &c.a.x);
+  __sincosf(r0.y, &s.a.y, &c.a.y);
+  __sincosf(r1.x, &s.b.x, &c.b.x);
+  __sincosf(r1.y, &s.b.y, &c.b.y);
+}
+__device__ __forceinline__ void phasor4(double k, double base, const D4& dT, const D4& dR, D4& c, D4& s) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const double x = fma(k, dT.v[v] + dR.v[v], base);
+    sincospi(2.0 * (x - rint(x)), &s.v[v], &c.v[v]);
+  }
+}
+
+// adjoint: h += iT·e^{+jθ}·w  (w = conj(p)/(4π)·r, one complex per channel)
+__device__ __forceinline__ void adj_acc(const F4& iT, const F4& c, const F4& s, float wr, float wi, F4& hr,
+                                        F4& hi) {
+  const float2 a0 = mul2(iT.a, c.a), b0 = mul2(iT.a, s.a);
+  const float2 a1 = mul2(iT.b, c.b), b1 = mul2(iT.b, s.b);
+  hr.a = fma2(b0, bc(-wi), fma2(a0, bc(wr), hr.a));
+  hr.b = fma2(b1, bc(-wi), fma2(a1, bc(wr), hr.b));
+  hi.a = fma2(b0, bc(wr), fma2(a0, bc(wi), hi.a));
+  hi.b = fma2(b1, bc(wr), fma2(a1, bc(wi), hi.b));
+}
+__device__ __forceinline__ void adj_acc(const D4& iT, const D4& c, const D4& s, double wr, double wi, D4& hr,
+                                        D4& hi) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const double a = iT.v[v] * c.v[v], b = iT.v[v] * s.v[v];
+    hr.v[v] = fma(-b, wi, fma(a, wr, hr.v[v]));
+    hi.v[v] = fma(b, wr, fma(a, wi, hi.v[v]));
+  }
+}
+// end of an rx run: g += iR·h, h = 0
+__device__ __forceinline__ void flush(const F4& iR, F4& hr, F4& hi, F4& gr, F4& gi) {
+  gr.a = fma2(iR.a, hr.a, gr.a);
+  gr.b = fma2(iR.b, hr.b, gr.b);
+  gi.a = fma2(iR.a, hi.a, gi.a);
+  gi.b = fma2(iR.b, hi.b, gi.b);
+  zero(hr);
+  zero(hi);
+}
+__device__ __forceinline__ void flush(const D4& iR, D4& hr, D4& hi, D4& gr, D4& gi) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    gr.v[v] = fma(iR.v[v], hr.v[v], gr.v[v]);
+    gi.v[v] = fma(iR.v[v], hi.v[v], gi.v[v]);
+  }
+  zero(hr);
+  zero(hi);
+}
+// forward: ŝ = iR·s for the current rx run
+__device__ __forceinline__ void scale_s(const F4& iR, const F4& sr, const F4& si, F4& shr, F4& shi) {
+  shr.a = mul2(iR.a, sr.a);
+  shr.b = mul2(iR.b, sr.b);
+  shi.a = mul2(iR.a, si.a);
+  shi.b = mul2(iR.b, si.b);
+}
+__device__ __forceinline__ void scale_s(const D4& iR, const D4& sr, const D4& si, D4& shr, D4& shi) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    shr.v[v] = iR.v[v] * sr.v[v];
+    shi.v[v] = iR.v[v] * si.v[v];
+  }
+}
+// forward: Σ_v iT·e^{-jθ}·ŝ over the lane's 4 voxels
+__device__ __forceinline__ float2 fwd_part(const F4& iT, const F4& c, const F4& s, const F4& shr, const F4& shi) {
+  const float2 a0 = mul2(iT.a, c.a), b0 = mul2(iT.a, s.a);
+  const float2 a1 = mul2(iT.b, c.b), b1 = mul2(iT.b, s.b);
+  float2 pr = fma2(a0, shr.a, mul2(b0, shi.a));
+  pr = fma2(b1, shi.b, fma2(a1, shr.b, pr));
+  float2 pi = fma2(a0, shi.a, mul2(b0, make_float2(-shr.a.x, -shr.a.y)));
+  pi = fma2(b1, make_float2(-shr.b.x, -shr.b.y), fma2(a1, shi.b, pi));
+  return make_float2(pr.x + pr.y, pi.x + pi.y);
+}
+__device__ __forceinline__ double2 fwd_part(const D4& iT, const D4& c, const D4& s, const D4& shr, const D4& shi) {
+  double pr = 0, pi = 0;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const double a = iT.v[v] * c.v[v], b = iT.v[v] * s.v[v];
+    pr = fma(b, shi.v[v], fma(a, shr.v[v], pr));
+    pi = fma(-b, shr.v[v], fma(a, shi.v[v], pi));
+  }
+  return make_double2(pr, pi);
 }
 
 template <typename Real>
-struct Vec4T;
+struct Real2T;
 template <>
-struct Vec4T<float> {
+struct Real2T<float> {
+  using T = float2;
+};
+template <>
+struct Real2T<double> {
+  using T = double2;
+};
+template <typename Real>
+using R2 = typename Real2T<Real>::T;
+template <typename Real>
+struct Real4T;
+template <>
+struct Real4T<float> {
   using T = float4;
 };
 template <>
-struct Vec4T<double> {
-  using T = double4;
+struct Real4T<double> {
+  struct T {
+    double x, y, z, w;
+  };
 };
-
 template <typename Real>
-__device__ __forceinline__ void ld4(const Real* p, Real (&v)[4]) {
-  using V4 = typename Vec4T<Real>::T;
-  V4 q = *reinterpret_cast<const V4*>(p);
-  v[0] = q.x;
-  v[1] = q.y;
-  v[2] = q.z;
-  v[3] = q.w;
-}
+using R4 = typename Real4T<Real>::T;
 
 // ------------------------------------------------------------------ geometry
 struct Geo {
@@ -109,20 +251,19 @@ struct Geo {
 
 __device__ __forceinline__ void tile_coords(const Geo& g, int tile, int& tx, int& ty, int& tz) {
   tz = tile / (g.ntx * g.nty);
-  int rem = tile - tz * g.ntx * g.nty;
+  const int rem = tile - tz * g.ntx * g.nty;
   ty = rem / g.ntx;
   tx = rem - ty * g.ntx;
 }
 
 // lane L of tile (tx,ty,tz) owns voxels x = 8tx + 4(L&1) + v, y = 4ty + ((L>>1)&3), z = 4tz + (L>>3)
-__device__ __forceinline__ void lane_voxel(const Geo& g, int tx, int ty, int tz, int L, int& x0, int& y,
-                                           int& z) {
+__device__ __forceinline__ void lane_voxel(int tx, int ty, int tz, int L, int& x0, int& y, int& z) {
   x0 = tx * TILE_X + (L & 1) * V;
   y = ty * TILE_Y + ((L >> 1) & 3);
   z = tz * TILE_Z + (L >> 3);
 }
 
-// table[tile][a][2][32][4]: [0] = δ, [1] = 1/d for the lane's 4 voxels; D0[tile][a] fp64.
+// table[tile][a][2][32][4]: [0] = δ = d − D0, [1] = 1/d for the lane's 4 voxels; D0[tile][a] in fp64.
 template <typename Real>
 __global__ void build_table_kernel(Geo g, const double* __restrict__ ant, Real* __restrict__ tab,
                                    double* __restrict__ D0) {
@@ -136,8 +277,8 @@ __global__ void build_table_kernel(Geo g, const double* __restrict__ ant, Real* 
   const double d0 = sqrt((ax - px) * (ax - px) + (ay - py) * (ay - py) + (az - pz) * (az - pz));
   if (L == 0) D0[(size_t)tile * g.A + a] = d0;
   int x0, y, z;
-  lane_voxel(g, tx, ty, tz, L, x0, y, z);
-  Real* out = tab + ((size_t)tile * g.A + a) * (2 * 32 * V);
+  lane_voxel(tx, ty, tz, L, x0, y, z);
+  Real* out = tab + ((size_t)tile * g.A + a) * TABW;
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int x = x0 + v;
@@ -152,7 +293,7 @@ __global__ void build_table_kernel(Geo g, const double* __restrict__ ant, Real* 
       iv = (Real)(1.0 / d);
     }
     out[L * V + v] = dl;
-    out[32 * V + L * V + v] = iv;
+    out[TILE + L * V + v] = iv;
   }
 }
 
@@ -169,16 +310,14 @@ __device__ __forceinline__ int key_of(const KeyMap& k, int m) {
   const int tg = t / k.Tg, tl = t - tg * k.Tg;
   return ((tg * k.R + r) * k.Tg + tl) * k.F + f;
 }
-__device__ __forceinline__ int m_of_key(const KeyMap& k, int key, bool& ok) {
+__device__ __forceinline__ int4 chan_of_key(const KeyMap& k, int key) {  // {f, t, r, tg}
   const int f = key % k.F;
   int q = key / k.F;
   const int tl = q % k.Tg;
   q /= k.Tg;
   const int r = q % k.R;
   const int tg = q / k.R;
-  const int t = tg * k.Tg + tl;
-  ok = t < k.T;
-  return r + k.R * (t + k.T * f);
+  return make_int4(f, tg * k.Tg + tl, r, tg);
 }
 
 __global__ void mark_kernel(KeyMap km, const int* __restrict__ idx, int B, int* __restrict__ pos_of_key) {
@@ -187,12 +326,11 @@ __global__ void mark_kernel(KeyMap km, const int* __restrict__ idx, int B, int* 
 }
 
 __device__ __forceinline__ int block_excl_scan_1024(int v, int* sh, int& total) {
-  // 1024 threads; sh >= 32 ints
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
+    const int y = __shfl_up_sync(FULL, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) sh[wid] = x;
@@ -201,7 +339,7 @@ __device__ __forceinline__ int block_excl_scan_1024(int v, int* sh, int& total) 
     int w = sh[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, w, o);
+      const int y = __shfl_up_sync(FULL, w, o);
       if (lane >= o) w += y;
     }
     sh[lane] = w;
@@ -215,11 +353,9 @@ __device__ __forceinline__ int block_excl_scan_1024(int v, int* sh, int& total) 
 
 __global__ void __launch_bounds__(1024) count_kernel(const int* __restrict__ pos_of_key, int KS,
                                                       int* __restrict__ cnt) {
-  __shared__ int sh[32];
   const int key = blockIdx.x * 1024 + threadIdx.x;
   const int f = (key < KS && pos_of_key[key] >= 0) ? 1 : 0;
   const int c = __syncthreads_count(f);
-  (void)sh;
   if (threadIdx.x == 0) cnt[blockIdx.x] = c;
 }
 
@@ -236,19 +372,38 @@ __global__ void __launch_bounds__(1024) scan_kernel(int* __restrict__ cnt, int n
   }
 }
 
+// Per sorted position: everything a warp needs about a channel except its tile-dependent
+// phase offset. pk = t | r << 8 | tg << 16 (T, R <= 255 since T + R <= A_MAX).
+struct ChanRec {
+  double kd;  // f / c (fp64, for the anchor phase)
+  float kf;   // f / c (fp32, per-entry slope)
+  int pk;
+};
+__device__ __forceinline__ int pk_t(int pk) { return pk & 0xff; }
+__device__ __forceinline__ int pk_r(int pk) { return (pk >> 8) & 0xff; }
+__device__ __forceinline__ int pk_tg(int pk) { return pk >> 16; }
+
+// sorted position j <- key order; crec[j], sf[j] = f
 __global__ void __launch_bounds__(1024) compact_kernel(KeyMap km, int* __restrict__ pos_of_key, int KS,
                                                         const int* __restrict__ off, int* __restrict__ sm,
-                                                        int* __restrict__ spos) {
+                                                        int* __restrict__ spos, ChanRec* __restrict__ crec,
+                                                        int* __restrict__ sf, const double* __restrict__ kd) {
   __shared__ int sh[32];
   const int key = blockIdx.x * 1024 + threadIdx.x;
   const int p = key < KS ? pos_of_key[key] : -1;
   int total;
   const int pre = block_excl_scan_1024(p >= 0 ? 1 : 0, sh, total);
   if (p >= 0) {
-    bool ok;
     const int j = off[blockIdx.x] + pre;
-    sm[j] = m_of_key(km, key, ok);
+    const int4 c = chan_of_key(km, key);
+    sm[j] = c.z + km.R * (c.y + km.T * c.x);
     spos[j] = p;
+    ChanRec q;
+    q.kd = kd[c.x];
+    q.kf = (float)q.kd;
+    q.pk = c.y | (c.z << 8) | (c.w << 16);
+    crec[j] = q;
+    sf[j] = c.x;
     pos_of_key[key] = -1;
   }
 }
@@ -267,7 +422,7 @@ __device__ __forceinline__ uint32_t feistel(uint32_t x, int hb, uint64_t key) {
   uint32_t l = x >> hb, r = x & mask;
 #pragma unroll
   for (int round = 0; round < 6; ++round) {
-    const uint32_t k = (uint32_t)(key >> (round & 1 ? 32 : 0)) ^ (0x9e3779b9u * (round + 1));
+    const uint32_t k = (uint32_t)(key >> ((round & 1) ? 32 : 0)) ^ (0x9e3779b9u * (round + 1));
     const uint32_t f = hash32(r ^ k) & mask;
     const uint32_t nl = r;
     r = l ^ f;
@@ -285,203 +440,112 @@ __global__ void sample_kernel(uint64_t key, int hb, int M, int B, int* __restric
   idx[j] = (int)x;
 }
 
-// ------------------------------------------------------------------ forward
+// ------------------------------------------------------------------ per-warp shared state
 template <typename Real>
-struct FwdRec {
-  Real k, base;
-  int tl, r, tg, pad;
+struct WarpSmem {
+  Real* tside;    // [Tg][2][32][4]
+  double* d0;     // [A]
+  R4<Real>* rec;  // [32] {k, base, wr, wi}
+  int2* rect;     // [32] {tside offset, run key}
 };
-
+__host__ __device__ constexpr int d0_slots(int A) { return (A + 1) & ~1; }  // keep 16-byte alignment
 template <typename Real>
-struct FwdArgs {
-  Geo g;
-  const Real* __restrict__ tab;
-  const double* __restrict__ D0;
-  const double* __restrict__ kd;
-  const Real* __restrict__ kf;
-  const Real* __restrict__ s;  // complex, slab-local flat order
-  const int* __restrict__ sm;  // sorted channel ids
-  int j0, j1;                  // sorted positions of this chunk
-  int Q;                       // channel splits (gridDim.y)
-  Real* __restrict__ partials;  // [gridDim.x][j1-j0] complex
-};
-
+__host__ __device__ constexpr size_t warp_smem_bytes(int Tg, int A) {
+  return (size_t)Tg * TABW * sizeof(Real) + (size_t)d0_slots(A) * sizeof(double) + 32 * sizeof(R4<Real>) +
+         32 * sizeof(int2);
+}
 template <typename Real>
-__global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Geo& g = a.g;
-  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int tile = blockIdx.x * FWD_WARPS + w;
-  const bool tile_ok = tile < g.ntiles;
-  const int per_t = g.Tg * 2 * 32 * V;  // Reals per warp tx-group buffer
-  Real* tside = reinterpret_cast<Real*>(smem_raw) + (size_t)w * per_t;
-  FwdRec<Real>* rec =
-      reinterpret_cast<FwdRec<Real>*>(reinterpret_cast<Real*>(smem_raw) + (size_t)FWD_WARPS * per_t) +
-      w * 32;
-  Real* tb = reinterpret_cast<Real*>(reinterpret_cast<FwdRec<Real>*>(
-                 reinterpret_cast<Real*>(smem_raw) + (size_t)FWD_WARPS * per_t) +
-                                     FWD_WARPS * 32);
-  Real* cbuf = tb + (size_t)FWD_WARPS * 32 * 33 * 2;  // [2][W][32] complex
-  Real* mytb = tb + (size_t)w * 32 * 33 * 2;
+__device__ __forceinline__ WarpSmem<Real> carve(unsigned char* base, int Tg, int A) {
+  WarpSmem<Real> ws;
+  ws.tside = reinterpret_cast<Real*>(base);
+  ws.d0 = reinterpret_cast<double*>(base + (size_t)Tg * TABW * sizeof(Real));
+  ws.rec = reinterpret_cast<R4<Real>*>(reinterpret_cast<unsigned char*>(ws.d0) + d0_slots(A) * sizeof(double));
+  ws.rect = reinterpret_cast<int2*>(ws.rec + 32);
+  return ws;
+}
 
-  int tx = 0, ty = 0, tz = 0;
-  if (tile_ok) tile_coords(g, tile, tx, ty, tz);
-  int x0, y, z;
-  lane_voxel(g, tx, ty, tz, L, x0, y, z);
-  Real sr[V], si[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int x = x0 + v;
-    const bool ok = tile_ok && x < g.nx && y < g.ny && z < g.nzs;
-    const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
-    sr[v] = ok ? a.s[2 * n] : Real(0);
-    si[v] = ok ? a.s[2 * n + 1] : Real(0);
+// Copy the tx-side table rows of tx group tg for this tile into the warp's smem.
+template <typename Real>
+__device__ __forceinline__ void load_tgroup(const Geo& g, const Real* __restrict__ tabt, Real* tside, int tg,
+                                            int L) {
+  const int ta = tg * g.Tg;
+  const int nt = min(g.Tg, g.T - ta);
+  const float4* src = reinterpret_cast<const float4*>(tabt + (size_t)ta * TABW);
+  float4* dst = reinterpret_cast<float4*>(tside);
+  const int n = nt * TABW * (int)sizeof(Real) / 16;
+  __syncwarp();
+  for (int i = L; i < n; i += 32) dst[i] = src[i];
+  __syncwarp();
+}
+
+// Build the 32 channel records of one batch (lane L <-> sorted position jb+L) from the
+// prefetched ChanRec/w in registers, and prefetch the next batch's. Returns the bitmask of
+// run starts (a run = maximal stretch with equal (rx, tx group)).
+template <typename Real>
+__device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<Real>& ws,
+                                                  const ChanRec* __restrict__ crec,
+                                                  const R2<Real>* __restrict__ wrec, int jb, int nb, int jend,
+                                                  int L, int& carry, ChanRec& nxt, R2<Real>& nxtw) {
+  const ChanRec cr = nxt;
+  const R2<Real> w = nxtw;
+  if (jb + 32 + L < jend) {
+    nxt = crec[jb + 32 + L];
+    if (wrec) nxtw = wrec[jb + 32 + L];
   }
+  int key = -1;
+  if (L < nb) {
+    const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = pk_tg(cr.pk);
+    const double x = cr.kd * (ws.d0[t] + ws.d0[g.T + r]);
+    R4<Real> q;
+    if constexpr (std::is_same<Real, float>::value)
+      q.x = cr.kf;
+    else
+      q.x = cr.kd;
+    q.y = (Real)(x - rint(x));
+    q.z = w.x;
+    q.w = w.y;
+    ws.rec[L] = q;
+    key = r | (tg << 16);
+    ws.rect[L] = make_int2((t - tg * g.Tg) * TABW, key);
+  }
+  int prev = __shfl_up_sync(FULL, key, 1);
+  if (L == 0) prev = carry;
+  const unsigned starts = __ballot_sync(FULL, L < nb && key != prev);
+  carry = __shfl_sync(FULL, key, nb - 1);
+  __syncwarp();
+  return starts;
+}
 
-  const int span = a.j1 - a.j0;
-  const int c0 = a.j0 + (int)(((long long)span * blockIdx.y) / a.Q);
-  const int c1 = a.j0 + (int)(((long long)span * (blockIdx.y + 1)) / a.Q);
-  const size_t prow = (size_t)blockIdx.x * span;
-  const Real* tabt = a.tab + (size_t)(tile_ok ? tile : 0) * g.A * (2 * 32 * V);
-
-  int cur_tg = -1, cur_r = -1;
-  Real dR[V], iR[V], shr[V], shi[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) dR[v] = iR[v] = shr[v] = shi[v] = 0;
-  int par = 0;
-  for (int jb = c0; jb < c1; jb += 32) {
-    const int nb = min(32, c1 - jb);
-    if (L < nb) {
-      const int m = a.sm[jb + L];
-      const int TR = g.T * g.R;
-      const int f = m / TR, rem = m - f * TR, t = rem / g.R, r = rem - t * g.R;
-      const int tg = t / g.Tg;
-      double base = 0;
-      if (tile_ok) {
-        const double D = a.D0[(size_t)tile * g.A + t] + a.D0[(size_t)tile * g.A + g.T + r];
-        const double xx = a.kd[f] * D;
-        base = xx - rint(xx);
-      }
-      FwdRec<Real> q;
-      q.k = a.kf[f];
-      q.base = (Real)base;
-      q.tl = t - tg * g.Tg;
-      q.r = r;
-      q.tg = tg;
-      q.pad = 0;
-      rec[L] = q;
-    }
-    __syncwarp();
-    for (int c = 0; c < nb; ++c) {
-      const FwdRec<Real> q = rec[c];
-      if (q.tg != cur_tg) {
-        __syncwarp();
-        const int ta = q.tg * g.Tg;
-        const int nt = min(g.Tg, g.T - ta);
-        const Real* src = tabt + (size_t)ta * (2 * 32 * V);
-        for (int i = L; i < nt * 2 * 32; i += 32) {
-          Real v4[4];
-          ld4(src + (size_t)i * V, v4);
-#pragma unroll
-          for (int v = 0; v < V; ++v) tside[i * V + v] = v4[v];
-        }
-        __syncwarp();
-        cur_tg = q.tg;
-      }
-      if (q.r != cur_r) {
-        const Real* src = tabt + (size_t)(g.T + q.r) * (2 * 32 * V);
-        ld4(src + L * V, dR);
-        ld4(src + 32 * V + L * V, iR);
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          shr[v] = iR[v] * sr[v];
-          shi[v] = iR[v] * si[v];
-        }
-        cur_r = q.r;
-      }
-      Real dT[V], iT[V];
-      ld4(tside + (size_t)q.tl * (2 * 32 * V) + L * V, dT);
-      ld4(tside + (size_t)q.tl * (2 * 32 * V) + 32 * V + L * V, iT);
-      Real pr = 0, pi = 0;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        Real cs, sn;
-        phasor(q.k, q.base, dT[v] + dR[v], cs, sn);
-        const Real aa = iT[v] * cs, bb = iT[v] * sn;
-        pr += aa * shr[v] + bb * shi[v];
-        pi += aa * shi[v] - bb * shr[v];
-      }
-      mytb[(c * 33 + L) * 2] = pr;
-      mytb[(c * 33 + L) * 2 + 1] = pi;
-    }
-    __syncwarp();
-    Real Sr = 0, Si = 0;
-    if (L < nb) {
-#pragma unroll 8
-      for (int l = 0; l < 32; ++l) {
-        Sr += mytb[(L * 33 + l) * 2];
-        Si += mytb[(L * 33 + l) * 2 + 1];
-      }
-    }
-    cbuf[((par * FWD_WARPS + w) * 32 + L) * 2] = Sr;
-    cbuf[((par * FWD_WARPS + w) * 32 + L) * 2 + 1] = Si;
-    __syncthreads();
-    if (w == 0 && L < nb) {
-      Real tr = 0, ti = 0;
-#pragma unroll
-      for (int ww = 0; ww < FWD_WARPS; ++ww) {
-        tr += cbuf[((par * FWD_WARPS + ww) * 32 + L) * 2];
-        ti += cbuf[((par * FWD_WARPS + ww) * 32 + L) * 2 + 1];
-      }
-      const size_t o = prow + (jb + L - a.j0);
-      a.partials[2 * o] = tr;
-      a.partials[2 * o + 1] = ti;
-    }
-    par ^= 1;
+template <typename Real>
+__device__ __forceinline__ void prefetch_first(const ChanRec* __restrict__ crec, const R2<Real>* __restrict__ wrec,
+                                               int j0, int j1, int L, ChanRec& nxt, R2<Real>& nxtw) {
+  nxt.kd = 0;
+  nxt.kf = 0;
+  nxt.pk = 0;
+  nxtw.x = 0;
+  nxtw.y = 0;
+  if (j0 + L < j1) {
+    nxt = crec[j0 + L];
+    if (wrec) nxtw = wrec[j0 + L];
   }
 }
 
-// y[spos[j]] = p_f/(4π) Σ_x partials[x][j]  (fp64 accumulation, fixed order)
-template <typename Real>
-__global__ void fwd_reduce_kernel(const Real* __restrict__ partials, int nx_blocks, int span, int j0,
-                                  const int* __restrict__ sm, const int* __restrict__ spos, int TR,
-                                  const double* __restrict__ pulse, Real* __restrict__ y) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= span) return;
-  double sr = 0, si = 0;
-  for (int x = 0; x < nx_blocks; ++x) {
-    const size_t o = (size_t)x * span + j;
-    sr += (double)partials[2 * o];
-    si += (double)partials[2 * o + 1];
-  }
-  const int m = sm[j0 + j];
-  const int f = m / TR;
-  const double pr = pulse[2 * f] / (4.0 * PI), pim = pulse[2 * f + 1] / (4.0 * PI);
-  const int k = spos[j0 + j];
-  y[2 * (size_t)k] = (Real)(pr * sr - pim * si);
-  y[2 * (size_t)k + 1] = (Real)(pr * si + pim * sr);
+__device__ __forceinline__ int run_end(unsigned starts, int c, int nb) {
+  const unsigned later = (c + 1 < 32) ? (starts >> (c + 1)) << (c + 1) : 0u;
+  return later ? __ffs(later) - 1 : nb;
 }
 
 // ------------------------------------------------------------------ adjoint (+prox)
-template <typename Real>
-struct AdjRec {
-  Real k, base, wr, wi;
-  int tl, r, tg, pad;
-};
-
 template <typename Real>
 struct AdjArgs {
   Geo g;
   const Real* __restrict__ tab;
   const double* __restrict__ D0;
-  const double* __restrict__ kd;
-  const Real* __restrict__ kf;
-  const double* __restrict__ pulse;
-  const int* __restrict__ sm;
-  const int* __restrict__ spos;
-  int B;
-  const Real* __restrict__ r;      // subset order
-  const Real* __restrict__ ymeas;  // full M or null
+  const ChanRec* __restrict__ crec;
+  const R2<Real>* __restrict__ wrec;
+  int B, CH;
+  Real* __restrict__ gpart;  // [CH][ntiles][32][4] complex (CH > 1)
+  int* __restrict__ cnt;     // [ntiles] arrival counters (zero between launches)
   // plain adjoint
   Real* __restrict__ gout;
   double scale;
@@ -492,108 +556,161 @@ struct AdjArgs {
   double* __restrict__ stat_part;  // [ntiles][4]
 };
 
+// w_j = conj(p_f)/(4π)·(r[spos_j] − ymeas[m_j]) in sorted order; dpart[block] = Σ |r − y|²
+template <typename Real>
+__global__ void __launch_bounds__(256) resid_kernel(const int* __restrict__ sm, const int* __restrict__ spos,
+                                                    const int* __restrict__ sf, int B,
+                                                    const Real* __restrict__ r, const Real* __restrict__ ymeas,
+                                                    const double* __restrict__ pulse, R2<Real>* __restrict__ wrec,
+                                                    double* __restrict__ dpart) {
+  __shared__ double sh[8];
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  double e = 0;
+  if (j < B) {
+    const int k = spos[j];
+    double rr = (double)r[2 * (size_t)k], ri = (double)r[2 * (size_t)k + 1];
+    if (ymeas) {
+      const int m = sm[j];
+      rr -= (double)ymeas[2 * (size_t)m];
+      ri -= (double)ymeas[2 * (size_t)m + 1];
+    }
+    e = rr * rr + ri * ri;
+    const int f = sf[j];
+    const double pr = pulse[2 * f] / (4.0 * PI), pim = -pulse[2 * f + 1] / (4.0 * PI);
+    R2<Real> w;
+    w.x = (Real)(pr * rr - pim * ri);
+    w.y = (Real)(pr * ri + pim * rr);
+    wrec[j] = w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int i = 0; i < 8; ++i) t += sh[i];
+    dpart[blockIdx.x] = t;
+  }
+}
+
 template <typename Real, bool PROX>
 __global__ void __launch_bounds__(ADJ_WARPS * 32) adj_kernel(AdjArgs<Real> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int tile = blockIdx.x * ADJ_WARPS + w;
-  if (tile >= g.ntiles) return;  // warps are independent: no block barriers below
-  const int per_t = g.Tg * 2 * 32 * V;
-  Real* tside = reinterpret_cast<Real*>(smem_raw) + (size_t)w * per_t;
-  AdjRec<Real>* rec =
-      reinterpret_cast<AdjRec<Real>*>(reinterpret_cast<Real*>(smem_raw) + (size_t)ADJ_WARPS * per_t) +
-      w * 32;
+  const int unit = blockIdx.x * ADJ_WARPS + w;
+  if (unit >= g.ntiles * a.CH) return;  // warps are independent: no block barriers below
+  const int tile = unit / a.CH, chunk = unit - tile * a.CH;
+  const WarpSmem<Real> ws = carve<Real>(smem_raw + (size_t)w * warp_smem_bytes<Real>(g.Tg, g.A), g.Tg, g.A);
+  const int j0 = (int)(((long long)a.B * chunk) / a.CH);
+  const int j1 = (int)(((long long)a.B * (chunk + 1)) / a.CH);
+  for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
+  __syncwarp();
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
+  const Real* tsl = ws.tside + L * V;
+
+  Q4<Real> gr, gi, hr, hi, dR, iR, pdR, piR;
+  zero(gr);
+  zero(gi);
+  zero(hr);
+  zero(hi);
+  zero(dR);
+  zero(iR);
+  zero(pdR);
+  zero(piR);
+  int cur_tg = -1, pf_r = -1, carry = -1;
+  ChanRec nxt;
+  R2<Real> nxtw;
+  prefetch_first<Real>(a.crec, a.wrec, j0, j1, L, nxt, nxtw);
+
+  for (int jb = j0; jb < j1; jb += 32) {
+    const int nb = min(32, j1 - jb);
+    const unsigned starts = build_records<Real>(g, ws, a.crec, a.wrec, jb, nb, j1, L, carry, nxt, nxtw);
+    int c = 0;
+    while (c < nb) {
+      const int e = run_end(starts, c, nb);
+      if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c
+        const int key = ws.rect[c].y;
+        const int rr = key & 0xffff, tg = key >> 16;
+        if (tg != cur_tg) {
+          load_tgroup<Real>(g, tabt, ws.tside, tg, L);
+          cur_tg = tg;
+        }
+        flush(iR, hr, hi, gr, gi);
+        if (rr == pf_r) {
+          dR = pdR;
+          iR = piR;
+        } else {
+          const Real* src = tabt + (size_t)(g.T + rr) * TABW;
+          dR = ld4(src + L * V);
+          iR = ld4(src + TILE + L * V);
+        }
+        pf_r = rr + 1 < g.R ? rr + 1 : -1;
+        if (pf_r >= 0) {  // prefetch the next receiver's rows one run ahead
+          const Real* src = tabt + (size_t)(g.T + pf_r) * TABW;
+          pdR = ld4(src + L * V);
+          piR = ld4(src + TILE + L * V);
+        }
+      }
+      // software pipeline: channel c+1's record and tx-side rows load while c computes
+      R4<Real> q = ws.rec[c];
+      const Real* ts = tsl + ws.rect[c].x;
+      Q4<Real> dT = ld4(ts), iT = ld4(ts + TILE);
+#pragma unroll 2
+      for (; c < e; ++c) {
+        const int cn = c + 1 < e ? c + 1 : c;
+        const R4<Real> qn = ws.rec[cn];
+        const Real* tn = tsl + ws.rect[cn].x;
+        const Q4<Real> dTn = ld4(tn), iTn = ld4(tn + TILE);
+        Q4<Real> cs, sn;
+        phasor4(q.x, q.y, dT, dR, cs, sn);
+        adj_acc(iT, cs, sn, q.z, q.w, hr, hi);
+        q = qn;
+        dT = dTn;
+        iT = iTn;
+      }
+    }
+    __syncwarp();
+  }
+  flush(iR, hr, hi, gr, gi);
+
+  Real Gr[V], Gi[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    Gr[v] = get(gr, v);
+    Gi[v] = get(gi, v);
+  }
+  if (a.CH > 1) {
+    // publish this chunk's partial; the last of the CH warps of this tile combines in chunk order
+    Real* mine = a.gpart + (((size_t)chunk * g.ntiles + tile) * 32 + L) * (2 * V);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      mine[2 * v] = Gr[v];
+      mine[2 * v + 1] = Gi[v];
+    }
+    __threadfence();
+    int last = 0;
+    if (L == 0) last = atomicAdd(a.cnt + tile, 1) == a.CH - 1;
+    last = __shfl_sync(FULL, last, 0);
+    if (!last) return;
+    __threadfence();
+#pragma unroll
+    for (int v = 0; v < V; ++v) Gr[v] = Gi[v] = 0;
+    for (int ch = 0; ch < a.CH; ++ch) {
+      const Real* q = a.gpart + (((size_t)ch * g.ntiles + tile) * 32 + L) * (2 * V);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        Gr[v] += __ldcg(q + 2 * v);
+        Gi[v] += __ldcg(q + 2 * v + 1);
+      }
+    }
+    if (L == 0) a.cnt[tile] = 0;
+  }
+
   int tx, ty, tz;
   tile_coords(g, tile, tx, ty, tz);
   int x0, y, z;
-  lane_voxel(g, tx, ty, tz, L, x0, y, z);
-  const Real* tabt = a.tab + (size_t)tile * g.A * (2 * 32 * V);
-  const int TR = g.T * g.R;
-
-  Real gr[V], gi[V], hr[V], hi[V], dR[V], iR[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) gr[v] = gi[v] = hr[v] = hi[v] = dR[v] = iR[v] = 0;
-  int cur_tg = -1, cur_r = -1;
-  double dfid = 0;  // Σ |r - y|^2 over the batch (tile 0 only)
-
-  for (int jb = 0; jb < a.B; jb += 32) {
-    const int nb = min(32, a.B - jb);
-    __syncwarp();
-    if (L < nb) {
-      const int m = a.sm[jb + L];
-      const int f = m / TR, rem = m - f * TR, t = rem / g.R, r = rem - t * g.R;
-      const int tg = t / g.Tg;
-      const double D = a.D0[(size_t)tile * g.A + t] + a.D0[(size_t)tile * g.A + g.T + r];
-      const double xx = a.kd[f] * D;
-      const int k = a.spos[jb + L];
-      double rr = (double)a.r[2 * (size_t)k], ri = (double)a.r[2 * (size_t)k + 1];
-      if (a.ymeas) {
-        rr -= (double)a.ymeas[2 * (size_t)m];
-        ri -= (double)a.ymeas[2 * (size_t)m + 1];
-      }
-      if (tile == 0) dfid += rr * rr + ri * ri;
-      // w = conj(p_f)/(4π) · r
-      const double pr = a.pulse[2 * f] / (4.0 * PI), pim = -a.pulse[2 * f + 1] / (4.0 * PI);
-      AdjRec<Real> q;
-      q.k = a.kf[f];
-      q.base = (Real)(xx - rint(xx));
-      q.wr = (Real)(pr * rr - pim * ri);
-      q.wi = (Real)(pr * ri + pim * rr);
-      q.tl = t - tg * g.Tg;
-      q.r = r;
-      q.tg = tg;
-      q.pad = 0;
-      rec[L] = q;
-    }
-    __syncwarp();
-    for (int c = 0; c < nb; ++c) {
-      const AdjRec<Real> q = rec[c];
-      if (q.tg != cur_tg) {
-        __syncwarp();
-        const int ta = q.tg * g.Tg;
-        const int nt = min(g.Tg, g.T - ta);
-        const Real* src = tabt + (size_t)ta * (2 * 32 * V);
-        for (int i = L; i < nt * 2 * 32; i += 32) {
-          Real v4[4];
-          ld4(src + (size_t)i * V, v4);
-#pragma unroll
-          for (int v = 0; v < V; ++v) tside[i * V + v] = v4[v];
-        }
-        __syncwarp();
-        cur_tg = q.tg;
-      }
-      if (q.r != cur_r) {
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          gr[v] += iR[v] * hr[v];
-          gi[v] += iR[v] * hi[v];
-          hr[v] = hi[v] = 0;
-        }
-        const Real* src = tabt + (size_t)(g.T + q.r) * (2 * 32 * V);
-        ld4(src + L * V, dR);
-        ld4(src + 32 * V + L * V, iR);
-        cur_r = q.r;
-      }
-      Real dT[V], iT[V];
-      ld4(tside + (size_t)q.tl * (2 * 32 * V) + L * V, dT);
-      ld4(tside + (size_t)q.tl * (2 * 32 * V) + 32 * V + L * V, iT);
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        Real cs, sn;
-        phasor(q.k, q.base, dT[v] + dR[v], cs, sn);
-        const Real aa = iT[v] * cs, bb = iT[v] * sn;
-        hr[v] += aa * q.wr - bb * q.wi;
-        hi[v] += aa * q.wi + bb * q.wr;
-      }
-    }
-  }
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    gr[v] += iR[v] * hr[v];
-    gi[v] += iR[v] * hi[v];
-  }
-
+  lane_voxel(tx, ty, tz, L, x0, y, z);
   double st0 = 0, st1 = 0, st3 = 0;
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -601,12 +718,12 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) adj_kernel(AdjArgs<Real> a) {
     if (!(x < g.nx && y < g.ny && z < g.nzs)) continue;
     const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
     if (!PROX) {
-      a.gout[2 * n] = (Real)(a.scale * gr[v]);
-      a.gout[2 * n + 1] = (Real)(a.scale * gi[v]);
+      a.gout[2 * n] = (Real)(a.scale * Gr[v]);
+      a.gout[2 * n + 1] = (Real)(a.scale * Gi[v]);
     } else {
       const Real s_r = a.s_in[2 * n], s_i = a.s_in[2 * n + 1];
-      const Real ur = s_r - (Real)a.eta_over_b * gr[v];
-      const Real ui = s_i - (Real)a.eta_over_b * gi[v];
+      const Real ur = s_r - (Real)a.eta_over_b * Gr[v];
+      const Real ui = s_i - (Real)a.eta_over_b * Gi[v];
       const Real mag = sqrt(ur * ur + ui * ui);
       const Real al = (Real)a.alpha;
       const Real sc = mag > al ? (mag - al) / mag : Real(0);
@@ -623,28 +740,31 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) adj_kernel(AdjArgs<Real> a) {
   if (PROX) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      st0 += __shfl_xor_sync(0xffffffffu, st0, o);
-      st1 += __shfl_xor_sync(0xffffffffu, st1, o);
-      st3 += __shfl_xor_sync(0xffffffffu, st3, o);
-      dfid += __shfl_xor_sync(0xffffffffu, dfid, o);
+      st0 += __shfl_xor_sync(FULL, st0, o);
+      st1 += __shfl_xor_sync(FULL, st1, o);
+      st3 += __shfl_xor_sync(FULL, st3, o);
     }
     if (L == 0) {
       a.stat_part[(size_t)tile * 4 + 0] = st0;
       a.stat_part[(size_t)tile * 4 + 1] = st1;
-      a.stat_part[(size_t)tile * 4 + 2] = 0.5 * dfid;
+      a.stat_part[(size_t)tile * 4 + 2] = 0;
       a.stat_part[(size_t)tile * 4 + 3] = st3;
     }
   }
 }
 
-// stats[q] = Σ_tile part[tile][q] in a fixed order (deterministic)
+// stats = {Σ_tile part[.][0], Σ part[.][1], ½ Σ_block dpart, Σ part[.][3]} in a fixed order
 __global__ void __launch_bounds__(256) stats_reduce_kernel(const double* __restrict__ part, int n,
+                                                           const double* __restrict__ dpart, int nd,
                                                            double* __restrict__ out) {
   __shared__ double sh[4][256];
   double acc[4] = {0, 0, 0, 0};
-  for (int i = threadIdx.x; i < n; i += 256)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] += part[(size_t)i * 4 + q];
+  for (int i = threadIdx.x; i < n; i += 256) {
+    acc[0] += part[(size_t)i * 4 + 0];
+    acc[1] += part[(size_t)i * 4 + 1];
+    acc[3] += part[(size_t)i * 4 + 3];
+  }
+  for (int i = threadIdx.x; i < nd; i += 256) acc[2] += dpart[i];
 #pragma unroll
   for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] = acc[q];
   __syncthreads();
@@ -654,7 +774,205 @@ __global__ void __launch_bounds__(256) stats_reduce_kernel(const double* __restr
       for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + s];
     __syncthreads();
   }
-  if (threadIdx.x < 4) out[threadIdx.x] = sh[threadIdx.x][0];
+  if (threadIdx.x < 4) out[threadIdx.x] = threadIdx.x == 2 ? 0.5 * sh[2][0] : sh[threadIdx.x][0];
+}
+
+// ------------------------------------------------------------------ forward
+template <typename Real>
+struct FwdArgs {
+  Geo g;
+  const Real* __restrict__ tab;
+  const double* __restrict__ D0;
+  const ChanRec* __restrict__ crec;
+  const Real* __restrict__ s;  // complex, slab-local flat order
+  int w0, w1;                  // sorted positions of this launch window
+  int Q;                       // channel splits (gridDim.y)
+  Real* __restrict__ part;     // [gridDim.x][w1-w0] complex
+};
+
+constexpr int FCH = 256;  // max channels per forward unit (per-warp accumulator in smem)
+
+template <typename Real>
+__host__ __device__ constexpr size_t fwd_warp_bytes(int Tg, int A) {
+  return warp_smem_bytes<Real>(Tg, A) + (size_t)16 * 33 * sizeof(R2<Real>) + (size_t)FCH * sizeof(R2<Real>);
+}
+
+// Forward: CTA = FWD_WARPS warps on adjacent tiles × one chunk of <= FCH sorted channels.
+// Each warp keeps its per-channel tile sums for the chunk in smem; one CTA barrier at the
+// end combines the warps in a fixed order and writes part[blockIdx.x][j].
+template <typename Real>
+__global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geo& g = a.g;
+  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+  const int tile = blockIdx.x * FWD_WARPS + w;
+  const bool tile_ok = tile < g.ntiles;
+  unsigned char* wbase = smem_raw + (size_t)w * fwd_warp_bytes<Real>(g.Tg, g.A);
+  const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A);
+  R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A));  // [16][33]
+  R2<Real>* acc = tb + 16 * 33;                                                       // [FCH]
+
+  const int tsel = tile_ok ? tile : 0;
+  for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tsel * g.A + i];
+  const Real* tabt = a.tab + (size_t)tsel * g.A * TABW;
+  const Real* tsl = ws.tside + L * V;
+  int tx, ty, tz;
+  tile_coords(g, tsel, tx, ty, tz);
+  int x0, y, z;
+  lane_voxel(tx, ty, tz, L, x0, y, z);
+  Real srv[V], siv[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int x = x0 + v;
+    const bool ok = tile_ok && x < g.nx && y < g.ny && z < g.nzs;
+    const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
+    srv[v] = ok ? a.s[2 * n] : Real(0);
+    siv[v] = ok ? a.s[2 * n + 1] : Real(0);
+  }
+  Q4<Real> sr, si;
+  if constexpr (std::is_same<Real, float>::value) {
+    sr = F4{make_float2(srv[0], srv[1]), make_float2(srv[2], srv[3])};
+    si = F4{make_float2(siv[0], siv[1]), make_float2(siv[2], siv[3])};
+  } else {
+    sr = D4{{srv[0], srv[1], srv[2], srv[3]}};
+    si = D4{{siv[0], siv[1], siv[2], siv[3]}};
+  }
+  __syncwarp();
+
+  const int span = a.w1 - a.w0;
+  const int c0 = a.w0 + (int)(((long long)span * blockIdx.y) / a.Q);
+  const int c1 = a.w0 + (int)(((long long)span * (blockIdx.y + 1)) / a.Q);
+
+  Q4<Real> dR, iR, pdR, piR, shr, shi;
+  zero(dR);
+  zero(iR);
+  zero(pdR);
+  zero(piR);
+  zero(shr);
+  zero(shi);
+  int cur_tg = -1, pf_r = -1, carry = -1;
+  ChanRec nxt;
+  R2<Real> nxtw;
+  prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
+  for (int jb = c0; jb < c1; jb += 32) {
+    const int nb = min(32, c1 - jb);
+    const unsigned starts = build_records<Real>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
+    // two half-batches of 16 channels share one [16][33] transpose buffer
+    for (int h0 = 0; h0 < nb; h0 += 16) {
+      const int h1 = min(nb, h0 + 16);
+      int c = h0;
+      while (c < h1) {
+        const int e = min(run_end(starts, c, nb), h1);
+        if ((starts >> c) & 1u) {
+          const int key = ws.rect[c].y;
+          const int rr = key & 0xffff, tg = key >> 16;
+          if (tg != cur_tg) {
+            load_tgroup<Real>(g, tabt, ws.tside, tg, L);
+            cur_tg = tg;
+          }
+          if (rr == pf_r) {
+            dR = pdR;
+            iR = piR;
+          } else {
+            const Real* src = tabt + (size_t)(g.T + rr) * TABW;
+            dR = ld4(src + L * V);
+            iR = ld4(src + TILE + L * V);
+          }
+          scale_s(iR, sr, si, shr, shi);
+          pf_r = rr + 1 < g.R ? rr + 1 : -1;
+          if (pf_r >= 0) {
+            const Real* src = tabt + (size_t)(g.T + pf_r) * TABW;
+            pdR = ld4(src + L * V);
+            piR = ld4(src + TILE + L * V);
+          }
+        }
+        R4<Real> q = ws.rec[c];
+        const Real* ts = tsl + ws.rect[c].x;
+        Q4<Real> dT = ld4(ts), iT = ld4(ts + TILE);
+#pragma unroll 2
+        for (; c < e; ++c) {
+          const int cn = c + 1 < e ? c + 1 : c;
+          const R4<Real> qn = ws.rec[cn];
+          const Real* tn = tsl + ws.rect[cn].x;
+          const Q4<Real> dTn = ld4(tn), iTn = ld4(tn + TILE);
+          Q4<Real> cs, sn;
+          phasor4(q.x, q.y, dT, dR, cs, sn);
+          tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi);
+          q = qn;
+          dT = dTn;
+          iT = iTn;
+        }
+      }
+      __syncwarp();
+      // transpose-reduce: lanes L and L+16 each sum half of row L&15, then combine (fixed order)
+      const int row = L & 15, half = L >> 4;
+      R2<Real> S;
+      S.x = 0;
+      S.y = 0;
+#pragma unroll 8
+      for (int l = 0; l < 16; ++l) {
+        const R2<Real> t = tb[row * 33 + half * 16 + l];
+        S.x += t.x;
+        S.y += t.y;
+      }
+      S.x += __shfl_down_sync(FULL, S.x, 16);
+      S.y += __shfl_down_sync(FULL, S.y, 16);
+      if (L < h1 - h0) acc[jb - c0 + h0 + L] = S;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // combine the CTA's warps (fixed order) and publish the tile-group partial
+  R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)blockIdx.x * span;
+  for (int i = threadIdx.x; i < c1 - c0; i += FWD_WARPS * 32) {
+    R2<Real> T2;
+    T2.x = 0;
+    T2.y = 0;
+#pragma unroll
+    for (int ww = 0; ww < FWD_WARPS; ++ww) {
+      const R2<Real> t = reinterpret_cast<const R2<Real>*>(smem_raw + (size_t)ww * fwd_warp_bytes<Real>(g.Tg, g.A) +
+                                                           warp_smem_bytes<Real>(g.Tg, g.A))[16 * 33 + i];
+      T2.x += t.x;
+      T2.y += t.y;
+    }
+    out[c0 - a.w0 + i] = T2;
+  }
+}
+
+// level 1: tmp[seg][j] = Σ_{x in seg} part[x][j] (fp64, fixed order)
+template <typename Real>
+__global__ void fwd_reduce1_kernel(const Real* __restrict__ part, int nx, int span, int nseg,
+                                   double2* __restrict__ tmp) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int seg = blockIdx.y;
+  if (j >= span) return;
+  const int x0 = (int)(((long long)nx * seg) / nseg), x1 = (int)(((long long)nx * (seg + 1)) / nseg);
+  double sr = 0, si = 0;
+  for (int x = x0; x < x1; ++x) {
+    const R2<Real> v = reinterpret_cast<const R2<Real>*>(part)[(size_t)x * span + j];
+    sr += (double)v.x;
+    si += (double)v.y;
+  }
+  tmp[(size_t)seg * span + j] = make_double2(sr, si);
+}
+// level 2: y[spos[j]] = p_f/(4π) Σ_seg tmp[seg][j]
+template <typename Real>
+__global__ void fwd_reduce2_kernel(const double2* __restrict__ tmp, int span, int nseg, int w0,
+                                   const int* __restrict__ sf, const int* __restrict__ spos,
+                                   const double* __restrict__ pulse, Real* __restrict__ y) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= span) return;
+  double sr = 0, si = 0;
+  for (int s = 0; s < nseg; ++s) {
+    const double2 v = tmp[(size_t)s * span + j];
+    sr += v.x;
+    si += v.y;
+  }
+  const int f = sf[w0 + j];
+  const double pr = pulse[2 * f] / (4.0 * PI), pim = pulse[2 * f + 1] / (4.0 * PI);
+  const int k = spos[w0 + j];
+  y[2 * (size_t)k] = (Real)(pr * sr - pim * si);
+  y[2 * (size_t)k + 1] = (Real)(pr * si + pim * sr);
 }
 
 // ------------------------------------------------------------------ elementwise utilities
@@ -711,6 +1029,7 @@ struct nf_plan {
   int64_t nvox;
   int fwd_gridx;
   int fwd_chunk;
+  int adj_ch_cap;
   size_t dev_bytes = 0;
   int64_t launches = 0;
   int KS, ksblocks;
@@ -726,7 +1045,14 @@ struct nf_plan {
   int* d_cnt = nullptr;
   int* d_sm = nullptr;
   int* d_spos = nullptr;
-  void* d_partials = nullptr;
+  ChanRec* d_crec = nullptr;
+  int* d_sf = nullptr;
+  void* d_wrec = nullptr;
+  double* d_dpart = nullptr;
+  void* d_part = nullptr;
+  double2* d_tmp = nullptr;
+  void* d_gpart = nullptr;
+  int* d_tilecnt = nullptr;
   double* d_stat_part = nullptr;
 };
 
@@ -744,72 +1070,69 @@ int dalloc(nf_plan* p, T** ptr, size_t bytes) {
 
 void free_plan(nf_plan* p) {
   if (!p) return;
-  cudaFree(p->d_ant);
-  cudaFree(p->d_kd);
-  cudaFree(p->d_kf);
-  cudaFree(p->d_pulse);
-  cudaFree(p->d_tab);
-  cudaFree(p->d_D0);
-  cudaFree(p->d_pos_of_key);
-  cudaFree(p->d_cnt);
-  cudaFree(p->d_sm);
-  cudaFree(p->d_spos);
-  cudaFree(p->d_partials);
-  cudaFree(p->d_stat_part);
+  void* ptrs[] = {p->d_ant,  p->d_kd,   p->d_kf,    p->d_pulse, p->d_tab,  p->d_D0,      p->d_pos_of_key,
+                  p->d_cnt,  p->d_sm,   p->d_spos,  p->d_crec,  p->d_sf, p->d_wrec, p->d_dpart,   p->d_part,
+                  p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part};
+  for (void* q : ptrs) cudaFree(q);
   delete p;
 }
 
 size_t real_size(const nf_plan* p) { return p->dtype == NF_C64 ? sizeof(float) : sizeof(double); }
 
 size_t fwd_smem(const nf_plan* p) {
-  const size_t rs = real_size(p);
-  const size_t recsz = p->dtype == NF_C64 ? sizeof(FwdRec<float>) : sizeof(FwdRec<double>);
-  return (size_t)FWD_WARPS * p->g.Tg * 2 * 32 * V * rs + (size_t)FWD_WARPS * 32 * recsz +
-         (size_t)FWD_WARPS * 32 * 33 * 2 * rs + (size_t)2 * FWD_WARPS * 32 * 2 * rs;
+  const int Tg = p->g.Tg;
+  if (p->dtype == NF_C64) return FWD_WARPS * fwd_warp_bytes<float>(Tg, p->g.A);
+  return FWD_WARPS * fwd_warp_bytes<double>(Tg, p->g.A);
 }
 size_t adj_smem(const nf_plan* p) {
-  const size_t rs = real_size(p);
-  const size_t recsz = p->dtype == NF_C64 ? sizeof(AdjRec<float>) : sizeof(AdjRec<double>);
-  return (size_t)ADJ_WARPS * p->g.Tg * 2 * 32 * V * rs + (size_t)ADJ_WARPS * 32 * recsz;
+  return ADJ_WARPS * (p->dtype == NF_C64 ? warp_smem_bytes<float>(p->g.Tg, p->g.A)
+                                          : warp_smem_bytes<double>(p->g.Tg, p->g.A));
 }
 
 int channel_splits(const nf_plan* p, int span) {
-  // enough CTAs for ~8 waves of 2 CTAs/SM on 148 SMs; ≥ 32 channels per split
-  const long long target = 148LL * 2 * 8;
+  // ~8 waves of 3 CTAs/SM on 148 SMs, 32..FCH channels per split
+  const long long target = 148LL * 3 * 8;
   long long q = (target + p->fwd_gridx - 1) / p->fwd_gridx;
-  long long qmax = std::max(1, span / 32);
-  if (q > qmax) q = qmax;
-  if (q < 1) q = 1;
-  return (int)q;
+  q = std::min<long long>(q, std::max(1, span / 32));
+  q = std::max<long long>(q, (span + FCH - 1) / FCH);
+  return (int)std::max(1LL, q);
+}
+
+int adjoint_chunks(const nf_plan* p) {
+  // enough (tile, chunk) units for ~8 rounds of 16 warps/SM; at least 64 channels per chunk
+  long long ch = (148LL * 16 * 8 + p->g.ntiles - 1) / p->g.ntiles;
+  ch = std::min<long long>(ch, std::max(1, p->B / 64));
+  ch = std::min<long long>(ch, p->adj_ch_cap);
+  return (int)std::max(1LL, ch);
 }
 
 template <typename Real>
 int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const size_t sm = fwd_smem(p);
   CUDA_TRY(cudaFuncSetAttribute(fwd_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  for (int j0 = 0; j0 < p->B; j0 += p->fwd_chunk) {
-    const int j1 = std::min(p->B, j0 + p->fwd_chunk);
+  for (int w0 = 0; w0 < p->B; w0 += p->fwd_chunk) {
+    const int w1 = std::min(p->B, w0 + p->fwd_chunk);
+    const int span = w1 - w0;
     FwdArgs<Real> a;
     a.g = p->g;
     a.tab = (const Real*)p->d_tab;
     a.D0 = p->d_D0;
-    a.kd = p->d_kd;
-    a.kf = (const Real*)p->d_kf;
+    a.crec = p->d_crec;
     a.s = (const Real*)s;
-    a.sm = p->d_sm;
-    a.j0 = j0;
-    a.j1 = j1;
-    a.Q = channel_splits(p, j1 - j0);
-    a.partials = (Real*)p->d_partials;
-    dim3 grid(p->fwd_gridx, a.Q);
-    fwd_kernel<Real><<<grid, FWD_WARPS * 32, sm, st>>>(a);
+    a.w0 = w0;
+    a.w1 = w1;
+    a.Q = channel_splits(p, span);
+    a.part = (Real*)p->d_part;
+    fwd_kernel<Real><<<dim3(p->fwd_gridx, a.Q), FWD_WARPS * 32, sm, st>>>(a);
     CUDA_TRY(cudaGetLastError());
-    const int span = j1 - j0;
-    fwd_reduce_kernel<Real><<<(span + 255) / 256, 256, 0, st>>>(
-        (const Real*)p->d_partials, p->fwd_gridx, span, j0, p->d_sm, p->d_spos, p->g.T * p->g.R, p->d_pulse,
-        (Real*)y);
+    const int nseg = std::max(1, std::min(p->fwd_gridx, RED_THREADS / span));
+    fwd_reduce1_kernel<Real><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const Real*)p->d_part, p->fwd_gridx,
+                                                                             span, nseg, p->d_tmp);
     CUDA_TRY(cudaGetLastError());
-    p->launches += 2;
+    fwd_reduce2_kernel<Real><<<(span + 255) / 256, 256, 0, st>>>(p->d_tmp, span, nseg, w0, p->d_sf, p->d_spos,
+                                                                 p->d_pulse, (Real*)y);
+    CUDA_TRY(cudaGetLastError());
+    p->launches += 3;
   }
   return NF_OK;
 }
@@ -817,20 +1140,22 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
 template <typename Real, bool PROX>
 int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, double scale, const void* s_in,
                    void* s_out, double eta_over_b, double alpha, double* stats, cudaStream_t st) {
+  const int nblk = (p->B + 255) / 256;
+  resid_kernel<Real><<<nblk, 256, 0, st>>>(p->d_sm, p->d_spos, p->d_sf, p->B, (const Real*)r,
+                                            (const Real*)ymeas, p->d_pulse, (R2<Real>*)p->d_wrec, p->d_dpart);
+  CUDA_TRY(cudaGetLastError());
   const size_t sm = adj_smem(p);
   CUDA_TRY(cudaFuncSetAttribute(adj_kernel<Real, PROX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   AdjArgs<Real> a;
   a.g = p->g;
   a.tab = (const Real*)p->d_tab;
   a.D0 = p->d_D0;
-  a.kd = p->d_kd;
-  a.kf = (const Real*)p->d_kf;
-  a.pulse = p->d_pulse;
-  a.sm = p->d_sm;
-  a.spos = p->d_spos;
+  a.crec = p->d_crec;
+  a.wrec = (const R2<Real>*)p->d_wrec;
   a.B = p->B;
-  a.r = (const Real*)r;
-  a.ymeas = (const Real*)ymeas;
+  a.CH = adjoint_chunks(p);
+  a.gpart = (Real*)p->d_gpart;
+  a.cnt = p->d_tilecnt;
   a.gout = (Real*)gout;
   a.scale = scale;
   a.s_in = (const Real*)s_in;
@@ -838,12 +1163,12 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   a.eta_over_b = eta_over_b;
   a.alpha = alpha;
   a.stat_part = p->d_stat_part;
-  const int grid = (p->g.ntiles + ADJ_WARPS - 1) / ADJ_WARPS;
-  adj_kernel<Real, PROX><<<grid, ADJ_WARPS * 32, sm, st>>>(a);
+  const int units = p->g.ntiles * a.CH;
+  adj_kernel<Real, PROX><<<(units + ADJ_WARPS - 1) / ADJ_WARPS, ADJ_WARPS * 32, sm, st>>>(a);
   CUDA_TRY(cudaGetLastError());
-  p->launches += 1;
+  p->launches += 2;
   if (PROX) {
-    stats_reduce_kernel<<<1, 256, 0, st>>>(p->d_stat_part, p->g.ntiles, stats);
+    stats_reduce_kernel<<<1, 256, 0, st>>>(p->d_stat_part, p->g.ntiles, p->d_dpart, nblk, stats);
     CUDA_TRY(cudaGetLastError());
     p->launches += 1;
   }
@@ -865,6 +1190,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   if (!tx_xyz || !rx_xyz || !freq_hz || !pulse_reim || !corner || !spacing || !dims)
     return fail(NF_ERR_ARG, "null geometry pointer");
   if (n_tx < 1 || n_rx < 1 || n_f < 1) return fail(NF_ERR_ARG, "n_tx, n_rx, n_f must be >= 1");
+  if (n_tx + n_rx > A_MAX) return fail(NF_ERR_ARG, "at most 256 antennas (n_tx + n_rx) per plan");
   if (!(c > 0) || !std::isfinite(c)) return fail(NF_ERR_ARG, "speed of light must be positive and finite");
   if (dtype != NF_C64 && dtype != NF_C128) return fail(NF_ERR_ARG, "dtype must be NF_C64 or NF_C128");
   for (int i = 0; i < 3; ++i)
@@ -891,8 +1217,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   g.nty = (g.ny + TILE_Y - 1) / TILE_Y;
   g.ntz = (g.nzs + TILE_Z - 1) / TILE_Z;
   g.ntiles = g.ntx * g.nty * g.ntz;
-  const int tgmax = dtype == NF_C64 ? TG_MAX_F : TG_MAX_D;
-  g.ng = (n_tx + tgmax - 1) / tgmax;
+  g.ng = (n_tx + TG_MAX - 1) / TG_MAX;
   g.Tg = (n_tx + g.ng - 1) / g.ng;
   for (int i = 0; i < 3; ++i) {
     g.corner[i] = corner[i];
@@ -910,6 +1235,9 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     ch = std::max<long long>(ch, 1024);
     ch = std::min<long long>(ch, max_batch);
     p->fwd_chunk = (int)ch;
+    // bound the adjoint chunk partials to ~256 MB
+    const long long per = (long long)g.ntiles * TILE * 2 * rs;
+    p->adj_ch_cap = (int)std::max<long long>(1, std::min<long long>(64, (256LL << 20) / per));
   }
 
   int rc;
@@ -922,6 +1250,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     kd[i] = freq_hz[i] / c;
     kf32[i] = (float)kd[i];
   }
+  const size_t nred = (size_t)std::max(RED_THREADS, p->fwd_chunk) + 1024;
 #define ALLOC(ptr, bytes)                  \
   if ((rc = dalloc(p, &(ptr), (bytes)))) { \
     free_plan(p);                          \
@@ -931,14 +1260,21 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   ALLOC(p->d_kd, sizeof(double) * n_f);
   ALLOC(p->d_kf, rs * n_f);
   ALLOC(p->d_pulse, sizeof(double) * 2 * n_f);
-  ALLOC(p->d_tab, rs * (size_t)g.ntiles * g.A * 2 * 32 * V);
+  ALLOC(p->d_tab, rs * (size_t)g.ntiles * g.A * TABW);
   ALLOC(p->d_D0, sizeof(double) * (size_t)g.ntiles * g.A);
   ALLOC(p->d_pos_of_key, sizeof(int) * (size_t)p->KS);
   ALLOC(p->d_cnt, sizeof(int) * (size_t)p->ksblocks);
   ALLOC(p->d_sm, sizeof(int) * (size_t)max_batch);
   ALLOC(p->d_spos, sizeof(int) * (size_t)max_batch);
-  ALLOC(p->d_partials, 2 * rs * (size_t)p->fwd_gridx * p->fwd_chunk);
-  ALLOC(p->d_stat_part, sizeof(double) * 4 * (size_t)std::max(g.ntiles, 1024));
+  ALLOC(p->d_crec, sizeof(ChanRec) * (size_t)max_batch);
+  ALLOC(p->d_sf, sizeof(int) * (size_t)max_batch);
+  ALLOC(p->d_wrec, 2 * rs * (size_t)max_batch);
+  ALLOC(p->d_dpart, sizeof(double) * ((size_t)max_batch / 256 + 2));
+  ALLOC(p->d_part, 2 * rs * (size_t)p->fwd_gridx * p->fwd_chunk);
+  ALLOC(p->d_tmp, sizeof(double2) * nred);
+  ALLOC(p->d_gpart, 2 * rs * (size_t)p->adj_ch_cap * g.ntiles * TILE);
+  ALLOC(p->d_tilecnt, sizeof(int) * (size_t)g.ntiles);
+  ALLOC(p->d_stat_part, sizeof(double) * 4 * (size_t)g.ntiles);
 #undef ALLOC
   auto cp = [&](void* dst, const void* src, size_t n) -> int {
     cudaError_t e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
@@ -952,9 +1288,10 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     free_plan(p);
     return rc;
   }
-  if (cudaMemset(p->d_pos_of_key, 0xff, sizeof(int) * (size_t)p->KS) != cudaSuccess) {
+  if (cudaMemset(p->d_pos_of_key, 0xff, sizeof(int) * (size_t)p->KS) != cudaSuccess ||
+      cudaMemset(p->d_tilecnt, 0, sizeof(int) * (size_t)g.ntiles) != cudaSuccess) {
     free_plan(p);
-    return fail(NF_ERR_CUDA, "cudaMemset pos_of_key");
+    return fail(NF_ERR_CUDA, "cudaMemset");
   }
   dim3 grid(g.ntiles, g.A);
   if (dtype == NF_C64)
@@ -998,7 +1335,8 @@ int nf_batch_prepare(nf_plan* p, const int32_t* idx, int B, void* stream) {
   mark_kernel<<<(B + 255) / 256, 256, 0, st>>>(p->km, idx, B, p->d_pos_of_key);
   count_kernel<<<p->ksblocks, 1024, 0, st>>>(p->d_pos_of_key, p->KS, p->d_cnt);
   scan_kernel<<<1, 1024, 0, st>>>(p->d_cnt, p->ksblocks);
-  compact_kernel<<<p->ksblocks, 1024, 0, st>>>(p->km, p->d_pos_of_key, p->KS, p->d_cnt, p->d_sm, p->d_spos);
+  compact_kernel<<<p->ksblocks, 1024, 0, st>>>(p->km, p->d_pos_of_key, p->KS, p->d_cnt, p->d_sm, p->d_spos,
+                                               p->d_crec, p->d_sf, p->d_kd);
   CUDA_TRY(cudaGetLastError());
   p->launches += 4;
   p->B = B;
