@@ -43,13 +43,14 @@
 
 namespace {
 
-constexpr int V = 4;  // voxels per lane
-constexpr int TILE_X = 8, TILE_Y = 4, TILE_Z = 4;
-constexpr int TILE = TILE_X * TILE_Y * TILE_Z;  // 128 = 32 lanes × V
+constexpr int V = 8;  // voxels per lane (consecutive in x)
+constexpr int NP = V / 2;  // fp32x2 pairs per lane
+constexpr int TILE_X = 8, TILE_Y = 8, TILE_Z = 4;
+constexpr int TILE = TILE_X * TILE_Y * TILE_Z;  // 256 = 32 lanes × V
 constexpr int TABW = 2 * TILE;                  // Reals per (tile, antenna): δ block + 1/d block
 constexpr int FWD_WARPS = 4;
 constexpr int ADJ_WARPS = 4;
-constexpr int TG_MAX = 6;      // tx per shared-memory group
+constexpr int TG_MAX = 4;      // tx per shared-memory group
 constexpr int A_MAX = 256;     // antennas (T + R) per plan
 constexpr int RED_THREADS = 300000;
 constexpr unsigned FULL = 0xffffffffu;
@@ -94,84 +95,111 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
 }
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-// ------------------------------------------------------------------ 4-voxel lane vectors
-struct F4 {  // voxels (0,1) and (2,3) of a lane as fp32 pairs
-  float2 a, b;
+// ------------------------------------------------------------------ V-voxel lane vectors
+struct FV {  // the lane's V voxels as NP fp32 pairs: (0,1), (2,3), ...
+  float2 p[NP];
 };
-struct D4 {
-  double v[4];
+struct DV {
+  double v[V];
 };
 template <typename Real>
-using Q4 = typename std::conditional<std::is_same<Real, float>::value, F4, D4>::type;
+using QV = typename std::conditional<std::is_same<Real, float>::value, FV, DV>::type;
 
-__device__ __forceinline__ F4 ld4(const float* p) {
-  const float4 q = *reinterpret_cast<const float4*>(p);
-  return F4{make_float2(q.x, q.y), make_float2(q.z, q.w)};
+__device__ __forceinline__ FV ldv(const float* p) {
+  FV q;
+#pragma unroll
+  for (int i = 0; i < NP / 2; ++i) {
+    const float4 t = reinterpret_cast<const float4*>(p)[i];
+    q.p[2 * i] = make_float2(t.x, t.y);
+    q.p[2 * i + 1] = make_float2(t.z, t.w);
+  }
+  return q;
 }
-__device__ __forceinline__ D4 ld4(const double* p) {
-  const double2 q0 = reinterpret_cast<const double2*>(p)[0];
-  const double2 q1 = reinterpret_cast<const double2*>(p)[1];
-  return D4{{q0.x, q0.y, q1.x, q1.y}};
+__device__ __forceinline__ DV ldv(const double* p) {
+  DV q;
+#pragma unroll
+  for (int i = 0; i < V / 2; ++i) {
+    const double2 t = reinterpret_cast<const double2*>(p)[i];
+    q.v[2 * i] = t.x;
+    q.v[2 * i + 1] = t.y;
+  }
+  return q;
 }
-__device__ __forceinline__ float get(const F4& q, int v) { return v == 0 ? q.a.x : v == 1 ? q.a.y : v == 2 ? q.b.x : q.b.y; }
-__device__ __forceinline__ double get(const D4& q, int v) { return q.v[v]; }
-__device__ __forceinline__ void zero(F4& q) { q.a = q.b = make_float2(0.f, 0.f); }
-__device__ __forceinline__ void zero(D4& q) { q.v[0] = q.v[1] = q.v[2] = q.v[3] = 0.0; }
+__device__ __forceinline__ float get(const FV& q, int v) { return (v & 1) ? q.p[v >> 1].y : q.p[v >> 1].x; }
+__device__ __forceinline__ double get(const DV& q, int v) { return q.v[v]; }
+__device__ __forceinline__ void zero(FV& q) {
+#pragma unroll
+  for (int i = 0; i < NP; ++i) q.p[i] = make_float2(0.f, 0.f);
+}
+__device__ __forceinline__ void zero(DV& q) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) q.v[i] = 0.0;
+}
+__device__ __forceinline__ FV make_v(const float* x) {
+  FV q;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) q.p[i] = make_float2(x[2 * i], x[2 * i + 1]);
+  return q;
+}
+__device__ __forceinline__ DV make_v(const double* x) {
+  DV q;
+#pragma unroll
+  for (int i = 0; i < V; ++i) q.v[i] = x[i];
+  return q;
+}
 
 // cos/sin(2π·x_v), x_v = base + k·(dT_v + dR_v), reduced exactly to [-½, ½] revolutions
 // (magic-number round-to-nearest, exact for |x| < 2^22) before MUFU.SIN/COS.
-__device__ __forceinline__ void phasor4(float k, float base, const F4& dT, const F4& dR, F4& c, F4& s) {
+__device__ __forceinline__ void phasorv(float k, float base, const FV& dT, const FV& dR, FV& c, FV& s) {
   const float2 M2 = bc(12582912.0f);
-  const float2 x0 = fma2(bc(k), add2(dT.a, dR.a), bc(base));
-  const float2 x1 = fma2(bc(k), add2(dT.b, dR.b), bc(base));
-  const float2 f0 = sub2(x0, sub2(add2(x0, M2), M2));
-  const float2 f1 = sub2(x1, sub2(add2(x1, M2), M2));
-  const float2 r0 = mul2(f0, bc(6.28318530717958647692f));
-  const float2 r1 = mul2(f1, bc(6.28318530717958647692f));
-  __sincosf(r0.x, &s.a.x, &c.a.x);
-  __sincosf(r0.y, &s.a.y, &c.a.y);
-  __sincosf(r1.x, &s.b.x, &c.b.x);
-  __sincosf(r1.y, &s.b.y, &c.b.y);
-}
-__device__ __forceinline__ void phasor4(double k, double base, const D4& dT, const D4& dR, D4& c, D4& s) {
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
+  for (int i = 0; i < NP; ++i) {
+    const float2 x = fma2(bc(k), add2(dT.p[i], dR.p[i]), bc(base));
+    const float2 f = sub2(x, sub2(add2(x, M2), M2));
+    const float2 r = mul2(f, bc(6.28318530717958647692f));
+    __sincosf(r.x, &s.p[i].x, &c.p[i].x);
+    __sincosf(r.y, &s.p[i].y, &c.p[i].y);
+  }
+}
+__device__ __forceinline__ void phasorv(double k, double base, const DV& dT, const DV& dR, DV& c, DV& s) {
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
     const double x = fma(k, dT.v[v] + dR.v[v], base);
     sincospi(2.0 * (x - rint(x)), &s.v[v], &c.v[v]);
   }
 }
 
 // adjoint: h += iT·e^{+jθ}·w  (w = conj(p)/(4π)·r, one complex per channel)
-__device__ __forceinline__ void adj_acc(const F4& iT, const F4& c, const F4& s, float wr, float wi, F4& hr,
-                                        F4& hi) {
-  const float2 a0 = mul2(iT.a, c.a), b0 = mul2(iT.a, s.a);
-  const float2 a1 = mul2(iT.b, c.b), b1 = mul2(iT.b, s.b);
-  hr.a = fma2(b0, bc(-wi), fma2(a0, bc(wr), hr.a));
-  hr.b = fma2(b1, bc(-wi), fma2(a1, bc(wr), hr.b));
-  hi.a = fma2(b0, bc(wr), fma2(a0, bc(wi), hi.a));
-  hi.b = fma2(b1, bc(wr), fma2(a1, bc(wi), hi.b));
-}
-__device__ __forceinline__ void adj_acc(const D4& iT, const D4& c, const D4& s, double wr, double wi, D4& hr,
-                                        D4& hi) {
+__device__ __forceinline__ void adj_acc(const FV& iT, const FV& c, const FV& s, float wr, float wi, FV& hr, FV& hi) {
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
+  for (int i = 0; i < NP; ++i) {
+    const float2 a = mul2(iT.p[i], c.p[i]), b = mul2(iT.p[i], s.p[i]);
+    hr.p[i] = fma2(b, bc(-wi), fma2(a, bc(wr), hr.p[i]));
+    hi.p[i] = fma2(b, bc(wr), fma2(a, bc(wi), hi.p[i]));
+  }
+}
+__device__ __forceinline__ void adj_acc(const DV& iT, const DV& c, const DV& s, double wr, double wi, DV& hr,
+                                        DV& hi) {
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
     const double a = iT.v[v] * c.v[v], b = iT.v[v] * s.v[v];
     hr.v[v] = fma(-b, wi, fma(a, wr, hr.v[v]));
     hi.v[v] = fma(b, wr, fma(a, wi, hi.v[v]));
   }
 }
 // end of an rx run: g += iR·h, h = 0
-__device__ __forceinline__ void flush(const F4& iR, F4& hr, F4& hi, F4& gr, F4& gi) {
-  gr.a = fma2(iR.a, hr.a, gr.a);
-  gr.b = fma2(iR.b, hr.b, gr.b);
-  gi.a = fma2(iR.a, hi.a, gi.a);
-  gi.b = fma2(iR.b, hi.b, gi.b);
+__device__ __forceinline__ void flush(const FV& iR, FV& hr, FV& hi, FV& gr, FV& gi) {
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    gr.p[i] = fma2(iR.p[i], hr.p[i], gr.p[i]);
+    gi.p[i] = fma2(iR.p[i], hi.p[i], gi.p[i]);
+  }
   zero(hr);
   zero(hi);
 }
-__device__ __forceinline__ void flush(const D4& iR, D4& hr, D4& hi, D4& gr, D4& gi) {
+__device__ __forceinline__ void flush(const DV& iR, DV& hr, DV& hi, DV& gr, DV& gi) {
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
+  for (int v = 0; v < V; ++v) {
     gr.v[v] = fma(iR.v[v], hr.v[v], gr.v[v]);
     gi.v[v] = fma(iR.v[v], hi.v[v], gi.v[v]);
   }
@@ -179,33 +207,35 @@ __device__ __forceinline__ void flush(const D4& iR, D4& hr, D4& hi, D4& gr, D4& 
   zero(hi);
 }
 // forward: ŝ = iR·s for the current rx run
-__device__ __forceinline__ void scale_s(const F4& iR, const F4& sr, const F4& si, F4& shr, F4& shi) {
-  shr.a = mul2(iR.a, sr.a);
-  shr.b = mul2(iR.b, sr.b);
-  shi.a = mul2(iR.a, si.a);
-  shi.b = mul2(iR.b, si.b);
-}
-__device__ __forceinline__ void scale_s(const D4& iR, const D4& sr, const D4& si, D4& shr, D4& shi) {
+__device__ __forceinline__ void scale_s(const FV& iR, const FV& sr, const FV& si, FV& shr, FV& shi) {
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
+  for (int i = 0; i < NP; ++i) {
+    shr.p[i] = mul2(iR.p[i], sr.p[i]);
+    shi.p[i] = mul2(iR.p[i], si.p[i]);
+  }
+}
+__device__ __forceinline__ void scale_s(const DV& iR, const DV& sr, const DV& si, DV& shr, DV& shi) {
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
     shr.v[v] = iR.v[v] * sr.v[v];
     shi.v[v] = iR.v[v] * si.v[v];
   }
 }
-// forward: Σ_v iT·e^{-jθ}·ŝ over the lane's 4 voxels
-__device__ __forceinline__ float2 fwd_part(const F4& iT, const F4& c, const F4& s, const F4& shr, const F4& shi) {
-  const float2 a0 = mul2(iT.a, c.a), b0 = mul2(iT.a, s.a);
-  const float2 a1 = mul2(iT.b, c.b), b1 = mul2(iT.b, s.b);
-  float2 pr = fma2(a0, shr.a, mul2(b0, shi.a));
-  pr = fma2(b1, shi.b, fma2(a1, shr.b, pr));
-  float2 pi = fma2(a0, shi.a, mul2(b0, make_float2(-shr.a.x, -shr.a.y)));
-  pi = fma2(b1, make_float2(-shr.b.x, -shr.b.y), fma2(a1, shi.b, pi));
+// forward: Σ_v iT·e^{-jθ}·ŝ over the lane's V voxels
+__device__ __forceinline__ float2 fwd_part(const FV& iT, const FV& c, const FV& s, const FV& shr, const FV& shi) {
+  float2 pr = make_float2(0.f, 0.f), pi = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const float2 a = mul2(iT.p[i], c.p[i]), b = mul2(iT.p[i], s.p[i]);
+    pr = fma2(b, shi.p[i], fma2(a, shr.p[i], pr));
+    pi = fma2(b, make_float2(-shr.p[i].x, -shr.p[i].y), fma2(a, shi.p[i], pi));
+  }
   return make_float2(pr.x + pr.y, pi.x + pi.y);
 }
-__device__ __forceinline__ double2 fwd_part(const D4& iT, const D4& c, const D4& s, const D4& shr, const D4& shi) {
+__device__ __forceinline__ double2 fwd_part(const DV& iT, const DV& c, const DV& s, const DV& shr, const DV& shi) {
   double pr = 0, pi = 0;
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
+  for (int v = 0; v < V; ++v) {
     const double a = iT.v[v] * c.v[v], b = iT.v[v] * s.v[v];
     pr = fma(b, shi.v[v], fma(a, shr.v[v], pr));
     pi = fma(-b, shr.v[v], fma(a, shi.v[v], pi));
@@ -256,14 +286,14 @@ __device__ __forceinline__ void tile_coords(const Geo& g, int tile, int& tx, int
   tx = rem - ty * g.ntx;
 }
 
-// lane L of tile (tx,ty,tz) owns voxels x = 8tx + 4(L&1) + v, y = 4ty + ((L>>1)&3), z = 4tz + (L>>3)
+// lane L of tile (tx,ty,tz) owns voxels x = 8tx + v (v < 8), y = 8ty + (L&7), z = 4tz + (L>>3)
 __device__ __forceinline__ void lane_voxel(int tx, int ty, int tz, int L, int& x0, int& y, int& z) {
-  x0 = tx * TILE_X + (L & 1) * V;
-  y = ty * TILE_Y + ((L >> 1) & 3);
+  x0 = tx * TILE_X;
+  y = ty * TILE_Y + (L & 7);
   z = tz * TILE_Z + (L >> 3);
 }
 
-// table[tile][a][2][32][4]: [0] = δ = d − D0, [1] = 1/d for the lane's 4 voxels; D0[tile][a] in fp64.
+// table[tile][a][2][32][V]: [0] = δ = d − D0, [1] = 1/d for the lane's V voxels; D0[tile][a] in fp64.
 template <typename Real>
 __global__ void build_table_kernel(Geo g, const double* __restrict__ ant, Real* __restrict__ tab,
                                    double* __restrict__ D0) {
@@ -451,8 +481,8 @@ struct WarpSmem {
 __host__ __device__ constexpr int d0_slots(int A) { return (A + 1) & ~1; }  // keep 16-byte alignment
 template <typename Real>
 __host__ __device__ constexpr size_t warp_smem_bytes(int Tg, int A) {
-  return (size_t)Tg * TABW * sizeof(Real) + (size_t)d0_slots(A) * sizeof(double) + 32 * sizeof(R4<Real>) +
-         32 * sizeof(int2);
+  return (size_t)Tg * TABW * sizeof(Real) + (size_t)d0_slots(A) * sizeof(double) + 34 * sizeof(R4<Real>) +
+         34 * sizeof(int2);
 }
 template <typename Real>
 __device__ __forceinline__ WarpSmem<Real> carve(unsigned char* base, int Tg, int A) {
@@ -460,7 +490,7 @@ __device__ __forceinline__ WarpSmem<Real> carve(unsigned char* base, int Tg, int
   ws.tside = reinterpret_cast<Real*>(base);
   ws.d0 = reinterpret_cast<double*>(base + (size_t)Tg * TABW * sizeof(Real));
   ws.rec = reinterpret_cast<R4<Real>*>(reinterpret_cast<unsigned char*>(ws.d0) + d0_slots(A) * sizeof(double));
-  ws.rect = reinterpret_cast<int2*>(ws.rec + 32);
+  ws.rect = reinterpret_cast<int2*>(ws.rec + 34);
   return ws;
 }
 
@@ -605,11 +635,12 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) adj_kernel(AdjArgs<Real> a) {
   const int j0 = (int)(((long long)a.B * chunk) / a.CH);
   const int j1 = (int)(((long long)a.B * (chunk + 1)) / a.CH);
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
+  for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
   __syncwarp();
   const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
   const Real* tsl = ws.tside + L * V;
 
-  Q4<Real> gr, gi, hr, hi, dR, iR, pdR, piR;
+  QV<Real> gr, gi, hr, hi, dR, iR, pdR, piR;
   zero(gr);
   zero(gi);
   zero(hr);
@@ -642,32 +673,29 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) adj_kernel(AdjArgs<Real> a) {
           iR = piR;
         } else {
           const Real* src = tabt + (size_t)(g.T + rr) * TABW;
-          dR = ld4(src + L * V);
-          iR = ld4(src + TILE + L * V);
+          dR = ldv(src + L * V);
+          iR = ldv(src + TILE + L * V);
         }
-        pf_r = rr + 1 < g.R ? rr + 1 : -1;
-        if (pf_r >= 0) {  // prefetch the next receiver's rows one run ahead
+        pf_r = rr + 1 < g.R ? rr + 1 : 0;
+        {  // prefetch the next receiver's rows one run ahead (wrapping to the next tx group)
           const Real* src = tabt + (size_t)(g.T + pf_r) * TABW;
-          pdR = ld4(src + L * V);
-          piR = ld4(src + TILE + L * V);
+          pdR = ldv(src + L * V);
+          piR = ldv(src + TILE + L * V);
         }
       }
-      // software pipeline: channel c+1's record and tx-side rows load while c computes
+      // software pipeline: channel c+1's record loads while c computes
       R4<Real> q = ws.rec[c];
-      const Real* ts = tsl + ws.rect[c].x;
-      Q4<Real> dT = ld4(ts), iT = ld4(ts + TILE);
+      int off = ws.rect[c].x;
 #pragma unroll 2
       for (; c < e; ++c) {
-        const int cn = c + 1 < e ? c + 1 : c;
-        const R4<Real> qn = ws.rec[cn];
-        const Real* tn = tsl + ws.rect[cn].x;
-        const Q4<Real> dTn = ld4(tn), iTn = ld4(tn + TILE);
-        Q4<Real> cs, sn;
-        phasor4(q.x, q.y, dT, dR, cs, sn);
+        const R4<Real> qn = ws.rec[c + 1];
+        const int offn = ws.rect[c + 1].x;
+        const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
+        QV<Real> cs, sn;
+        phasorv(q.x, q.y, dT, dR, cs, sn);
         adj_acc(iT, cs, sn, q.z, q.w, hr, hi);
         q = qn;
-        dT = dTn;
-        iT = iTn;
+        off = offn;
       }
     }
     __syncwarp();
@@ -805,7 +833,10 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int tile = blockIdx.x * FWD_WARPS + w;
+  // blockIdx.x = channel chunk (fastest, so the chunks of one tile group run together and
+  // share its table rows in L2), blockIdx.y = tile group
+  const int tgrp = blockIdx.y, chunk = blockIdx.x;
+  const int tile = tgrp * FWD_WARPS + w;
   const bool tile_ok = tile < g.ntiles;
   unsigned char* wbase = smem_raw + (size_t)w * fwd_warp_bytes<Real>(g.Tg, g.A);
   const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A);
@@ -814,6 +845,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
 
   const int tsel = tile_ok ? tile : 0;
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tsel * g.A + i];
+  for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
   const Real* tabt = a.tab + (size_t)tsel * g.A * TABW;
   const Real* tsl = ws.tside + L * V;
   int tx, ty, tz;
@@ -829,21 +861,14 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
     srv[v] = ok ? a.s[2 * n] : Real(0);
     siv[v] = ok ? a.s[2 * n + 1] : Real(0);
   }
-  Q4<Real> sr, si;
-  if constexpr (std::is_same<Real, float>::value) {
-    sr = F4{make_float2(srv[0], srv[1]), make_float2(srv[2], srv[3])};
-    si = F4{make_float2(siv[0], siv[1]), make_float2(siv[2], siv[3])};
-  } else {
-    sr = D4{{srv[0], srv[1], srv[2], srv[3]}};
-    si = D4{{siv[0], siv[1], siv[2], siv[3]}};
-  }
+  const QV<Real> sr = make_v(srv), si = make_v(siv);
   __syncwarp();
 
   const int span = a.w1 - a.w0;
-  const int c0 = a.w0 + (int)(((long long)span * blockIdx.y) / a.Q);
-  const int c1 = a.w0 + (int)(((long long)span * (blockIdx.y + 1)) / a.Q);
+  const int c0 = a.w0 + (int)(((long long)span * chunk) / a.Q);
+  const int c1 = a.w0 + (int)(((long long)span * (chunk + 1)) / a.Q);
 
-  Q4<Real> dR, iR, pdR, piR, shr, shi;
+  QV<Real> dR, iR, pdR, piR, shr, shi;
   zero(dR);
   zero(iR);
   zero(pdR);
@@ -875,32 +900,29 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
             iR = piR;
           } else {
             const Real* src = tabt + (size_t)(g.T + rr) * TABW;
-            dR = ld4(src + L * V);
-            iR = ld4(src + TILE + L * V);
+            dR = ldv(src + L * V);
+            iR = ldv(src + TILE + L * V);
           }
           scale_s(iR, sr, si, shr, shi);
-          pf_r = rr + 1 < g.R ? rr + 1 : -1;
-          if (pf_r >= 0) {
+          pf_r = rr + 1 < g.R ? rr + 1 : 0;
+          {
             const Real* src = tabt + (size_t)(g.T + pf_r) * TABW;
-            pdR = ld4(src + L * V);
-            piR = ld4(src + TILE + L * V);
+            pdR = ldv(src + L * V);
+            piR = ldv(src + TILE + L * V);
           }
         }
         R4<Real> q = ws.rec[c];
-        const Real* ts = tsl + ws.rect[c].x;
-        Q4<Real> dT = ld4(ts), iT = ld4(ts + TILE);
+        int off = ws.rect[c].x;
 #pragma unroll 2
         for (; c < e; ++c) {
-          const int cn = c + 1 < e ? c + 1 : c;
-          const R4<Real> qn = ws.rec[cn];
-          const Real* tn = tsl + ws.rect[cn].x;
-          const Q4<Real> dTn = ld4(tn), iTn = ld4(tn + TILE);
-          Q4<Real> cs, sn;
-          phasor4(q.x, q.y, dT, dR, cs, sn);
+          const R4<Real> qn = ws.rec[c + 1];
+          const int offn = ws.rect[c + 1].x;
+          const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
+          QV<Real> cs, sn;
+          phasorv(q.x, q.y, dT, dR, cs, sn);
           tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi);
           q = qn;
-          dT = dTn;
-          iT = iTn;
+          off = offn;
         }
       }
       __syncwarp();
@@ -923,7 +945,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
   }
   __syncthreads();
   // combine the CTA's warps (fixed order) and publish the tile-group partial
-  R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)blockIdx.x * span;
+  R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tgrp * span;
   for (int i = threadIdx.x; i < c1 - c0; i += FWD_WARPS * 32) {
     R2<Real> T2;
     T2.x = 0;
@@ -1123,7 +1145,7 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.w1 = w1;
     a.Q = channel_splits(p, span);
     a.part = (Real*)p->d_part;
-    fwd_kernel<Real><<<dim3(p->fwd_gridx, a.Q), FWD_WARPS * 32, sm, st>>>(a);
+    fwd_kernel<Real><<<dim3(a.Q, p->fwd_gridx), FWD_WARPS * 32, sm, st>>>(a);
     CUDA_TRY(cudaGetLastError());
     const int nseg = std::max(1, std::min(p->fwd_gridx, RED_THREADS / span));
     fwd_reduce1_kernel<Real><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const Real*)p->d_part, p->fwd_gridx,
