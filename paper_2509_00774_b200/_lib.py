@@ -49,7 +49,11 @@ class NFError(RuntimeError):
 
 
 def library_path() -> Path:
-    return _build.LIB
+    """The in-tree libnfgpu.so (NFGPU_LIB overrides it, for tuning-variant experiments)."""
+    import os
+
+    override = os.environ.get("NFGPU_LIB")
+    return Path(override) if override else _build.LIB
 
 
 def load(build_if_missing: bool = True) -> ctypes.CDLL:
@@ -58,7 +62,9 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        if build_if_missing and _build.needs_build():
+        import os
+
+        if build_if_missing and not os.environ.get("NFGPU_LIB") and _build.needs_build():
             _build.build()
         path = library_path()
         if not path.exists():

@@ -43,14 +43,37 @@
 
 namespace {
 
-constexpr int V = 8;  // voxels per lane (consecutive in x)
+// Tuning knobs (compile-time; defaults are the measured best on B200).
+#ifndef NFGPU_V
+#define NFGPU_V 8
+#endif
+#ifndef NFGPU_TG
+#define NFGPU_TG 4
+#endif
+#ifndef NFGPU_UNROLL
+#define NFGPU_UNROLL 2
+#endif
+#ifndef NFGPU_FWD_WARPS
+#define NFGPU_FWD_WARPS 4
+#endif
+#ifndef NFGPU_ADJ_WARPS
+#define NFGPU_ADJ_WARPS 4
+#endif
+#ifndef NFGPU_TBR
+#define NFGPU_TBR 16
+#endif
+constexpr int V = NFGPU_V;  // voxels per lane (consecutive in x)
+static_assert(V == 4 || V == 8, "V must be 4 or 8");
 constexpr int NP = V / 2;  // fp32x2 pairs per lane
-constexpr int TILE_X = 8, TILE_Y = 8, TILE_Z = 4;
-constexpr int TILE = TILE_X * TILE_Y * TILE_Z;  // 256 = 32 lanes × V
+constexpr int TILE_X = 8, TILE_Y = V == 8 ? 8 : 4, TILE_Z = 4;
+constexpr int TILE = TILE_X * TILE_Y * TILE_Z;  // 32 lanes × V
 constexpr int TABW = 2 * TILE;                  // Reals per (tile, antenna): δ block + 1/d block
-constexpr int FWD_WARPS = 4;
-constexpr int ADJ_WARPS = 4;
-constexpr int TG_MAX = 4;      // tx per shared-memory group
+constexpr int FWD_WARPS = NFGPU_FWD_WARPS;
+constexpr int ADJ_WARPS = NFGPU_ADJ_WARPS;
+constexpr int TG_MAX = NFGPU_TG;  // tx per shared-memory group
+constexpr int UNROLL = NFGPU_UNROLL;
+constexpr int TBR = NFGPU_TBR;  // forward transpose depth (channels per lane-reduction)
+static_assert(TBR == 8 || TBR == 16, "TBR must be 8 or 16");
 constexpr int A_MAX = 256;     // antennas (T + R) per plan
 constexpr int RED_THREADS = 300000;
 constexpr unsigned FULL = 0xffffffffu;
@@ -105,11 +128,16 @@ struct DV {
 template <typename Real>
 using QV = typename std::conditional<std::is_same<Real, float>::value, FV, DV>::type;
 
+// Lane-data layout in every table row, shared-memory row and staging slot: 16-byte
+// quads interleaved across lanes, element (lane L, voxel v) at
+//   (v / QUAD) * 32 * QUAD + L * QUAD + v % QUAD,   QUAD = 16 / sizeof(Real),
+// so each warp-wide 16-byte load touches 512 contiguous bytes (no bank conflicts).
+// `p` points at the lane's first quad (row base + L * QUAD).
 __device__ __forceinline__ FV ldv(const float* p) {
   FV q;
 #pragma unroll
   for (int i = 0; i < NP / 2; ++i) {
-    const float4 t = reinterpret_cast<const float4*>(p)[i];
+    const float4 t = *reinterpret_cast<const float4*>(p + i * 128);
     q.p[2 * i] = make_float2(t.x, t.y);
     q.p[2 * i + 1] = make_float2(t.z, t.w);
   }
@@ -119,7 +147,7 @@ __device__ __forceinline__ DV ldv(const double* p) {
   DV q;
 #pragma unroll
   for (int i = 0; i < V / 2; ++i) {
-    const double2 t = reinterpret_cast<const double2*>(p)[i];
+    const double2 t = *reinterpret_cast<const double2*>(p + i * 64);
     q.v[2 * i] = t.x;
     q.v[2 * i + 1] = t.y;
   }
@@ -286,10 +314,16 @@ __device__ __forceinline__ void tile_coords(const Geo& g, int tile, int& tx, int
   tx = rem - ty * g.ntx;
 }
 
-// lane L of tile (tx,ty,tz) owns voxels x = 8tx + v (v < 8), y = 8ty + (L&7), z = 4tz + (L>>3)
+// V = 8: lane L of tile (tx,ty,tz) owns x = 8tx + v (v < 8), y = 8ty + (L&7), z = 4tz + (L>>3)
+// V = 4: x = 8tx + 4(L&1) + v, y = 4ty + ((L>>1)&3), z = 4tz + (L>>3)
 __device__ __forceinline__ void lane_voxel(int tx, int ty, int tz, int L, int& x0, int& y, int& z) {
-  x0 = tx * TILE_X;
-  y = ty * TILE_Y + (L & 7);
+  if (V == 8) {
+    x0 = tx * TILE_X;
+    y = ty * TILE_Y + (L & 7);
+  } else {
+    x0 = tx * TILE_X + (L & 1) * V;
+    y = ty * TILE_Y + ((L >> 1) & 3);
+  }
   z = tz * TILE_Z + (L >> 3);
 }
 
@@ -322,8 +356,10 @@ __global__ void build_table_kernel(Geo g, const double* __restrict__ ant, Real* 
       dl = (Real)(d - d0);
       iv = (Real)(1.0 / d);
     }
-    out[L * V + v] = dl;
-    out[TILE + L * V + v] = iv;
+    constexpr int QD = 16 / (int)sizeof(Real);
+    const int o = (v / QD) * 32 * QD + L * QD + v % QD;
+    out[o] = dl;
+    out[TILE + o] = iv;
   }
 }
 
@@ -473,25 +509,69 @@ __global__ void sample_kernel(uint64_t key, int hb, int M, int B, int* __restric
 // ------------------------------------------------------------------ per-warp shared state
 template <typename Real>
 struct WarpSmem {
-  Real* tside;    // [Tg][2][32][4]
+  Real* tside;    // [Tg][2][32][V] tx-side rows of the current tx group
+  Real* rslot;    // [2][2][32][V] rx-side rows, ping-pong staging (cp.async)
   double* d0;     // [A]
-  R4<Real>* rec;  // [32] {k, base, wr, wi}
-  int2* rect;     // [32] {tside offset, run key}
+  R4<Real>* rec;  // [34] {k, base, wr, wi}
+  int2* rect;     // [34] {tside offset, run key}
 };
 __host__ __device__ constexpr int d0_slots(int A) { return (A + 1) & ~1; }  // keep 16-byte alignment
 template <typename Real>
 __host__ __device__ constexpr size_t warp_smem_bytes(int Tg, int A) {
-  return (size_t)Tg * TABW * sizeof(Real) + (size_t)d0_slots(A) * sizeof(double) + 34 * sizeof(R4<Real>) +
+  return (size_t)(Tg + 2) * TABW * sizeof(Real) + (size_t)d0_slots(A) * sizeof(double) + 34 * sizeof(R4<Real>) +
          34 * sizeof(int2);
 }
 template <typename Real>
 __device__ __forceinline__ WarpSmem<Real> carve(unsigned char* base, int Tg, int A) {
   WarpSmem<Real> ws;
   ws.tside = reinterpret_cast<Real*>(base);
-  ws.d0 = reinterpret_cast<double*>(base + (size_t)Tg * TABW * sizeof(Real));
+  ws.rslot = ws.tside + (size_t)Tg * TABW;
+  ws.d0 = reinterpret_cast<double*>(base + (size_t)(Tg + 2) * TABW * sizeof(Real));
   ws.rec = reinterpret_cast<R4<Real>*>(reinterpret_cast<unsigned char*>(ws.d0) + d0_slots(A) * sizeof(double));
   ws.rect = reinterpret_cast<int2*>(ws.rec + 34);
   return ws;
+}
+
+// Stage receiver r's rows for this lane's voxels into a shared slot with per-lane cp.async
+// (LDGSTS): each lane copies and later reads back only its own 2·V Reals, so no warp sync
+// is needed, only cp.async.wait_all by the same lane.
+template <typename Real>
+__device__ __forceinline__ void stage_rx(const Geo& g, const Real* __restrict__ tabt, int r, Real* slot, int L) {
+  constexpr int QD = 16 / (int)sizeof(Real);
+  const Real* src = tabt + (size_t)(g.T + r) * TABW + L * QD;
+  Real* dst = slot + L * QD;
+  constexpr int n16 = V / QD;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < n16; ++i) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dst + h * TILE + i * 32 * QD);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + h * TILE + i * 32 * QD)
+                   : "memory");
+    }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Rows of receiver rr for the run that starts now: from the ping-pong slot if it was
+// prefetched, else straight from global. Then prefetch the next receiver (wrapping to 0,
+// the first receiver of the next tx group) into the other slot.
+template <typename Real>
+__device__ __forceinline__ void rx_run_rows(const Geo& g, const Real* __restrict__ tabt, const WarpSmem<Real>& ws,
+                                            int rr, int& pf_r, int& slot, int L, QV<Real>& dR, QV<Real>& iR) {
+  stage_wait();
+  if (rr == pf_r) {
+    const Real* sl = ws.rslot + (size_t)slot * TABW + L * (16 / (int)sizeof(Real));
+    dR = ldv(sl);
+    iR = ldv(sl + TILE);
+  } else {
+    const Real* src = tabt + (size_t)(g.T + rr) * TABW + L * (16 / (int)sizeof(Real));
+    dR = ldv(src);
+    iR = ldv(src + TILE);
+  }
+  slot ^= 1;
+  pf_r = rr + 1 < g.R ? rr + 1 : 0;
+  stage_rx<Real>(g, tabt, pf_r, ws.rslot + (size_t)slot * TABW, L);
 }
 
 // Copy the tx-side table rows of tx group tg for this tile into the warp's smem.
@@ -638,18 +718,16 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) adj_kernel(AdjArgs<Real> a) {
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
   __syncwarp();
   const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
-  const Real* tsl = ws.tside + L * V;
+  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
 
-  QV<Real> gr, gi, hr, hi, dR, iR, pdR, piR;
+  QV<Real> gr, gi, hr, hi, dR, iR;
   zero(gr);
   zero(gi);
   zero(hr);
   zero(hi);
   zero(dR);
   zero(iR);
-  zero(pdR);
-  zero(piR);
-  int cur_tg = -1, pf_r = -1, carry = -1;
+  int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
   ChanRec nxt;
   R2<Real> nxtw;
   prefetch_first<Real>(a.crec, a.wrec, j0, j1, L, nxt, nxtw);
@@ -668,25 +746,12 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) adj_kernel(AdjArgs<Real> a) {
           cur_tg = tg;
         }
         flush(iR, hr, hi, gr, gi);
-        if (rr == pf_r) {
-          dR = pdR;
-          iR = piR;
-        } else {
-          const Real* src = tabt + (size_t)(g.T + rr) * TABW;
-          dR = ldv(src + L * V);
-          iR = ldv(src + TILE + L * V);
-        }
-        pf_r = rr + 1 < g.R ? rr + 1 : 0;
-        {  // prefetch the next receiver's rows one run ahead (wrapping to the next tx group)
-          const Real* src = tabt + (size_t)(g.T + pf_r) * TABW;
-          pdR = ldv(src + L * V);
-          piR = ldv(src + TILE + L * V);
-        }
+        rx_run_rows<Real>(g, tabt, ws, rr, pf_r, rslot, L, dR, iR);
       }
       // software pipeline: channel c+1's record loads while c computes
       R4<Real> q = ws.rec[c];
       int off = ws.rect[c].x;
-#pragma unroll 2
+#pragma unroll UNROLL
       for (; c < e; ++c) {
         const R4<Real> qn = ws.rec[c + 1];
         const int offn = ws.rect[c + 1].x;
@@ -701,6 +766,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) adj_kernel(AdjArgs<Real> a) {
     __syncwarp();
   }
   flush(iR, hr, hi, gr, gi);
+  stage_wait();
 
   Real Gr[V], Gi[V];
 #pragma unroll
@@ -818,45 +884,41 @@ struct FwdArgs {
   Real* __restrict__ part;     // [gridDim.x][w1-w0] complex
 };
 
-constexpr int FCH = 256;  // max channels per forward unit (per-warp accumulator in smem)
-
 template <typename Real>
 __host__ __device__ constexpr size_t fwd_warp_bytes(int Tg, int A) {
-  return warp_smem_bytes<Real>(Tg, A) + (size_t)16 * 33 * sizeof(R2<Real>) + (size_t)FCH * sizeof(R2<Real>);
+  return warp_smem_bytes<Real>(Tg, A) + (size_t)TBR * 33 * sizeof(R2<Real>);
 }
 
-// Forward: CTA = FWD_WARPS warps on adjacent tiles × one chunk of <= FCH sorted channels.
-// Each warp keeps its per-channel tile sums for the chunk in smem; one CTA barrier at the
-// end combines the warps in a fixed order and writes part[blockIdx.x][j].
+// Forward: a warp owns (tile, channel chunk) like the adjoint. Per channel, each lane forms
+// the sum over its V voxels. Every 16 channels, a transpose through smem reduces over the
+// 32 lanes in a fixed order, and the tile's per-channel sum goes to part[tile][j].
+// Chunks of one tile are adjacent units, so they run together and share the tile's table
+// rows in L2.
 template <typename Real>
 __global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-  // blockIdx.x = channel chunk (fastest, so the chunks of one tile group run together and
-  // share its table rows in L2), blockIdx.y = tile group
-  const int tgrp = blockIdx.y, chunk = blockIdx.x;
-  const int tile = tgrp * FWD_WARPS + w;
-  const bool tile_ok = tile < g.ntiles;
+  const int unit = blockIdx.x * FWD_WARPS + w;
+  if (unit >= g.ntiles * a.Q) return;  // warps are independent: no block barriers
+  const int tile = unit / a.Q, chunk = unit - tile * a.Q;
   unsigned char* wbase = smem_raw + (size_t)w * fwd_warp_bytes<Real>(g.Tg, g.A);
   const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A);
-  R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A));  // [16][33]
-  R2<Real>* acc = tb + 16 * 33;                                                       // [FCH]
+  R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A));  // [TBR][33]
 
-  const int tsel = tile_ok ? tile : 0;
-  for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tsel * g.A + i];
+  for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
-  const Real* tabt = a.tab + (size_t)tsel * g.A * TABW;
-  const Real* tsl = ws.tside + L * V;
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
+  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
   int tx, ty, tz;
-  tile_coords(g, tsel, tx, ty, tz);
+  tile_coords(g, tile, tx, ty, tz);
   int x0, y, z;
   lane_voxel(tx, ty, tz, L, x0, y, z);
   Real srv[V], siv[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int x = x0 + v;
-    const bool ok = tile_ok && x < g.nx && y < g.ny && z < g.nzs;
+    const bool ok = x < g.nx && y < g.ny && z < g.nzs;
     const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
     srv[v] = ok ? a.s[2 * n] : Real(0);
     siv[v] = ok ? a.s[2 * n + 1] : Real(0);
@@ -867,24 +929,23 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
   const int span = a.w1 - a.w0;
   const int c0 = a.w0 + (int)(((long long)span * chunk) / a.Q);
   const int c1 = a.w0 + (int)(((long long)span * (chunk + 1)) / a.Q);
+  R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * span - a.w0;
 
-  QV<Real> dR, iR, pdR, piR, shr, shi;
+  QV<Real> dR, iR, shr, shi;
   zero(dR);
   zero(iR);
-  zero(pdR);
-  zero(piR);
   zero(shr);
   zero(shi);
-  int cur_tg = -1, pf_r = -1, carry = -1;
+  int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
   ChanRec nxt;
   R2<Real> nxtw;
   prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
   for (int jb = c0; jb < c1; jb += 32) {
     const int nb = min(32, c1 - jb);
     const unsigned starts = build_records<Real>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
-    // two half-batches of 16 channels share one [16][33] transpose buffer
-    for (int h0 = 0; h0 < nb; h0 += 16) {
-      const int h1 = min(nb, h0 + 16);
+    // sub-batches of TBR channels share one [TBR][33] transpose buffer
+    for (int h0 = 0; h0 < nb; h0 += TBR) {
+      const int h1 = min(nb, h0 + TBR);
       int c = h0;
       while (c < h1) {
         const int e = min(run_end(starts, c, nb), h1);
@@ -895,25 +956,12 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
             load_tgroup<Real>(g, tabt, ws.tside, tg, L);
             cur_tg = tg;
           }
-          if (rr == pf_r) {
-            dR = pdR;
-            iR = piR;
-          } else {
-            const Real* src = tabt + (size_t)(g.T + rr) * TABW;
-            dR = ldv(src + L * V);
-            iR = ldv(src + TILE + L * V);
-          }
+          rx_run_rows<Real>(g, tabt, ws, rr, pf_r, rslot, L, dR, iR);
           scale_s(iR, sr, si, shr, shi);
-          pf_r = rr + 1 < g.R ? rr + 1 : 0;
-          {
-            const Real* src = tabt + (size_t)(g.T + pf_r) * TABW;
-            pdR = ldv(src + L * V);
-            piR = ldv(src + TILE + L * V);
-          }
         }
         R4<Real> q = ws.rec[c];
         int off = ws.rect[c].x;
-#pragma unroll 2
+#pragma unroll UNROLL
         for (; c < e; ++c) {
           const R4<Real> qn = ws.rec[c + 1];
           const int offn = ws.rect[c + 1].x;
@@ -926,39 +974,29 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
         }
       }
       __syncwarp();
-      // transpose-reduce: lanes L and L+16 each sum half of row L&15, then combine (fixed order)
-      const int row = L & 15, half = L >> 4;
+      // transpose-reduce: 32/TBR lanes per row each sum a 32/(32/TBR) slice of row L % TBR,
+      // then combine with shuffles (fixed order)
+      constexpr int PER = 32 / TBR, SL = 32 / PER;
+      const int row = L % TBR, part = L / TBR;
       R2<Real> S;
       S.x = 0;
       S.y = 0;
 #pragma unroll 8
-      for (int l = 0; l < 16; ++l) {
-        const R2<Real> t = tb[row * 33 + half * 16 + l];
+      for (int l = 0; l < SL; ++l) {
+        const R2<Real> t = tb[row * 33 + part * SL + l];
         S.x += t.x;
         S.y += t.y;
       }
-      S.x += __shfl_down_sync(FULL, S.x, 16);
-      S.y += __shfl_down_sync(FULL, S.y, 16);
-      if (L < h1 - h0) acc[jb - c0 + h0 + L] = S;
+#pragma unroll
+      for (int o = 16; o >= TBR; o >>= 1) {
+        S.x += __shfl_down_sync(FULL, S.x, o);
+        S.y += __shfl_down_sync(FULL, S.y, o);
+      }
+      if (L < h1 - h0) out[jb + h0 + L] = S;
       __syncwarp();
     }
   }
-  __syncthreads();
-  // combine the CTA's warps (fixed order) and publish the tile-group partial
-  R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tgrp * span;
-  for (int i = threadIdx.x; i < c1 - c0; i += FWD_WARPS * 32) {
-    R2<Real> T2;
-    T2.x = 0;
-    T2.y = 0;
-#pragma unroll
-    for (int ww = 0; ww < FWD_WARPS; ++ww) {
-      const R2<Real> t = reinterpret_cast<const R2<Real>*>(smem_raw + (size_t)ww * fwd_warp_bytes<Real>(g.Tg, g.A) +
-                                                           warp_smem_bytes<Real>(g.Tg, g.A))[16 * 33 + i];
-      T2.x += t.x;
-      T2.y += t.y;
-    }
-    out[c0 - a.w0 + i] = T2;
-  }
+  stage_wait();
 }
 
 // level 1: tmp[seg][j] = Σ_{x in seg} part[x][j] (fp64, fixed order)
@@ -1112,11 +1150,10 @@ size_t adj_smem(const nf_plan* p) {
 }
 
 int channel_splits(const nf_plan* p, int span) {
-  // ~8 waves of 3 CTAs/SM on 148 SMs, 32..FCH channels per split
-  const long long target = 148LL * 3 * 8;
-  long long q = (target + p->fwd_gridx - 1) / p->fwd_gridx;
-  q = std::min<long long>(q, std::max(1, span / 32));
-  q = std::max<long long>(q, (span + FCH - 1) / FCH);
+  // enough (tile, chunk) warp units for ~6 rounds of 16 warps/SM; >= 64 channels per chunk
+  const long long target = 148LL * 16 * 6;
+  long long q = (target + p->g.ntiles - 1) / p->g.ntiles;
+  q = std::min<long long>(q, std::max(1, span / 64));
   return (int)std::max(1LL, q);
 }
 
@@ -1145,7 +1182,8 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.w1 = w1;
     a.Q = channel_splits(p, span);
     a.part = (Real*)p->d_part;
-    fwd_kernel<Real><<<dim3(a.Q, p->fwd_gridx), FWD_WARPS * 32, sm, st>>>(a);
+    const long long units = (long long)p->g.ntiles * a.Q;
+    fwd_kernel<Real><<<(unsigned)((units + FWD_WARPS - 1) / FWD_WARPS), FWD_WARPS * 32, sm, st>>>(a);
     CUDA_TRY(cudaGetLastError());
     const int nseg = std::max(1, std::min(p->fwd_gridx, RED_THREADS / span));
     fwd_reduce1_kernel<Real><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const Real*)p->d_part, p->fwd_gridx,
@@ -1249,7 +1287,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   p->km = KeyMap{g.T, g.R, g.F, g.Tg};
   p->KS = g.ng * g.R * g.Tg * g.F;
   p->ksblocks = (p->KS + 1023) / 1024;
-  p->fwd_gridx = (g.ntiles + FWD_WARPS - 1) / FWD_WARPS;
+  p->fwd_gridx = g.ntiles;  // rows of the forward partial buffer (one per tile)
   const size_t rs = real_size(p);
   {
     // bound the forward partial buffer to ~512 MB
