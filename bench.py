@@ -37,6 +37,9 @@ UNIT = "entries/s"
 # SFU roofline: 2 MUFU (sin, cos) per entry, 16 MUFU/clk/SM, 148 SMs
 ENTRIES_PER_CLK_SM = 8.0
 N_SM = 148
+# measured on this pool's B200 with tools/peaks.cu (profiles/r01_peaks.json): 4.622e12 MUFU sin/cos
+# ops/s at 1965 MHz = 15.89 per clk per SM -> 2.311e12 entries/s
+SFU_ENTRY_PEAK_MEASURED = 4.622e12 / 2
 
 
 def parse():
@@ -61,7 +64,8 @@ def env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled every 100 ms during the timed region
+    (one persistent `nvidia-smi -lms 100` process)."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -69,38 +73,50 @@ class ClockSampler:
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
+        self.proc = None
         self.rows = []
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is None:
+            return
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.splitlines():
+            cols = [c.strip() for c in line.split(",")]
+            if len(cols) == 7:
+                self.rows.append(cols)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [v for v in (num(r[0]) for r in self.rows) if v is not None]
+        mx = [v for v in (num(r[1]) for r in self.rows) if v is not None]
+        pw = [v for v in (num(r[2]) for r in self.rows) if v is not None]
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle port)
@@ -109,7 +125,8 @@ class ClockSampler:
 def cpu_baseline(workload: str, steps: int, budget_s: float, rank_sample_seed: int = 0):
     """The reference's CPU algorithm (phasor tables + BLAS dots, forward.py:183-336),
     restated in oracle/ and run with all host threads on a voxel sample of the same
-    workload: the first n voxels (flat order) of the grid, the same |B| and flat sampling."""
+    workload: the whole grid when its tables fit (<= 131072 voxels), else z-plane 0, with the
+    same |B| and flat sampling."""
     from oracle import nfmimo_oracle as O
     from paper_2509_00774_b200 import configs
 
@@ -117,12 +134,15 @@ def cpu_baseline(workload: str, steps: int, budget_s: float, rank_sample_seed: i
     geo_full = O.geom_from_scenario(w.scenario) if w.scenario.n_voxels <= 1 << 17 else None
     if geo_full is None:
         v = w.scenario.voxels
-        n_sample = 4096
-        cen = O.centers_of(v.corner.as_array(), v.spacing, v.dims, (0, 1))[:n_sample]
+        cen = O.centers_of(v.corner.as_array(), v.spacing, v.dims, (0, 1))
+        n_sample = cen.shape[0]
         freqs = w.scenario.frequencies.values()
         geo = O.Geom(w.scenario.array.tx_positions(), w.scenario.array.rx_positions(), freqs,
                      w.scenario.pulse.evaluate(freqs), cen, w.scenario.c)
-        sample = f"first {n_sample} voxels (of {w.scenario.n_voxels}) of the {workload} grid, all M channels"
+        scn = w.scenario
+        full_tables = 16 * scn.frequencies.count * (scn.array.n_tx + scn.array.n_rx) * scn.n_voxels
+        sample = (f"z-plane 0 ({n_sample} of {scn.n_voxels} voxels) of the {workload} grid, all M channels "
+                  f"(the full grid's phasor tables would need {full_tables / 1e9:.0f} GB)")
     else:
         geo = geo_full
         sample = f"full {workload} grid ({geo.N} voxels)"
@@ -268,19 +288,23 @@ def run_ours(args):
         e2e = e2e_run(eng, scn, B, N, args, pg, local)
 
     clocks = clk.summary()
-    local_entries = 2.0 * B * plan.n_local
-    peak = N_SM * ENTRIES_PER_CLK_SM * 1.965e9
+    peak = SFU_ENTRY_PEAK_MEASURED
     dom = "adjoint_prox" if kt["adj_ms"] >= kt["fwd_ms"] else "forward"
     dom_ms = max(kt["adj_ms"], kt["fwd_ms"])
-    achieved = (B * plan.n_local) / (dom_ms * 1e-3)
+    per_launch = B * plan.n_local
+    achieved = per_launch / (dom_ms * 1e-3)
+    clk = clocks.get("sm_mhz") or 1965.0
     roof = {
         "bound": "fp32+sfu", "kernel": dom, "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gentry/s",
         "frac": achieved / peak,
-        "peak_source": "nominal SFU roof: 148 SM x 16 MUFU/clk / 2 MUFU per entry x 1.965 GHz (MEASURED_PEAKS.json "
-                       "has no SFU figure)",
-        "frac_at_observed_clock": (achieved / (N_SM * ENTRIES_PER_CLK_SM * clocks["sm_mhz"] * 1e6)
-                                   if clocks.get("sm_mhz") else None),
-        "fwd_ms": kt["fwd_ms"], "adj_ms": kt["adj_ms"], "entries_per_launch": B * plan.n_local,
+        "peak_source": "measured MUFU sin/cos rate on this pool's B200 (tools/peaks.cu, profiles/r01_peaks.json): "
+                       "15.89 MUFU/clk/SM x 148 SM x 1.965 GHz / 2 MUFU per entry; MEASURED_PEAKS.json has no SFU "
+                       "figure; nominal 2326.6 Gentry/s",
+        "frac_at_observed_clock": achieved / (peak * clk / 1965.0),
+        "fwd_ms": kt["fwd_ms"], "adj_ms": kt["adj_ms"], "entries_per_launch": per_launch,
+        "frac_forward": per_launch / (kt["fwd_ms"] * 1e-3) / peak,
+        "frac_adjoint_prox": per_launch / (kt["adj_ms"] * 1e-3) / peak,
+        "frac_step": value / (world * peak),
         "traffic": None,
     }
     out = None
