@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-graph", action="store_true", help="launch steps eagerly instead of a CUDA graph")
+    ap.add_argument("--no-extras", action="store_true", help="skip the Medium extra line")
+    ap.add_argument("--force-dist", action="store_true", help="use the NCCL path even at world size 1")
     return ap.parse_args()
 
 
@@ -203,79 +206,107 @@ def slab(nz: int, rank: int, world: int):
     return slab_range(nz, rank, world)
 
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-
+def build_engine(workload, dev, rank, world, pg):
+    """Setup (not timed): plan for this rank's slab, synthetic scene and measurements, the
+    power-iteration Lipschitz constant (20 iterations, as BASELINE.json), λ and α."""
     from paper_2509_00774_b200 import configs
     from paper_2509_00774_b200.plan import DevicePlan
     from paper_2509_00774_b200.sharding import ShardedSetup
     from paper_2509_00774_b200.solver import SPGMEngine
 
+    w = configs.WORKLOADS[workload]()
+    scn = w.scenario
+    zr = slab(scn.voxels.dims[2], rank, world)
+    t0 = time.perf_counter()
+    setup = ShardedSetup(scn, dtype=w.dtype, device=dev, z_range=zr, process_group=pg)
+    clean = setup.forward_full(configs.make_scene(w))
+    y = configs.add_noise(clean, configs.noise_sigma(clean, w.snr_db))
+    L = setup.lipschitz(n_iters=20, rng_seed=configs.SEEDS["power"])
+    lam = 1e-3 * setup.max_abs_adjoint(y) / scn.n_channels
+    eta, alpha = 1.0 / L, lam / L
+    setup.release()
+    plan = DevicePlan(scn, dtype=w.dtype, device=dev, z_range=zr, max_batch=w.batch)
+    eng = SPGMEngine(plan, y, eta, alpha, process_group=pg)
+    return w, plan, eng, eta, alpha, time.perf_counter() - t0
+
+
+def timed_steps(eng, plan, w, steps, warmup, pg, local, use_graph, clk=None):
+    """W untimed + K timed SPGM iterations (device sampler); CUDA events on the launching
+    stream, barrier + synchronize on both sides, max over ranks. Returns (ms, launches/step, K)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_00774_b200 import configs
+
+    seed, B = configs.SEEDS["minibatch"], w.batch
+    l0 = plan.info()["launches"]
+    eng.sample_device(seed, None, B)
+    eng.step_staged()
+    per_step = plan.info()["launches"] - l0
+    graph = eng.graph(seed, B, pairs=1) if use_graph else None
+
+    def run(n):
+        if graph is not None:
+            for _ in range((n + 1) // 2):
+                graph.replay()
+            return 2 * ((n + 1) // 2)
+        for _ in range(n):
+            eng.sample_device(seed, None, B)
+            eng.step_staged()
+        return n
+
+    run(max(warmup, 3))
+    torch.cuda.synchronize()
+    if pg is not None:
+        dist.barrier(device_ids=[local])
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clk is not None:
+        clk.__enter__()
+    e0.record(st)
+    done = run(steps)
+    e1.record(st)
+    torch.cuda.synchronize()
+    if clk is not None:
+        clk.__exit__()
+    if pg is not None:
+        dist.barrier(device_ids=[local])
+    ms = e0.elapsed_time(e1)
+    if pg is not None:
+        t = torch.tensor([ms], device=plan.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, per_step, done
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or args.force_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         pg = dist.group.WORLD
-    w = configs.WORKLOADS[args.workload]()
+    w, plan, eng, eta, alpha, setup_s = build_engine(args.workload, dev, rank, world, pg)
     scn = w.scenario
     B, N, M = w.batch, scn.n_voxels, scn.n_channels
-    nz = scn.voxels.dims[2]
-    zr = slab(nz, rank, world)
-
-    t_setup = time.perf_counter()
-    setup = ShardedSetup(scn, dtype=w.dtype, device=dev, z_range=zr, process_group=pg)
-    s_true = configs.make_scene(w)
-    clean = setup.forward_full(s_true)
-    y = configs.add_noise(clean, configs.noise_sigma(clean, w.snr_db))
-    L = setup.lipschitz(n_iters=20, rng_seed=configs.SEEDS["power"])
-    lam = 1e-3 * setup.max_abs_adjoint(y) / M
-    eta, alpha = 1.0 / L, lam / L
-    setup.release()
-    plan = DevicePlan(scn, dtype=w.dtype, device=dev, z_range=zr, max_batch=B)
-    eng = SPGMEngine(plan, y, eta, alpha, process_group=pg)
-    setup_s = time.perf_counter() - t_setup
-    seed = configs.SEEDS["minibatch"]
-
-    def step(k):
-        eng.sample_device(seed, k, B)
-        eng.step_staged()
-
-    def barrier():
-        if pg is not None:
-            dist.barrier(device_ids=[local])
-
-    launches0 = plan.info()["launches"]
-    for k in range(args.warmup):
-        step(k)
-    torch.cuda.synchronize()
-    launches_warm = plan.info()["launches"]
-    barrier()
-    torch.cuda.synchronize()
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(st)
-        for k in range(args.steps):
-            step(args.warmup + k)
-        e1.record(st)
-        torch.cuda.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1)
-    launches_timed = plan.info()["launches"] - launches_warm
-    if pg is not None:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    use_graph = pg is None and not args.no_graph
+    clk = ClockSampler(local)
+    ms, per_step, steps = timed_steps(eng, plan, w, args.steps, args.warmup, pg, local, use_graph, clk)
     change = eng.magnitude_change()
-    ms_step = ms / args.steps
-    entries_step = 2.0 * B * N
-    value = entries_step / (ms_step * 1e-3)
+    ms_step = ms / steps
+    value = 2.0 * B * N / (ms_step * 1e-3)
 
     # per-kernel timing of the two fused kernels (same stream, CUDA events, steady state)
-    kt = kernel_times(eng, plan, seed, args.warmup + args.steps, reps=max(5, min(args.steps, 20)))
+    from paper_2509_00774_b200 import configs
+
+    kt = kernel_times(eng, plan, configs.SEEDS["minibatch"], 10_000, reps=max(5, min(args.steps, 20)))
     if pg is not None:
         t = torch.tensor([kt["fwd_ms"], kt["adj_ms"]], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -283,10 +314,7 @@ def run_ours(args):
 
     # e2e: public-API semantics, host buffers: host-sampled indices (numpy, as the reference)
     # H2D each step, the termination statistic D2H each step
-    e2e = None
-    if not args.no_e2e:
-        e2e = e2e_run(eng, scn, B, N, args, pg, local)
-
+    e2e = None if args.no_e2e else e2e_run(eng, scn, B, N, args, pg, local)
     clocks = clk.summary()
     peak = SFU_ENTRY_PEAK_MEASURED
     dom = "adjoint_prox" if kt["adj_ms"] >= kt["fwd_ms"] else "forward"
@@ -310,19 +338,22 @@ def run_ours(args):
     out = None
     if rank == 0:
         out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "c64" if w.dtype == "c64" else "c128", "data": "synthetic",
+            "vs_baseline": None, "dtype": "c64" if w.dtype == "c64" else "c128",
+            "data": "synthetic (seeded scene/array/noise with the BASELINE shapes; no dataset)",
             "iters_per_s": 1e3 / ms_step,
             "config": {"workload": args.workload, "M": M, "N": N, "batch": B, "sampler": "device flat (Feistel)",
                        "parallelism": f"voxel-slab x{world}", "l2": "inputs larger than L2 (distance table "
                        f"{plan.info()['device_bytes'] / 2**30:.2f} GiB streamed per kernel)",
-                       "eta": eta, "alpha": alpha, "setup_s": setup_s},
-            "roofline": roof, "clocks": clocks, "gpu_launches": launches_timed,
+                       "cuda_graph": use_graph, "eta": eta, "alpha": alpha, "setup_s": setup_s},
+            "roofline": roof, "clocks": clocks, "gpu_launches": per_step * steps, "launches_per_step": per_step,
             "final_change": change,
         }
         if e2e is not None:
             out["e2e"] = e2e
+        if world == 1 and not args.no_extras and args.workload == "large":
+            out["extra_workloads"] = {"medium": medium_line(args, dev)}
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args.workload, 30, args.cpu_seconds)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
@@ -330,8 +361,17 @@ def run_ours(args):
     if pg is not None:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
-    del launches0
     return 0
+
+
+def medium_line(args, dev):
+    """BASELINE config 1 (Medium, |B| = 512, c64) on the same GPU: entries/s and iterations/s."""
+    w, plan, eng, eta, alpha, setup_s = build_engine("medium", dev, 0, 1, None)
+    ms, per_step, steps = timed_steps(eng, plan, w, 200, 10, None, 0, not args.no_graph)
+    N = w.scenario.n_voxels
+    return {"value": 2.0 * w.batch * N / (ms / steps * 1e-3), "unit": UNIT, "ms_per_step": ms / steps,
+            "iters_per_s": 1e3 * steps / ms, "steps": steps, "batch": w.batch, "N": N, "M": w.scenario.n_channels,
+            "frac_step": 2.0 * w.batch * N / (ms / steps * 1e-3) / SFU_ENTRY_PEAK_MEASURED, "cuda_graph": not args.no_graph}
 
 
 def kernel_times(eng, plan, seed, k0, reps):

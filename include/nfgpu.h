@@ -16,7 +16,7 @@
  *   nf_adjoint_prox       replaces  solver._gradient + soft_threshold +
  *                                   relative_magnitude_change (one SPGM step)  solver.py:181-183, 228-251, 287-289
  *   nf_sample_flat        replaces  host minibatch sampling (flat uniform w/o replacement; the
- *                                   structured Cartesian sampler solver.py:206-225 stays on the host)
+ *   nf_plan_set_iter                structured Cartesian sampler solver.py:206-225 stays on the host)
  *   nf_soft_threshold     replaces  solver.soft_threshold                      solver.py:228-241
  *   nf_magnitude_change   replaces  solver.relative_magnitude_change           solver.py:244-251
  *
@@ -95,9 +95,15 @@ int nf_adjoint_prox(nf_plan* plan, const void* r_dev, const void* ymeas_dev, con
                     void* s_out_dev, double eta_over_b, double alpha, double* stats_dev, void* stream);
 
 /* Device flat sampler: idx[j] = pi_{seed,iter}(j) for j < batch, where pi is a keyed
- * Feistel bijection of [0, M). Distinct by construction; unordered. */
+ * Feistel bijection of [0, M). Distinct by construction; unordered.
+ * iter == NF_ITER_DEVICE uses the plan's device-resident iteration counter and advances
+ * it by one, so a captured CUDA graph of SPGM steps draws a fresh batch on every replay. */
+#define NF_ITER_DEVICE 0xffffffffffffffffULL
 int nf_sample_flat(nf_plan* plan, uint64_t seed, uint64_t iter, int batch, int32_t* idx_dev,
                    void* stream);
+
+/* Set the plan's device iteration counter (stream-ordered). */
+int nf_plan_set_iter(nf_plan* plan, uint64_t iter, void* stream);
 
 /* Elementwise complex soft threshold over n values of the given dtype (v may alias out). */
 int nf_soft_threshold(int dtype, const void* v_dev, void* out_dev, int64_t n, double alpha,

@@ -62,6 +62,15 @@ namespace {
 #ifndef NFGPU_TBR
 #define NFGPU_TBR 16
 #endif
+#ifndef NFGPU_MINB_FWD
+#define NFGPU_MINB_FWD 1
+#endif
+#ifndef NFGPU_MINB_ADJ
+#define NFGPU_MINB_ADJ 1
+#endif
+#ifndef NFGPU_FWD_TREE
+#define NFGPU_FWD_TREE 0
+#endif
 constexpr int V = NFGPU_V;  // voxels per lane (consecutive in x)
 static_assert(V == 4 || V == 8, "V must be 4 or 8");
 constexpr int NP = V / 2;  // fp32x2 pairs per lane
@@ -251,6 +260,24 @@ __device__ __forceinline__ void scale_s(const DV& iR, const DV& sr, const DV& si
 }
 // forward: Σ_v iT·e^{-jθ}·ŝ over the lane's V voxels
 __device__ __forceinline__ float2 fwd_part(const FV& iT, const FV& c, const FV& s, const FV& shr, const FV& shi) {
+#if NFGPU_FWD_TREE
+  // per-pair products, then a pairwise tree (dependency depth 4 instead of 2·NP)
+  float2 pr[NP], pi[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const float2 a = mul2(iT.p[i], c.p[i]), b = mul2(iT.p[i], s.p[i]);
+    pr[i] = fma2(b, shi.p[i], mul2(a, shr.p[i]));
+    pi[i] = fma2(b, make_float2(-shr.p[i].x, -shr.p[i].y), mul2(a, shi.p[i]));
+  }
+#pragma unroll
+  for (int w = 1; w < NP; w <<= 1)
+#pragma unroll
+    for (int i = 0; i + w < NP; i += 2 * w) {
+      pr[i] = add2(pr[i], pr[i + w]);
+      pi[i] = add2(pi[i], pi[i + w]);
+    }
+  return make_float2(pr[0].x + pr[0].y, pi[0].x + pi[0].y);
+#else
   float2 pr = make_float2(0.f, 0.f), pi = make_float2(0.f, 0.f);
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
@@ -259,6 +286,7 @@ __device__ __forceinline__ float2 fwd_part(const FV& iT, const FV& c, const FV& 
     pi = fma2(b, make_float2(-shr.p[i].x, -shr.p[i].y), fma2(a, shi.p[i], pi));
   }
   return make_float2(pr.x + pr.y, pi.x + pi.y);
+#endif
 }
 __device__ __forceinline__ double2 fwd_part(const DV& iT, const DV& c, const DV& s, const DV& shr, const DV& shi) {
   double pr = 0, pi = 0;
@@ -496,15 +524,23 @@ __device__ __forceinline__ uint32_t feistel(uint32_t x, int hb, uint64_t key) {
   }
   return (l << hb) | r;
 }
-__global__ void sample_kernel(uint64_t key, int hb, int M, int B, int* __restrict__ idx) {
+__host__ __device__ __forceinline__ uint64_t sample_key(uint64_t seed, uint64_t iter) {
+  return (seed * 0x9E3779B97F4A7C15ULL) ^ (iter * 0xD1B54A32D192ED03ULL) ^ 0x2545F4914F6CDD1DULL;
+}
+// iter_dev != null: the iteration number is read from device memory (graph-capturable loop)
+__global__ void sample_kernel(uint64_t seed, uint64_t iter, const unsigned long long* __restrict__ iter_dev, int hb,
+                              int M, int B, int* __restrict__ idx) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= B) return;
+  const uint64_t key = sample_key(seed, iter_dev ? (uint64_t)*iter_dev : iter);
   uint32_t x = (uint32_t)j;
   do {
     x = feistel(x, hb, key);
   } while (x >= (uint32_t)M);
   idx[j] = (int)x;
 }
+__global__ void bump_kernel(unsigned long long* it) { *it += 1ULL; }
+__global__ void set_kernel(unsigned long long* it, unsigned long long v) { *it = v; }
 
 // ------------------------------------------------------------------ per-warp shared state
 template <typename Real>
@@ -704,7 +740,7 @@ __global__ void __launch_bounds__(256) resid_kernel(const int* __restrict__ sm, 
 }
 
 template <typename Real, bool PROX>
-__global__ void __launch_bounds__(ADJ_WARPS * 32) adj_kernel(AdjArgs<Real> a) {
+__global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(AdjArgs<Real> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
@@ -895,7 +931,7 @@ __host__ __device__ constexpr size_t fwd_warp_bytes(int Tg, int A) {
 // Chunks of one tile are adjacent units, so they run together and share the tile's table
 // rows in L2.
 template <typename Real>
-__global__ void __launch_bounds__(FWD_WARPS * 32) fwd_kernel(FwdArgs<Real> a) {
+__global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(FwdArgs<Real> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
@@ -1114,6 +1150,7 @@ struct nf_plan {
   void* d_gpart = nullptr;
   int* d_tilecnt = nullptr;
   double* d_stat_part = nullptr;
+  unsigned long long* d_iter = nullptr;
 };
 
 namespace {
@@ -1132,7 +1169,7 @@ void free_plan(nf_plan* p) {
   if (!p) return;
   void* ptrs[] = {p->d_ant,  p->d_kd,   p->d_kf,    p->d_pulse, p->d_tab,  p->d_D0,      p->d_pos_of_key,
                   p->d_cnt,  p->d_sm,   p->d_spos,  p->d_crec,  p->d_sf, p->d_wrec, p->d_dpart,   p->d_part,
-                  p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part};
+                  p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part, p->d_iter};
   for (void* q : ptrs) cudaFree(q);
   delete p;
 }
@@ -1335,6 +1372,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   ALLOC(p->d_gpart, 2 * rs * (size_t)p->adj_ch_cap * g.ntiles * TILE);
   ALLOC(p->d_tilecnt, sizeof(int) * (size_t)g.ntiles);
   ALLOC(p->d_stat_part, sizeof(double) * 4 * (size_t)g.ntiles);
+  ALLOC(p->d_iter, sizeof(unsigned long long));
 #undef ALLOC
   auto cp = [&](void* dst, const void* src, size_t n) -> int {
     cudaError_t e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
@@ -1349,7 +1387,8 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     return rc;
   }
   if (cudaMemset(p->d_pos_of_key, 0xff, sizeof(int) * (size_t)p->KS) != cudaSuccess ||
-      cudaMemset(p->d_tilecnt, 0, sizeof(int) * (size_t)g.ntiles) != cudaSuccess) {
+      cudaMemset(p->d_tilecnt, 0, sizeof(int) * (size_t)g.ntiles) != cudaSuccess ||
+      cudaMemset(p->d_iter, 0, sizeof(unsigned long long)) != cudaSuccess) {
     free_plan(p);
     return fail(NF_ERR_CUDA, "cudaMemset");
   }
@@ -1436,8 +1475,22 @@ int nf_sample_flat(nf_plan* p, uint64_t seed, uint64_t iter, int B, int32_t* idx
   if (B < 1 || B > p->M) return fail(NF_ERR_ARG, "batch must be in [1, M]");
   int bits = 2;
   while ((1LL << bits) < p->M) bits += 2;
-  const uint64_t key = (seed * 0x9E3779B97F4A7C15ULL) ^ (iter * 0xD1B54A32D192ED03ULL) ^ 0x2545F4914F6CDD1DULL;
-  sample_kernel<<<(B + 255) / 256, 256, 0, (cudaStream_t)stream>>>(key, bits / 2, p->M, B, idx);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool dev = iter == NF_ITER_DEVICE;
+  sample_kernel<<<(B + 255) / 256, 256, 0, st>>>(seed, iter, dev ? p->d_iter : nullptr, bits / 2, p->M, B, idx);
+  CUDA_TRY(cudaGetLastError());
+  p->launches += 1;
+  if (dev) {
+    bump_kernel<<<1, 1, 0, st>>>(p->d_iter);
+    CUDA_TRY(cudaGetLastError());
+    p->launches += 1;
+  }
+  return NF_OK;
+}
+
+int nf_plan_set_iter(nf_plan* p, uint64_t iter, void* stream) {
+  if (!p) return fail(NF_ERR_ARG, "null argument");
+  set_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(p->d_iter, (unsigned long long)iter);
   CUDA_TRY(cudaGetLastError());
   p->launches += 1;
   return NF_OK;

@@ -165,13 +165,19 @@ class DevicePlan:
             "nf_adjoint_prox",
         )
 
-    def sample_flat(self, seed: int, it: int, batch: int, out: torch.Tensor) -> torch.Tensor:
+    def sample_flat(self, seed: int, it: int | None, batch: int, out: torch.Tensor) -> torch.Tensor:
+        """Flat batch for iteration ``it``; ``it=None`` uses (and advances) the plan's device
+        iteration counter, so the call can be captured in a CUDA graph."""
+        itv = _lib.NF_ITER_DEVICE if it is None else int(it)
         _lib.check(
-            self.lib.nf_sample_flat(self._h, int(seed) & (2**64 - 1), int(it), int(batch), _ptr(out),
+            self.lib.nf_sample_flat(self._h, int(seed) & (2**64 - 1), itv, int(batch), _ptr(out),
                                     _stream(self.device)),
             "nf_sample_flat",
         )
         return out
+
+    def set_iter(self, it: int) -> None:
+        _lib.check(self.lib.nf_plan_set_iter(self._h, int(it), _stream(self.device)), "nf_plan_set_iter")
 
 
 def soft_threshold_dev(v: torch.Tensor, alpha: float, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -328,9 +328,27 @@ class SPGMEngine:
         self.plan.prepare(t)
         return int(t.numel())
 
-    def sample_device(self, seed: int, it: int, batch: int) -> None:
+    def sample_device(self, seed: int, it: int | None, batch: int) -> None:
+        """Device flat sampler; ``it=None`` uses the plan's device iteration counter."""
         self.plan.sample_flat(seed, it, batch, self.idx_dev)
         self.plan.prepare(self.idx_dev[:batch])
+
+    def graph(self, seed: int, batch: int, pairs: int = 1):
+        """Capture ``2·pairs`` device-sampled SPGM iterations in one CUDA graph (an even count,
+        so the iterate ends in the buffer it started in). Replays draw fresh batches from the
+        plan's device iteration counter. Single-GPU only (the slab all-reduce is not captured)."""
+        if self.pg is not None:
+            raise RuntimeError("graph capture is single-GPU only")
+        # one eager step outside capture so every kernel attribute is set
+        self.sample_device(seed, None, batch)
+        self.step_staged()
+        torch.cuda.synchronize(self.plan.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(2 * pairs):
+                self.sample_device(seed, None, batch)
+                self.step_staged()
+        return g
 
     def step_staged(self) -> None:
         """One iteration on the staged batch: forward, [allreduce], adjoint+prox, swap."""

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Build tuning variants of libnfgpu.so into tools/variants/ (name:flags pairs).
+# Build tuning variants of libnfgpu.so into tools/variants/.
 set -e
 cd "$(dirname "$0")/.."
 rm -rf tools/variants; mkdir -p tools/variants
@@ -8,13 +8,10 @@ build() {
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
        -diag-suppress 177,550 "$@" -o tools/variants/libnfgpu_$name.so paper_2509_00774_b200/csrc/nfgpu.cu &
 }
-build v8tg4u2t16 -DNFGPU_TG=4 -DNFGPU_TBR=16
-build v8tg4u2t8 -DNFGPU_TG=4 -DNFGPU_TBR=8
-build v8tg3u2t8 -DNFGPU_TG=3 -DNFGPU_TBR=8
-build v8tg3u2t8w2 -DNFGPU_TG=3 -DNFGPU_TBR=8 -DNFGPU_FWD_WARPS=2 -DNFGPU_ADJ_WARPS=2
-build v8tg4u2t8w1 -DNFGPU_TG=4 -DNFGPU_TBR=8 -DNFGPU_FWD_WARPS=1 -DNFGPU_ADJ_WARPS=1
-build v8tg5u2t8 -DNFGPU_TG=5 -DNFGPU_TBR=8
-build v4tg6u2t16 -DNFGPU_V=4 -DNFGPU_TG=6 -DNFGPU_TBR=16
-build v8tg4u4t16 -DNFGPU_TG=4 -DNFGPU_UNROLL=4
+build base_tree0 -DNFGPU_FWD_TREE=0
+build tree1
+build tree1_mb5 -DNFGPU_MINB_FWD=4 -DNFGPU_MINB_ADJ=5
+build tree1_mb6 -DNFGPU_MINB_FWD=5 -DNFGPU_MINB_ADJ=6
+build tree1_t8tg3_mb5 -DNFGPU_TBR=8 -DNFGPU_TG=3 -DNFGPU_MINB_FWD=5 -DNFGPU_MINB_ADJ=5
 wait
-ls tools/variants
+for f in tools/variants/*.so; do echo $f; done
