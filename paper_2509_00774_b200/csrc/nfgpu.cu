@@ -66,7 +66,7 @@ namespace {
 #define NFGPU_MINB_FWD 1
 #endif
 #ifndef NFGPU_MINB_ADJ
-#define NFGPU_MINB_ADJ 1
+#define NFGPU_MINB_ADJ 4
 #endif
 #ifndef NFGPU_FWD_TREE
 #define NFGPU_FWD_TREE 0
@@ -1206,6 +1206,8 @@ template <typename Real>
 int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const size_t sm = fwd_smem(p);
   CUDA_TRY(cudaFuncSetAttribute(fwd_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CUDA_TRY(cudaFuncSetAttribute(fwd_kernel<Real>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
   for (int w0 = 0; w0 < p->B; w0 += p->fwd_chunk) {
     const int w1 = std::min(p->B, w0 + p->fwd_chunk);
     const int span = w1 - w0;
@@ -1222,7 +1224,9 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     const long long units = (long long)p->g.ntiles * a.Q;
     fwd_kernel<Real><<<(unsigned)((units + FWD_WARPS - 1) / FWD_WARPS), FWD_WARPS * 32, sm, st>>>(a);
     CUDA_TRY(cudaGetLastError());
-    const int nseg = std::max(1, std::min(p->fwd_gridx, RED_THREADS / span));
+    // two-level reduce: ~sqrt(rows) segments so both levels have short serial sums
+    int nseg = (int)std::ceil(std::sqrt((double)p->fwd_gridx));
+    nseg = std::max(1, std::min({nseg, p->fwd_gridx, std::max(1, RED_THREADS / span)}));
     fwd_reduce1_kernel<Real><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const Real*)p->d_part, p->fwd_gridx,
                                                                              span, nseg, p->d_tmp);
     CUDA_TRY(cudaGetLastError());
@@ -1243,6 +1247,8 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   CUDA_TRY(cudaGetLastError());
   const size_t sm = adj_smem(p);
   CUDA_TRY(cudaFuncSetAttribute(adj_kernel<Real, PROX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CUDA_TRY(cudaFuncSetAttribute(adj_kernel<Real, PROX>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
   AdjArgs<Real> a;
   a.g = p->g;
   a.tab = (const Real*)p->d_tab;
