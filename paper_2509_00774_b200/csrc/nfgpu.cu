@@ -60,10 +60,10 @@ namespace {
 #define NFGPU_ADJ_WARPS 4
 #endif
 #ifndef NFGPU_TBR
-#define NFGPU_TBR 16
+#define NFGPU_TBR 8
 #endif
 #ifndef NFGPU_MINB_FWD
-#define NFGPU_MINB_FWD 1
+#define NFGPU_MINB_FWD 4
 #endif
 #ifndef NFGPU_MINB_ADJ
 #define NFGPU_MINB_ADJ 4
@@ -553,16 +553,16 @@ struct WarpSmem {
 };
 __host__ __device__ constexpr int d0_slots(int A) { return (A + 1) & ~1; }  // keep 16-byte alignment
 template <typename Real>
-__host__ __device__ constexpr size_t warp_smem_bytes(int Tg, int A) {
-  return (size_t)(Tg + 2) * TABW * sizeof(Real) + (size_t)d0_slots(A) * sizeof(double) + 34 * sizeof(R4<Real>) +
-         34 * sizeof(int2);
+__host__ __device__ constexpr size_t warp_smem_bytes(int Tg, int A, int nslots = 2) {
+  return (size_t)(Tg + nslots) * TABW * sizeof(Real) + (size_t)d0_slots(A) * sizeof(double) +
+         34 * sizeof(R4<Real>) + 34 * sizeof(int2);
 }
 template <typename Real>
-__device__ __forceinline__ WarpSmem<Real> carve(unsigned char* base, int Tg, int A) {
+__device__ __forceinline__ WarpSmem<Real> carve(unsigned char* base, int Tg, int A, int nslots = 2) {
   WarpSmem<Real> ws;
   ws.tside = reinterpret_cast<Real*>(base);
   ws.rslot = ws.tside + (size_t)Tg * TABW;
-  ws.d0 = reinterpret_cast<double*>(base + (size_t)(Tg + 2) * TABW * sizeof(Real));
+  ws.d0 = reinterpret_cast<double*>(base + (size_t)(Tg + nslots) * TABW * sizeof(Real));
   ws.rec = reinterpret_cast<R4<Real>*>(reinterpret_cast<unsigned char*>(ws.d0) + d0_slots(A) * sizeof(double));
   ws.rect = reinterpret_cast<int2*>(ws.rec + 34);
   return ws;
@@ -922,7 +922,22 @@ struct FwdArgs {
 
 template <typename Real>
 __host__ __device__ constexpr size_t fwd_warp_bytes(int Tg, int A) {
-  return warp_smem_bytes<Real>(Tg, A) + (size_t)TBR * 33 * sizeof(R2<Real>);
+  return warp_smem_bytes<Real>(Tg, A, 1) + (size_t)TBR * 33 * sizeof(R2<Real>);
+}
+
+// Forward variant with ONE staging slot: read the prefetched rows, and defer the prefetch
+// of the next receiver until the rows have been consumed by arithmetic (caller issues
+// stage_rx after the run's first entry). This keeps the slot free of write-after-read races.
+template <typename Real>
+__device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __restrict__ tabt,
+                                                  const WarpSmem<Real>& ws, int rr, int& pf_r, int L, QV<Real>& dR,
+                                                  QV<Real>& iR) {
+  stage_wait();
+  const Real* src = rr == pf_r ? ws.rslot + L * (16 / (int)sizeof(Real))
+                               : tabt + (size_t)(g.T + rr) * TABW + L * (16 / (int)sizeof(Real));
+  dR = ldv(src);
+  iR = ldv(src + TILE);
+  pf_r = rr + 1 < g.R ? rr + 1 : 0;
 }
 
 // Forward: a warp owns (tile, channel chunk) like the adjoint. Per channel, each lane forms
@@ -939,8 +954,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   if (unit >= g.ntiles * a.Q) return;  // warps are independent: no block barriers
   const int tile = unit / a.Q, chunk = unit - tile * a.Q;
   unsigned char* wbase = smem_raw + (size_t)w * fwd_warp_bytes<Real>(g.Tg, g.A);
-  const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A);
-  R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A));  // [TBR][33]
+  const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A, 1);
+  R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A, 1));  // [TBR][33]
 
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
@@ -972,7 +987,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   zero(iR);
   zero(shr);
   zero(shi);
-  int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
+  int cur_tg = -1, pf_r = -1, carry = -1;
+  bool stage_pending = false;
   ChanRec nxt;
   R2<Real> nxtw;
   prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
@@ -992,8 +1008,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
             load_tgroup<Real>(g, tabt, ws.tside, tg, L);
             cur_tg = tg;
           }
-          rx_run_rows<Real>(g, tabt, ws, rr, pf_r, rslot, L, dR, iR);
+          rx_run_rows_1slot<Real>(g, tabt, ws, rr, pf_r, L, dR, iR);
           scale_s(iR, sr, si, shr, shi);
+          stage_pending = true;
         }
         R4<Real> q = ws.rec[c];
         int off = ws.rect[c].x;
@@ -1004,6 +1021,10 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
           QV<Real> cs, sn;
           phasorv(q.x, q.y, dT, dR, cs, sn);
+          if (stage_pending) {  // dR/iR are consumed: refill the single slot for the next run
+            stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
+            stage_pending = false;
+          }
           tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi);
           q = qn;
           off = offn;
