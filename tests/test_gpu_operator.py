@@ -241,3 +241,44 @@ def test_simulate_measurements_noise_convention(small_scenario, rng):
     b = simulate_measurements(s, small_scenario, noise_sigma=0.5, rng_seed=9)
     c = simulate_measurements(s, small_scenario, noise_sigma=0.5, rng_seed=9)
     assert np.array_equal(b.values, c.values)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_microbenchmark_full_M_spot_check(dtype):
+    """BASELINE config 4 (operator microbenchmark): one forward and one adjoint at full
+    M = 64 Tx x 64 Rx x 256 f = 1,048,576 on the 64^3 grid, N(0,1) complex inputs; sampled
+    output rows / voxels against the table-free oracle (precision study: c64 and c128)."""
+    scn = configs.micro_scenario("64^3")
+    geo = O.geom_from_scenario(scn)
+    rng = np.random.default_rng(11)
+    dt = np.complex64 if dtype == "c64" else np.complex128
+    s = rc(rng, scn.n_voxels).astype(dt).astype(np.complex128)
+    r = rc(rng, scn.n_channels).astype(dt).astype(np.complex128)
+    plan = DevicePlan(scn, dtype=dtype)
+    plan.prepare(torch.arange(scn.n_channels, dtype=torch.int32, device=plan.device))
+    y = plan.forward(plan._as_dev(s, scn.n_voxels, "s")).to(torch.complex128).cpu().numpy()
+    rows = np.sort(rng.choice(scn.n_channels, 16, replace=False))
+    assert rel_l2(y[rows], O.direct_forward(geo, s, rows, chunk=32768)) <= TOL[dtype]
+    g = plan.adjoint(plan._as_dev(r, scn.n_channels, "r")).to(torch.complex128).cpu().numpy()
+    vox = np.sort(rng.choice(scn.n_voxels, 8, replace=False))
+    ref = np.concatenate([O.direct_adjoint(geo, r[a:a + 131072], np.arange(a, min(a + 131072, scn.n_channels)),
+                                           voxels=vox) for a in range(0, scn.n_channels, 131072)])
+    ref = ref.reshape(-1, vox.size).sum(axis=0)
+    assert rel_l2(g[vox], ref) <= TOL[dtype]
+
+
+def test_large_batch_paths_agree():
+    """|B| = M (ISTA) on Medium goes through the chunked forward window and the chunked adjoint;
+    its result equals the concatenation of smaller batches (forward) and their sum (adjoint)."""
+    scn = configs.medium_scenario()
+    rng = np.random.default_rng(12)
+    s = rc(rng, scn.n_voxels)
+    M = scn.n_channels
+    y_full = forward_apply(s, scn, dtype="c64")
+    parts = [forward_apply(s, scn, subset=np.arange(a, min(a + 4096, M)), dtype="c64") for a in range(0, M, 4096)]
+    assert np.array_equal(np.concatenate(parts), y_full)  # subset restriction is bit-exact
+    r = rc(rng, M)
+    g_full = adjoint_apply(r, scn, dtype="c64")
+    g_sum = sum(adjoint_apply(r[a:a + 4096], scn, subset=np.arange(a, min(a + 4096, M)), dtype="c64")
+                for a in range(0, M, 4096))
+    assert rel_l2(g_full, g_sum) <= 1e-5
