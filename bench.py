@@ -296,7 +296,7 @@ def run_ours(args):
     w, plan, eng, eta, alpha, setup_s = build_engine(args.workload, dev, rank, world, pg)
     scn = w.scenario
     B, N, M = w.batch, scn.n_voxels, scn.n_channels
-    use_graph = pg is None and not args.no_graph
+    use_graph = not args.no_graph
     clk = ClockSampler(local)
     ms, per_step, steps = timed_steps(eng, plan, w, args.steps, args.warmup, pg, local, use_graph, clk)
     change = eng.magnitude_change()

@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -1147,6 +1148,8 @@ struct nf_plan {
   int fwd_gridx;
   int fwd_chunk;
   int adj_ch_cap;
+  long long fwd_target = 148LL * 16 * 4;  // warp work units per forward launch (env NFGPU_FWD_TARGET)
+  long long adj_target = 148LL * 16 * 4;  // warp work units per adjoint launch (env NFGPU_ADJ_TARGET)
   size_t dev_bytes = 0;
   int64_t launches = 0;
   int KS, ksblocks;
@@ -1208,16 +1211,16 @@ size_t adj_smem(const nf_plan* p) {
 }
 
 int channel_splits(const nf_plan* p, int span) {
-  // enough (tile, chunk) warp units for ~6 rounds of 16 warps/SM; >= 64 channels per chunk
-  const long long target = 148LL * 16 * 6;
+  // enough (tile, chunk) warp units for the target number of units; >= 64 channels per chunk
+  const long long target = p->fwd_target;
   long long q = (target + p->g.ntiles - 1) / p->g.ntiles;
   q = std::min<long long>(q, std::max(1, span / 64));
   return (int)std::max(1LL, q);
 }
 
 int adjoint_chunks(const nf_plan* p) {
-  // enough (tile, chunk) units for ~8 rounds of 16 warps/SM; at least 64 channels per chunk
-  long long ch = (148LL * 16 * 8 + p->g.ntiles - 1) / p->g.ntiles;
+  // enough (tile, chunk) units for the target number of units; at least 64 channels per chunk
+  long long ch = (p->adj_target + p->g.ntiles - 1) / p->g.ntiles;
   ch = std::min<long long>(ch, std::max(1, p->B / 64));
   ch = std::min<long long>(ch, p->adj_ch_cap);
   return (int)std::max(1LL, ch);
@@ -1352,6 +1355,8 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   p->KS = g.ng * g.R * g.Tg * g.F;
   p->ksblocks = (p->KS + 1023) / 1024;
   p->fwd_gridx = g.ntiles;  // rows of the forward partial buffer (one per tile)
+  if (const char* e = std::getenv("NFGPU_FWD_TARGET")) p->fwd_target = std::max(1LL, std::atoll(e));
+  if (const char* e = std::getenv("NFGPU_ADJ_TARGET")) p->adj_target = std::max(1LL, std::atoll(e));
   const size_t rs = real_size(p);
   {
     // bound the forward partial buffer to ~512 MB

@@ -336,10 +336,9 @@ class SPGMEngine:
     def graph(self, seed: int, batch: int, pairs: int = 1):
         """Capture ``2·pairs`` device-sampled SPGM iterations in one CUDA graph (an even count,
         so the iterate ends in the buffer it started in). Replays draw fresh batches from the
-        plan's device iteration counter. Single-GPU only (the slab all-reduce is not captured)."""
-        if self.pg is not None:
-            raise RuntimeError("graph capture is single-GPU only")
-        # one eager step outside capture so every kernel attribute is set
+        plan's device iteration counter. With a process group the NCCL all-reduce of the
+        forward partials is captured into the graph as well."""
+        # one eager step outside capture so every kernel attribute is set (and NCCL is warm)
         self.sample_device(seed, None, batch)
         self.step_staged()
         torch.cuda.synchronize(self.plan.device)

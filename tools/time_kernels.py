@@ -21,13 +21,16 @@ from paper_2509_00774_b200.solver import SPGMEngine  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="large")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--zslab", type=int, default=0, help="time one rank's slab: the first Z z-planes (0 = all)")
 a = ap.parse_args()
 w = configs.WORKLOADS[a.workload]()
 scn = w.scenario
 rng = np.random.default_rng(0)
 y = (rng.standard_normal(scn.n_channels) + 1j * rng.standard_normal(scn.n_channels)).astype(np.complex64)
-plan = DevicePlan(scn, dtype=w.dtype, device="cuda:0", max_batch=w.batch)
-eng = SPGMEngine(plan, y, eta=1e-2, alpha=1e-6, initial=configs.make_scene(w))
+zr = (0, a.zslab) if a.zslab else None
+plan = DevicePlan(scn, dtype=w.dtype, device="cuda:0", max_batch=w.batch, z_range=zr)
+s0 = configs.make_scene(w)[plan.vox_offset:plan.vox_offset + plan.n_local]
+eng = SPGMEngine(plan, y, eta=1e-2, alpha=1e-6, initial=s0)
 st = torch.cuda.current_stream()
 f_ms, a_ms = [], []
 for i in range(a.reps + 3):
@@ -44,8 +47,9 @@ for i in range(a.reps + 3):
     if i >= 3:
         f_ms.append(e0.elapsed_time(e1))
         a_ms.append(e1.elapsed_time(e2))
-entries = w.batch * scn.n_voxels
+entries = w.batch * plan.n_local
 fm, am = float(np.median(f_ms)), float(np.median(a_ms))
-print(json.dumps({"lib": os.environ.get("NFGPU_LIB", "default"), "workload": a.workload, "fwd_ms": fm, "adj_ms": am,
+print(json.dumps({"lib": os.environ.get("NFGPU_LIB", "default"), "workload": a.workload, "zslab": a.zslab,
+                  "fwd_ms": fm, "adj_ms": am,
                   "fwd_Gentry_s": entries / fm / 1e6, "adj_Gentry_s": entries / am / 1e6,
                   "step_Gentry_s": 2 * entries / (fm + am) / 1e6}))
