@@ -72,6 +72,9 @@ namespace {
 #ifndef NFGPU_FWD_TREE
 #define NFGPU_FWD_TREE 0
 #endif
+#ifndef NFGPU_FWD_PAIR
+#define NFGPU_FWD_PAIR 1
+#endif
 constexpr int V = NFGPU_V;  // voxels per lane (consecutive in x)
 static_assert(V == 4 || V == 8, "V must be 4 or 8");
 constexpr int NP = V / 2;  // fp32x2 pairs per lane
@@ -1013,6 +1016,40 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           scale_s(iR, sr, si, shr, shi);
           stage_pending = true;
         }
+#if NFGPU_FWD_PAIR
+        // two channels per iteration, both results stored after both are computed, so the
+        // compiler can overlap their dependency chains (a store in between would be a barrier)
+        for (; c + 1 < e; c += 2) {
+          const R4<Real> q0 = ws.rec[c], q1 = ws.rec[c + 1];
+          const int o0 = ws.rect[c].x, o1 = ws.rect[c + 1].x;
+          const QV<Real> dT0 = ldv(tsl + o0), iT0 = ldv(tsl + o0 + TILE);
+          const QV<Real> dT1 = ldv(tsl + o1), iT1 = ldv(tsl + o1 + TILE);
+          QV<Real> cs0, sn0, cs1, sn1;
+          phasorv(q0.x, q0.y, dT0, dR, cs0, sn0);
+          phasorv(q1.x, q1.y, dT1, dR, cs1, sn1);
+          if (stage_pending) {  // dR/iR are consumed: refill the single slot for the next run
+            stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
+            stage_pending = false;
+          }
+          const R2<Real> p0 = fwd_part(iT0, cs0, sn0, shr, shi);
+          const R2<Real> p1 = fwd_part(iT1, cs1, sn1, shr, shi);
+          tb[(c - h0) * 33 + L] = p0;
+          tb[(c + 1 - h0) * 33 + L] = p1;
+        }
+        if (c < e) {
+          const R4<Real> q = ws.rec[c];
+          const int off = ws.rect[c].x;
+          const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
+          QV<Real> cs, sn;
+          phasorv(q.x, q.y, dT, dR, cs, sn);
+          if (stage_pending) {
+            stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
+            stage_pending = false;
+          }
+          tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi);
+          ++c;
+        }
+#else
         R4<Real> q = ws.rec[c];
         int off = ws.rect[c].x;
 #pragma unroll UNROLL
@@ -1030,6 +1067,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           q = qn;
           off = offn;
         }
+#endif
       }
       __syncwarp();
       // transpose-reduce: 32/TBR lanes per row each sum a 32/(32/TBR) slice of row L % TBR,
