@@ -75,6 +75,9 @@ namespace {
 #ifndef NFGPU_FWD_PAIR
 #define NFGPU_FWD_PAIR 1
 #endif
+#ifndef NFGPU_EXACT_REDUCE
+#define NFGPU_EXACT_REDUCE 1
+#endif
 constexpr int V = NFGPU_V;  // voxels per lane (consecutive in x)
 static_assert(V == 4 || V == 8, "V must be 4 or 8");
 constexpr int NP = V / 2;  // fp32x2 pairs per lane
@@ -91,6 +94,7 @@ constexpr int A_MAX = 256;     // antennas (T + R) per plan
 constexpr int RED_THREADS = 300000;
 constexpr unsigned FULL = 0xffffffffu;
 constexpr double PI = 3.14159265358979323846;
+constexpr double EXACT_FREE_REV = 12.0;  // largest |phase| (revolutions) fed to MUFU unreduced
 
 thread_local std::string g_err;
 
@@ -191,17 +195,24 @@ __device__ __forceinline__ DV make_v(const double* x) {
 
 // cos/sin(2π·x_v), x_v = base + k·(dT_v + dR_v), reduced exactly to [-½, ½] revolutions
 // (magic-number round-to-nearest, exact for |x| < 2^22) before MUFU.SIN/COS.
+//
+// EXACT = false (the plan picks it when |x| <= 12 rev is guaranteed): skip the
+// explicit reduction and let MUFU.SIN/COS reduce the revolution count. This costs ~1e-6 relative
+// precision and saves 3 packed FADDs per voxel pair.
+template <bool EXACT>
 __device__ __forceinline__ void phasorv(float k, float base, const FV& dT, const FV& dR, FV& c, FV& s) {
   const float2 M2 = bc(12582912.0f);
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
     const float2 x = fma2(bc(k), add2(dT.p[i], dR.p[i]), bc(base));
-    const float2 f = sub2(x, sub2(add2(x, M2), M2));
+    float2 f = x;
+    if (EXACT && NFGPU_EXACT_REDUCE) f = sub2(x, sub2(add2(x, M2), M2));
     const float2 r = mul2(f, bc(6.28318530717958647692f));
     __sincosf(r.x, &s.p[i].x, &c.p[i].x);
     __sincosf(r.y, &s.p[i].y, &c.p[i].y);
   }
 }
+template <bool EXACT>
 __device__ __forceinline__ void phasorv(double k, double base, const DV& dT, const DV& dR, DV& c, DV& s) {
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -743,7 +754,7 @@ __global__ void __launch_bounds__(256) resid_kernel(const int* __restrict__ sm, 
   }
 }
 
-template <typename Real, bool PROX>
+template <typename Real, bool PROX, bool EXACT>
 __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(AdjArgs<Real> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
@@ -797,7 +808,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
         const int offn = ws.rect[c + 1].x;
         const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
         QV<Real> cs, sn;
-        phasorv(q.x, q.y, dT, dR, cs, sn);
+        phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
         adj_acc(iT, cs, sn, q.z, q.w, hr, hi);
         q = qn;
         off = offn;
@@ -949,7 +960,7 @@ __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __re
 // 32 lanes in a fixed order, and the tile's per-channel sum goes to part[tile][j].
 // Chunks of one tile are adjacent units, so they run together and share the tile's table
 // rows in L2.
-template <typename Real>
+template <typename Real, bool EXACT>
 __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(FwdArgs<Real> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
@@ -1025,8 +1036,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const QV<Real> dT0 = ldv(tsl + o0), iT0 = ldv(tsl + o0 + TILE);
           const QV<Real> dT1 = ldv(tsl + o1), iT1 = ldv(tsl + o1 + TILE);
           QV<Real> cs0, sn0, cs1, sn1;
-          phasorv(q0.x, q0.y, dT0, dR, cs0, sn0);
-          phasorv(q1.x, q1.y, dT1, dR, cs1, sn1);
+          phasorv<EXACT>(q0.x, q0.y, dT0, dR, cs0, sn0);
+          phasorv<EXACT>(q1.x, q1.y, dT1, dR, cs1, sn1);
           if (stage_pending) {  // dR/iR are consumed: refill the single slot for the next run
             stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
             stage_pending = false;
@@ -1041,7 +1052,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const int off = ws.rect[c].x;
           const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
           QV<Real> cs, sn;
-          phasorv(q.x, q.y, dT, dR, cs, sn);
+          phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
           if (stage_pending) {
             stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
             stage_pending = false;
@@ -1058,7 +1069,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const int offn = ws.rect[c + 1].x;
           const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
           QV<Real> cs, sn;
-          phasorv(q.x, q.y, dT, dR, cs, sn);
+          phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
           if (stage_pending) {  // dR/iR are consumed: refill the single slot for the next run
             stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
             stage_pending = false;
@@ -1186,6 +1197,8 @@ struct nf_plan {
   int fwd_gridx;
   int fwd_chunk;
   int adj_ch_cap;
+  bool exact = true;  // explicit phase reduction (false when |x| <= EXACT_FREE_REV is guaranteed)
+  double phase_bound_rev = 0;
   long long fwd_target = 148LL * 16 * 4;  // warp work units per forward launch (env NFGPU_FWD_TARGET)
   long long adj_target = 148LL * 16 * 4;  // warp work units per adjoint launch (env NFGPU_ADJ_TARGET)
   size_t dev_bytes = 0;
@@ -1267,9 +1280,9 @@ int adjoint_chunks(const nf_plan* p) {
 template <typename Real>
 int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const size_t sm = fwd_smem(p);
-  CUDA_TRY(cudaFuncSetAttribute(fwd_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  CUDA_TRY(cudaFuncSetAttribute(fwd_kernel<Real>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                cudaSharedmemCarveoutMaxShared));
+  auto kern = p->exact ? fwd_kernel<Real, true> : fwd_kernel<Real, false>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   for (int w0 = 0; w0 < p->B; w0 += p->fwd_chunk) {
     const int w1 = std::min(p->B, w0 + p->fwd_chunk);
     const int span = w1 - w0;
@@ -1284,7 +1297,7 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.Q = channel_splits(p, span);
     a.part = (Real*)p->d_part;
     const long long units = (long long)p->g.ntiles * a.Q;
-    fwd_kernel<Real><<<(unsigned)((units + FWD_WARPS - 1) / FWD_WARPS), FWD_WARPS * 32, sm, st>>>(a);
+    kern<<<(unsigned)((units + FWD_WARPS - 1) / FWD_WARPS), FWD_WARPS * 32, sm, st>>>(a);
     CUDA_TRY(cudaGetLastError());
     // two-level reduce: ~sqrt(rows) segments so both levels have short serial sums
     int nseg = (int)std::ceil(std::sqrt((double)p->fwd_gridx));
@@ -1308,9 +1321,9 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
                                             (const Real*)ymeas, p->d_pulse, (R2<Real>*)p->d_wrec, p->d_dpart);
   CUDA_TRY(cudaGetLastError());
   const size_t sm = adj_smem(p);
-  CUDA_TRY(cudaFuncSetAttribute(adj_kernel<Real, PROX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  CUDA_TRY(cudaFuncSetAttribute(adj_kernel<Real, PROX>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                cudaSharedmemCarveoutMaxShared));
+  auto kern = p->exact ? adj_kernel<Real, PROX, true> : adj_kernel<Real, PROX, false>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   AdjArgs<Real> a;
   a.g = p->g;
   a.tab = (const Real*)p->d_tab;
@@ -1329,7 +1342,7 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   a.alpha = alpha;
   a.stat_part = p->d_stat_part;
   const int units = p->g.ntiles * a.CH;
-  adj_kernel<Real, PROX><<<(units + ADJ_WARPS - 1) / ADJ_WARPS, ADJ_WARPS * 32, sm, st>>>(a);
+  kern<<<(units + ADJ_WARPS - 1) / ADJ_WARPS, ADJ_WARPS * 32, sm, st>>>(a);
   CUDA_TRY(cudaGetLastError());
   p->launches += 2;
   if (PROX) {
@@ -1393,6 +1406,16 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   p->KS = g.ng * g.R * g.Tg * g.F;
   p->ksblocks = (p->KS + 1023) / 1024;
   p->fwd_gridx = g.ntiles;  // rows of the forward partial buffer (one per tile)
+  {
+    // |x| = |base + (f/c)(δT + δR)| <= 1/2 + (f_max/c) * 2 * (tile half-diagonal), since |δ| <= distance
+    // from the tile centre to the voxel (triangle inequality).
+    const double hx = 0.5 * (TILE_X - 1) * spacing[0], hy = 0.5 * (TILE_Y - 1) * spacing[1];
+    const double hz = 0.5 * (TILE_Z - 1) * spacing[2];
+    double fmax = 0;
+    for (int i = 0; i < n_f; ++i) fmax = std::max(fmax, std::fabs(freq_hz[i]));
+    p->phase_bound_rev = 0.5 + fmax / c * 2.0 * std::sqrt(hx * hx + hy * hy + hz * hz);
+    p->exact = dtype != NF_C64 || p->phase_bound_rev > EXACT_FREE_REV || std::getenv("NFGPU_FORCE_EXACT");
+  }
   if (const char* e = std::getenv("NFGPU_FWD_TARGET")) p->fwd_target = std::max(1LL, std::atoll(e));
   if (const char* e = std::getenv("NFGPU_ADJ_TARGET")) p->adj_target = std::max(1LL, std::atoll(e));
   const size_t rs = real_size(p);
