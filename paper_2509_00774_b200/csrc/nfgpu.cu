@@ -199,15 +199,16 @@ __device__ __forceinline__ DV make_v(const double* x) {
 // EXACT = false (the plan picks it when |x| <= 12 rev is guaranteed): skip the
 // explicit reduction and let MUFU.SIN/COS reduce the revolution count. This costs ~1e-6 relative
 // precision and saves 3 packed FADDs per voxel pair.
+// With EXACT = false the channel record already holds 2π·k and 2π·base (radians), so x is
+// the phase in radians and no scaling multiply is needed before __sincosf.
 template <bool EXACT>
 __device__ __forceinline__ void phasorv(float k, float base, const FV& dT, const FV& dR, FV& c, FV& s) {
   const float2 M2 = bc(12582912.0f);
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
     const float2 x = fma2(bc(k), add2(dT.p[i], dR.p[i]), bc(base));
-    float2 f = x;
-    if (EXACT && NFGPU_EXACT_REDUCE) f = sub2(x, sub2(add2(x, M2), M2));
-    const float2 r = mul2(f, bc(6.28318530717958647692f));
+    float2 r = x;
+    if (EXACT) r = mul2(sub2(x, sub2(add2(x, M2), M2)), bc(6.28318530717958647692f));
     __sincosf(r.x, &s.p[i].x, &c.p[i].x);
     __sincosf(r.y, &s.p[i].y, &c.p[i].y);
   }
@@ -642,7 +643,7 @@ __device__ __forceinline__ void load_tgroup(const Geo& g, const Real* __restrict
 // Build the 32 channel records of one batch (lane L <-> sorted position jb+L) from the
 // prefetched ChanRec/w in registers, and prefetch the next batch's. Returns the bitmask of
 // run starts (a run = maximal stretch with equal (rx, tx group)).
-template <typename Real>
+template <typename Real, bool EXACT>
 __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<Real>& ws,
                                                   const ChanRec* __restrict__ crec,
                                                   const R2<Real>* __restrict__ wrec, int jb, int nb, int jend,
@@ -658,11 +659,18 @@ __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<R
     const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = pk_tg(cr.pk);
     const double x = cr.kd * (ws.d0[t] + ws.d0[g.T + r]);
     R4<Real> q;
-    if constexpr (std::is_same<Real, float>::value)
-      q.x = cr.kf;
-    else
+    if constexpr (std::is_same<Real, float>::value) {
+      if (EXACT) {
+        q.x = cr.kf;
+        q.y = (float)(x - rint(x));
+      } else {  // radians: slope 2π f/c and offset 2π frac(...)
+        q.x = (float)(2.0 * PI * cr.kd);
+        q.y = (float)(2.0 * PI * (x - rint(x)));
+      }
+    } else {
       q.x = cr.kd;
-    q.y = (Real)(x - rint(x));
+      q.y = (Real)(x - rint(x));
+    }
     q.z = w.x;
     q.w = w.y;
     ws.rec[L] = q;
@@ -785,7 +793,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
 
   for (int jb = j0; jb < j1; jb += 32) {
     const int nb = min(32, j1 - jb);
-    const unsigned starts = build_records<Real>(g, ws, a.crec, a.wrec, jb, nb, j1, L, carry, nxt, nxtw);
+    const unsigned starts = build_records<Real, EXACT>(g, ws, a.crec, a.wrec, jb, nb, j1, L, carry, nxt, nxtw);
     int c = 0;
     while (c < nb) {
       const int e = run_end(starts, c, nb);
@@ -1009,7 +1017,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
   for (int jb = c0; jb < c1; jb += 32) {
     const int nb = min(32, c1 - jb);
-    const unsigned starts = build_records<Real>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
+    const unsigned starts = build_records<Real, EXACT>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
     // sub-batches of TBR channels share one [TBR][33] transpose buffer
     for (int h0 = 0; h0 < nb; h0 += TBR) {
       const int h1 = min(nb, h0 + TBR);
