@@ -333,7 +333,7 @@ def run_ours(args):
         "frac_forward": per_launch / (kt["fwd_ms"] * 1e-3) / peak,
         "frac_adjoint_prox": per_launch / (kt["adj_ms"] * 1e-3) / peak,
         "frac_step": value / (world * peak),
-        "traffic": None,
+        "traffic": ncu_traffic(dom),
     }
     out = None
     if rank == 0:
@@ -372,6 +372,21 @@ def medium_line(args, dev):
     return {"value": 2.0 * w.batch * N / (ms / steps * 1e-3), "unit": UNIT, "ms_per_step": ms / steps,
             "iters_per_s": 1e3 * steps / ms, "steps": steps, "batch": w.batch, "N": N, "M": w.scenario.n_channels,
             "frac_step": 2.0 * w.batch * N / (ms / steps * 1e-3) / SFU_ENTRY_PEAK_MEASURED, "cuda_graph": not args.no_graph}
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/*_ncu_summary.json; ncu's numbers, not measured by this run), or None."""
+    files = sorted((ROOT / "profiles").glob("r*_ncu_summary.json"))
+    if not files:
+        return None
+    try:
+        d = json.load(open(files[-1]))
+        key = next(k for k in d if k.startswith("fwd_kernel" if kernel == "forward" else "adj_kernel<float, 1"))
+        b = d[key]["dram__bytes_read.sum"] + d[key]["dram__bytes_write.sum"]  # base units (bytes)
+        return {"bytes_per_launch": b, "source": files[-1].name, "unit": "B"}
+    except Exception:
+        return None
 
 
 def kernel_times(eng, plan, seed, k0, reps):

@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""Regenerate profiles/<round>_ncu_summary.json and the measured tables of
+"""Regenerate profiles/<round>_ncu_summary.json (base units: bytes, ns, cycles/s) and the measured tables of
 profiles/<round>_summary.md from the committed bench JSON lines, the peaks JSON, the launch
 list and an ncu --set full report (read here with `ncu -i`; the .ncu-rep itself is scratch).
 
@@ -25,7 +25,8 @@ STALLS = ["wait", "short_scoreboard", "long_scoreboard", "math_pipe_throttle", "
 
 
 def ncu_summary(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"], capture_output=True,
+                         text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     h = rows[0]
     out = {}
