@@ -611,33 +611,36 @@ __device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;"
 template <typename Real>
 __device__ __forceinline__ void rx_run_rows(const Geo& g, const Real* __restrict__ tabt, const WarpSmem<Real>& ws,
                                             int rr, int& pf_r, int& slot, int L, QV<Real>& dR, QV<Real>& iR) {
-  stage_wait();
-  if (rr == pf_r) {
-    const Real* sl = ws.rslot + (size_t)slot * TABW + L * (16 / (int)sizeof(Real));
-    dR = ldv(sl);
-    iR = ldv(sl + TILE);
-  } else {
-    const Real* src = tabt + (size_t)(g.T + rr) * TABW + L * (16 / (int)sizeof(Real));
-    dR = ldv(src);
-    iR = ldv(src + TILE);
+  if (rr != pf_r) {  // not prefetched: drain any stale prefetch into this slot, then stage rr
+    stage_wait();
+    stage_rx<Real>(g, tabt, rr, ws.rslot + (size_t)slot * TABW, L);
   }
+  stage_wait();
+  __syncwarp();  // a tx-group copy issued at this run start is complete for every lane
+  const Real* sl = ws.rslot + (size_t)slot * TABW + L * (16 / (int)sizeof(Real));
+  dR = ldv(sl);
+  iR = ldv(sl + TILE);
   slot ^= 1;
   pf_r = rr + 1 < g.R ? rr + 1 : 0;
   stage_rx<Real>(g, tabt, pf_r, ws.rslot + (size_t)slot * TABW, L);
 }
 
-// Copy the tx-side table rows of tx group tg for this tile into the warp's smem.
+// Start copying the tx-side table rows of tx group tg for this tile into the warp's smem
+// (cp.async, no wait). The caller's stage_wait() + __syncwarp() completes it, overlapped
+// with the rx-row staging of the same run start.
 template <typename Real>
-__device__ __forceinline__ void load_tgroup(const Geo& g, const Real* __restrict__ tabt, Real* tside, int tg,
-                                            int L) {
+__device__ __forceinline__ void load_tgroup_async(const Geo& g, const Real* __restrict__ tabt, Real* tside, int tg,
+                                                  int L) {
   const int ta = tg * g.Tg;
   const int nt = min(g.Tg, g.T - ta);
-  const float4* src = reinterpret_cast<const float4*>(tabt + (size_t)ta * TABW);
-  float4* dst = reinterpret_cast<float4*>(tside);
+  const char* src = reinterpret_cast<const char*>(tabt + (size_t)ta * TABW);
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(tside);
   const int n = nt * TABW * (int)sizeof(Real) / 16;
-  __syncwarp();
-  for (int i = L; i < n; i += 32) dst[i] = src[i];
-  __syncwarp();
+  __syncwarp();  // every lane is done reading the previous group
+  for (int i = L; i < n; i += 32)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(src + 16 * (size_t)i)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 // Build the 32 channel records of one batch (lane L <-> sorted position jb+L) from the
@@ -773,6 +776,9 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   const WarpSmem<Real> ws = carve<Real>(smem_raw + (size_t)w * warp_smem_bytes<Real>(g.Tg, g.A), g.Tg, g.A);
   const int j0 = (int)(((long long)a.B * chunk) / a.CH);
   const int j1 = (int)(((long long)a.B * (chunk + 1)) / a.CH);
+  ChanRec nxt;  // start-up loads issued together: first channel records, then the D0 row
+  R2<Real> nxtw;
+  prefetch_first<Real>(a.crec, a.wrec, j0, j1, L, nxt, nxtw);
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
   __syncwarp();
@@ -787,9 +793,6 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   zero(dR);
   zero(iR);
   int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
-  ChanRec nxt;
-  R2<Real> nxtw;
-  prefetch_first<Real>(a.crec, a.wrec, j0, j1, L, nxt, nxtw);
 
   for (int jb = j0; jb < j1; jb += 32) {
     const int nb = min(32, j1 - jb);
@@ -801,7 +804,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
         const int key = ws.rect[c].y;
         const int rr = key & 0xffff, tg = key >> 16;
         if (tg != cur_tg) {
-          load_tgroup<Real>(g, tabt, ws.tside, tg, L);
+          load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
           cur_tg = tg;
         }
         flush(iR, hr, hi, gr, gi);
@@ -955,9 +958,13 @@ template <typename Real>
 __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __restrict__ tabt,
                                                   const WarpSmem<Real>& ws, int rr, int& pf_r, int L, QV<Real>& dR,
                                                   QV<Real>& iR) {
+  if (rr != pf_r) {  // not prefetched: drain any stale prefetch into the slot, then stage rr
+    stage_wait();
+    stage_rx<Real>(g, tabt, rr, ws.rslot, L);
+  }
   stage_wait();
-  const Real* src = rr == pf_r ? ws.rslot + L * (16 / (int)sizeof(Real))
-                               : tabt + (size_t)(g.T + rr) * TABW + L * (16 / (int)sizeof(Real));
+  __syncwarp();  // a tx-group copy issued at this run start is complete for every lane
+  const Real* src = ws.rslot + L * (16 / (int)sizeof(Real));
   dR = ldv(src);
   iR = ldv(src + TILE);
   pf_r = rr + 1 < g.R ? rr + 1 : 0;
@@ -980,10 +987,14 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A, 1);
   R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A, 1));  // [TBR][33]
 
-  for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
-  for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
-  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
-  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
+  // start-up loads issued together: first channel records, the lane's s values, the D0 row
+  const int span = a.w1 - a.w0;
+  const int c0 = a.w0 + (int)(((long long)span * chunk) / a.Q);
+  const int c1 = a.w0 + (int)(((long long)span * (chunk + 1)) / a.Q);
+  R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * span - a.w0;
+  ChanRec nxt;
+  R2<Real> nxtw;
+  prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
   int tx, ty, tz;
   tile_coords(g, tile, tx, ty, tz);
   int x0, y, z;
@@ -997,13 +1008,12 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
     srv[v] = ok ? a.s[2 * n] : Real(0);
     siv[v] = ok ? a.s[2 * n + 1] : Real(0);
   }
+  for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
+  for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
+  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
   const QV<Real> sr = make_v(srv), si = make_v(siv);
   __syncwarp();
-
-  const int span = a.w1 - a.w0;
-  const int c0 = a.w0 + (int)(((long long)span * chunk) / a.Q);
-  const int c1 = a.w0 + (int)(((long long)span * (chunk + 1)) / a.Q);
-  R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * span - a.w0;
 
   QV<Real> dR, iR, shr, shi;
   zero(dR);
@@ -1012,9 +1022,6 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   zero(shi);
   int cur_tg = -1, pf_r = -1, carry = -1;
   bool stage_pending = false;
-  ChanRec nxt;
-  R2<Real> nxtw;
-  prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
   for (int jb = c0; jb < c1; jb += 32) {
     const int nb = min(32, c1 - jb);
     const unsigned starts = build_records<Real, EXACT>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
@@ -1028,7 +1035,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const int key = ws.rect[c].y;
           const int rr = key & 0xffff, tg = key >> 16;
           if (tg != cur_tg) {
-            load_tgroup<Real>(g, tabt, ws.tside, tg, L);
+            load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
             cur_tg = tg;
           }
           rx_run_rows_1slot<Real>(g, tabt, ws, rr, pf_r, L, dR, iR);
