@@ -18,11 +18,9 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 

@@ -36,6 +36,7 @@ from .forward import (
     MeasurementSet,
     ReflectivityVolume,
     _subset_indices,
+    _volume_values,
     adjoint_values,
     default_dtype,
     forward_values,
@@ -151,6 +152,13 @@ class SolverConfig:
             self.flat_batch = int(self.flat_batch)
         if int(self.check_every) < 1:
             raise ValueError("check_every must be >= 1")
+        if self.sampler == "device" and self.composition is not None:
+            raise ValueError("sampler='device' draws flat batches; use flat_batch, not composition")
+        if self.sampler == "table":
+            if self.index_table is None:
+                raise ValueError("sampler='table' needs index_table")
+            if len(self.index_table) < self.max_iters:
+                raise ValueError("index_table has fewer rows than max_iters")
 
 
 @dataclass
@@ -217,8 +225,6 @@ def _gradient(s, yv, scenario, idx, dtype=None) -> np.ndarray:
 
 def data_fidelity(s, y, scenario: ImagingScenario, subset=None, threads: int = 1, *, dtype=None) -> float:
     """(1/B) Σ ½|A_sub s − y_sub|² (solver.py:172-178)."""
-    from .forward import _volume_values
-
     yv = _measurement_values(y, scenario)
     idx = _subset_or_all(subset, scenario)
     _subset_indices(idx, scenario)
@@ -257,16 +263,12 @@ def sample_flat(scenario: ImagingScenario, batch: int, rng) -> np.ndarray:
     return np.sort(rng.choice(scenario.n_channels, batch, replace=False)).astype(np.int64)
 
 
-def _device_or_default():
-    return require_cuda(None)
-
-
 def soft_threshold(v, alpha: float) -> np.ndarray:
     """v·max(|v|−α, 0)/|v|; magnitudes ≤ α map to exactly 0 (solver.py:228-241)."""
     if not (math.isfinite(alpha) and alpha >= 0):
         raise ValueError(f"alpha must be >= 0, got {alpha}")
     arr = np.asarray(v, dtype=np.complex128)
-    dev = _device_or_default()
+    dev = require_cuda(None)
     out = soft_threshold_dev(torch.from_numpy(np.ascontiguousarray(arr).ravel()).to(dev), alpha)
     return out.cpu().numpy().reshape(arr.shape)
 
@@ -277,7 +279,7 @@ def relative_magnitude_change(s_prev, s_next) -> float:
     b = np.asarray(s_next)
     if a.shape != b.shape:
         raise ValueError(f"iterate shapes differ: {a.shape} vs {b.shape}")
-    dev = _device_or_default()
+    dev = require_cuda(None)
     ta = torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128).ravel()).to(dev)
     tb = torch.from_numpy(np.ascontiguousarray(b, dtype=np.complex128).ravel()).to(dev)
     st = magnitude_change_dev(ta, tb).cpu().numpy()
@@ -294,9 +296,10 @@ def check_termination(s_prev, s_next, tol: float) -> bool:
 class SPGMEngine:
     """GPU-resident SPGM state for one voxel slab.
 
-    ``step(idx)`` enqueues one full iteration without synchronising. With a
-    process group the forward partial sums over voxel slabs are all-reduced
-    (one NCCL all-reduce of 2·B reals) before the adjoint.
+    ``stage(idx)`` / ``sample_device(...)`` stage a batch and ``step_staged()`` enqueues one
+    full iteration without synchronising. With a process group the forward partial sums
+    over voxel slabs are all-reduced (one NCCL all-reduce of 2·B reals)
+    before the adjoint.
     """
 
     def __init__(self, plan: DevicePlan, y: np.ndarray | torch.Tensor, eta: float, alpha: float,
@@ -384,7 +387,6 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
     termination = TERMINATION_MAX_ITERS
     iterations = 0
     staged_full = False
-    pending: list[tuple[int, float, int]] = []
 
     t_start = time.perf_counter()
     for k in range(1, config.max_iters + 1):
@@ -395,7 +397,7 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
                 staged_full = True
             B = m
         elif config.sampler == "device":
-            B = config.flat_batch or (config.composition.batch_size if config.composition else m)
+            B = config.flat_batch
             eng.sample_device(config.rng_seed, k, B)
         elif config.sampler == "table":
             B = eng.stage(np.asarray(config.index_table[k - 1]))
@@ -419,7 +421,6 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
         if config.time_budget_s is not None and time.perf_counter() - t_start > config.time_budget_s:
             termination = TERMINATION_TIME_BUDGET
             break
-    del pending
     vol = eng.volume()
     wall = time.perf_counter() - t_start
     return SolveReport(
@@ -446,6 +447,9 @@ def spgm_solve(y, scenario: ImagingScenario, config: SolverConfig | None = None,
     config = config or SolverConfig()
     if config.composition is None and config.flat_batch is None and config.sampler != "table":
         raise ValueError("spgm_solve requires config.composition")
+    if config.sampler == "table":
+        for row in config.index_table[: config.max_iters]:
+            _subset_indices(ChannelSubset(np.asarray(row)).indices, scenario)
     if config.composition is not None:
         config.composition.validate_for(scenario)
     if config.flat_batch is not None and config.flat_batch > scenario.n_channels:
