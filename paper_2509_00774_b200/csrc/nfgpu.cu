@@ -643,6 +643,15 @@ __device__ __forceinline__ void load_tgroup_async(const Geo& g, const Real* __re
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+template <typename Real>
+__device__ __forceinline__ Real int_bits(int v);
+template <>
+__device__ __forceinline__ float int_bits<float>(int v) { return __int_as_float(v); }
+template <>
+__device__ __forceinline__ double int_bits<double>(int v) { return __longlong_as_double((long long)v); }
+__device__ __forceinline__ int bits_int(float v) { return __float_as_int(v); }
+__device__ __forceinline__ int bits_int(double v) { return (int)__double_as_longlong(v); }
+
 // Build the 32 channel records of one batch (lane L <-> sorted position jb+L) from the
 // prefetched ChanRec/w in registers, and prefetch the next batch's. Returns the bitmask of
 // run starts (a run = maximal stretch with equal (rx, tx group)).
@@ -674,8 +683,13 @@ __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<R
       q.x = cr.kd;
       q.y = (Real)(x - rint(x));
     }
-    q.z = w.x;
-    q.w = w.y;
+    if (wrec) {
+      q.z = w.x;
+      q.w = w.y;
+    } else {  // forward: the tx-row offset rides in .z as a bit pattern (one broadcast load per channel)
+      q.z = int_bits<Real>((t - tg * g.Tg) * TABW);
+      q.w = 0;
+    }
     ws.rec[L] = q;
     key = r | (tg << 16);
     ws.rect[L] = make_int2((t - tg * g.Tg) * TABW, key);
@@ -1047,7 +1061,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
         // compiler can overlap their dependency chains (a store in between would be a barrier)
         for (; c + 1 < e; c += 2) {
           const R4<Real> q0 = ws.rec[c], q1 = ws.rec[c + 1];
-          const int o0 = ws.rect[c].x, o1 = ws.rect[c + 1].x;
+          const int o0 = bits_int(q0.z), o1 = bits_int(q1.z);
           const QV<Real> dT0 = ldv(tsl + o0), iT0 = ldv(tsl + o0 + TILE);
           const QV<Real> dT1 = ldv(tsl + o1), iT1 = ldv(tsl + o1 + TILE);
           QV<Real> cs0, sn0, cs1, sn1;
@@ -1064,7 +1078,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
         }
         if (c < e) {
           const R4<Real> q = ws.rec[c];
-          const int off = ws.rect[c].x;
+          const int off = bits_int(q.z);
           const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
           QV<Real> cs, sn;
           phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
@@ -1106,8 +1120,12 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
 #pragma unroll 8
       for (int l = 0; l < SL; ++l) {
         const R2<Real> t = tb[row * 33 + part * SL + l];
-        S.x += t.x;
-        S.y += t.y;
+        if constexpr (std::is_same<Real, float>::value) {
+          S = add2(S, t);
+        } else {
+          S.x += t.x;
+          S.y += t.y;
+        }
       }
 #pragma unroll
       for (int o = 16; o >= TBR; o >>= 1) {
