@@ -11,6 +11,9 @@
  *                                   (phasor tables F×(T+R)×N are NOT built; a frequency-free
  *                                    per-(antenna, voxel) distance table is built instead)
  *   nf_batch_prepare      replaces  forward._subset_indices + _channel_groups  forward.py:227-258
+ *   nf_batch_prepare_structured  replaces the same for the Cartesian subsets that
+ *                                 solver.sample_minibatch draws (solver.py:205-225) and for the
+ *                                 full channel set (forward.py:233-236); separable fast path
  *   nf_forward            replaces  forward.forward_apply / _forward_values    forward.py:342-350, 268-289
  *   nf_adjoint            replaces  forward.adjoint_apply / _adjoint_values    forward.py:353-359, 292-336
  *   nf_adjoint_prox       replaces  solver._gradient + soft_threshold +
@@ -77,6 +80,15 @@ int nf_plan_info(const nf_plan* plan, int64_t info[8]);
  * distinct, 0 <= m < M). Sorts it into the kernels' work order on the device. The staged
  * batch is used by every following forward/adjoint call until the next prepare. */
 int nf_batch_prepare(nf_plan* plan, const int32_t* idx_dev, int batch, void* stream);
+
+/* Stage the structured subset Fs × Ts × Rs (HOST int32 lists, each strictly increasing and
+ * in range; validated here). Its channels m = r + R(t + T f) in lexicographic (f, t, r) order,
+ * which is ascending m, form the subset order (batch = nf·nt·nr). The kernels then use the
+ * factorisation A[(f,t,r), n] = p_f/(4π)·U_ft(n)·V_fr(n): n_t + n_r phasors per
+ * (frequency, voxel) instead of n_t·n_r, and complex multiply-adds for the contraction.
+ * Results equal nf_batch_prepare on the same channel list to within rounding. */
+int nf_batch_prepare_structured(nf_plan* plan, const int32_t* fs, int nf, const int32_t* ts, int nt,
+                                const int32_t* rs, int nr, void* stream);
 
 /* y[k] = sum_{n in slab} A[m_k, n] s[n] for the staged batch, k in subset order. */
 int nf_forward(nf_plan* plan, const void* s_dev, void* y_dev, void* stream);

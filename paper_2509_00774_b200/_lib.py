@@ -32,6 +32,7 @@ SIGNATURES = {
     "nf_plan_destroy": (_I, [_P]),
     "nf_plan_info": (_I, [_P, ctypes.POINTER(ctypes.c_int64)]),
     "nf_batch_prepare": (_I, [_P, _P, _I, _P]),
+    "nf_batch_prepare_structured": (_I, [_P, _IP, _I, _IP, _I, _IP, _I, _P]),
     "nf_forward": (_I, [_P, _P, _P, _P]),
     "nf_adjoint": (_I, [_P, _P, _P, _P, _D, _P]),
     "nf_adjoint_prox": (_I, [_P, _P, _P, _P, _P, _D, _D, _P, _P]),

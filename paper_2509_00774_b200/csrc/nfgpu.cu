@@ -779,71 +779,13 @@ __global__ void __launch_bounds__(256) resid_kernel(const int* __restrict__ sm, 
   }
 }
 
-template <typename Real, bool PROX, bool EXACT>
-__global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(AdjArgs<Real> a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// Adjoint epilogue shared by the flat and structured kernels: publish this (tile, chunk)
+// partial; the last of the tile's CH warps sums the partials in chunk order and writes
+// g (plain adjoint) or applies the prox and the termination statistics (SPGM step).
+template <typename Real, bool PROX>
+__device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, int chunk, int L, const QV<Real>& gr,
+                                             const QV<Real>& gi) {
   const Geo& g = a.g;
-  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int unit = blockIdx.x * ADJ_WARPS + w;
-  if (unit >= g.ntiles * a.CH) return;  // warps are independent: no block barriers below
-  const int tile = unit / a.CH, chunk = unit - tile * a.CH;
-  const WarpSmem<Real> ws = carve<Real>(smem_raw + (size_t)w * warp_smem_bytes<Real>(g.Tg, g.A), g.Tg, g.A);
-  const int j0 = (int)(((long long)a.B * chunk) / a.CH);
-  const int j1 = (int)(((long long)a.B * (chunk + 1)) / a.CH);
-  ChanRec nxt;  // start-up loads issued together: first channel records, then the D0 row
-  R2<Real> nxtw;
-  prefetch_first<Real>(a.crec, a.wrec, j0, j1, L, nxt, nxtw);
-  for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
-  for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
-  __syncwarp();
-  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
-  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
-
-  QV<Real> gr, gi, hr, hi, dR, iR;
-  zero(gr);
-  zero(gi);
-  zero(hr);
-  zero(hi);
-  zero(dR);
-  zero(iR);
-  int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
-
-  for (int jb = j0; jb < j1; jb += 32) {
-    const int nb = min(32, j1 - jb);
-    const unsigned starts = build_records<Real, EXACT>(g, ws, a.crec, a.wrec, jb, nb, j1, L, carry, nxt, nxtw);
-    int c = 0;
-    while (c < nb) {
-      const int e = run_end(starts, c, nb);
-      if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c
-        const int key = ws.rect[c].y;
-        const int rr = key & 0xffff, tg = key >> 16;
-        if (tg != cur_tg) {
-          load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
-          cur_tg = tg;
-        }
-        flush(iR, hr, hi, gr, gi);
-        rx_run_rows<Real>(g, tabt, ws, rr, pf_r, rslot, L, dR, iR);
-      }
-      // software pipeline: channel c+1's record loads while c computes
-      R4<Real> q = ws.rec[c];
-      int off = ws.rect[c].x;
-#pragma unroll UNROLL
-      for (; c < e; ++c) {
-        const R4<Real> qn = ws.rec[c + 1];
-        const int offn = ws.rect[c + 1].x;
-        const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
-        QV<Real> cs, sn;
-        phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
-        adj_acc(iT, cs, sn, q.z, q.w, hr, hi);
-        q = qn;
-        off = offn;
-      }
-    }
-    __syncwarp();
-  }
-  flush(iR, hr, hi, gr, gi);
-  stage_wait();
-
   Real Gr[V], Gi[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -921,6 +863,74 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
       a.stat_part[(size_t)tile * 4 + 3] = st3;
     }
   }
+}
+
+template <typename Real, bool PROX, bool EXACT>
+__global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(AdjArgs<Real> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geo& g = a.g;
+  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+  const int unit = blockIdx.x * ADJ_WARPS + w;
+  if (unit >= g.ntiles * a.CH) return;  // warps are independent: no block barriers below
+  const int tile = unit / a.CH, chunk = unit - tile * a.CH;
+  const WarpSmem<Real> ws = carve<Real>(smem_raw + (size_t)w * warp_smem_bytes<Real>(g.Tg, g.A), g.Tg, g.A);
+  const int j0 = (int)(((long long)a.B * chunk) / a.CH);
+  const int j1 = (int)(((long long)a.B * (chunk + 1)) / a.CH);
+  ChanRec nxt;  // start-up loads issued together: first channel records, then the D0 row
+  R2<Real> nxtw;
+  prefetch_first<Real>(a.crec, a.wrec, j0, j1, L, nxt, nxtw);
+  for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
+  for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
+  __syncwarp();
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
+  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
+
+  QV<Real> gr, gi, hr, hi, dR, iR;
+  zero(gr);
+  zero(gi);
+  zero(hr);
+  zero(hi);
+  zero(dR);
+  zero(iR);
+  int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
+
+  for (int jb = j0; jb < j1; jb += 32) {
+    const int nb = min(32, j1 - jb);
+    const unsigned starts = build_records<Real, EXACT>(g, ws, a.crec, a.wrec, jb, nb, j1, L, carry, nxt, nxtw);
+    int c = 0;
+    while (c < nb) {
+      const int e = run_end(starts, c, nb);
+      if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c
+        const int key = ws.rect[c].y;
+        const int rr = key & 0xffff, tg = key >> 16;
+        if (tg != cur_tg) {
+          load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
+          cur_tg = tg;
+        }
+        flush(iR, hr, hi, gr, gi);
+        rx_run_rows<Real>(g, tabt, ws, rr, pf_r, rslot, L, dR, iR);
+      }
+      // software pipeline: channel c+1's record loads while c computes
+      R4<Real> q = ws.rec[c];
+      int off = ws.rect[c].x;
+#pragma unroll UNROLL
+      for (; c < e; ++c) {
+        const R4<Real> qn = ws.rec[c + 1];
+        const int offn = ws.rect[c + 1].x;
+        const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
+        QV<Real> cs, sn;
+        phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
+        adj_acc(iT, cs, sn, q.z, q.w, hr, hi);
+        q = qn;
+        off = offn;
+      }
+    }
+    __syncwarp();
+  }
+  flush(iR, hr, hi, gr, gi);
+  stage_wait();
+
+  adj_epilogue<Real, PROX>(a, tile, chunk, L, gr, gi);
 }
 
 // stats = {Σ_tile part[.][0], Σ part[.][1], ½ Σ_block dpart, Σ part[.][3]} in a fixed order
@@ -1139,6 +1149,376 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   stage_wait();
 }
 
+// ------------------------------------------------------------------ structured (Cartesian) batches
+//
+// SURVEY.md §8(f) #2. A structured minibatch (solver.py:206-225, the reference's own sampler) is
+// Fs × Ts × Rs in lexicographic (f, t, r) order. Then
+//     A[(f,t,r), n] = p_f/(4π) · U_ft(n) · V_fr(n),   U = e^{-j2π(f/c) d_T}/d_T,  V = e^{-j2π(f/c) d_R}/d_R
+// so per frequency a voxel needs n_t + n_r phasors instead of n_t·n_r. The contraction over the
+// batch becomes complex multiply-adds on the FMA pipe: the adjoint computes
+// Σ_t conj(U_ft)·Σ_r conj(V_fr)·w_ftr, and the forward computes Σ_n U_ft·(V_fr·s) per (t, r).
+// Each warp owns (tile, frequency chunk). The rx factors of a block of RB receivers are staged
+// in shared memory once per frequency and reused by every transmitter.
+
+constexpr int RB = 8;  // receivers per staged block
+
+struct StructArgs {
+  const int* __restrict__ fs;
+  const int* __restrict__ ts;
+  const int* __restrict__ rs;
+  int nf, nt, nr;
+};
+
+template <typename Real>
+__host__ __device__ constexpr size_t struct_warp_bytes(int A) {
+  return (size_t)RB * 2 * TILE * sizeof(Real) + (size_t)d0_slots(A) * sizeof(double) +
+         (size_t)16 * 33 * sizeof(R2<Real>) + 16 * sizeof(int);
+}
+
+__device__ __forceinline__ void stv(float* p, const FV& q) {
+#pragma unroll
+  for (int i = 0; i < NP / 2; ++i)
+    *reinterpret_cast<float4*>(p + i * 128) = make_float4(q.p[2 * i].x, q.p[2 * i].y, q.p[2 * i + 1].x, q.p[2 * i + 1].y);
+}
+__device__ __forceinline__ void stv(double* p, const DV& q) {
+#pragma unroll
+  for (int i = 0; i < V / 2; ++i) *reinterpret_cast<double2*>(p + i * 64) = make_double2(q.v[2 * i], q.v[2 * i + 1]);
+}
+
+// One-sided phase parameters for antenna a at frequency f on this tile: slope k and offset b,
+// in revolutions (exact path, c128) or radians (fast c64 path), x = b + k·δ.
+template <typename Real, bool EXACT>
+__device__ __forceinline__ void side_params(double kd, double d0, Real& k, Real& b) {
+  const double x = kd * d0;
+  const double fr = x - rint(x);
+  if (std::is_same<Real, float>::value && !EXACT) {
+    k = (Real)(2.0 * PI * kd);
+    b = (Real)(2.0 * PI * fr);
+  } else {
+    k = (Real)kd;
+    b = (Real)fr;
+  }
+}
+
+// amplitude-weighted one-sided phasor: (re, im) = amp·(cos x, sgn·sin x)
+template <bool EXACT>
+__device__ __forceinline__ void side_phasor(float k, float b, const FV& d, const FV& amp, float sgn, FV& re, FV& im) {
+  const float2 M2 = bc(12582912.0f);
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const float2 x = fma2(bc(k), d.p[i], bc(b));
+    float2 r = x;
+    if (EXACT) r = mul2(sub2(x, sub2(add2(x, M2), M2)), bc(6.28318530717958647692f));
+    float2 c, sn;
+    __sincosf(r.x, &sn.x, &c.x);
+    __sincosf(r.y, &sn.y, &c.y);
+    re.p[i] = mul2(amp.p[i], c);
+    im.p[i] = mul2(amp.p[i], mul2(sn, bc(sgn)));
+  }
+}
+template <bool EXACT>
+__device__ __forceinline__ void side_phasor(double k, double b, const DV& d, const DV& amp, double sgn, DV& re, DV& im) {
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double x = fma(k, d.v[v], b);
+    double c, sn;
+    sincospi(2.0 * (x - rint(x)), &sn, &c);
+    re.v[v] = amp.v[v] * c;
+    im.v[v] = amp.v[v] * sgn * sn;
+  }
+}
+
+// z += v · w  (lane vector × complex scalar)
+__device__ __forceinline__ void cmac_s(const FV& vr, const FV& vi, float wr, float wi, FV& zr, FV& zi) {
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    zr.p[i] = fma2(vi.p[i], bc(-wi), fma2(vr.p[i], bc(wr), zr.p[i]));
+    zi.p[i] = fma2(vi.p[i], bc(wr), fma2(vr.p[i], bc(wi), zi.p[i]));
+  }
+}
+__device__ __forceinline__ void cmac_s(const DV& vr, const DV& vi, double wr, double wi, DV& zr, DV& zi) {
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    zr.v[v] = fma(-vi.v[v], wi, fma(vr.v[v], wr, zr.v[v]));
+    zi.v[v] = fma(vi.v[v], wr, fma(vr.v[v], wi, zi.v[v]));
+  }
+}
+// z += u · x  (elementwise complex lane vectors)
+__device__ __forceinline__ void cmac_v(const FV& ur, const FV& ui, const FV& xr, const FV& xi, FV& zr, FV& zi) {
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    zr.p[i] = fma2(ui.p[i], make_float2(-xi.p[i].x, -xi.p[i].y), fma2(ur.p[i], xr.p[i], zr.p[i]));
+    zi.p[i] = fma2(ui.p[i], xr.p[i], fma2(ur.p[i], xi.p[i], zi.p[i]));
+  }
+}
+__device__ __forceinline__ void cmac_v(const DV& ur, const DV& ui, const DV& xr, const DV& xi, DV& zr, DV& zi) {
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    zr.v[v] = fma(-ui.v[v], xi.v[v], fma(ur.v[v], xr.v[v], zr.v[v]));
+    zi.v[v] = fma(ui.v[v], xr.v[v], fma(ur.v[v], xi.v[v], zi.v[v]));
+  }
+}
+// Σ_v u·w over the lane's voxels (complex)
+__device__ __forceinline__ float2 cdot(const FV& ur, const FV& ui, const FV& wr, const FV& wi) {
+  float2 pr = make_float2(0.f, 0.f), pi = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    pr = fma2(ui.p[i], make_float2(-wi.p[i].x, -wi.p[i].y), fma2(ur.p[i], wr.p[i], pr));
+    pi = fma2(ui.p[i], wr.p[i], fma2(ur.p[i], wi.p[i], pi));
+  }
+  return make_float2(pr.x + pr.y, pi.x + pi.y);
+}
+__device__ __forceinline__ double2 cdot(const DV& ur, const DV& ui, const DV& wr, const DV& wi) {
+  double pr = 0, pi = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    pr = fma(-ui.v[v], wi.v[v], fma(ur.v[v], wr.v[v], pr));
+    pi = fma(ui.v[v], wr.v[v], fma(ur.v[v], wi.v[v], pi));
+  }
+  return make_double2(pr, pi);
+}
+
+// Rows u = fi·nt + ti of a structured batch; a unit owns the row range [u0, u1). Per frequency
+// it stages the rx factors of RB receivers at a time in shared memory, then walks its
+// transmitters two at a time so each shared-memory load feeds two transmitters.
+__device__ __forceinline__ void row_span(const StructArgs& sa, int u0, int u1, int fi, int& ta, int& tb) {
+  ta = max(u0, fi * sa.nt) - fi * sa.nt;
+  tb = min(u1, (fi + 1) * sa.nt) - fi * sa.nt;
+}
+
+// Structured adjoint (+prox): g = Σ_f Σ_t conj(U_ft)·Σ_r conj(V_fr)·w_ftr. Unit = (tile, row chunk).
+template <typename Real, bool PROX, bool EXACT>
+__global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_struct_kernel(AdjArgs<Real> a, StructArgs sa,
+                                                                                  const double* __restrict__ kd) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geo& g = a.g;
+  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+  const int unit = blockIdx.x * ADJ_WARPS + w;
+  if (unit >= g.ntiles * a.CH) return;
+  const int tile = unit / a.CH, chunk = unit - tile * a.CH;
+  unsigned char* wbase = smem_raw + (size_t)w * struct_warp_bytes<Real>(g.A);
+  Real* vb = reinterpret_cast<Real*>(wbase);  // [RB][re, im][TILE]
+  double* d0 = reinterpret_cast<double*>(wbase + (size_t)RB * 2 * TILE * sizeof(Real));
+  for (int i = L; i < g.A; i += 32) d0[i] = a.D0[(size_t)tile * g.A + i];
+  __syncwarp();
+  constexpr int QD = 16 / (int)sizeof(Real);
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW + L * QD;
+  Real* vbl = vb + L * QD;
+  const int rows = sa.nf * sa.nt;
+  const int u0 = (int)(((long long)rows * chunk) / a.CH), u1 = (int)(((long long)rows * (chunk + 1)) / a.CH);
+
+  QV<Real> gr, gi;
+  zero(gr);
+  zero(gi);
+  for (int fi = u0 / sa.nt; fi * sa.nt < u1; ++fi) {
+    int ta, tb;
+    row_span(sa, u0, u1, fi, ta, tb);
+    const double kf = kd[sa.fs[fi]];
+    for (int r0 = 0; r0 < sa.nr; r0 += RB) {
+      const int nrb = min(RB, sa.nr - r0);
+      __syncwarp();
+      for (int q = 0; q < nrb; ++q) {  // conj(V_fr) for the block, into shared memory
+        const Real* row = tabt + (size_t)(g.T + sa.rs[r0 + q]) * TABW;
+        Real k, b;
+        side_params<Real, EXACT>(kf, d0[g.T + sa.rs[r0 + q]], k, b);
+        QV<Real> re, im;
+        side_phasor<EXACT>(k, b, ldv(row), ldv(row + TILE), Real(1), re, im);
+        stv(vbl + (size_t)q * 2 * TILE, re);
+        stv(vbl + (size_t)q * 2 * TILE + TILE, im);
+      }
+      __syncwarp();
+      const R2<Real>* wf = a.wrec + ((size_t)fi * sa.nt) * sa.nr + r0;
+      int ti = ta;
+      for (; ti + 1 < tb; ti += 2) {  // transmitter pairs
+        QV<Real> z0r, z0i, z1r, z1i;
+        zero(z0r);
+        zero(z0i);
+        zero(z1r);
+        zero(z1i);
+        const R2<Real>* w0p = wf + (size_t)ti * sa.nr;
+        const R2<Real>* w1p = w0p + sa.nr;
+        for (int q = 0; q < nrb; ++q) {
+          const R2<Real> w0 = w0p[q], w1 = w1p[q];
+          const QV<Real> vr = ldv(vbl + (size_t)q * 2 * TILE), vi = ldv(vbl + (size_t)q * 2 * TILE + TILE);
+          cmac_s(vr, vi, w0.x, w0.y, z0r, z0i);
+          cmac_s(vr, vi, w1.x, w1.y, z1r, z1i);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int t = sa.ts[ti + h];
+          const Real* row = tabt + (size_t)t * TABW;
+          Real k, b;
+          side_params<Real, EXACT>(kf, d0[t], k, b);
+          QV<Real> ur, ui;
+          side_phasor<EXACT>(k, b, ldv(row), ldv(row + TILE), Real(1), ur, ui);
+          cmac_v(ur, ui, h ? z1r : z0r, h ? z1i : z0i, gr, gi);
+        }
+      }
+      if (ti < tb) {  // odd transmitter
+        QV<Real> zr, zi;
+        zero(zr);
+        zero(zi);
+        const R2<Real>* w0p = wf + (size_t)ti * sa.nr;
+        for (int q = 0; q < nrb; ++q) {
+          const R2<Real> w0 = w0p[q];
+          cmac_s(ldv(vbl + (size_t)q * 2 * TILE), ldv(vbl + (size_t)q * 2 * TILE + TILE), w0.x, w0.y, zr, zi);
+        }
+        const int t = sa.ts[ti];
+        const Real* row = tabt + (size_t)t * TABW;
+        Real k, b;
+        side_params<Real, EXACT>(kf, d0[t], k, b);
+        QV<Real> ur, ui;
+        side_phasor<EXACT>(k, b, ldv(row), ldv(row + TILE), Real(1), ur, ui);
+        cmac_v(ur, ui, zr, zi, gr, gi);
+      }
+    }
+  }
+  adj_epilogue<Real, PROX>(a, tile, chunk, L, gr, gi);
+}
+
+// Structured forward: y_ftr = p_f/(4π) Σ_n U_ft(n)·(V_fr(n) s_n). Per (t, r) each lane sums its
+// voxels; every 16 rows a transpose through shared memory reduces over the 32 lanes in a fixed
+// order and writes one partial per (tile, channel), which fwd_reduce1/2 finish.
+// The launch window is the row range [ua, ub) (channels [ua·nr, ub·nr)).
+template <typename Real, bool EXACT>
+__global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_struct_kernel(FwdArgs<Real> a, StructArgs sa,
+                                                                                  const double* __restrict__ kd) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geo& g = a.g;
+  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+  const int unit = blockIdx.x * FWD_WARPS + w;
+  if (unit >= g.ntiles * a.Q) return;
+  const int tile = unit / a.Q, chunk = unit - tile * a.Q;
+  unsigned char* wbase = smem_raw + (size_t)w * struct_warp_bytes<Real>(g.A);
+  Real* wb = reinterpret_cast<Real*>(wbase);  // [RB][re, im][TILE]: V_fr·s
+  double* d0 = reinterpret_cast<double*>(wbase + (size_t)RB * 2 * TILE * sizeof(Real));
+  R2<Real>* tbuf = reinterpret_cast<R2<Real>*>(reinterpret_cast<unsigned char*>(d0) + d0_slots(g.A) * sizeof(double));
+  int* jrow = reinterpret_cast<int*>(tbuf + 16 * 33);
+  for (int i = L; i < g.A; i += 32) d0[i] = a.D0[(size_t)tile * g.A + i];
+  constexpr int QD = 16 / (int)sizeof(Real);
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW + L * QD;
+  Real* wbl = wb + L * QD;
+  int tx, ty, tz;
+  tile_coords(g, tile, tx, ty, tz);
+  int x0, y, z;
+  lane_voxel(tx, ty, tz, L, x0, y, z);
+  Real srv[V], siv[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int x = x0 + v;
+    const bool ok = x < g.nx && y < g.ny && z < g.nzs;
+    const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
+    srv[v] = ok ? a.s[2 * n] : Real(0);
+    siv[v] = ok ? a.s[2 * n + 1] : Real(0);
+  }
+  const QV<Real> sr = make_v(srv), si = make_v(siv);
+  __syncwarp();
+  const int span = a.w1 - a.w0;
+  R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * span - a.w0;
+  const int ua = a.w0 / sa.nr, nrows = span / sa.nr;
+  const int u0 = ua + (int)(((long long)nrows * chunk) / a.Q), u1 = ua + (int)(((long long)nrows * (chunk + 1)) / a.Q);
+  int nrow = 0;
+
+  auto flush_rows = [&](int cnt) {
+    __syncwarp();
+    const int row = L & 15, half = L >> 4;
+    R2<Real> S;
+    S.x = 0;
+    S.y = 0;
+#pragma unroll 8
+    for (int l = 0; l < 16; ++l) {
+      const R2<Real> t = tbuf[row * 33 + half * 16 + l];
+      S.x += t.x;
+      S.y += t.y;
+    }
+    S.x += __shfl_down_sync(FULL, S.x, 16);
+    S.y += __shfl_down_sync(FULL, S.y, 16);
+    if (L < cnt) out[jrow[L]] = S;
+    __syncwarp();
+  };
+  auto emit = [&](const R2<Real>& v, int j) {
+    tbuf[nrow * 33 + L] = v;
+    if (L == 0) jrow[nrow] = j;
+    if (++nrow == 16) {
+      flush_rows(16);
+      nrow = 0;
+    }
+  };
+
+  for (int fi = u0 / sa.nt; fi * sa.nt < u1; ++fi) {
+    int ta, tb;
+    row_span(sa, u0, u1, fi, ta, tb);
+    const double kf = kd[sa.fs[fi]];
+    for (int r0 = 0; r0 < sa.nr; r0 += RB) {
+      const int nrb = min(RB, sa.nr - r0);
+      __syncwarp();
+      for (int q = 0; q < nrb; ++q) {  // W_fr = V_fr·s for the block, into shared memory
+        const Real* row = tabt + (size_t)(g.T + sa.rs[r0 + q]) * TABW;
+        Real k, b;
+        side_params<Real, EXACT>(kf, d0[g.T + sa.rs[r0 + q]], k, b);
+        QV<Real> vr, vi, wr, wi;
+        side_phasor<EXACT>(k, b, ldv(row), ldv(row + TILE), Real(-1), vr, vi);
+        zero(wr);
+        zero(wi);
+        cmac_v(vr, vi, sr, si, wr, wi);
+        stv(wbl + (size_t)q * 2 * TILE, wr);
+        stv(wbl + (size_t)q * 2 * TILE + TILE, wi);
+      }
+      __syncwarp();
+      const int jf = fi * sa.nt * sa.nr + r0;
+      int ti = ta;
+      for (; ti + 1 < tb; ti += 2) {  // transmitter pairs share each W load
+        QV<Real> u0r, u0i, u1r, u1i;
+        {
+          const int t = sa.ts[ti];
+          Real k, b;
+          side_params<Real, EXACT>(kf, d0[t], k, b);
+          side_phasor<EXACT>(k, b, ldv(tabt + (size_t)t * TABW), ldv(tabt + (size_t)t * TABW + TILE), Real(-1), u0r,
+                             u0i);
+        }
+        {
+          const int t = sa.ts[ti + 1];
+          Real k, b;
+          side_params<Real, EXACT>(kf, d0[t], k, b);
+          side_phasor<EXACT>(k, b, ldv(tabt + (size_t)t * TABW), ldv(tabt + (size_t)t * TABW + TILE), Real(-1), u1r,
+                             u1i);
+        }
+        for (int q = 0; q < nrb; ++q) {
+          const QV<Real> wr = ldv(wbl + (size_t)q * 2 * TILE), wi = ldv(wbl + (size_t)q * 2 * TILE + TILE);
+          const R2<Real> p0 = cdot(u0r, u0i, wr, wi), p1 = cdot(u1r, u1i, wr, wi);
+          emit(p0, jf + ti * sa.nr + q);
+          emit(p1, jf + (ti + 1) * sa.nr + q);
+        }
+      }
+      if (ti < tb) {
+        const int t = sa.ts[ti];
+        Real k, b;
+        side_params<Real, EXACT>(kf, d0[t], k, b);
+        QV<Real> ur, ui;
+        side_phasor<EXACT>(k, b, ldv(tabt + (size_t)t * TABW), ldv(tabt + (size_t)t * TABW + TILE), Real(-1), ur, ui);
+        for (int q = 0; q < nrb; ++q)
+          emit(cdot(ur, ui, ldv(wbl + (size_t)q * 2 * TILE), ldv(wbl + (size_t)q * 2 * TILE + TILE)),
+               jf + ti * sa.nr + q);
+      }
+    }
+  }
+  if (nrow) flush_rows(nrow);
+}
+
+// sorted-order bookkeeping of a structured batch: position j = (fi·nt + ti)·nr + ri is
+// both the work order and the subset order (ascending channel id)
+__global__ void struct_prep_kernel(StructArgs sa, int T, int R, int* __restrict__ sm, int* __restrict__ spos,
+                                   int* __restrict__ sf) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tr = sa.nt * sa.nr;
+  if (j >= sa.nf * tr) return;
+  const int fi = j / tr, rem = j - fi * tr, ti = rem / sa.nr, ri = rem - ti * sa.nr;
+  const int f = sa.fs[fi];
+  sm[j] = sa.rs[ri] + R * (sa.ts[ti] + T * f);
+  spos[j] = j;
+  sf[j] = f;
+}
+
 // level 1: tmp[seg][j] = Σ_{x in seg} part[x][j] (fp64, fixed order)
 template <typename Real>
 __global__ void fwd_reduce1_kernel(const Real* __restrict__ part, int nx, int span, int nseg,
@@ -1259,6 +1639,10 @@ struct nf_plan {
   int* d_tilecnt = nullptr;
   double* d_stat_part = nullptr;
   unsigned long long* d_iter = nullptr;
+  // structured (Cartesian) batch: sorted frequency / tx / rx index lists at fixed offsets [F | T | R]
+  bool structured = false;
+  int snf = 0, snt = 0, snr = 0;
+  int* d_struct = nullptr;
 };
 
 namespace {
@@ -1277,7 +1661,7 @@ void free_plan(nf_plan* p) {
   if (!p) return;
   void* ptrs[] = {p->d_ant,  p->d_kd,   p->d_kf,    p->d_pulse, p->d_tab,  p->d_D0,      p->d_pos_of_key,
                   p->d_cnt,  p->d_sm,   p->d_spos,  p->d_crec,  p->d_sf, p->d_wrec, p->d_dpart,   p->d_part,
-                  p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part, p->d_iter};
+                  p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part, p->d_iter, p->d_struct};
   for (void* q : ptrs) cudaFree(q);
   delete p;
 }
@@ -1346,6 +1730,66 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   return NF_OK;
 }
 
+StructArgs struct_args(const nf_plan* p) {
+  StructArgs sa;
+  sa.fs = p->d_struct;
+  sa.ts = p->d_struct + p->g.F;
+  sa.rs = p->d_struct + p->g.F + p->g.T;
+  sa.nf = p->snf;
+  sa.nt = p->snt;
+  sa.nr = p->snr;
+  return sa;
+}
+
+size_t struct_smem(const nf_plan* p, int warps) {
+  return warps * (p->dtype == NF_C64 ? struct_warp_bytes<float>(p->g.A) : struct_warp_bytes<double>(p->g.A));
+}
+
+// (f, t) rows per unit: enough units for the target, at least 4 rows each
+int struct_splits(long long target, int ntiles, int rows) {
+  long long q = (target + ntiles - 1) / ntiles;
+  q = std::min<long long>(q, std::max(1, rows / 4));
+  return (int)std::max(1LL, q);
+}
+
+template <typename Real>
+int launch_forward_struct(nf_plan* p, const void* s, void* y, cudaStream_t st) {
+  const size_t sm = struct_smem(p, FWD_WARPS);
+  auto kern = p->exact ? fwd_struct_kernel<Real, true> : fwd_struct_kernel<Real, false>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+  const StructArgs sa = struct_args(p);
+  const int rows = sa.nf * sa.nt;
+  const int win = std::max(1, p->fwd_chunk / sa.nr);  // rows per launch window (part buffer bound)
+  for (int ua = 0; ua < rows; ua += win) {
+    const int ub = std::min(rows, ua + win);
+    FwdArgs<Real> a;
+    a.g = p->g;
+    a.tab = (const Real*)p->d_tab;
+    a.D0 = p->d_D0;
+    a.crec = nullptr;
+    a.s = (const Real*)s;
+    a.w0 = ua * sa.nr;
+    a.w1 = ub * sa.nr;
+    const int span = a.w1 - a.w0;
+    a.Q = struct_splits(p->fwd_target, p->g.ntiles, ub - ua);
+    a.part = (Real*)p->d_part;
+    const long long units = (long long)p->g.ntiles * a.Q;
+    kern<<<(unsigned)((units + FWD_WARPS - 1) / FWD_WARPS), FWD_WARPS * 32, sm, st>>>(a, sa, p->d_kd);
+    CUDA_TRY(cudaGetLastError());
+    int nseg = (int)std::ceil(std::sqrt((double)p->fwd_gridx));
+    nseg = std::max(1, std::min({nseg, p->fwd_gridx, std::max(1, RED_THREADS / span)}));
+    fwd_reduce1_kernel<Real><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const Real*)p->d_part, p->fwd_gridx,
+                                                                             span, nseg, p->d_tmp);
+    CUDA_TRY(cudaGetLastError());
+    fwd_reduce2_kernel<Real><<<(span + 255) / 256, 256, 0, st>>>(p->d_tmp, span, nseg, a.w0, p->d_sf, p->d_spos,
+                                                                 p->d_pulse, (Real*)y);
+    CUDA_TRY(cudaGetLastError());
+    p->launches += 3;
+  }
+  return NF_OK;
+}
+
 template <typename Real, bool PROX>
 int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, double scale, const void* s_in,
                    void* s_out, double eta_over_b, double alpha, double* stats, cudaStream_t st) {
@@ -1353,10 +1797,6 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   resid_kernel<Real><<<nblk, 256, 0, st>>>(p->d_sm, p->d_spos, p->d_sf, p->B, (const Real*)r,
                                             (const Real*)ymeas, p->d_pulse, (R2<Real>*)p->d_wrec, p->d_dpart);
   CUDA_TRY(cudaGetLastError());
-  const size_t sm = adj_smem(p);
-  auto kern = p->exact ? adj_kernel<Real, PROX, true> : adj_kernel<Real, PROX, false>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   AdjArgs<Real> a;
   a.g = p->g;
   a.tab = (const Real*)p->d_tab;
@@ -1374,8 +1814,25 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   a.eta_over_b = eta_over_b;
   a.alpha = alpha;
   a.stat_part = p->d_stat_part;
-  const int units = p->g.ntiles * a.CH;
-  kern<<<(units + ADJ_WARPS - 1) / ADJ_WARPS, ADJ_WARPS * 32, sm, st>>>(a);
+  if (p->structured) {
+    const StructArgs sa = struct_args(p);
+    a.CH = std::min(struct_splits(p->adj_target, p->g.ntiles, sa.nf * sa.nt), p->adj_ch_cap);
+    const size_t sm = struct_smem(p, ADJ_WARPS);
+    auto kern = p->exact ? adj_struct_kernel<Real, PROX, true> : adj_struct_kernel<Real, PROX, false>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CUDA_TRY(
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    const int units = p->g.ntiles * a.CH;
+    kern<<<(units + ADJ_WARPS - 1) / ADJ_WARPS, ADJ_WARPS * 32, sm, st>>>(a, sa, p->d_kd);
+  } else {
+    const size_t sm = adj_smem(p);
+    auto kern = p->exact ? adj_kernel<Real, PROX, true> : adj_kernel<Real, PROX, false>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CUDA_TRY(
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    const int units = p->g.ntiles * a.CH;
+    kern<<<(units + ADJ_WARPS - 1) / ADJ_WARPS, ADJ_WARPS * 32, sm, st>>>(a);
+  }
   CUDA_TRY(cudaGetLastError());
   p->launches += 2;
   if (PROX) {
@@ -1499,6 +1956,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   ALLOC(p->d_tilecnt, sizeof(int) * (size_t)g.ntiles);
   ALLOC(p->d_stat_part, sizeof(double) * 4 * (size_t)g.ntiles);
   ALLOC(p->d_iter, sizeof(unsigned long long));
+  ALLOC(p->d_struct, sizeof(int) * (size_t)(n_f + n_tx + n_rx));
 #undef ALLOC
   auto cp = [&](void* dst, const void* src, size_t n) -> int {
     cudaError_t e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
@@ -1565,6 +2023,45 @@ int nf_batch_prepare(nf_plan* p, const int32_t* idx, int B, void* stream) {
   CUDA_TRY(cudaGetLastError());
   p->launches += 4;
   p->B = B;
+  p->structured = false;
+  return NF_OK;
+}
+
+int nf_batch_prepare_structured(nf_plan* p, const int32_t* fs, int nf, const int32_t* ts, int nt, const int32_t* rs,
+                                int nr, void* stream) {
+  if (!p || !fs || !ts || !rs) return fail(NF_ERR_ARG, "null argument");
+  const int lim[3] = {p->g.F, p->g.T, p->g.R};
+  const int cnt[3] = {nf, nt, nr};
+  const int32_t* lists[3] = {fs, ts, rs};
+  const char* names[3] = {"frequency", "tx", "rx"};
+  for (int k = 0; k < 3; ++k) {
+    if (cnt[k] < 1 || cnt[k] > lim[k])
+      return fail(NF_ERR_ARG, std::string(names[k]) + " count must be in [1, " + std::to_string(lim[k]) + "]");
+    for (int i = 0; i < cnt[k]; ++i) {
+      if (lists[k][i] < 0 || lists[k][i] >= lim[k])
+        return fail(NF_ERR_ARG, std::string(names[k]) + " index out of range");
+      if (i && lists[k][i] <= lists[k][i - 1])
+        return fail(NF_ERR_ARG, std::string(names[k]) + " indices must be strictly increasing");
+    }
+  }
+  const long long B = (long long)nf * nt * nr;
+  if (B > p->max_batch) return fail(NF_ERR_ARG, "batch larger than the plan's max_batch");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int32_t> h((size_t)p->g.F + p->g.T + p->g.R, 0);
+  std::memcpy(h.data(), fs, sizeof(int32_t) * nf);
+  std::memcpy(h.data() + p->g.F, ts, sizeof(int32_t) * nt);
+  std::memcpy(h.data() + p->g.F + p->g.T, rs, sizeof(int32_t) * nr);
+  // pageable source: staged by the driver before the call returns, so h may go out of scope
+  CUDA_TRY(cudaMemcpyAsync(p->d_struct, h.data(), sizeof(int32_t) * h.size(), cudaMemcpyHostToDevice, st));
+  p->snf = nf;
+  p->snt = nt;
+  p->snr = nr;
+  const StructArgs sa = struct_args(p);
+  struct_prep_kernel<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(sa, p->g.T, p->g.R, p->d_sm, p->d_spos, p->d_sf);
+  CUDA_TRY(cudaGetLastError());
+  p->launches += 1;
+  p->B = (int)B;
+  p->structured = true;
   return NF_OK;
 }
 
@@ -1572,6 +2069,8 @@ int nf_forward(nf_plan* p, const void* s, void* y, void* stream) {
   if (!p || !s || !y) return fail(NF_ERR_ARG, "null argument");
   if (p->B < 1) return fail(NF_ERR_STATE, "no batch staged (call nf_batch_prepare first)");
   cudaStream_t st = (cudaStream_t)stream;
+  if (p->structured)
+    return p->dtype == NF_C64 ? launch_forward_struct<float>(p, s, y, st) : launch_forward_struct<double>(p, s, y, st);
   return p->dtype == NF_C64 ? launch_forward<float>(p, s, y, st) : launch_forward<double>(p, s, y, st);
 }
 

@@ -171,6 +171,8 @@ def _upload(plan: DevicePlan, x: np.ndarray) -> torch.Tensor:
 
 
 def _stage(plan: DevicePlan, idx: np.ndarray) -> None:
+    # Always the flat path: the reference guarantees forward_apply(s, subset=sub) == full[sub]
+    # bit for bit (pkg/tests/test_forward.py:142-149), which needs one arithmetic for every subset.
     plan.prepare(torch.from_numpy(idx.astype(np.int32)).to(plan.device))
 
 

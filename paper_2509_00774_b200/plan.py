@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import functools
+import os
 
 import numpy as np
 import torch
@@ -19,6 +20,31 @@ from . import _lib
 from .geometry import ImagingScenario
 
 DTYPES = {"c64": (_lib.NF_C64, torch.complex64), "c128": (_lib.NF_C128, torch.complex128)}
+
+# Structured (Cartesian) batches with at least this many (tx, rx) pairs per frequency take the
+# separable kernels (nf_batch_prepare_structured); smaller ones stay on the flat path.
+STRUCT_MIN_PAIRS = 16
+STRUCT_POLICIES = ("auto", "always", "never")
+
+
+def cartesian_factors(idx: np.ndarray, n_tx: int, n_rx: int):
+    """(fs, ts, rs) when ``idx`` is exactly the sorted product Fs × Ts × Rs in (f, t, r) order,
+    else None. That is the layout of the reference's sample_minibatch (solver.py:205-225) and
+    of the full channel set (forward.py:233-236)."""
+    idx = np.asarray(idx)
+    if idx.ndim != 1 or idx.size == 0:
+        return None
+    idx = idx.astype(np.int64, copy=False)
+    per_f = n_tx * n_rx
+    fs = np.unique(idx // per_f)
+    ts = np.unique((idx // n_rx) % n_tx)
+    rs = np.unique(idx % n_rx)
+    if fs.size * ts.size * rs.size != idx.size:
+        return None
+    expect = (rs[None, None, :] + n_rx * (ts[None, :, None] + n_tx * fs[:, None, None])).reshape(-1)
+    if not np.array_equal(expect, idx):
+        return None
+    return fs.astype(np.int32), ts.astype(np.int32), rs.astype(np.int32)
 
 
 def _dptr(x: np.ndarray):
@@ -57,7 +83,11 @@ class DevicePlan:
         device=None,
         z_range: tuple[int, int] | None = None,
         max_batch: int | None = None,
+        structured: str | None = None,
     ):
+        """``structured``: "auto" (default; env NFGPU_STRUCTURED overrides) routes Cartesian
+        host batches with >= STRUCT_MIN_PAIRS (tx, rx) pairs to the separable kernels,
+        "always" routes every Cartesian host batch there, "never" keeps the flat path."""
         if dtype not in DTYPES:
             raise ValueError(f"dtype must be one of {sorted(DTYPES)}, got {dtype!r}")
         self.lib = _lib.load()
@@ -71,6 +101,12 @@ class DevicePlan:
         self.z_range = (z0, z1)
         self.n_local = nx * ny * (z1 - z0)
         self.vox_offset = nx * ny * z0
+        self.structured = structured or os.environ.get("NFGPU_STRUCTURED", "auto")
+        if self.structured not in STRUCT_POLICIES:
+            raise ValueError(f"structured must be one of {STRUCT_POLICIES}, got {self.structured!r}")
+        self.n_tx = scenario.array.n_tx
+        self.n_rx = scenario.array.n_rx
+        self.n_f = scenario.frequencies.count
         self.M = scenario.n_channels
         self.max_batch = self.M if max_batch is None else int(max_batch)
 
@@ -93,6 +129,7 @@ class DevicePlan:
         self._h = out
         self.B = 0
         self._idx = None  # keeps the staged index tensor alive
+        self.staged_structured = False
 
     # ---------------------------------------------------------------- lifecycle
     def __del__(self):
@@ -137,6 +174,47 @@ class DevicePlan:
         _lib.check(self.lib.nf_batch_prepare(self._h, _ptr(idx), B, _stream(self.device)), "nf_batch_prepare")
         self.B = B
         self._idx = idx
+        self.staged_structured = False
+
+    def prepare_structured(self, fs, ts, rs) -> None:
+        """Stage the Cartesian subset fs × ts × rs (sorted host index lists; the C ABI validates)."""
+        arrs = [np.ascontiguousarray(np.asarray(a), dtype=np.int32) for a in (fs, ts, rs)]
+        ip = [a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)) for a in arrs]
+        _lib.check(
+            self.lib.nf_batch_prepare_structured(self._h, ip[0], arrs[0].size, ip[1], arrs[1].size, ip[2],
+                                                 arrs[2].size, _stream(self.device)),
+            "nf_batch_prepare_structured",
+        )
+        self.B = int(arrs[0].size * arrs[1].size * arrs[2].size)
+        self._idx = None
+        self.staged_structured = True
+
+    def prepare_full(self) -> None:
+        """Stage all M channels (a Cartesian product; structured unless the policy is "never")."""
+        if self.structured != "never":
+            self.prepare_structured(np.arange(self.n_f), np.arange(self.n_tx), np.arange(self.n_rx))
+        else:
+            self.prepare(torch.arange(self.M, dtype=torch.int32, device=self.device))
+
+    def try_structured(self, idx) -> bool:
+        """Stage host index list ``idx`` through the separable path when it is a sorted Cartesian
+        product and the policy allows; returns False (nothing staged) otherwise."""
+        if self.structured == "never":
+            return False
+        fac = cartesian_factors(idx, self.n_tx, self.n_rx)
+        if fac is None:
+            return False
+        if self.structured == "auto" and fac[1].size * fac[2].size < STRUCT_MIN_PAIRS:
+            return False
+        self.prepare_structured(*fac)
+        return True
+
+    def stage_host(self, idx) -> int:
+        """Stage a host (numpy) index list in subset order; returns B."""
+        idx = np.asarray(idx)
+        if not self.try_structured(idx):
+            self.prepare(torch.from_numpy(idx.astype(np.int32)).to(self.device))
+        return self.B
 
     def forward(self, s: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """out[k] = Σ_{n in slab} A[m_k, n] s[n] (subset order)."""

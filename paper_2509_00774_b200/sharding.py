@@ -54,7 +54,7 @@ class ShardedSetup:
         self.pg = process_group
         self.plan = DevicePlan(scenario, dtype=dtype, device=device, z_range=z_range)
         self.M = scenario.n_channels
-        self.plan.prepare(torch.arange(self.M, dtype=torch.int32, device=self.plan.device))
+        self.plan.prepare_full()
 
     def _slab(self, x_full: np.ndarray) -> torch.Tensor:
         p = self.plan

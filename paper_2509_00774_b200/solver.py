@@ -322,6 +322,8 @@ class SPGMEngine:
         """Stage a host (numpy) or device index list; returns B."""
         if isinstance(idx, torch.Tensor) and idx.device == self.plan.device:
             t = idx.to(torch.int32)
+        elif self.plan.try_structured(np.asarray(idx)):
+            return self.plan.B
         else:
             t = torch.from_numpy(np.ascontiguousarray(np.asarray(idx, dtype=np.int32)))
             t = t.pin_memory() if not t.is_pinned() else t
@@ -466,7 +468,7 @@ def lipschitz_estimate(scenario: ImagingScenario, n_iters: int = 50, rng_seed: i
     x0 = rng.standard_normal(n) + 1j * rng.standard_normal(n)
     x0 /= np.linalg.norm(x0)
     x = plan._as_dev(x0, n, "x")
-    plan.prepare(torch.arange(m, dtype=torch.int32, device=plan.device))
+    plan.prepare_full()
     y = plan.vec(m)
     z = plan.vec(n)
     lam = 0.0
