@@ -1157,10 +1157,39 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
 // so per frequency a voxel needs n_t + n_r phasors instead of n_t·n_r. The contraction over the
 // batch becomes complex multiply-adds on the FMA pipe: the adjoint computes
 // Σ_t conj(U_ft)·Σ_r conj(V_fr)·w_ftr, and the forward computes Σ_n U_ft·(V_fr·s) per (t, r).
-// Each warp owns (tile, frequency chunk). The rx factors of a block of RB receivers are staged
-// in shared memory once per frequency and reused by every transmitter.
+// A block of SW warps owns (tile, chunk of (f, t) rows). Per frequency, the warps jointly stage
+// the rx factors of RBS receivers in shared memory (each warp computes every SW-th row). Each
+// warp then takes its own blocks of TB transmitters, held in registers, so one shared-memory
+// load of an rx factor feeds TB complex multiply-adds. The tx table rows of the next
+// transmitter block are prefetched per lane with cp.async while the contraction runs.
 
-constexpr int RB = 8;  // receivers per staged block
+constexpr int SW = 4;  // warps per structured block
+template <typename Real>
+struct SCfg;
+template <>
+struct SCfg<float> {
+  static constexpr int TB = 4, RBA = 16, RBF = 12;
+};
+template <>
+struct SCfg<double> {
+  static constexpr int TB = 2, RBA = 8, RBF = 6;
+};
+
+// block shared-memory layout: stage | s (forward) | D0 row | SW × per-warp area
+template <typename Real, bool FWD>
+struct SLayout {
+  static constexpr int TB = SCfg<Real>::TB;
+  static constexpr int RBS = FWD ? SCfg<Real>::RBF : SCfg<Real>::RBA;
+  static constexpr size_t stage = (size_t)RBS * 2 * TILE * sizeof(Real);
+  static constexpr size_t sv = FWD ? (size_t)2 * TILE * sizeof(Real) : 0;
+  static constexpr size_t trow = (size_t)TB * TABW * sizeof(Real);
+  static constexpr size_t wsm = FWD ? 0 : (size_t)RBS * TB * sizeof(R2<Real>);
+  static constexpr size_t tbuf = FWD ? (size_t)TBR * 33 * sizeof(R2<Real>) + 16 * sizeof(int) : 0;
+  static constexpr size_t warp = trow + wsm + ((tbuf + 15) & ~(size_t)15);
+  __host__ __device__ static constexpr size_t bytes(int A) {
+    return stage + sv + (size_t)d0_slots(A) * sizeof(double) + SW * warp;
+  }
+};
 
 struct StructArgs {
   const int* __restrict__ fs;
@@ -1169,11 +1198,24 @@ struct StructArgs {
   int nf, nt, nr;
 };
 
+// copy antenna a's table rows (δ and 1/d blocks) for this lane's voxels into slot; each lane
+// copies and later reads back only its own quads (see stage_rx)
 template <typename Real>
-__host__ __device__ constexpr size_t struct_warp_bytes(int A) {
-  return (size_t)RB * 2 * TILE * sizeof(Real) + (size_t)d0_slots(A) * sizeof(double) +
-         (size_t)16 * 33 * sizeof(R2<Real>) + 16 * sizeof(int);
+__device__ __forceinline__ void stage_row(const Real* __restrict__ tabt, int a, Real* slot, int L) {
+  constexpr int QD = 16 / (int)sizeof(Real);
+  const Real* src = tabt + (size_t)a * TABW + L * QD;
+  Real* dst = slot + L * QD;
+  constexpr int n16 = V / QD;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < n16; ++i) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dst + h * TILE + i * 32 * QD);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + h * TILE + i * 32 * QD)
+                   : "memory");
+    }
 }
+__device__ __forceinline__ void stage_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
 __device__ __forceinline__ void stv(float* p, const FV& q) {
 #pragma unroll
@@ -1258,161 +1300,203 @@ __device__ __forceinline__ void cmac_v(const DV& ur, const DV& ui, const DV& xr,
     zi.v[v] = fma(ui.v[v], xr.v[v], fma(ur.v[v], xi.v[v], zi.v[v]));
   }
 }
-// Σ_v u·w over the lane's voxels (complex)
+// Σ_v u·w over the lane's voxels (complex); two accumulator chains per component
 __device__ __forceinline__ float2 cdot(const FV& ur, const FV& ui, const FV& wr, const FV& wi) {
-  float2 pr = make_float2(0.f, 0.f), pi = make_float2(0.f, 0.f);
+  float2 pr0 = make_float2(0.f, 0.f), pi0 = pr0, pr1 = pr0, pi1 = pr0;
 #pragma unroll
-  for (int i = 0; i < NP; ++i) {
-    pr = fma2(ui.p[i], make_float2(-wi.p[i].x, -wi.p[i].y), fma2(ur.p[i], wr.p[i], pr));
-    pi = fma2(ui.p[i], wr.p[i], fma2(ur.p[i], wi.p[i], pi));
+  for (int i = 0; i < NP; i += 2) {
+    pr0 = fma2(ui.p[i], make_float2(-wi.p[i].x, -wi.p[i].y), fma2(ur.p[i], wr.p[i], pr0));
+    pi0 = fma2(ui.p[i], wr.p[i], fma2(ur.p[i], wi.p[i], pi0));
+    pr1 = fma2(ui.p[i + 1], make_float2(-wi.p[i + 1].x, -wi.p[i + 1].y), fma2(ur.p[i + 1], wr.p[i + 1], pr1));
+    pi1 = fma2(ui.p[i + 1], wr.p[i + 1], fma2(ur.p[i + 1], wi.p[i + 1], pi1));
   }
+  const float2 pr = add2(pr0, pr1), pi = add2(pi0, pi1);
   return make_float2(pr.x + pr.y, pi.x + pi.y);
 }
 __device__ __forceinline__ double2 cdot(const DV& ur, const DV& ui, const DV& wr, const DV& wi) {
-  double pr = 0, pi = 0;
+  double pr0 = 0, pi0 = 0, pr1 = 0, pi1 = 0;
 #pragma unroll
-  for (int v = 0; v < V; ++v) {
-    pr = fma(-ui.v[v], wi.v[v], fma(ur.v[v], wr.v[v], pr));
-    pi = fma(ui.v[v], wr.v[v], fma(ur.v[v], wi.v[v], pi));
+  for (int v = 0; v < V; v += 2) {
+    pr0 = fma(-ui.v[v], wi.v[v], fma(ur.v[v], wr.v[v], pr0));
+    pi0 = fma(ui.v[v], wr.v[v], fma(ur.v[v], wi.v[v], pi0));
+    pr1 = fma(-ui.v[v + 1], wi.v[v + 1], fma(ur.v[v + 1], wr.v[v + 1], pr1));
+    pi1 = fma(ui.v[v + 1], wr.v[v + 1], fma(ur.v[v + 1], wi.v[v + 1], pi1));
   }
-  return make_double2(pr, pi);
+  return make_double2(pr0 + pr1, pi0 + pi1);
 }
 
-// Rows u = fi·nt + ti of a structured batch; a unit owns the row range [u0, u1). Per frequency
-// it stages the rx factors of RB receivers at a time in shared memory, then walks its
-// transmitters two at a time so each shared-memory load feeds two transmitters.
+// Rows u = fi·nt + ti of a structured batch; a block owns the row range [u0, u1), which
+// covers transmitters [ta, tb) of frequency fi.
 __device__ __forceinline__ void row_span(const StructArgs& sa, int u0, int u1, int fi, int& ta, int& tb) {
   ta = max(u0, fi * sa.nt) - fi * sa.nt;
   tb = min(u1, (fi + 1) * sa.nt) - fi * sa.nt;
 }
 
-// Structured adjoint (+prox): g = Σ_f Σ_t conj(U_ft)·Σ_r conj(V_fr)·w_ftr. Unit = (tile, row chunk).
+#ifndef NFGPU_MINB_STRUCT
+#define NFGPU_MINB_STRUCT 3
+#endif
+
+// Structured adjoint (+prox): g = Σ_f Σ_t conj(U_ft)·Σ_r conj(V_fr)·w_ftr. Block = (tile, row chunk).
 template <typename Real, bool PROX, bool EXACT>
-__global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_struct_kernel(AdjArgs<Real> a, StructArgs sa,
-                                                                                  const double* __restrict__ kd) {
+__global__ void __launch_bounds__(SW * 32, NFGPU_MINB_STRUCT) adj_struct_kernel(AdjArgs<Real> a, StructArgs sa,
+                                                                              const double* __restrict__ kd) {
+  using LY = SLayout<Real, false>;
+  constexpr int TB = LY::TB, RBS = LY::RBS;
+  constexpr int QD = 16 / (int)sizeof(Real);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int unit = blockIdx.x * ADJ_WARPS + w;
-  if (unit >= g.ntiles * a.CH) return;
-  const int tile = unit / a.CH, chunk = unit - tile * a.CH;
-  unsigned char* wbase = smem_raw + (size_t)w * struct_warp_bytes<Real>(g.A);
-  Real* vb = reinterpret_cast<Real*>(wbase);  // [RB][re, im][TILE]
-  double* d0 = reinterpret_cast<double*>(wbase + (size_t)RB * 2 * TILE * sizeof(Real));
-  for (int i = L; i < g.A; i += 32) d0[i] = a.D0[(size_t)tile * g.A + i];
-  __syncwarp();
-  constexpr int QD = 16 / (int)sizeof(Real);
-  const Real* tabt = a.tab + (size_t)tile * g.A * TABW + L * QD;
-  Real* vbl = vb + L * QD;
+  const int tile = blockIdx.x / a.CH, chunk = blockIdx.x - tile * a.CH;
+  Real* stage = reinterpret_cast<Real*>(smem_raw);
+  double* d0 = reinterpret_cast<double*>(smem_raw + LY::stage);
+  unsigned char* wb = smem_raw + LY::stage + (size_t)d0_slots(g.A) * sizeof(double) + (size_t)w * LY::warp;
+  Real* trow = reinterpret_cast<Real*>(wb);
+  R2<Real>* wsm = reinterpret_cast<R2<Real>*>(wb + LY::trow);
+  for (int i = threadIdx.x; i < g.A; i += SW * 32) d0[i] = a.D0[(size_t)tile * g.A + i];
+  __syncthreads();
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
+  Real* stl = stage + L * QD;
+  const Real* trl = trow + L * QD;
   const int rows = sa.nf * sa.nt;
   const int u0 = (int)(((long long)rows * chunk) / a.CH), u1 = (int)(((long long)rows * (chunk + 1)) / a.CH);
 
   QV<Real> gr, gi;
   zero(gr);
   zero(gi);
+  int ld_t0 = -1, ld_tc = 0;  // transmitter block whose rows are in trow
   for (int fi = u0 / sa.nt; fi * sa.nt < u1; ++fi) {
     int ta, tb;
     row_span(sa, u0, u1, fi, ta, tb);
     const double kf = kd[sa.fs[fi]];
-    for (int r0 = 0; r0 < sa.nr; r0 += RB) {
-      const int nrb = min(RB, sa.nr - r0);
-      __syncwarp();
-      for (int q = 0; q < nrb; ++q) {  // conj(V_fr) for the block, into shared memory
-        const Real* row = tabt + (size_t)(g.T + sa.rs[r0 + q]) * TABW;
+    for (int r0 = 0; r0 < sa.nr; r0 += RBS) {
+      const int nrb = min(RBS, sa.nr - r0);
+      for (int q = w; q < nrb; q += SW) {  // conj(V_fr) rows, shared by the block
+        const int ant = g.T + sa.rs[r0 + q];
+        const Real* row = tabt + (size_t)ant * TABW + L * QD;
         Real k, b;
-        side_params<Real, EXACT>(kf, d0[g.T + sa.rs[r0 + q]], k, b);
+        side_params<Real, EXACT>(kf, d0[ant], k, b);
         QV<Real> re, im;
         side_phasor<EXACT>(k, b, ldv(row), ldv(row + TILE), Real(1), re, im);
-        stv(vbl + (size_t)q * 2 * TILE, re);
-        stv(vbl + (size_t)q * 2 * TILE + TILE, im);
+        stv(stl + (size_t)q * 2 * TILE, re);
+        stv(stl + (size_t)q * 2 * TILE + TILE, im);
       }
-      __syncwarp();
-      const R2<Real>* wf = a.wrec + ((size_t)fi * sa.nt) * sa.nr + r0;
-      int ti = ta;
-      for (; ti + 1 < tb; ti += 2) {  // transmitter pairs
-        QV<Real> z0r, z0i, z1r, z1i;
-        zero(z0r);
-        zero(z0i);
-        zero(z1r);
-        zero(z1i);
-        const R2<Real>* w0p = wf + (size_t)ti * sa.nr;
-        const R2<Real>* w1p = w0p + sa.nr;
-        for (int q = 0; q < nrb; ++q) {
-          const R2<Real> w0 = w0p[q], w1 = w1p[q];
-          const QV<Real> vr = ldv(vbl + (size_t)q * 2 * TILE), vi = ldv(vbl + (size_t)q * 2 * TILE + TILE);
-          cmac_s(vr, vi, w0.x, w0.y, z0r, z0i);
-          cmac_s(vr, vi, w1.x, w1.y, z1r, z1i);
+      __syncthreads();
+      for (int t0 = ta + w * TB; t0 < tb; t0 += SW * TB) {
+        const int tc = min(TB, tb - t0);
+        if (t0 != ld_t0 || tc > ld_tc) {  // rows arrive while the contraction runs
+          for (int k = 0; k < tc; ++k) stage_row<Real>(tabt, sa.ts[t0 + k], trow + (size_t)k * TABW, L);
+          stage_commit();
+          ld_t0 = t0;
+          ld_tc = tc;
         }
+        __syncwarp();
+        for (int i = L; i < nrb * TB; i += 32) {
+          const int q = i / TB, k = i - q * TB;
+          R2<Real> v;
+          v.x = 0;
+          v.y = 0;
+          if (k < tc) v = a.wrec[((size_t)fi * sa.nt + t0 + k) * sa.nr + r0 + q];
+          wsm[i] = v;
+        }
+        __syncwarp();
+        QV<Real> zr[TB], zi[TB];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int t = sa.ts[ti + h];
-          const Real* row = tabt + (size_t)t * TABW;
-          Real k, b;
-          side_params<Real, EXACT>(kf, d0[t], k, b);
-          QV<Real> ur, ui;
-          side_phasor<EXACT>(k, b, ldv(row), ldv(row + TILE), Real(1), ur, ui);
-          cmac_v(ur, ui, h ? z1r : z0r, h ? z1i : z0i, gr, gi);
+        for (int k = 0; k < TB; ++k) {
+          zero(zr[k]);
+          zero(zi[k]);
         }
-      }
-      if (ti < tb) {  // odd transmitter
-        QV<Real> zr, zi;
-        zero(zr);
-        zero(zi);
-        const R2<Real>* w0p = wf + (size_t)ti * sa.nr;
         for (int q = 0; q < nrb; ++q) {
-          const R2<Real> w0 = w0p[q];
-          cmac_s(ldv(vbl + (size_t)q * 2 * TILE), ldv(vbl + (size_t)q * 2 * TILE + TILE), w0.x, w0.y, zr, zi);
+          const QV<Real> vr = ldv(stl + (size_t)q * 2 * TILE), vi = ldv(stl + (size_t)q * 2 * TILE + TILE);
+#pragma unroll
+          for (int k = 0; k < TB; ++k) {
+            const R2<Real> wq = wsm[q * TB + k];
+            cmac_s(vr, vi, wq.x, wq.y, zr[k], zi[k]);
+          }
         }
-        const int t = sa.ts[ti];
-        const Real* row = tabt + (size_t)t * TABW;
-        Real k, b;
-        side_params<Real, EXACT>(kf, d0[t], k, b);
-        QV<Real> ur, ui;
-        side_phasor<EXACT>(k, b, ldv(row), ldv(row + TILE), Real(1), ur, ui);
-        cmac_v(ur, ui, zr, zi, gr, gi);
+        stage_wait();
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          if (k < tc) {
+            const int t = sa.ts[t0 + k];
+            Real kk, b;
+            side_params<Real, EXACT>(kf, d0[t], kk, b);
+            QV<Real> ur, ui;
+            side_phasor<EXACT>(kk, b, ldv(trl + (size_t)k * TABW), ldv(trl + (size_t)k * TABW + TILE), Real(1), ur,
+                               ui);
+            cmac_v(ur, ui, zr[k], zi[k], gr, gi);
+          }
+        }
       }
+      __syncthreads();
     }
   }
-  adj_epilogue<Real, PROX>(a, tile, chunk, L, gr, gi);
+  // the block's warps each hold a partial over their transmitters: combine in warp order
+  Real* cb = stage + (size_t)(w * 32 + L) * (2 * V);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    cb[2 * v] = get(gr, v);
+    cb[2 * v + 1] = get(gi, v);
+  }
+  __syncthreads();
+  if (w != 0) return;
+  Real Gr[V], Gi[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) Gr[v] = Gi[v] = 0;
+  for (int ww = 0; ww < SW; ++ww) {
+    const Real* q = stage + (size_t)(ww * 32 + L) * (2 * V);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      Gr[v] += q[2 * v];
+      Gi[v] += q[2 * v + 1];
+    }
+  }
+  adj_epilogue<Real, PROX>(a, tile, chunk, L, make_v(Gr), make_v(Gi));
 }
 
-// Structured forward: y_ftr = p_f/(4π) Σ_n U_ft(n)·(V_fr(n) s_n). Per (t, r) each lane sums its
-// voxels; every 16 rows a transpose through shared memory reduces over the 32 lanes in a fixed
-// order and writes one partial per (tile, channel), which fwd_reduce1/2 finish.
-// The launch window is the row range [ua, ub) (channels [ua·nr, ub·nr)).
+// Structured forward: y_ftr = p_f/(4π) Σ_n U_ft(n)·(V_fr(n) s_n). The block stages W_fr = V_fr·s;
+// each warp forms, per transmitter of its block and staged receiver, the lane sums over its
+// voxels, then a [TBR][33] transpose reduces over the 32 lanes in a fixed order and writes one
+// partial per (tile, channel), which fwd_reduce1/2 finish. The launch window is the row range
+// [w0/nr, w1/nr) of whole (f, t) rows.
 template <typename Real, bool EXACT>
-__global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_struct_kernel(FwdArgs<Real> a, StructArgs sa,
-                                                                                  const double* __restrict__ kd) {
+__global__ void __launch_bounds__(SW * 32, NFGPU_MINB_STRUCT) fwd_struct_kernel(FwdArgs<Real> a, StructArgs sa,
+                                                                              const double* __restrict__ kd) {
+  using LY = SLayout<Real, true>;
+  constexpr int TB = LY::TB, RBS = LY::RBS;
+  constexpr int QD = 16 / (int)sizeof(Real);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int unit = blockIdx.x * FWD_WARPS + w;
-  if (unit >= g.ntiles * a.Q) return;
-  const int tile = unit / a.Q, chunk = unit - tile * a.Q;
-  unsigned char* wbase = smem_raw + (size_t)w * struct_warp_bytes<Real>(g.A);
-  Real* wb = reinterpret_cast<Real*>(wbase);  // [RB][re, im][TILE]: V_fr·s
-  double* d0 = reinterpret_cast<double*>(wbase + (size_t)RB * 2 * TILE * sizeof(Real));
-  R2<Real>* tbuf = reinterpret_cast<R2<Real>*>(reinterpret_cast<unsigned char*>(d0) + d0_slots(g.A) * sizeof(double));
-  int* jrow = reinterpret_cast<int*>(tbuf + 16 * 33);
-  for (int i = L; i < g.A; i += 32) d0[i] = a.D0[(size_t)tile * g.A + i];
-  constexpr int QD = 16 / (int)sizeof(Real);
-  const Real* tabt = a.tab + (size_t)tile * g.A * TABW + L * QD;
-  Real* wbl = wb + L * QD;
-  int tx, ty, tz;
-  tile_coords(g, tile, tx, ty, tz);
-  int x0, y, z;
-  lane_voxel(tx, ty, tz, L, x0, y, z);
-  Real srv[V], siv[V];
+  const int tile = blockIdx.x / a.Q, chunk = blockIdx.x - tile * a.Q;
+  Real* stage = reinterpret_cast<Real*>(smem_raw);
+  Real* sv = reinterpret_cast<Real*>(smem_raw + LY::stage);
+  double* d0 = reinterpret_cast<double*>(smem_raw + LY::stage + LY::sv);
+  unsigned char* wb = smem_raw + LY::stage + LY::sv + (size_t)d0_slots(g.A) * sizeof(double) + (size_t)w * LY::warp;
+  Real* trow = reinterpret_cast<Real*>(wb);
+  R2<Real>* tbuf = reinterpret_cast<R2<Real>*>(wb + LY::trow);
+  int* jrow = reinterpret_cast<int*>(tbuf + TBR * 33);
+  for (int i = threadIdx.x; i < g.A; i += SW * 32) d0[i] = a.D0[(size_t)tile * g.A + i];
+  if (w == 0) {  // the tile's s values, in the table's lane layout
+    int tx, ty, tz;
+    tile_coords(g, tile, tx, ty, tz);
+    int x0, y, z;
+    lane_voxel(tx, ty, tz, L, x0, y, z);
+    Real srv[V], siv[V];
 #pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int x = x0 + v;
-    const bool ok = x < g.nx && y < g.ny && z < g.nzs;
-    const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
-    srv[v] = ok ? a.s[2 * n] : Real(0);
-    siv[v] = ok ? a.s[2 * n + 1] : Real(0);
+    for (int v = 0; v < V; ++v) {
+      const int x = x0 + v;
+      const bool ok = x < g.nx && y < g.ny && z < g.nzs;
+      const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
+      srv[v] = ok ? a.s[2 * n] : Real(0);
+      siv[v] = ok ? a.s[2 * n + 1] : Real(0);
+    }
+    stv(sv + L * QD, make_v(srv));
+    stv(sv + TILE + L * QD, make_v(siv));
   }
-  const QV<Real> sr = make_v(srv), si = make_v(siv);
-  __syncwarp();
+  __syncthreads();
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
+  Real* stl = stage + L * QD;
+  const Real* trl = trow + L * QD;
   const int span = a.w1 - a.w0;
   R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * span - a.w0;
   const int ua = a.w0 / sa.nr, nrows = span / sa.nr;
@@ -1421,88 +1505,104 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_struct_ker
 
   auto flush_rows = [&](int cnt) {
     __syncwarp();
-    const int row = L & 15, half = L >> 4;
+    constexpr int PER = 32 / TBR, SL = 32 / PER;
+    const int row = L % TBR, part = L / TBR;
     R2<Real> S;
     S.x = 0;
     S.y = 0;
-#pragma unroll 8
-    for (int l = 0; l < 16; ++l) {
-      const R2<Real> t = tbuf[row * 33 + half * 16 + l];
+#pragma unroll
+    for (int l = 0; l < SL; ++l) {
+      const R2<Real> t = tbuf[row * 33 + part * SL + l];
       S.x += t.x;
       S.y += t.y;
     }
-    S.x += __shfl_down_sync(FULL, S.x, 16);
-    S.y += __shfl_down_sync(FULL, S.y, 16);
+#pragma unroll
+    for (int o = 16; o >= TBR; o >>= 1) {
+      S.x += __shfl_down_sync(FULL, S.x, o);
+      S.y += __shfl_down_sync(FULL, S.y, o);
+    }
     if (L < cnt) out[jrow[L]] = S;
     __syncwarp();
   };
-  auto emit = [&](const R2<Real>& v, int j) {
-    tbuf[nrow * 33 + L] = v;
-    if (L == 0) jrow[nrow] = j;
-    if (++nrow == 16) {
-      flush_rows(16);
-      nrow = 0;
-    }
+  auto load_rows = [&](int t0, int tc) {
+    for (int k = 0; k < tc; ++k) stage_row<Real>(tabt, sa.ts[t0 + k], trow + (size_t)k * TABW, L);
+    stage_commit();
   };
 
+  int ld_t0 = -1, ld_tc = 0;
   for (int fi = u0 / sa.nt; fi * sa.nt < u1; ++fi) {
     int ta, tb;
     row_span(sa, u0, u1, fi, ta, tb);
     const double kf = kd[sa.fs[fi]];
-    for (int r0 = 0; r0 < sa.nr; r0 += RB) {
-      const int nrb = min(RB, sa.nr - r0);
-      __syncwarp();
-      for (int q = 0; q < nrb; ++q) {  // W_fr = V_fr·s for the block, into shared memory
-        const Real* row = tabt + (size_t)(g.T + sa.rs[r0 + q]) * TABW;
-        Real k, b;
-        side_params<Real, EXACT>(kf, d0[g.T + sa.rs[r0 + q]], k, b);
-        QV<Real> vr, vi, wr, wi;
-        side_phasor<EXACT>(k, b, ldv(row), ldv(row + TILE), Real(-1), vr, vi);
-        zero(wr);
-        zero(wi);
-        cmac_v(vr, vi, sr, si, wr, wi);
-        stv(wbl + (size_t)q * 2 * TILE, wr);
-        stv(wbl + (size_t)q * 2 * TILE + TILE, wi);
+    for (int r0 = 0; r0 < sa.nr; r0 += RBS) {
+      const int nrb = min(RBS, sa.nr - r0);
+      const int first = ta + w * TB;
+      if (first < tb && (first != ld_t0 || min(TB, tb - first) > ld_tc)) {  // overlaps the staging below
+        ld_t0 = first;
+        ld_tc = min(TB, tb - first);
+        load_rows(ld_t0, ld_tc);
       }
-      __syncwarp();
-      const int jf = fi * sa.nt * sa.nr + r0;
-      int ti = ta;
-      for (; ti + 1 < tb; ti += 2) {  // transmitter pairs share each W load
-        QV<Real> u0r, u0i, u1r, u1i;
-        {
-          const int t = sa.ts[ti];
+      {
+        const QV<Real> sr = ldv(sv + L * QD), si = ldv(sv + TILE + L * QD);
+        for (int q = w; q < nrb; q += SW) {  // W_fr = V_fr·s rows, shared by the block
+          const int ant = g.T + sa.rs[r0 + q];
+          const Real* row = tabt + (size_t)ant * TABW + L * QD;
           Real k, b;
-          side_params<Real, EXACT>(kf, d0[t], k, b);
-          side_phasor<EXACT>(k, b, ldv(tabt + (size_t)t * TABW), ldv(tabt + (size_t)t * TABW + TILE), Real(-1), u0r,
-                             u0i);
+          side_params<Real, EXACT>(kf, d0[ant], k, b);
+          QV<Real> vr, vi, wr, wi;
+          side_phasor<EXACT>(k, b, ldv(row), ldv(row + TILE), Real(-1), vr, vi);
+          zero(wr);
+          zero(wi);
+          cmac_v(vr, vi, sr, si, wr, wi);
+          stv(stl + (size_t)q * 2 * TILE, wr);
+          stv(stl + (size_t)q * 2 * TILE + TILE, wi);
         }
-        {
-          const int t = sa.ts[ti + 1];
-          Real k, b;
-          side_params<Real, EXACT>(kf, d0[t], k, b);
-          side_phasor<EXACT>(k, b, ldv(tabt + (size_t)t * TABW), ldv(tabt + (size_t)t * TABW + TILE), Real(-1), u1r,
-                             u1i);
+      }
+      __syncthreads();
+      for (int t0 = first; t0 < tb; t0 += SW * TB) {
+        const int tc = min(TB, tb - t0);
+        stage_wait();
+        QV<Real> ur[TB], ui[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          zero(ur[k]);
+          zero(ui[k]);
+          if (k < tc) {
+            const int t = sa.ts[t0 + k];
+            Real kk, b;
+            side_params<Real, EXACT>(kf, d0[t], kk, b);
+            side_phasor<EXACT>(kk, b, ldv(trl + (size_t)k * TABW), ldv(trl + (size_t)k * TABW + TILE), Real(-1),
+                               ur[k], ui[k]);
+          }
         }
+        const int n0 = t0 + SW * TB;
+        if (n0 < tb) {  // rows are consumed: prefetch the next block of this warp
+          ld_t0 = n0;
+          ld_tc = min(TB, tb - n0);
+          load_rows(ld_t0, ld_tc);
+        }
+        const int jb = (fi * sa.nt + t0) * sa.nr + r0;
         for (int q = 0; q < nrb; ++q) {
-          const QV<Real> wr = ldv(wbl + (size_t)q * 2 * TILE), wi = ldv(wbl + (size_t)q * 2 * TILE + TILE);
-          const R2<Real> p0 = cdot(u0r, u0i, wr, wi), p1 = cdot(u1r, u1i, wr, wi);
-          emit(p0, jf + ti * sa.nr + q);
-          emit(p1, jf + (ti + 1) * sa.nr + q);
+          const QV<Real> wr = ldv(stl + (size_t)q * 2 * TILE), wi = ldv(stl + (size_t)q * 2 * TILE + TILE);
+          R2<Real> pv[TB];  // all TB dot products first (independent chains), then the row stores
+#pragma unroll
+          for (int k = 0; k < TB; ++k) pv[k] = cdot(ur[k], ui[k], wr, wi);
+#pragma unroll
+          for (int k = 0; k < TB; ++k)
+            if (k < tc) tbuf[(nrow + k) * 33 + L] = pv[k];
+          if (L < tc) jrow[nrow + L] = jb + L * sa.nr + q;
+          nrow += tc;
+          if (nrow > TBR - TB) {
+            flush_rows(nrow);
+            nrow = 0;
+          }
         }
       }
-      if (ti < tb) {
-        const int t = sa.ts[ti];
-        Real k, b;
-        side_params<Real, EXACT>(kf, d0[t], k, b);
-        QV<Real> ur, ui;
-        side_phasor<EXACT>(k, b, ldv(tabt + (size_t)t * TABW), ldv(tabt + (size_t)t * TABW + TILE), Real(-1), ur, ui);
-        for (int q = 0; q < nrb; ++q)
-          emit(cdot(ur, ui, ldv(wbl + (size_t)q * 2 * TILE), ldv(wbl + (size_t)q * 2 * TILE + TILE)),
-               jf + ti * sa.nr + q);
-      }
+      __syncthreads();
     }
   }
   if (nrow) flush_rows(nrow);
+  stage_wait();
 }
 
 // sorted-order bookkeeping of a structured batch: position j = (fi·nt + ti)·nr + ri is
@@ -1614,6 +1714,7 @@ struct nf_plan {
   double phase_bound_rev = 0;
   long long fwd_target = 148LL * 16 * 4;  // warp work units per forward launch (env NFGPU_FWD_TARGET)
   long long adj_target = 148LL * 16 * 4;  // warp work units per adjoint launch (env NFGPU_ADJ_TARGET)
+  long long struct_target = 148LL * 3 * 4;  // blocks per structured launch (env NFGPU_STRUCT_TARGET)
   size_t dev_bytes = 0;
   int64_t launches = 0;
   int KS, ksblocks;
@@ -1741,20 +1842,21 @@ StructArgs struct_args(const nf_plan* p) {
   return sa;
 }
 
-size_t struct_smem(const nf_plan* p, int warps) {
-  return warps * (p->dtype == NF_C64 ? struct_warp_bytes<float>(p->g.A) : struct_warp_bytes<double>(p->g.A));
+template <typename Real, bool FWD>
+size_t struct_smem(const nf_plan* p) {
+  return SLayout<Real, FWD>::bytes(p->g.A);
 }
 
-// (f, t) rows per unit: enough units for the target, at least 4 rows each
-int struct_splits(long long target, int ntiles, int rows) {
-  long long q = (target + ntiles - 1) / ntiles;
-  q = std::min<long long>(q, std::max(1, rows / 4));
+// (f, t) row chunks per tile: enough blocks for the target, at least SW·4 rows each
+int struct_splits(long long target_blocks, int ntiles, int rows) {
+  long long q = (target_blocks + ntiles - 1) / ntiles;
+  q = std::min<long long>(q, std::max(1, rows / (SW * 4)));
   return (int)std::max(1LL, q);
 }
 
 template <typename Real>
 int launch_forward_struct(nf_plan* p, const void* s, void* y, cudaStream_t st) {
-  const size_t sm = struct_smem(p, FWD_WARPS);
+  const size_t sm = struct_smem<Real, true>(p);
   auto kern = p->exact ? fwd_struct_kernel<Real, true> : fwd_struct_kernel<Real, false>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
@@ -1772,10 +1874,9 @@ int launch_forward_struct(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.w0 = ua * sa.nr;
     a.w1 = ub * sa.nr;
     const int span = a.w1 - a.w0;
-    a.Q = struct_splits(p->fwd_target, p->g.ntiles, ub - ua);
+    a.Q = struct_splits(p->struct_target, p->g.ntiles, ub - ua);
     a.part = (Real*)p->d_part;
-    const long long units = (long long)p->g.ntiles * a.Q;
-    kern<<<(unsigned)((units + FWD_WARPS - 1) / FWD_WARPS), FWD_WARPS * 32, sm, st>>>(a, sa, p->d_kd);
+    kern<<<(unsigned)((long long)p->g.ntiles * a.Q), SW * 32, sm, st>>>(a, sa, p->d_kd);
     CUDA_TRY(cudaGetLastError());
     int nseg = (int)std::ceil(std::sqrt((double)p->fwd_gridx));
     nseg = std::max(1, std::min({nseg, p->fwd_gridx, std::max(1, RED_THREADS / span)}));
@@ -1816,14 +1917,13 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   a.stat_part = p->d_stat_part;
   if (p->structured) {
     const StructArgs sa = struct_args(p);
-    a.CH = std::min(struct_splits(p->adj_target, p->g.ntiles, sa.nf * sa.nt), p->adj_ch_cap);
-    const size_t sm = struct_smem(p, ADJ_WARPS);
+    a.CH = std::min(struct_splits(p->struct_target, p->g.ntiles, sa.nf * sa.nt), p->adj_ch_cap);
+    const size_t sm = struct_smem<Real, false>(p);
     auto kern = p->exact ? adj_struct_kernel<Real, PROX, true> : adj_struct_kernel<Real, PROX, false>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CUDA_TRY(
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-    const int units = p->g.ntiles * a.CH;
-    kern<<<(units + ADJ_WARPS - 1) / ADJ_WARPS, ADJ_WARPS * 32, sm, st>>>(a, sa, p->d_kd);
+    kern<<<(unsigned)(p->g.ntiles * a.CH), SW * 32, sm, st>>>(a, sa, p->d_kd);
   } else {
     const size_t sm = adj_smem(p);
     auto kern = p->exact ? adj_kernel<Real, PROX, true> : adj_kernel<Real, PROX, false>;
@@ -1908,6 +2008,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   }
   if (const char* e = std::getenv("NFGPU_FWD_TARGET")) p->fwd_target = std::max(1LL, std::atoll(e));
   if (const char* e = std::getenv("NFGPU_ADJ_TARGET")) p->adj_target = std::max(1LL, std::atoll(e));
+  if (const char* e = std::getenv("NFGPU_STRUCT_TARGET")) p->struct_target = std::max(1LL, std::atoll(e));
   const size_t rs = real_size(p);
   {
     // bound the forward partial buffer to ~512 MB

@@ -25,7 +25,6 @@ from paper_2509_00774_b200 import (
     configs,
     spgm_solve,
 )
-from paper_2509_00774_b200._lib import NFError
 from paper_2509_00774_b200.forward import get_plan
 from paper_2509_00774_b200.plan import DevicePlan, cartesian_factors
 
@@ -133,7 +132,8 @@ def test_structured_adjoint_prox_equals_flat(dtype):
     tol = {"c128": 1e-11, "c64": 1e-5}[dtype]
     assert rel_l2(outs[1][0], outs[0][0]) <= tol
     assert np.allclose(outs[1][1], outs[0][1], rtol=tol * 10)
-    assert outs[1][1][2] == outs[0][1][2]  # ½‖r − y_B‖² does not depend on the kernel
+    # ½‖r − y_B‖²: same terms, summed in each path's own sorted order
+    assert outs[1][1][2] == pytest.approx(outs[0][1][2], rel=1e-12)
 
 
 def test_structured_slab_plans_sum_to_full():
@@ -153,7 +153,8 @@ def test_structured_slab_plans_sum_to_full():
         y_sum += p.forward(p._as_dev(s[p.vox_offset:p.vox_offset + p.n_local], p.n_local, "s")).cpu().numpy()
         g_cat.append(p.adjoint(p._as_dev(r, p.M, "r")).cpu().numpy())
     assert rel_l2(y_sum, y_full) <= 1e-12
-    assert np.array_equal(np.concatenate(g_cat), g_full)  # voxel-local: slabs are bit-exact
+    # voxel-local; the chunk count (summation order over channels) follows the slab's tile count
+    assert rel_l2(np.concatenate(g_cat), g_full) <= 1e-12
 
 
 def test_structured_large_window_chunking():
@@ -184,17 +185,17 @@ def test_structured_large_window_chunking():
 def test_structured_validation(small_scenario):
     plan = DevicePlan(small_scenario, dtype="c64", max_batch=8)
     T, R, F = small_scenario.array.n_tx, small_scenario.array.n_rx, small_scenario.frequencies.count
-    with pytest.raises(NFError, match="increasing"):
+    with pytest.raises(ValueError, match="increasing"):
         plan.prepare_structured([1, 0], [0], [0])
-    with pytest.raises(NFError, match="increasing"):
+    with pytest.raises(ValueError, match="increasing"):
         plan.prepare_structured([0], [0, 0], [0])
-    with pytest.raises(NFError, match="out of range"):
+    with pytest.raises(ValueError, match="out of range"):
         plan.prepare_structured([0], [T], [0])
-    with pytest.raises(NFError, match="out of range"):
+    with pytest.raises(ValueError, match="out of range"):
         plan.prepare_structured([-1], [0], [0])
-    with pytest.raises(NFError, match="count"):
+    with pytest.raises(ValueError, match="count"):
         plan.prepare_structured([], [0], [0])
-    with pytest.raises(NFError, match="max_batch"):
+    with pytest.raises(ValueError, match="max_batch"):
         plan.prepare_structured(np.arange(F), np.arange(T), np.arange(R))
 
 
