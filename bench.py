@@ -351,7 +351,8 @@ def run_ours(args):
         if e2e is not None:
             out["e2e"] = e2e
         if world == 1 and not args.no_extras and args.workload == "large":
-            out["extra_workloads"] = {"medium": medium_line(args, dev)}
+            out["extra_workloads"] = {"medium": medium_line(args, dev),
+                                      "large_structured": structured_line(eng, w)}
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args.workload, 30, args.cpu_seconds)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
@@ -370,6 +371,56 @@ def medium_line(args, dev):
     return {"value": 2.0 * w.batch * N / (ms / steps * 1e-3), "unit": UNIT, "ms_per_step": ms / steps,
             "iters_per_s": 1e3 * steps / ms, "steps": steps, "batch": w.batch, "N": N, "M": w.scenario.n_channels,
             "frac_step": 2.0 * w.batch * N / (ms / steps * 1e-3) / SFU_ENTRY_PEAK_MEASURED, "cuda_graph": not args.no_graph}
+
+
+def structured_line(eng, w):
+    """The reference's own minibatch sampler (solver.sample_minibatch: a sorted Cartesian
+    n_f × n_tx × n_rx product, solver.py:205-225) on Large through the separable kernels
+    (nf_batch_prepare_structured): composition 4 × 32 × 32 = 4096 channels, host-sampled each
+    step like the reference, plus the full-batch proximal-gradient (ISTA, |B| = M) step."""
+    import torch
+
+    from paper_2509_00774_b200 import configs
+    from paper_2509_00774_b200.plan import DevicePlan
+    from paper_2509_00774_b200.solver import MinibatchComposition, SPGMEngine, sample_minibatch
+
+    scn = w.scenario
+    N, M = scn.n_voxels, scn.n_channels
+    st = torch.cuda.current_stream()
+
+    def timed(fn, warm, reps):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    comp = MinibatchComposition(4, 32, 32)
+    rng = np.random.default_rng(configs.SEEDS["minibatch"])
+
+    def spgm_step():
+        eng.stage(sample_minibatch(comp, scn, rng).indices)
+        eng.step_staged()
+
+    ms = timed(spgm_step, 5, 100)
+    B = comp.n_f * comp.n_tx * comp.n_rx
+    out = {"composition": [comp.n_f, comp.n_tx, comp.n_rx], "batch": B, "structured": eng.plan.staged_structured,
+           "value": 2.0 * B * N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "iters_per_s": 1e3 / ms,
+           "sampler": "host numpy (reference sample_minibatch), indices uploaded every step"}
+    pf = DevicePlan(scn, dtype=w.dtype, device=eng.plan.device, max_batch=M)
+    ef = SPGMEngine(pf, eng.y, eng.eta, eng.alpha, initial=eng.s)
+    ef.stage(np.arange(M))
+    ms_full = timed(ef.step_staged, 1, 3)
+    out["ista_full_batch"] = {"batch": M, "structured": pf.staged_structured, "value": 2.0 * M * N / (ms_full * 1e-3),
+                              "unit": UNIT, "ms_per_step": ms_full}
+    del ef, pf
+    torch.cuda.empty_cache()
+    return out
 
 
 def ncu_traffic(kernel: str):

@@ -22,8 +22,9 @@ from .geometry import ImagingScenario
 DTYPES = {"c64": (_lib.NF_C64, torch.complex64), "c128": (_lib.NF_C128, torch.complex128)}
 
 # Structured (Cartesian) batches with at least this many (tx, rx) pairs per frequency take the
-# separable kernels (nf_batch_prepare_structured); smaller ones stay on the flat path.
-STRUCT_MIN_PAIRS = 16
+# separable kernels (nf_batch_prepare_structured); smaller ones stay on the flat path. On Large
+# the two paths break even at 8 × 8 pairs (tools/time_structured.py, profiles/r01_structured.jsonl).
+STRUCT_MIN_PAIRS = 64
 STRUCT_POLICIES = ("auto", "always", "never")
 
 
