@@ -1605,6 +1605,329 @@ __global__ void __launch_bounds__(SW * 32, NFGPU_MINB_STRUCT) fwd_struct_kernel(
   stage_wait();
 }
 
+// ------------------------------------------------------------------ structured adjoint on tcgen05
+//
+// Per (tile, f) the structured adjoint's contraction is a real GEMM (c64 only):
+//   Z[n][2t+c'] = Σ_k A[n][k] · B[2t+c'][k],   k = 2r + c,
+//   A[n][2r] + j·A[n][2r+1] = conj(V_fr(n))  (generated on the fly),
+//   B = the 2x2 real form [[wr, wi], [-wi, wr]] of w_ftr  (prepared once per launch),
+// so Re/Im z_ft(n) = Z[n][2t], Z[n][2t+1], then g(n) += Σ_t conj(U_ft(n))·z_ft(n).
+// tcgen05.mma kind::tf32 with a 3xTF32 split (hi·hi + hi·lo + lo·hi) keeps fp32-level
+// accuracy (tools/umma_probe.cu: 3.9e-7 relative L2).
+//
+// A CTA owns half a tile (128 table positions = one M=128 block) and a range of frequencies.
+// At start it stages the half-tile's table rows of every batch antenna in shared memory (bulk
+// copies), so the phasor work reads shared memory only. K runs in chunks of 16 receivers:
+// 512 threads (4 per voxel row) generate the A chunk into one of two shared-memory stages,
+// B chunks arrive by bulk copy, and one thread issues the MMAs into one of two TMEM regions per
+// frequency. The epilogue of frequency f-1 (tcgen05.ld, conj(U) phasors, complex MACs) runs
+// while the tensor core works on frequency f. Each CTA publishes its half-tile partial through
+// the flat adjoint's chunk combine (adj_epilogue), which applies the prox.
+
+#ifndef NFGPU_TC
+#define NFGPU_TC 1
+#endif
+constexpr int TC_CW = 16;                     // compute warps (4 per TMEM lane quarter)
+constexpr int TC_CT = TC_CW * 32;             // compute threads
+constexpr int TC_THREADS = TC_CT + 64;        // + B-loader warp + MMA warp
+constexpr int TC_SUB = TC_CT / 128;           // compute threads per voxel row
+constexpr int TC_RCH = 8;                     // receivers per pipeline step (K = 16 reals = two MMAs of K = 8)
+constexpr int TC_NS = 3;                      // pipeline stages
+constexpr int TC_NMAX = 128;                  // max padded 2·n_t (TMEM: 2 regions × N ≤ 256 columns)
+constexpr uint32_t TC_A_BYTES = 128 * 2 * TC_RCH * 4;  // one of hi/lo: 8 KB
+constexpr uint32_t TC_SMEM_MAX = 227 * 1024;
+
+// dynamic shared-memory layout of adj_tc_kernel (bytes), from the batch shape
+struct TcLayout {
+  uint32_t a_off, b_off, b_stage, tab_off, d0_off, par_off, bar_off, bytes;
+  __host__ __device__ TcLayout(int npad, int nant) {
+    a_off = 0;                                   // [stage][hi, lo][128 x 16]
+    b_off = TC_NS * 2 * TC_A_BYTES;              // [stage][hi, lo][npad x 16]
+    b_stage = (uint32_t)npad * 2 * TC_RCH * 4 * 2;
+    tab_off = b_off + TC_NS * b_stage;           // [antenna slot][δ 128 | 1/d 128]
+    d0_off = tab_off + (uint32_t)nant * 1024;    // [A_MAX] fp64
+    par_off = d0_off + A_MAX * 8;                // rx [2][kr 256 | br 256], tx [2][kt 64 | bt 64]
+    bar_off = par_off + (1024 + 256) * 4;        // 13 mbarriers + TMEM base
+    bytes = bar_off + 128;
+  }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// K-major, no swizzle (canonical UMMA layout): 8-row x 16-B core matrices; byte offset of
+// element (row, k) of a [rows][K] operand
+__host__ __device__ __forceinline__ uint32_t kmaj(int row, int k, int rows) {
+  return (uint32_t)((k >> 2) * (rows >> 3) * 128 + (row >> 3) * 128 + (row & 7) * 16 + (k & 3) * 4);
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // version 1, no swizzle
+}
+__host__ __device__ constexpr uint32_t umma_idesc_tf32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ float tf32_round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// amplitude-weighted one-sided phasor of one voxel: amp·(cos x, sgn·sin x), x = b + k·δ
+template <bool EXACT>
+__device__ __forceinline__ void phasor1(float k, float b, float dl, float amp, float sgn, float& re, float& im) {
+  float x = fmaf(k, dl, b);
+  if (EXACT) x = (x - ((x + 12582912.0f) - 12582912.0f)) * 6.28318530717958647692f;
+  float s, c;
+  __sincosf(x, &s, &c);
+  re = amp * c;
+  im = amp * sgn * s;
+}
+
+// B images of every (batch frequency, K chunk): [hi | lo] x [npad rows][32 k] in the smem layout
+__global__ void tc_bprep_kernel(StructArgs sa, const float2* __restrict__ wrec, int npad, int nch,
+                                float* __restrict__ out) {
+  const int fi = blockIdx.x / nch, c = blockIdx.x - fi * nch;
+  constexpr int KC = 2 * TC_RCH;
+  float* img = out + (size_t)blockIdx.x * npad * KC * 2;
+  for (int idx = threadIdx.x; idx < npad * KC; idx += blockDim.x) {
+    const int n = idx / KC, k = idx - n * KC;
+    const int t = n >> 1, cp = n & 1, q = k >> 1, cc = k & 1, r = c * TC_RCH + q;
+    float v = 0.f;
+    if (t < sa.nt && r < sa.nr) {
+      const float2 w = wrec[((size_t)fi * sa.nt + t) * sa.nr + r];
+      v = cc == 0 ? (cp == 0 ? w.x : w.y) : (cp == 0 ? -w.y : w.x);
+    }
+    const float h = tf32_round(v);
+    const uint32_t o = kmaj(n, k, npad) >> 2;
+    img[o] = h;
+    img[npad * KC + o] = v - h;
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Warp-specialised: warps 0..7 generate A stages, warps 8..15 run the epilogue (two per TMEM
+// lane quarter), warp 16 loads B, warp 17 issues the MMAs. Barriers: afull/sfree/bfull per
+// stage, zfull/zfree per TMEM region; each role keeps its own per-frequency side parameters.
+template <bool PROX, bool EXACT>
+__global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a, StructArgs sa,
+                                                               const double* __restrict__ kd,
+                                                               const float* __restrict__ bimg, int npad, int nch,
+                                                               int fch) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const TcLayout ly(npad, sa.nt + sa.nr);
+  const Geo& g = a.g;
+  const int tid = threadIdx.x, w = tid >> 5, L = tid & 31;
+  // CTA = (tile, half hb, frequency chunk fc); it is chunk hb·fch + fc of the tile for adj_epilogue
+  const int tile = blockIdx.x / (2 * fch), rem = blockIdx.x - tile * 2 * fch, hb = rem / fch, fc = rem - hb * fch;
+  double* d0 = reinterpret_cast<double*>(sm + ly.d0_off);
+  float* tsm = reinterpret_cast<float*>(sm + ly.tab_off);  // slot: δ[128], 1/d[128]; tx slots then rx slots
+  float* par = reinterpret_cast<float*>(sm + ly.par_off);  // rx [2][kr 256 | br 256], tx [2][kt 64 | bt 64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + ly.bar_off);
+  uint64_t *afull = bars, *sfree = bars + 3, *bfull = bars + 6, *zfull = bars + 9, *zfree = bars + 11;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 13);
+  const float* tabt = a.tab + (size_t)tile * g.A * TABW + hb * 128;
+  const int nant = sa.nt + sa.nr;
+  if (tid < TC_CT) {  // the half tile's table rows of every batch antenna (per-thread cp.async)
+    for (int i = tid; i < nant * 64; i += TC_CT) {
+      const int sl = i >> 6, part = i & 63, blk = part >> 5, q = part & 31;
+      const int ant = sl < sa.nt ? sa.ts[sl] : g.T + sa.rs[sl - sa.nt];
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(tsm + sl * 256 + blk * 128 + q * 4)),
+                   "l"(tabt + (size_t)ant * TABW + blk * TILE + q * 4)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int i = tid; i < g.A; i += TC_CT) d0[i] = a.D0[(size_t)tile * g.A + i];
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&afull[i], TC_CW / 2);
+      mbar_init(&sfree[i], 1);
+      mbar_init(&bfull[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&zfull[i], 1);
+      mbar_init(&zfree[i], TC_CW / 2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (w == TC_CW + 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int f0 = (int)(((long long)sa.nf * fc) / fch), f1 = (int)(((long long)sa.nf * (fc + 1)) / fch);
+  const int nfl = f1 - f0, nsteps = nfl * nch;
+  const uint32_t bbytes = ly.b_stage;
+  constexpr int HT = TC_CT / 2;  // threads per role
+
+  if (w == TC_CW) {  // ---------------- B loader
+    if (L == 0)
+      for (int s = 0; s < nsteps; ++s) {
+        const int st = s % TC_NS, k = s / TC_NS;
+        if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);
+        const int fi = f0 + s / nch, c = s % nch;
+        mbar_expect(&bfull[st], bbytes);
+        bulk_g2s(sm + ly.b_off + st * bbytes, bimg + ((size_t)fi * nch + c) * (bbytes / 4), bbytes, &bfull[st]);
+      }
+  } else if (w == TC_CW + 1) {  // ---------------- MMA issuer
+    if (L == 0) {
+      const uint32_t idesc = umma_idesc_tf32(128, npad), lboB = (uint32_t)(npad >> 3) * 128;
+      for (int s = 0; s < nsteps; ++s) {
+        const int st = s % TC_NS, k = s / TC_NS, fl = s / nch, c = s % nch;
+        mbar_wait(&afull[st], k & 1);
+        mbar_wait(&bfull[st], k & 1);
+        if (c == 0 && fl >= 2) mbar_wait(&zfree[fl & 1], ((fl - 2) >> 1) & 1);  // region read by epilogue(fl-2)
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)((fl & 1) * npad);
+        const uint32_t a0 = smem_u32(sm + ly.a_off + st * 2 * TC_A_BYTES);
+        const uint32_t b0 = smem_u32(sm + ly.b_off + st * bbytes);
+#pragma unroll
+        for (int pass = 0; pass < 3; ++pass) {
+          const int ah = pass == 2 ? 1 : 0, bh = pass == 1 ? 1 : 0;  // hi·hi, hi·lo, lo·hi
+#pragma unroll
+          for (int ks = 0; ks < 2 * TC_RCH / 8; ++ks) {
+            const uint64_t ad = umma_desc(a0 + ah * TC_A_BYTES + ks * 2 * 2048, 2048, 128);
+            const uint64_t bd = umma_desc(b0 + bh * (bbytes / 2) + ks * 2 * lboB, lboB, 128);
+            umma_tf32(d, ad, bd, idesc, (c > 0 || pass > 0 || ks > 0) ? 1u : 0u);
+          }
+        }
+        umma_commit(&sfree[st]);
+        if (c == nch - 1) umma_commit(&zfull[fl & 1]);
+      }
+    }
+  } else if (w < TC_CW / 2) {  // ---------------- A generation: conj(V) of 8 receivers per step
+    const int row = tid & 127, sub = tid >> 7;  // 2 threads per voxel row
+    for (int fl = 0; fl < nfl; ++fl) {
+      float* kr = par + (fl & 1) * 512;
+      float* br = kr + 256;
+      const double kf = kd[sa.fs[f0 + fl]];
+      for (int q = tid; q < sa.nr; q += HT) side_params<float, EXACT>(kf, d0[g.T + sa.rs[q]], kr[q], br[q]);
+      named_bar(1, HT);
+      for (int c = 0; c < nch; ++c) {
+        const int s = fl * nch + c, st = s % TC_NS, k = s / TC_NS;
+        if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);  // MMAs of step s - NS released the stage
+        unsigned char* Ast = sm + ly.a_off + st * 2 * TC_A_BYTES;
+#pragma unroll
+        for (int qq = 0; qq < TC_RCH / 2; ++qq) {
+          const int q = sub * (TC_RCH / 2) + qq, r = c * TC_RCH + q;
+          float re = 0.f, im = 0.f;
+          if (r < sa.nr) {
+            const float* rowp = tsm + (sa.nt + r) * 256 + row;
+            phasor1<EXACT>(kr[r], br[r], rowp[0], rowp[128], 1.f, re, im);
+          }
+          const float rh = tf32_round(re), ih = tf32_round(im);
+          const uint32_t off = kmaj(row, 2 * q, 128);
+          *reinterpret_cast<float2*>(Ast + off) = make_float2(rh, ih);
+          *reinterpret_cast<float2*>(Ast + TC_A_BYTES + off) = make_float2(re - rh, im - ih);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (L == 0) mbar_arrive(&afull[st]);
+      }
+    }
+  } else {  // ---------------- epilogue: g += Σ_t conj(U_t)·z_t
+    const int et = tid - HT, row = et & 127, sub = et >> 7;  // 2 threads per voxel row
+    float gr = 0.f, gi = 0.f;
+    for (int fl = 0; fl < nfl; ++fl) {
+      float* kt = par + 1024 + (fl & 1) * 128;
+      float* bt = kt + 64;
+      const double kf = kd[sa.fs[f0 + fl]];
+      for (int q = et; q < sa.nt; q += HT) side_params<float, EXACT>(kf, d0[sa.ts[q]], kt[q], bt[q]);
+      named_bar(2, HT);
+      mbar_wait(&zfull[fl & 1], (fl >> 1) & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + (uint32_t)((fl & 1) * npad) + ((uint32_t)(32 * (w & 3)) << 16);
+      for (int t4 = sub; t4 * 4 < sa.nt; t4 += 2) {
+        float z[8];
+        tmem_ld8(base + t4 * 8, z);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = t4 * 4 + j;
+          if (t < sa.nt) {
+            float ur, ui;
+            phasor1<EXACT>(kt[t], bt[t], tsm[t * 256 + row], tsm[t * 256 + 128 + row], 1.f, ur, ui);
+            gr = fmaf(ur, z[2 * j], fmaf(-ui, z[2 * j + 1], gr));
+            gi = fmaf(ur, z[2 * j + 1], fmaf(ui, z[2 * j], gi));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (L == 0) mbar_arrive(&zfree[fl & 1]);
+    }
+    // combine the two sub-threads; every MMA is complete, so the A stages are free
+    float* cb = reinterpret_cast<float*>(sm + ly.a_off);  // [2][128][2]
+    cb[(sub * 128 + row) * 2] = gr;
+    cb[(sub * 128 + row) * 2 + 1] = gi;
+    named_bar(2, HT);
+    if (w == TC_CW / 2) {
+      float Gr[V], Gi[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        Gr[v] = Gi[v] = 0.f;
+        if ((v >> 2) == hb) {
+          const int p = 4 * L + (v & 3);
+          Gr[v] = cb[p * 2] + cb[(128 + p) * 2];
+          Gi[v] = cb[p * 2 + 1] + cb[(128 + p) * 2 + 1];
+        }
+      }
+      adj_epilogue<float, PROX>(a, tile, hb * fch + fc, L, make_v(Gr), make_v(Gi));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == TC_CW + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 // sorted-order bookkeeping of a structured batch: position j = (fi·nt + ti)·nr + ri is
 // both the work order and the subset order (ascending channel id)
 __global__ void struct_prep_kernel(StructArgs sa, int T, int R, int* __restrict__ sm, int* __restrict__ spos,
@@ -1744,6 +2067,10 @@ struct nf_plan {
   bool structured = false;
   int snf = 0, snt = 0, snr = 0;
   int* d_struct = nullptr;
+  // tensor-core structured adjoint (c64): B images [batch frequency][K chunk][hi|lo][npad][16]
+  bool use_tc = false;
+  bool tc_force = false;  // NFGPU_TC=2: tensor-core adjoint whenever eligible (tests)
+  float* d_bimg = nullptr;
 };
 
 namespace {
@@ -1762,7 +2089,7 @@ void free_plan(nf_plan* p) {
   if (!p) return;
   void* ptrs[] = {p->d_ant,  p->d_kd,   p->d_kf,    p->d_pulse, p->d_tab,  p->d_D0,      p->d_pos_of_key,
                   p->d_cnt,  p->d_sm,   p->d_spos,  p->d_crec,  p->d_sf, p->d_wrec, p->d_dpart,   p->d_part,
-                  p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part, p->d_iter, p->d_struct};
+                  p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part, p->d_iter, p->d_struct, p->d_bimg};
   for (void* q : ptrs) cudaFree(q);
   delete p;
 }
@@ -1915,6 +2242,37 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   a.eta_over_b = eta_over_b;
   a.alpha = alpha;
   a.stat_part = p->d_stat_part;
+  if constexpr (std::is_same<Real, float>::value) {
+    const int npad = (2 * p->snt + 15) / 16 * 16;
+    // the tensor core pays off once the contraction dominates the phasor work: both antenna
+    // counts >= 24 and enough frequencies per tile (tools/time_structured.py crossover)
+    const int amin = std::min(p->snt, p->snr);
+    const bool worth = p->tc_force || (amin >= 24 && p->snf * amin >= 192);
+    if (p->structured && p->use_tc && worth && npad <= TC_NMAX &&
+        TcLayout(npad, p->snt + p->snr).bytes <= TC_SMEM_MAX) {
+      const StructArgs sa = struct_args(p);
+      const int nch = (sa.nr + TC_RCH - 1) / TC_RCH;
+      tc_bprep_kernel<<<sa.nf * nch, 256, 0, st>>>(sa, (const float2*)p->d_wrec, npad, nch, p->d_bimg);
+      CUDA_TRY(cudaGetLastError());
+      // one CTA per SM, two per tile (halves); split frequencies for at least two waves
+      int fch = (int)std::min<long long>(sa.nf, std::max<long long>(1, (2LL * 148 + 2 * p->g.ntiles - 1) /
+                                                                          (2 * p->g.ntiles)));
+      fch = std::max(1, std::min(fch, p->adj_ch_cap / 2));
+      a.CH = 2 * fch;
+      const uint32_t smem = TcLayout(npad, sa.nt + sa.nr).bytes;
+      auto kern = p->exact ? adj_tc_kernel<PROX, true> : adj_tc_kernel<PROX, false>;
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<(unsigned)(p->g.ntiles * a.CH), TC_THREADS, smem, st>>>(a, sa, p->d_kd, p->d_bimg, npad, nch, fch);
+      CUDA_TRY(cudaGetLastError());
+      p->launches += 3;
+      if (PROX) {
+        stats_reduce_kernel<<<1, 256, 0, st>>>(p->d_stat_part, p->g.ntiles, p->d_dpart, nblk, stats);
+        CUDA_TRY(cudaGetLastError());
+        p->launches += 1;
+      }
+      return NF_OK;
+    }
+  }
   if (p->structured) {
     const StructArgs sa = struct_args(p);
     a.CH = std::min(struct_splits(p->struct_target, p->g.ntiles, sa.nf * sa.nt), p->adj_ch_cap);
@@ -2058,6 +2416,15 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   ALLOC(p->d_stat_part, sizeof(double) * 4 * (size_t)g.ntiles);
   ALLOC(p->d_iter, sizeof(unsigned long long));
   ALLOC(p->d_struct, sizeof(int) * (size_t)(n_f + n_tx + n_rx));
+  p->use_tc = NFGPU_TC && dtype == NF_C64 && 2 * n_tx <= TC_NMAX;
+  if (const char* e = std::getenv("NFGPU_TC")) {
+    p->use_tc = p->use_tc && std::atoi(e) != 0;
+    p->tc_force = std::atoi(e) == 2;
+  }
+  if (p->use_tc) {
+    const size_t npad_max = (size_t)((2 * n_tx + 15) / 16) * 16;
+    ALLOC(p->d_bimg, (size_t)n_f * ((n_rx + TC_RCH - 1) / TC_RCH) * npad_max * (2 * TC_RCH) * 4 * 2);
+  }
 #undef ALLOC
   auto cp = [&](void* dst, const void* src, size_t n) -> int {
     cudaError_t e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);

@@ -48,6 +48,21 @@ def ragged_scenario(n_tx=5, n_rx=11, n_f=4, dims=(13, 6, 5)):
                            voxels=VoxelGrid(center=Vec3(0, 0, 0.35), extent=(0.1, 0.06, 0.05), dims=dims))
 
 
+@pytest.fixture(params=["ffma", "tc"])
+def adj_kernel(request, monkeypatch):
+    """Structured c64 adjoint on the FFMA kernel (NFGPU_TC=0) or forced onto the tcgen05 kernel
+    (NFGPU_TC=2, whatever the batch shape); read at plan creation."""
+    monkeypatch.setenv("NFGPU_TC", "0" if request.param == "ffma" else "2")
+    return request.param
+
+
+def adjoint_launches(plan, r):
+    """Kernel launches of one plain adjoint: 2 on the FFMA path, 3 on the tensor-core path (B prep)."""
+    n0 = plan.info()["launches"]
+    plan.adjoint(r)
+    return plan.info()["launches"] - n0
+
+
 def draw(rng, n, k):
     return np.sort(rng.choice(n, size=k, replace=False)).astype(np.int32)
 
@@ -71,7 +86,9 @@ def test_cartesian_detection():
 
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("builder", [small, ragged_scenario], ids=["small", "ragged"])
-def test_structured_matches_oracle(builder, dtype):
+def test_structured_matches_oracle(builder, dtype, adj_kernel):
+    if dtype == "c128" and adj_kernel == "tc":
+        pytest.skip("the tensor-core adjoint is c64 only")
     scn = builder()
     plan = DevicePlan(scn, dtype=dtype)
     g = O.geom_from_scenario(scn)
@@ -108,7 +125,9 @@ def test_structured_equals_flat_on_medium_full_set(dtype):
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_structured_adjoint_prox_equals_flat(dtype):
+def test_structured_adjoint_prox_equals_flat(dtype, adj_kernel):
+    if dtype == "c128" and adj_kernel == "tc":
+        pytest.skip("the tensor-core adjoint is c64 only")
     scn = configs.medium_scenario()
     plan = DevicePlan(scn, dtype=dtype)
     rng = np.random.default_rng(8)
@@ -132,6 +151,8 @@ def test_structured_adjoint_prox_equals_flat(dtype):
     tol = {"c128": 1e-11, "c64": 1e-5}[dtype]
     assert rel_l2(outs[1][0], outs[0][0]) <= tol
     assert np.allclose(outs[1][1], outs[0][1], rtol=tol * 10)
+    if dtype == "c64":
+        assert adjoint_launches(plan, r) == (3 if adj_kernel == "tc" else 2)
     # ½‖r − y_B‖²: same terms, summed in each path's own sorted order
     assert outs[1][1][2] == pytest.approx(outs[0][1][2], rel=1e-12)
 
@@ -155,6 +176,28 @@ def test_structured_slab_plans_sum_to_full():
     assert rel_l2(y_sum, y_full) <= 1e-12
     # voxel-local; the chunk count (summation order over channels) follows the slab's tile count
     assert rel_l2(np.concatenate(g_cat), g_full) <= 1e-12
+
+
+@pytest.mark.parametrize("comp", [(3, 48, 48), (2, 24, 40), (5, 7, 33)])
+def test_tensor_core_adjoint_shapes(comp, monkeypatch):
+    """The tcgen05 adjoint (forced) on Large sub-slabs: several K chunks, padded N (2·n_t not a
+    multiple of 16), receivers not a multiple of the 8-receiver step, against the direct formula."""
+    monkeypatch.setenv("NFGPU_TC", "2")
+    scn = configs.large_scenario()
+    z = (20, 24)
+    plan = DevicePlan(scn, dtype="c64", z_range=z)
+    g = O.geom_from_scenario(scn, z_range=z)
+    rng = np.random.default_rng(sum(comp))
+    T, R, F = scn.array.n_tx, scn.array.n_rx, scn.frequencies.count
+    fs, ts, rs = draw(rng, F, comp[0]), draw(rng, T, comp[1]), draw(rng, R, comp[2])
+    idx = product_indices(fs, ts, rs, T, R)
+    r = rc(rng, idx.size)
+    plan.prepare_structured(fs, ts, rs)
+    rd = plan._as_dev(r, plan.B, "r")
+    assert adjoint_launches(plan, rd) == 3
+    gg = plan.adjoint(rd).to(torch.complex128).cpu().numpy()
+    vox = rng.choice(plan.n_local, 96, replace=False)
+    assert rel_l2(gg[vox], O.direct_adjoint(g, r, idx, voxels=vox)) <= 1e-5
 
 
 def test_structured_large_window_chunking():
