@@ -1632,7 +1632,8 @@ constexpr int TC_CT = TC_CW * 32;             // compute threads
 constexpr int TC_THREADS = TC_CT + 64;        // + B-loader warp + MMA warp
 constexpr int TC_SUB = TC_CT / 128;           // compute threads per voxel row
 constexpr int TC_RCH = 8;                     // receivers per pipeline step (K = 16 reals = two MMAs of K = 8)
-constexpr int TC_NS = 3;                      // pipeline stages
+constexpr int TC_NS = 4;                      // adjoint pipeline stages
+constexpr int TCF_NS = 5;                     // forward pipeline stages
 constexpr int TC_NMAX = 128;                  // max padded 2·n_t (TMEM: 2 regions × N ≤ 256 columns)
 constexpr uint32_t TC_A_BYTES = 128 * 2 * TC_RCH * 4;  // one of hi/lo: 8 KB
 constexpr uint32_t TC_SMEM_MAX = 227 * 1024;
@@ -1647,8 +1648,8 @@ struct TcLayout {
     tab_off = b_off + TC_NS * b_stage;           // [antenna slot][δ 128 | 1/d 128]
     d0_off = tab_off + (uint32_t)nant * 1024;    // [A_MAX] fp64
     par_off = d0_off + A_MAX * 8;                // rx [2][kr 256 | br 256], tx [2][kt 64 | bt 64]
-    bar_off = par_off + (1024 + 256) * 4;        // 13 mbarriers + TMEM base
-    bytes = bar_off + 128;
+    bar_off = par_off + (1024 + 256) * 4;        // 3·NS + 4 mbarriers + TMEM base
+    bytes = bar_off + (3 * TC_NS + 6) * 8;
   }
 };
 
@@ -1768,8 +1769,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
   float* tsm = reinterpret_cast<float*>(sm + ly.tab_off);  // slot: δ[128], 1/d[128]; tx slots then rx slots
   float* par = reinterpret_cast<float*>(sm + ly.par_off);  // rx [2][kr 256 | br 256], tx [2][kt 64 | bt 64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + ly.bar_off);
-  uint64_t *afull = bars, *sfree = bars + 3, *bfull = bars + 6, *zfull = bars + 9, *zfree = bars + 11;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t *afull = bars, *sfree = bars + TC_NS, *bfull = bars + 2 * TC_NS, *zfull = bars + 3 * TC_NS,
+           *zfree = bars + 3 * TC_NS + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3 * TC_NS + 4);
   const float* tabt = a.tab + (size_t)tile * g.A * TABW + hb * 128;
   const int nant = sa.nt + sa.nr;
   if (tid < TC_CT) {  // the half tile's table rows of every batch antenna (per-thread cp.async)
@@ -1784,7 +1786,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
     for (int i = tid; i < g.A; i += TC_CT) d0[i] = a.D0[(size_t)tile * g.A + i];
   }
   if (tid == 0) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < TC_NS; ++i) {
       mbar_init(&afull[i], TC_CW / 2);
       mbar_init(&sfree[i], 1);
       mbar_init(&bfull[i], 1);
@@ -1857,17 +1859,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);  // MMAs of step s - NS released the stage
         unsigned char* Ast = sm + ly.a_off + st * 2 * TC_A_BYTES;
 #pragma unroll
-        for (int qq = 0; qq < TC_RCH / 2; ++qq) {
-          const int q = sub * (TC_RCH / 2) + qq, r = c * TC_RCH + q;
-          float re = 0.f, im = 0.f;
-          if (r < sa.nr) {
-            const float* rowp = tsm + (sa.nt + r) * 256 + row;
-            phasor1<EXACT>(kr[r], br[r], rowp[0], rowp[128], 1.f, re, im);
+        for (int qq = 0; qq < TC_RCH / 2; qq += 2) {  // two receivers = one 16-B chunk of the row
+          const int q = sub * (TC_RCH / 2) + qq;
+          float v4[4];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = c * TC_RCH + q + e;
+            v4[2 * e] = v4[2 * e + 1] = 0.f;
+            if (r < sa.nr) {
+              const float* rowp = tsm + (sa.nt + r) * 256 + row;
+              phasor1<EXACT>(kr[r], br[r], rowp[0], rowp[128], 1.f, v4[2 * e], v4[2 * e + 1]);
+            }
           }
-          const float rh = tf32_round(re), ih = tf32_round(im);
+          const float4 h = make_float4(tf32_round(v4[0]), tf32_round(v4[1]), tf32_round(v4[2]), tf32_round(v4[3]));
           const uint32_t off = kmaj(row, 2 * q, 128);
-          *reinterpret_cast<float2*>(Ast + off) = make_float2(rh, ih);
-          *reinterpret_cast<float2*>(Ast + TC_A_BYTES + off) = make_float2(re - rh, im - ih);
+          *reinterpret_cast<float4*>(Ast + off) = h;
+          *reinterpret_cast<float4*>(Ast + TC_A_BYTES + off) =
+              make_float4(v4[0] - h.x, v4[1] - h.y, v4[2] - h.z, v4[3] - h.w);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -1926,6 +1934,234 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
   tc_fence_before();
   __syncthreads();
   if (w == TC_CW + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// ------------------------------------------------------------------ structured forward on tcgen05
+//
+// Per (half tile, f) the structured forward is a real GEMM (c64 only):
+//   D[2t+c'][r] = Σ_k A[2t+c'][k] · B[r][k],   k = 2v + c over the half tile's 128 voxels,
+//   A = the 2x2 real form [[Ur, -Ui], [Ui, Ur]] of U_ft(v),  B[r][2v] + j·B[r][2v+1] = V_fr(v)·s_v,
+// so D[2t][r] + j·D[2t+1][r] = Σ_v U_ft(v)·V_fr(v)·s_v. Both operands are generated on the fly
+// (3xTF32 split), 8 voxels (K = 16) per pipeline step. Warps 0..7 generate, warps 8..15 drain TMEM
+// (the pair of lanes 2t, 2t+1 combined by a shuffle) into one partial per (half tile, channel),
+// warp 17 issues the MMAs; fwd_reduce1/2 finish the sum over the 2·tiles partial rows.
+
+struct TcfLayout {
+  uint32_t a_off, b_off, b_stage, s_off, tab_off, d0_off, par_off, bar_off, bytes;
+  __host__ __device__ TcfLayout(int npr, int nant) {
+    a_off = 0;                                  // [stage][hi, lo][128 x 16]
+    b_off = TCF_NS * 2 * 128 * 16 * 4;          // [stage][hi, lo][npr x 16]
+    b_stage = (uint32_t)npr * 16 * 4 * 2;
+    s_off = b_off + TCF_NS * b_stage;           // s of the half tile: [128] complex
+    tab_off = s_off + 128 * 8;                  // [voxel 128][slot, stride nant|1] (δ, 1/d)
+    d0_off = tab_off + (uint32_t)(nant | 1) * 1024;
+    par_off = d0_off + A_MAX * 8;               // [2][kt 64 | bt 64 | kr 256 | br 256]
+    bar_off = par_off + 2 * 640 * 4;
+    bytes = bar_off + (2 * TCF_NS + 6) * 8;
+  }
+};
+
+template <bool EXACT>
+__global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a, StructArgs sa,
+                                                               const double* __restrict__ kd, int npr, int fa, int fb,
+                                                               int fch, float2* __restrict__ part) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const TcfLayout ly(npr, sa.nt + sa.nr);
+  const Geo& g = a.g;
+  const int tid = threadIdx.x, w = tid >> 5, L = tid & 31;
+  const int tile = blockIdx.x / (2 * fch), rem = blockIdx.x - tile * 2 * fch, hb = rem / fch, fc = rem - hb * fch;
+  float2* ssm = reinterpret_cast<float2*>(sm + ly.s_off);
+  double* d0 = reinterpret_cast<double*>(sm + ly.d0_off);
+  float2* tv = reinterpret_cast<float2*>(sm + ly.tab_off);  // voxel-major: [vi * TS + slot] = (δ, 1/d)
+  float* par = reinterpret_cast<float*>(sm + ly.par_off);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + ly.bar_off);
+  uint64_t *afull = bars, *sfree = bars + TCF_NS, *zfull = bars + 2 * TCF_NS, *zfree = bars + 2 * TCF_NS + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * TCF_NS + 4);
+  const float* tabt = a.tab + (size_t)tile * g.A * TABW + hb * 128;
+  const int nant = sa.nt + sa.nr, mrows = 2 * sa.nt;
+  const int TS = nant | 1;  // odd slot stride: neighbouring voxels of one slot land in different banks
+  uint32_t tcols = 32;
+  while (tcols < 2u * npr) tcols <<= 1;
+  if (tid < TC_CT) {
+    for (int i = tid; i < nant * 128; i += TC_CT) {  // coalesced global reads, transposed into smem
+      const int sl = i >> 7, vi = i & 127;
+      const int ant = sl < sa.nt ? sa.ts[sl] : g.T + sa.rs[sl - sa.nt];
+      const float* src = tabt + (size_t)ant * TABW + vi;
+      tv[vi * TS + sl] = make_float2(src[0], src[TILE]);
+    }
+    for (int i = tid; i < g.A; i += TC_CT) d0[i] = a.D0[(size_t)tile * g.A + i];
+    if (tid < 128) {  // s at the half tile's table positions
+      int tx, ty, tz;
+      tile_coords(g, tile, tx, ty, tz);
+      const int p = hb * 128 + tid, Lp = (p & 127) >> 2, v = 4 * (p >> 7) + (p & 3);
+      int x0, y, z;
+      lane_voxel(tx, ty, tz, Lp, x0, y, z);
+      const int x = x0 + v;
+      float2 sv = make_float2(0.f, 0.f);
+      if (x < g.nx && y < g.ny && z < g.nzs) {
+        const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
+        sv = make_float2(a.s[2 * n], a.s[2 * n + 1]);
+      }
+      ssm[tid] = sv;
+    }
+    // zero the padding rows of every stage once (A rows >= 2 n_t, B rows >= n_r); generation never writes them
+    for (int st = 0; st < TCF_NS; ++st)
+      for (int hl = 0; hl < 2; ++hl) {
+        float* A0 = reinterpret_cast<float*>(sm + ly.a_off + (st * 2 + hl) * 8192);
+        for (int i = tid; i < (128 - mrows) * 16; i += TC_CT) A0[kmaj(mrows + i / 16, i % 16, 128) >> 2] = 0.f;
+        float* B0 = reinterpret_cast<float*>(sm + ly.b_off + st * ly.b_stage + hl * (ly.b_stage / 2));
+        for (int i = tid; i < (npr - sa.nr) * 16; i += TC_CT) B0[kmaj(sa.nr + i / 16, i % 16, npr) >> 2] = 0.f;
+      }
+  }
+  if (tid == 0) {
+    for (int i = 0; i < TCF_NS; ++i) {
+      mbar_init(&afull[i], TC_CW);
+      mbar_init(&sfree[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&zfull[i], 1);
+      mbar_init(&zfree[i], TC_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (w == TC_CW + 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the zero padding is read by the MMAs
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int nwin = fb - fa;
+  const int f0 = fa + (int)(((long long)nwin * fc) / fch), f1 = fa + (int)(((long long)nwin * (fc + 1)) / fch);
+  const int nfl = f1 - f0;
+  constexpr int SPF = 128 / 8;  // pipeline steps per frequency (8 voxels each)
+  const int nsteps = nfl * SPF;
+
+  if (w == TC_CW + 1) {  // ---------------- MMA issuer
+    if (L == 0) {
+      const uint32_t idesc = umma_idesc_tf32(128, npr), lboB = (uint32_t)(npr >> 3) * 128;
+      for (int s = 0; s < nsteps; ++s) {
+        const int st = s % TCF_NS, k = s / TCF_NS, fl = s / SPF, c = s % SPF;
+        mbar_wait(&afull[st], k & 1);
+        if (c == 0 && fl >= 2) mbar_wait(&zfree[fl & 1], ((fl - 2) >> 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)((fl & 1) * npr);
+        const uint32_t a0 = smem_u32(sm + ly.a_off + st * 2 * 8192);
+        const uint32_t b0 = smem_u32(sm + ly.b_off + st * ly.b_stage);
+#pragma unroll
+        for (int pass = 0; pass < 3; ++pass) {
+          const int ah = pass == 2 ? 1 : 0, bh = pass == 1 ? 1 : 0;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint64_t ad = umma_desc(a0 + ah * 8192 + ks * 2 * 2048, 2048, 128);
+            const uint64_t bd = umma_desc(b0 + bh * (ly.b_stage / 2) + ks * 2 * lboB, lboB, 128);
+            umma_tf32(d, ad, bd, idesc, (c > 0 || pass > 0 || ks > 0) ? 1u : 0u);
+          }
+        }
+        umma_commit(&sfree[st]);
+        if (c == SPF - 1) umma_commit(&zfull[fl & 1]);
+      }
+    }
+  } else if (w < TC_CW) {  // ---------------- compute warps: generate U (A) and W = V·s (B); drain TMEM
+    const int span = a.w1 - a.w0;
+    float2* out = part + (size_t)(2 * tile + hb) * span - a.w0;
+    // epilogue of local frequency fl: TMEM rows 2t, 2t+1 -> one complex partial per (half tile, channel);
+    // the four warps of a lane quarter take every fourth 16-receiver column chunk
+    auto epilogue = [&](int fl) {
+      mbar_wait(&zfull[fl & 1], (fl >> 1) & 1);
+      tc_fence_after();
+      const int row = 32 * (w & 3) + L, t = row >> 1, cp = row & 1;
+      if (32 * (w & 3) < mrows) {
+        const uint32_t base = tmem + (uint32_t)((fl & 1) * npr) + ((uint32_t)(32 * (w & 3)) << 16);
+        const int jb = (f0 + fl) * sa.nt * sa.nr;
+        for (int r16 = w >> 2; r16 * 16 < sa.nr; r16 += TC_CW / 4) {
+          uint32_t rr[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]),
+                "=r"(rr[7]), "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]), "=r"(rr[12]), "=r"(rr[13]),
+                "=r"(rr[14]), "=r"(rr[15])
+              : "r"(base + r16 * 16));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float v = __uint_as_float(rr[j]);
+            const float o = __shfl_xor_sync(FULL, v, 1);
+            const int r = r16 * 16 + j;
+            if (cp == 0 && t < sa.nt && r < sa.nr) out[jb + t * sa.nr + r] = make_float2(v, o);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (L == 0) mbar_arrive(&zfree[fl & 1]);
+    };
+    constexpr int EPI_STEP = 4;  // drain frequency f-1 this many steps into f (its MMAs are done by then)
+    for (int fl = 0; fl < nfl; ++fl) {
+      float* kt = par + (fl & 1) * 640;
+      float* bt = kt + 64;
+      float* kr = kt + 128;
+      float* br = kt + 384;
+      const double kf = kd[sa.fs[f0 + fl]];
+      for (int q = tid; q < sa.nt; q += TC_CT) side_params<float, EXACT>(kf, d0[sa.ts[q]], kt[q], bt[q]);
+      for (int q = tid; q < sa.nr; q += TC_CT) side_params<float, EXACT>(kf, d0[g.T + sa.rs[q]], kr[q], br[q]);
+      named_bar(1, TC_CT);
+      for (int c = 0; c < SPF; ++c) {
+        const int s = fl * SPF + c, st = s % TCF_NS, k = s / TCF_NS;
+        if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);
+        unsigned char* Ast = sm + ly.a_off + st * 2 * 8192;
+        unsigned char* Bst = sm + ly.b_off + st * ly.b_stage;
+        // U (A operand): lane m of a row pair computes voxel 2vp + (m & 1) of transmitter m >> 1 and
+        // swaps with lane m ^ 1; each lane then writes its own row's 16-B chunk (conflict-free)
+        for (int i = tid; i < mrows * 4; i += TC_CT) {
+          const int m = i % mrows, vp = i / mrows, tt = m >> 1, vi = c * 8 + 2 * vp + (m & 1);
+          float ur, ui;
+          const float2 e = tv[vi * TS + tt];
+          phasor1<EXACT>(kt[tt], bt[tt], e.x, e.y, -1.f, ur, ui);
+          const unsigned pm = __activemask();
+          const float pr = __shfl_xor_sync(pm, ur, 1), pi = __shfl_xor_sync(pm, ui, 1);
+          const float r0 = (m & 1) ? pr : ur, i0 = (m & 1) ? pi : ui;  // voxel 2vp
+          const float r1 = (m & 1) ? ur : pr, i1 = (m & 1) ? ui : pi;  // voxel 2vp + 1
+          const float4 q = (m & 1) ? make_float4(i0, r0, i1, r1) : make_float4(r0, -i0, r1, -i1);
+          const float4 h = make_float4(tf32_round(q.x), tf32_round(q.y), tf32_round(q.z), tf32_round(q.w));
+          const uint32_t o = kmaj(m, 4 * vp, 128);
+          *reinterpret_cast<float4*>(Ast + o) = h;
+          *reinterpret_cast<float4*>(Ast + 8192 + o) = make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
+        }
+        // W = V·s (B operand): one receiver row, two voxels, one 16-B chunk per thread
+        for (int i = tid; i < sa.nr * 4; i += TC_CT) {
+          const int r = i % sa.nr, vp = i / sa.nr;
+          const float2* colp = tv + (c * 8 + 2 * vp) * TS + sa.nt + r;
+          float w4[4];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            float vr, vim;
+            const float2 tb = colp[e * TS];
+            phasor1<EXACT>(kr[r], br[r], tb.x, tb.y, -1.f, vr, vim);
+            const float2 sv = ssm[c * 8 + 2 * vp + e];
+            w4[2 * e] = vr * sv.x - vim * sv.y;
+            w4[2 * e + 1] = vr * sv.y + vim * sv.x;
+          }
+          const float4 h = make_float4(tf32_round(w4[0]), tf32_round(w4[1]), tf32_round(w4[2]), tf32_round(w4[3]));
+          const uint32_t o = kmaj(r, 4 * vp, npr);
+          *reinterpret_cast<float4*>(Bst + o) = h;
+          *reinterpret_cast<float4*>(Bst + ly.b_stage / 2 + o) =
+              make_float4(w4[0] - h.x, w4[1] - h.y, w4[2] - h.z, w4[3] - h.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (L == 0) mbar_arrive(&afull[st]);
+        if (fl > 0 && c == EPI_STEP) epilogue(fl - 1);
+      }
+    }
+    if (nfl > 0) epilogue(nfl - 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == TC_CW + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
 }
 
 // sorted-order bookkeeping of a structured batch: position j = (fi·nt + ti)·nr + ri is
@@ -2069,8 +2305,12 @@ struct nf_plan {
   int* d_struct = nullptr;
   // tensor-core structured adjoint (c64): B images [batch frequency][K chunk][hi|lo][npad][16]
   bool use_tc = false;
-  bool tc_force = false;  // NFGPU_TC=2: tensor-core adjoint whenever eligible (tests)
+  bool tc_force = false;  // NFGPU_TC=2: tensor-core kernels whenever eligible (tests)
+  bool tc_fwd = false;    // NFGPU_TC_FWD=1: route structured forwards to the tcgen05 forward
   float* d_bimg = nullptr;
+  // tensor-core structured forward: per-(half tile, channel) partials, allocated on first use
+  float2* d_tcpart = nullptr;
+  size_t tcpart_elems = 0;
 };
 
 namespace {
@@ -2089,7 +2329,7 @@ void free_plan(nf_plan* p) {
   if (!p) return;
   void* ptrs[] = {p->d_ant,  p->d_kd,   p->d_kf,    p->d_pulse, p->d_tab,  p->d_D0,      p->d_pos_of_key,
                   p->d_cnt,  p->d_sm,   p->d_spos,  p->d_crec,  p->d_sf, p->d_wrec, p->d_dpart,   p->d_part,
-                  p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part, p->d_iter, p->d_struct, p->d_bimg};
+                  p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part, p->d_iter, p->d_struct, p->d_bimg, p->d_tcpart};
   for (void* q : ptrs) cudaFree(q);
   delete p;
 }
@@ -2181,6 +2421,69 @@ int struct_splits(long long target_blocks, int ntiles, int rows) {
   return (int)std::max(1LL, q);
 }
 
+// tensor-core structured forward (c64): windows of whole frequencies, 2·tiles partial rows
+int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
+  const StructArgs sa = struct_args(p);
+  const int npr = (sa.nr + 15) / 16 * 16;
+  const long long rows = 2LL * p->g.ntiles, per_f = (long long)sa.nt * sa.nr;
+  // partial buffer: up to 2 GB, at least one frequency; windows of whole frequencies
+  long long fwin = std::max(1LL, std::min<long long>(sa.nf, (2LL << 30) / (rows * 8 * per_f)));
+  fwin = std::min<long long>(fwin, std::max(1LL, (long long)RED_THREADS / per_f));
+  const size_t need = (size_t)(rows * per_f * fwin);
+  if (need > p->tcpart_elems) {
+    cudaFree(p->d_tcpart);
+    p->d_tcpart = nullptr;
+    p->tcpart_elems = 0;
+    int rc = dalloc(p, &p->d_tcpart, need * sizeof(float2));
+    if (rc) return rc;
+    p->tcpart_elems = need;
+  }
+  const uint32_t smem = TcfLayout(npr, sa.nt + sa.nr).bytes;
+  auto kern = p->exact ? fwd_tc_kernel<true> : fwd_tc_kernel<false>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int fa = 0; fa < sa.nf; fa += (int)fwin) {
+    const int fb = std::min(sa.nf, fa + (int)fwin);
+    FwdArgs<float> a;
+    a.g = p->g;
+    a.tab = (const float*)p->d_tab;
+    a.D0 = p->d_D0;
+    a.crec = nullptr;
+    a.s = (const float*)s;
+    a.w0 = (int)(fa * per_f);
+    a.w1 = (int)(fb * per_f);
+    a.Q = 1;
+    a.part = nullptr;
+    const int span = a.w1 - a.w0;
+    // one CTA per SM, two per tile: split the window's frequencies for at least two waves
+    const int fch = (int)std::min<long long>(fb - fa, std::max<long long>(1, (2LL * 148 + rows - 1) / rows));
+    kern<<<(unsigned)(rows * fch), TC_THREADS, smem, st>>>(a, sa, p->d_kd, npr, fa, fb, fch, p->d_tcpart);
+    CUDA_TRY(cudaGetLastError());
+    int nseg = (int)std::ceil(std::sqrt((double)rows));
+    nseg = std::max(1, std::min({nseg, (int)rows, std::max(1, RED_THREADS / span)}));
+    fwd_reduce1_kernel<float><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const float*)p->d_tcpart, (int)rows,
+                                                                              span, nseg, p->d_tmp);
+    CUDA_TRY(cudaGetLastError());
+    fwd_reduce2_kernel<float><<<(span + 255) / 256, 256, 0, st>>>(p->d_tmp, span, nseg, a.w0, p->d_sf, p->d_spos,
+                                                                  p->d_pulse, (float*)y);
+    CUDA_TRY(cudaGetLastError());
+    p->launches += 3;
+  }
+  return NF_OK;
+}
+
+bool use_tc_struct(const nf_plan* p, bool forward) {
+  if (!p->structured || !p->use_tc || 2 * p->snt > TC_NMAX) return false;
+  const int amin = std::min(p->snt, p->snr);
+  // the tensor core pays off once the contraction dominates the phasor work: both antenna
+  // counts >= 24 and enough frequencies per tile (tools/time_structured.py crossover)
+  if (!p->tc_force && !(amin >= 24 && p->snf * amin >= 192)) return false;
+  if (forward) {  // the tcgen05 forward is not yet faster than the FFMA one: opt-in
+    if (!p->tc_force && !p->tc_fwd) return false;
+    return p->snr <= 256 && TcfLayout((p->snr + 15) / 16 * 16, p->snt + p->snr).bytes <= TC_SMEM_MAX;
+  }
+  return TcLayout((2 * p->snt + 15) / 16 * 16, p->snt + p->snr).bytes <= TC_SMEM_MAX;
+}
+
 template <typename Real>
 int launch_forward_struct(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const size_t sm = struct_smem<Real, true>(p);
@@ -2244,12 +2547,7 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   a.stat_part = p->d_stat_part;
   if constexpr (std::is_same<Real, float>::value) {
     const int npad = (2 * p->snt + 15) / 16 * 16;
-    // the tensor core pays off once the contraction dominates the phasor work: both antenna
-    // counts >= 24 and enough frequencies per tile (tools/time_structured.py crossover)
-    const int amin = std::min(p->snt, p->snr);
-    const bool worth = p->tc_force || (amin >= 24 && p->snf * amin >= 192);
-    if (p->structured && p->use_tc && worth && npad <= TC_NMAX &&
-        TcLayout(npad, p->snt + p->snr).bytes <= TC_SMEM_MAX) {
+    if (use_tc_struct(p, false)) {
       const StructArgs sa = struct_args(p);
       const int nch = (sa.nr + TC_RCH - 1) / TC_RCH;
       tc_bprep_kernel<<<sa.nf * nch, 256, 0, st>>>(sa, (const float2*)p->d_wrec, npad, nch, p->d_bimg);
@@ -2421,6 +2719,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     p->use_tc = p->use_tc && std::atoi(e) != 0;
     p->tc_force = std::atoi(e) == 2;
   }
+  if (const char* e = std::getenv("NFGPU_TC_FWD")) p->tc_fwd = std::atoi(e) != 0;
   if (p->use_tc) {
     const size_t npad_max = (size_t)((2 * n_tx + 15) / 16) * 16;
     ALLOC(p->d_bimg, (size_t)n_f * ((n_rx + TC_RCH - 1) / TC_RCH) * npad_max * (2 * TC_RCH) * 4 * 2);
@@ -2537,6 +2836,7 @@ int nf_forward(nf_plan* p, const void* s, void* y, void* stream) {
   if (!p || !s || !y) return fail(NF_ERR_ARG, "null argument");
   if (p->B < 1) return fail(NF_ERR_STATE, "no batch staged (call nf_batch_prepare first)");
   cudaStream_t st = (cudaStream_t)stream;
+  if (p->structured && p->dtype == NF_C64 && use_tc_struct(p, true)) return launch_forward_tc(p, s, y, st);
   if (p->structured)
     return p->dtype == NF_C64 ? launch_forward_struct<float>(p, s, y, st) : launch_forward_struct<double>(p, s, y, st);
   return p->dtype == NF_C64 ? launch_forward<float>(p, s, y, st) : launch_forward<double>(p, s, y, st);

@@ -179,9 +179,10 @@ def test_structured_slab_plans_sum_to_full():
 
 
 @pytest.mark.parametrize("comp", [(3, 48, 48), (2, 24, 40), (5, 7, 33)])
-def test_tensor_core_adjoint_shapes(comp, monkeypatch):
-    """The tcgen05 adjoint (forced) on Large sub-slabs: several K chunks, padded N (2·n_t not a
-    multiple of 16), receivers not a multiple of the 8-receiver step, against the direct formula."""
+def test_tensor_core_shapes(comp, monkeypatch):
+    """The tcgen05 forward and adjoint (forced) on Large sub-slabs: several K chunks, padded M/N
+    (2·n_t, n_r not multiples of 16), receivers not a multiple of the 8-receiver step, against the
+    direct formula."""
     monkeypatch.setenv("NFGPU_TC", "2")
     scn = configs.large_scenario()
     z = (20, 24)
@@ -198,6 +199,9 @@ def test_tensor_core_adjoint_shapes(comp, monkeypatch):
     gg = plan.adjoint(rd).to(torch.complex128).cpu().numpy()
     vox = rng.choice(plan.n_local, 96, replace=False)
     assert rel_l2(gg[vox], O.direct_adjoint(g, r, idx, voxels=vox)) <= 1e-5
+    s = rc(rng, plan.n_local)
+    y = plan.forward(plan._as_dev(s, plan.n_local, "s")).to(torch.complex128).cpu().numpy()
+    assert rel_l2(y, O.direct_forward(g, s, idx)) <= 1e-5
 
 
 def test_structured_large_window_chunking():
