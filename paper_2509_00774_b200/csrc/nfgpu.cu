@@ -2100,6 +2100,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
       if (L == 0) mbar_arrive(&zfree[fl & 1]);
     };
     constexpr int EPI_STEP = 4;  // drain frequency f-1 this many steps into f (its MMAs are done by then)
+    // this thread's (at most two) generation items per step, decoded once. Items pair up on adjacent
+    // lanes: U items (row m = 2t + c', voxel pair vp) compute voxel 2vp + (m & 1) and write row m;
+    // W items (receiver r, voxel pair vp, e) compute voxel 2vp + e, and lane e = 0 / 1 writes hi / lo.
+    int icode[2];
+    uint32_t ioff[2];
+    {
+      const int nu = 4 * mrows, nw = 8 * sa.nr;
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int j = tid + it * TC_CT;
+        icode[it] = -1;
+        ioff[it] = 0;
+        if (j < nu) {
+          const int m = j % mrows, vp = j / mrows;
+          icode[it] = (m >> 1) | ((2 * vp + (m & 1)) << 10);
+          ioff[it] = kmaj(m, 4 * vp, 128);
+        } else if (j < nu + nw) {
+          const int jw = j - nu, pr = jw >> 1, e = jw & 1, r = pr % sa.nr, vp = pr / sa.nr;
+          icode[it] = (sa.nt + r) | ((2 * vp + e) << 10) | ((1 + e) << 13);
+          ioff[it] = kmaj(r, 4 * vp, npr);
+        }
+      }
+    }
     for (int fl = 0; fl < nfl; ++fl) {
       float* kt = par + (fl & 1) * 640;
       float* bt = kt + 64;
@@ -2114,42 +2137,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);
         unsigned char* Ast = sm + ly.a_off + st * 2 * 8192;
         unsigned char* Bst = sm + ly.b_off + st * ly.b_stage;
-        // U (A operand): lane m of a row pair computes voxel 2vp + (m & 1) of transmitter m >> 1 and
-        // swaps with lane m ^ 1; each lane then writes its own row's 16-B chunk (conflict-free)
-        for (int i = tid; i < mrows * 4; i += TC_CT) {
-          const int m = i % mrows, vp = i / mrows, tt = m >> 1, vi = c * 8 + 2 * vp + (m & 1);
-          float ur, ui;
-          const float2 e = tv[vi * TS + tt];
-          phasor1<EXACT>(kt[tt], bt[tt], e.x, e.y, -1.f, ur, ui);
-          const unsigned pm = __activemask();
-          const float pr = __shfl_xor_sync(pm, ur, 1), pi = __shfl_xor_sync(pm, ui, 1);
-          const float r0 = (m & 1) ? pr : ur, i0 = (m & 1) ? pi : ui;  // voxel 2vp
-          const float r1 = (m & 1) ? ur : pr, i1 = (m & 1) ? ui : pi;  // voxel 2vp + 1
-          const float4 q = (m & 1) ? make_float4(i0, r0, i1, r1) : make_float4(r0, -i0, r1, -i1);
-          const float4 h = make_float4(tf32_round(q.x), tf32_round(q.y), tf32_round(q.z), tf32_round(q.w));
-          const uint32_t o = kmaj(m, 4 * vp, 128);
-          *reinterpret_cast<float4*>(Ast + o) = h;
-          *reinterpret_cast<float4*>(Ast + 8192 + o) = make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
-        }
-        // W = V·s (B operand): one receiver row, two voxels, one 16-B chunk per thread
-        for (int i = tid; i < sa.nr * 4; i += TC_CT) {
-          const int r = i % sa.nr, vp = i / sa.nr;
-          const float2* colp = tv + (c * 8 + 2 * vp) * TS + sa.nt + r;
-          float w4[4];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
+        for (int it = 0; it < 2; ++it) {
+          const int code = icode[it];
+          if (code < 0) continue;
+          const int slot = code & 0x3ff, vv = (code >> 10) & 7, kind = code >> 13;  // kind 0: U row, 1/2: W hi/lo
+          const float2 e = tv[(c * 8 + vv) * TS + slot];
+          float pr_, pi_;
+          if (kind == 0) {
+            phasor1<EXACT>(kt[slot], bt[slot], e.x, e.y, -1.f, pr_, pi_);
+          } else {
             float vr, vim;
-            const float2 tb = colp[e * TS];
-            phasor1<EXACT>(kr[r], br[r], tb.x, tb.y, -1.f, vr, vim);
-            const float2 sv = ssm[c * 8 + 2 * vp + e];
-            w4[2 * e] = vr * sv.x - vim * sv.y;
-            w4[2 * e + 1] = vr * sv.y + vim * sv.x;
+            phasor1<EXACT>(kr[slot - sa.nt], br[slot - sa.nt], e.x, e.y, -1.f, vr, vim);
+            const float2 sv = ssm[c * 8 + vv];
+            pr_ = vr * sv.x - vim * sv.y;
+            pi_ = vr * sv.y + vim * sv.x;
           }
-          const float4 h = make_float4(tf32_round(w4[0]), tf32_round(w4[1]), tf32_round(w4[2]), tf32_round(w4[3]));
-          const uint32_t o = kmaj(r, 4 * vp, npr);
-          *reinterpret_cast<float4*>(Bst + o) = h;
-          *reinterpret_cast<float4*>(Bst + ly.b_stage / 2 + o) =
-              make_float4(w4[0] - h.x, w4[1] - h.y, w4[2] - h.z, w4[3] - h.w);
+          // the partner lane holds the other voxel of the pair (every pair is lane-adjacent)
+          const unsigned pm = __activemask();
+          const float qr = __shfl_xor_sync(pm, pr_, 1), qi = __shfl_xor_sync(pm, pi_, 1);
+          const bool odd = L & 1;
+          const float r0 = odd ? qr : pr_, i0 = odd ? qi : pi_, r1 = odd ? pr_ : qr, i1 = odd ? pi_ : qi;
+          float4 q;
+          if (kind == 0)
+            q = odd ? make_float4(i0, r0, i1, r1) : make_float4(r0, -i0, r1, -i1);  // rows 2t+1 / 2t
+          else
+            q = make_float4(r0, i0, r1, i1);
+          const float4 h = make_float4(tf32_round(q.x), tf32_round(q.y), tf32_round(q.z), tf32_round(q.w));
+          unsigned char* base = kind == 0 ? Ast : Bst;
+          const uint32_t off = ioff[it];
+          if (kind == 0) {
+            *reinterpret_cast<float4*>(base + off) = h;
+            *reinterpret_cast<float4*>(base + 8192 + off) = make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
+          } else if (kind == 1) {
+            *reinterpret_cast<float4*>(base + off) = h;
+          } else {
+            *reinterpret_cast<float4*>(base + ly.b_stage / 2 + off) =
+                make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
