@@ -66,6 +66,10 @@ def test_exit_codes(tmp_path, capsys):
     assert main(["benchmark", "--scenario", "a", "--measurements", "b", "--compositions", ";", "--seeds", "1",
                  "--out", "c"]) == 2
     assert main([]) == 2
+    assert main(["frobnicate"]) == 2
+    assert main(["info", "--bogus"]) == 2
+    assert main(["info"]) == 2
+    assert main(["--help"]) == 0
     err = capsys.readouterr().err
     assert "usage error: --method spgm requires --batch f,tx,rx" in err
     assert "# paper_2509_00774_b200 " in err and "command=reconstruct" in err

@@ -58,3 +58,69 @@ def test_benchmark_sweep_csv(tmp_path, capsys):
                                          ["2", "2", "2", "8", "1", "20"], ["2", "2", "2", "8", "2", "20"]]
     assert rows[1][7] == rows[2][7] == "inf"  # the full composition reproduces PGM exactly
     assert "wrote" in capsys.readouterr().out
+
+
+def _small_case(tmp_path):
+    """A small custom scenario and noiseless point-scatterer measurements through the CLI."""
+    scn = tmp_path / "s.json"
+    assert main(["scenario-init", "--custom", "--tx", "4", "--rx", "4", "--radius", "0.1", "--f-start", "20e9",
+                 "--f-stop", "24e9", "--f-count", "4", "--center", "0,0,0.3", "--extent", "0.06,0.06,0",
+                 "--dims", "7,7,1", "--out", str(scn)]) == 0
+    meas = tmp_path / "m.nfms"
+    assert main(["simulate", "--scenario", str(scn), "--phantom", "points:1", "--seed", "4", "--out", str(meas)]) == 0
+    return scn, meas
+
+
+def test_simulate_semantics(tmp_path):
+    from paper_2509_00774_b200 import forward_apply
+
+    scn, meas = _small_case(tmp_path)
+    truth = read_volume(tmp_path / "m_truth.nfmv")
+    s = read_scenario(scn)
+    assert rel_l2(read_measurements(meas).values, forward_apply(truth.values, s)) <= 1e-12  # zero noise
+    again = tmp_path / "again.nfms"
+    assert main(["simulate", "--scenario", str(scn), "--phantom", "points:1", "--seed", "4", "--out", str(again)]) == 0
+    assert again.read_bytes() == meas.read_bytes()
+    bad = tmp_path / "bad.nfms"
+    assert main(["simulate", "--scenario", str(scn), "--phantom", "sphere", "--out", str(bad)]) == 1
+    other = tmp_path / "o.json"
+    assert main(["scenario-init", "--custom", "--dims", "3,3,1", "--out", str(other)]) == 0
+    assert main(["simulate", "--scenario", str(other), "--phantom", f"file:{tmp_path / 'm_truth.nfmv'}",
+                 "--out", str(bad)]) == 1
+
+
+def _eta(scn) -> str:
+    from paper_2509_00774_b200 import lipschitz_estimate
+
+    return repr(1.0 / lipschitz_estimate(read_scenario(scn), n_iters=30))
+
+
+def test_reconstruct_semantics(tmp_path, capsys):
+    scn, meas = _small_case(tmp_path)
+    truth = read_volume(tmp_path / "m_truth.nfmv").values
+    base = ["reconstruct", "--scenario", str(scn), "--measurements", str(meas), "--eta", _eta(scn), "--alpha", "1e-6",
+            "--tol", "1e-300", "--max-iters", "60"]
+    assert main(base + ["--method", "pgm", "--out", str(tmp_path / "p.nfmv")]) == 0
+    rec = read_volume(tmp_path / "p.nfmv").values
+    assert int(np.argmax(np.abs(rec))) == int(np.argmax(np.abs(truth)))  # localises the scatterer
+    assert main(base + ["--method", "spgm", "--batch", "4,4,4", "--out", str(tmp_path / "q.nfmv")]) == 0
+    capsys.readouterr()
+    assert main(["psnr", "--recon", str(tmp_path / "q.nfmv"), "--reference", str(tmp_path / "p.nfmv")]) == 0
+    assert capsys.readouterr().out.startswith("psnr_db=inf")  # the full composition is PGM
+    rep = tmp_path / "r.json"
+    assert main(["reconstruct", "--scenario", str(scn), "--measurements", str(meas), "--method", "pgm",
+                 "--max-iters", "100000000", "--tol", "1e-300", "--time-budget-s", "0.2", "--out",
+                 str(tmp_path / "t.nfmv"), "--report", str(rep)]) == 0
+    assert json.loads(rep.read_text())["termination"] == "time_budget"
+
+
+def test_benchmark_repeat_is_deterministic(tmp_path):
+    scn, meas = _small_case(tmp_path)
+    cols = []
+    for k in range(2):
+        out = tmp_path / f"b{k}.csv"
+        assert main(["benchmark", "--scenario", str(scn), "--measurements", str(meas), "--compositions", "2,2,2",
+                     "--seeds", "1,2", "--max-iters", "15", "--tol", "1e-300", "--eta", _eta(scn), "--alpha", "1e-6",
+                     "--out", str(out)]) == 0
+        cols.append([r[7] for r in csv.reader(out.open())][1:])
+    assert cols[0] == cols[1]
