@@ -56,7 +56,26 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if verbose and res.stderr:
         print(res.stderr)
     os.replace(tmp, LIB)
+    build_abi_demo()
     return LIB
+
+
+DEMO_SRC = ROOT / "examples" / "abi_demo.c"
+DEMO_BIN = ROOT / "examples" / "abi_demo"
+
+
+def build_abi_demo() -> Path | None:
+    """Compile examples/abi_demo.c, a plain-C host of the C ABI, against the in-tree library."""
+    if not DEMO_SRC.exists():
+        return None
+    cuda = Path(nvcc()).resolve().parent.parent
+    cmd = [shutil.which("gcc") or "gcc", "-O2", "-std=c11", "-o", str(DEMO_BIN), str(DEMO_SRC),
+           f"-I{ROOT / 'include'}", f"-I{cuda / 'include'}", f"-L{PKG}", f"-L{cuda / 'lib64'}",
+           "-lnfgpu", "-lcudart", "-lm", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../paper_2509_00774_b200"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"gcc failed building {DEMO_SRC.name}:\n{res.stderr}")
+    return DEMO_BIN
 
 
 if __name__ == "__main__":
