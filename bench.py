@@ -467,37 +467,72 @@ def kernel_times(eng, plan, seed, k0, reps):
 
 
 def e2e_run(eng, scn, B, N, args, pg, local):
+    """End to end through the public engine: per step, the host draws the flat minibatch with numpy
+    (sorted choice without replacement, as the reference's sampler does on the CPU), uploads it from
+    pinned memory, runs the step, and reads the step's termination statistics back. The loop is
+    pipelined like a production driver: the host draws batch k+1 and reads step k's statistics
+    (one async D2H per step into a pinned double buffer) while the GPU runs step k+1."""
     import torch
     import torch.distributed as dist
 
     rng = np.random.default_rng(1234)
     M = scn.n_channels
     steps = args.steps
-    host_idx = torch.empty(B, dtype=torch.int32).pin_memory()
-    for _ in range(2):
-        host_idx.copy_(torch.from_numpy(np.sort(rng.choice(M, B, replace=False)).astype(np.int32)))
-        eng.stage(host_idx)
+    dev = eng.plan.device
+    bufs = [torch.empty(B, dtype=torch.int32).pin_memory() for _ in range(2)]
+    stats_host = torch.empty((2, 4), dtype=torch.float64).pin_memory()
+    events = [torch.cuda.Event() for _ in range(2)]
+    st = torch.cuda.current_stream()
+    changes = []
+
+    def draw(k):
+        bufs[k % 2].copy_(torch.from_numpy(np.sort(rng.choice(M, B, replace=False)).astype(np.int32)))
+
+    def launch(k):
+        eng.idx_dev[:B].copy_(bufs[k % 2], non_blocking=True)  # H2D of this step's indices
+        eng.plan.prepare(eng.idx_dev[:B])
         eng.step_staged()
-        eng.magnitude_change()
+        stats = eng.stats
+        if pg is not None:
+            stats = stats.clone()
+            dist.all_reduce(stats, group=pg)
+        stats_host[k % 2].copy_(stats, non_blocking=True)  # D2H of this step's result
+        events[k % 2].record(st)
+
+    def consume(k):
+        events[k % 2].synchronize()
+        s0, s1 = float(stats_host[k % 2, 0]), float(stats_host[k % 2, 1])
+        changes.append(s1 ** 0.5 / max(s0 ** 0.5, 1e-300))
+
+    for k in range(2):  # warm-up
+        draw(k)
+        launch(k)
+        consume(k)
     if pg is not None:
         dist.barrier(device_ids=[local])
-    torch.cuda.synchronize()
+    torch.cuda.synchronize(dev)
+    changes.clear()
     t0 = time.perf_counter()
-    for _ in range(steps):
-        host_idx.copy_(torch.from_numpy(np.sort(rng.choice(M, B, replace=False)).astype(np.int32)))
-        eng.stage(host_idx)
-        eng.step_staged()
-        eng.magnitude_change()  # D2H of the 4-double stats vector (+ all-reduce when sharded)
-    torch.cuda.synchronize()
+    draw(0)
+    for k in range(steps):
+        launch(k)
+        if k + 1 < steps:
+            draw(k + 1)  # host work overlaps step k on the GPU
+        if k > 0:
+            consume(k - 1)
+    consume(steps - 1)
+    torch.cuda.synchronize(dev)
     dt = time.perf_counter() - t0
     if pg is not None:
-        t = torch.tensor([dt], device=eng.plan.device, dtype=torch.float64)
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
+    assert len(changes) == steps
     return {"value": 2.0 * B * N * steps / dt, "unit": UNIT, "h2d_bytes_per_step": 4 * B,
             "d2h_bytes_per_step": 32, "ms_per_step": dt / steps * 1e3,
-            "how": "wall clock around spgm steps with host numpy flat sampling (sorted choice without "
-                   "replacement, as the reference), pinned H2D of the index list, D2H of the termination stats"}
+            "how": "wall clock around spgm steps: host numpy flat sampling (sorted choice without replacement, "
+                   "as the reference), pinned H2D of each step's index list, D2H of each step's termination "
+                   "stats; the host samples step k+1 and reads step k's stats while the GPU runs step k+1"}
 
 
 def main():
