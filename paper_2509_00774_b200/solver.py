@@ -390,7 +390,64 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
     iterations = 0
     staged_full = False
 
+    def stage_iteration(k):  # host side of iteration k: draw (or reuse) its batch and stage it; returns B
+        nonlocal staged_full
+        if not stochastic:
+            if not staged_full:
+                eng.stage(full_idx)
+                staged_full = True
+            return m
+        if config.sampler == "device":
+            eng.sample_device(config.rng_seed, k, config.flat_batch)
+            return config.flat_batch
+        if config.sampler == "table":
+            return eng.stage(np.asarray(config.index_table[k - 1]))
+        if config.flat_batch is not None:
+            return eng.stage(sample_flat(scenario, config.flat_batch, rng))
+        return eng.stage(sample_minibatch(config.composition, scenario, rng).indices)
+
     t_start = time.perf_counter()
+    if progress is None and config.check_every == 1:
+        # Pipelined: iteration k+1 is drawn and launched before iteration k's statistics are read
+        # (async D2H into a pinned double buffer), so host sampling and the read-back overlap the
+        # GPU. If k terminates, the speculative step k+1 is dropped: its input, the iterate after
+        # k, is still intact in the engine's other buffer, so results equal the serial loop's.
+        stats_host = torch.empty((2, 4), dtype=torch.float64).pin_memory()
+        events = [torch.cuda.Event(), torch.cuda.Event()]
+        stream = torch.cuda.current_stream(plan.device)
+        batch = {}
+        t_launch = {}
+
+        def launch(k):
+            t_launch[k] = time.perf_counter()
+            batch[k] = stage_iteration(k)
+            eng.step_staged()
+            stats_host[k % 2].copy_(eng.stats, non_blocking=True)
+            events[k % 2].record(stream)
+
+        launch(1)
+        for k in range(1, config.max_iters + 1):
+            if k < config.max_iters:
+                launch(k + 1)
+            events[k % 2].synchronize()
+            st = stats_host[k % 2].tolist()
+            change = math.sqrt(st[1]) / max(math.sqrt(st[0]), _ZERO_NORM_GUARD)
+            iterations = k
+            records.append(IterationRecord(k, change, time.perf_counter() - t_launch[k], batch[k]))
+            stop = None
+            if change < config.tol:
+                stop = TERMINATION_TOLERANCE
+            elif config.time_budget_s is not None and time.perf_counter() - t_start > config.time_budget_s:
+                stop = TERMINATION_TIME_BUDGET
+            if stop is not None:
+                termination = stop
+                if k < config.max_iters:  # drop the speculative step k+1
+                    eng.s, eng.s_next = eng.s_next, eng.s
+                break
+        vol = eng.volume()
+        return SolveReport(volume=ReflectivityVolume(vol, scenario.voxels), iterations=iterations,
+                           wall_time_s=time.perf_counter() - t_start, per_iteration=records, termination=termination)
+
     for k in range(1, config.max_iters + 1):
         t_iter = time.perf_counter()
         if not stochastic:

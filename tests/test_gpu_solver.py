@@ -292,3 +292,27 @@ def test_cuda_graph_steps_match_eager():
         torch.cuda.synchronize()
         out.append(eng.volume())
     assert np.array_equal(out[0], out[1])
+
+
+def test_pipelined_solver_equals_serial_loop(small_scenario, rng):
+    """With no progress callback the solver launches iteration k+1 before reading k's statistics.
+    A tolerance stop must drop the speculative step: volume, iteration count and records equal the
+    serial loop's (the serial loop runs when a progress callback is given)."""
+    y = rc(rng, small_scenario.n_channels)
+    base = SolverConfig(max_iters=60, tol=1e-300, composition=MinibatchComposition(2, 2, 1), rng_seed=3)
+    serial = spgm_solve(y, small_scenario, base, progress=lambda k, s: None)
+    changes = [r.magnitude_change for r in serial.per_iteration]
+    tol = 0.5 * (changes[20] + changes[21]) if changes[20] != changes[21] else changes[20]
+    cfgs = [SolverConfig(max_iters=60, tol=tol, composition=MinibatchComposition(2, 2, 1), rng_seed=3),
+            SolverConfig(max_iters=40, tol=1e-300, flat_batch=7, rng_seed=5)]
+    for cfg in cfgs:
+        a = spgm_solve(y, small_scenario, cfg)
+        b = spgm_solve(y, small_scenario, cfg, progress=lambda k, s: None)
+        assert (a.iterations, a.termination) == (b.iterations, b.termination)
+        assert np.array_equal(a.volume.values, b.volume.values)
+        assert [r.magnitude_change for r in a.per_iteration] == [r.magnitude_change for r in b.per_iteration]
+        assert [r.batch_size for r in a.per_iteration] == [r.batch_size for r in b.per_iteration]
+    assert spgm_solve(y, small_scenario, cfgs[0]).termination == "tolerance_reached"
+    p1 = pgm_solve(y, small_scenario, SolverConfig(max_iters=15, tol=1e-300))
+    p2 = pgm_solve(y, small_scenario, SolverConfig(max_iters=15, tol=1e-300), progress=lambda k, s: None)
+    assert np.array_equal(p1.volume.values, p2.volume.values)
