@@ -244,7 +244,7 @@ def test_simulate_measurements_noise_convention(small_scenario, rng):
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_microbenchmark_full_M_spot_check(dtype):
+def test_microbenchmark_full_M_spot_check(dtype, structured=False):
     """BASELINE config 4 (operator microbenchmark): one forward and one adjoint at full
     M = 64 Tx x 64 Rx x 256 f = 1,048,576 on the 64^3 grid, N(0,1) complex inputs; sampled
     output rows / voxels against the table-free oracle (precision study: c64 and c128)."""
@@ -255,7 +255,11 @@ def test_microbenchmark_full_M_spot_check(dtype):
     s = rc(rng, scn.n_voxels).astype(dt).astype(np.complex128)
     r = rc(rng, scn.n_channels).astype(dt).astype(np.complex128)
     plan = DevicePlan(scn, dtype=dtype)
-    plan.prepare(torch.arange(scn.n_channels, dtype=torch.int32, device=plan.device))
+    if structured:
+        plan.prepare_full()
+        assert plan.staged_structured
+    else:
+        plan.prepare(torch.arange(scn.n_channels, dtype=torch.int32, device=plan.device))
     y = plan.forward(plan._as_dev(s, scn.n_voxels, "s")).to(torch.complex128).cpu().numpy()
     rows = np.sort(rng.choice(scn.n_channels, 16, replace=False))
     assert rel_l2(y[rows], O.direct_forward(geo, s, rows, chunk=32768)) <= TOL[dtype]
@@ -265,6 +269,12 @@ def test_microbenchmark_full_M_spot_check(dtype):
                                            voxels=vox) for a in range(0, scn.n_channels, 131072)])
     ref = ref.reshape(-1, vox.size).sum(axis=0)
     assert rel_l2(g[vox], ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_microbenchmark_full_M_structured_spot_check(dtype):
+    """The same full-M microbenchmark through the separable kernels (the full set is Cartesian)."""
+    test_microbenchmark_full_M_spot_check(dtype, structured=True)
 
 
 def test_large_batch_paths_agree():
