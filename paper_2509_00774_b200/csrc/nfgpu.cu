@@ -1632,7 +1632,7 @@ constexpr int TC_CT = TC_CW * 32;             // compute threads
 constexpr int TC_THREADS = TC_CT + 64;        // + B-loader warp + MMA warp
 constexpr int TC_SUB = TC_CT / 128;           // compute threads per voxel row
 constexpr int TC_RCH = 8;                     // receivers per pipeline step (K = 16 reals = two MMAs of K = 8)
-constexpr int TC_NS = 4;                      // adjoint pipeline stages
+constexpr int TC_NS = 4;                      // adjoint pipeline stages (at most; fewer when the table is large)
 constexpr int TCF_NS = 5;                     // forward pipeline stages
 constexpr int TC_NMAX = 128;                  // max padded 2·n_t (TMEM: 2 regions × N ≤ 256 columns)
 constexpr uint32_t TC_A_BYTES = 128 * 2 * TC_RCH * 4;  // one of hi/lo: 8 KB
@@ -1641,11 +1641,11 @@ constexpr uint32_t TC_SMEM_MAX = 227 * 1024;
 // dynamic shared-memory layout of adj_tc_kernel (bytes), from the batch shape
 struct TcLayout {
   uint32_t a_off, b_off, b_stage, tab_off, d0_off, par_off, bar_off, bytes;
-  __host__ __device__ TcLayout(int npad, int nant) {
+  __host__ __device__ TcLayout(int npad, int nant, int ns = TC_NS) {
     a_off = 0;                                   // [stage][hi, lo][128 x 16]
-    b_off = TC_NS * 2 * TC_A_BYTES;              // [stage][hi, lo][npad x 16]
+    b_off = ns * 2 * TC_A_BYTES;                 // [stage][hi, lo][npad x 16]
     b_stage = (uint32_t)npad * 2 * TC_RCH * 4 * 2;
-    tab_off = b_off + TC_NS * b_stage;           // [antenna slot][δ 128 | 1/d 128]
+    tab_off = b_off + ns * b_stage;              // [antenna slot][δ 128 | 1/d 128]
     d0_off = tab_off + (uint32_t)nant * 1024;    // [A_MAX] fp64
     par_off = d0_off + A_MAX * 8;                // rx [2][kr 256 | br 256], tx [2][kt 64 | bt 64]
     bar_off = par_off + (1024 + 256) * 4;        // 3·NS + 4 mbarriers + TMEM base
@@ -1758,9 +1758,9 @@ template <bool PROX, bool EXACT>
 __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a, StructArgs sa,
                                                                const double* __restrict__ kd,
                                                                const float* __restrict__ bimg, int npad, int nch,
-                                                               int fch) {
+                                                               int fch, int ns) {
   extern __shared__ __align__(1024) unsigned char sm[];
-  const TcLayout ly(npad, sa.nt + sa.nr);
+  const TcLayout ly(npad, sa.nt + sa.nr, ns);
   const Geo& g = a.g;
   const int tid = threadIdx.x, w = tid >> 5, L = tid & 31;
   // CTA = (tile, half hb, frequency chunk fc); it is chunk hb·fch + fc of the tile for adj_epilogue
@@ -1786,7 +1786,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
     for (int i = tid; i < g.A; i += TC_CT) d0[i] = a.D0[(size_t)tile * g.A + i];
   }
   if (tid == 0) {
-    for (int i = 0; i < TC_NS; ++i) {
+    for (int i = 0; i < ns; ++i) {
       mbar_init(&afull[i], TC_CW / 2);
       mbar_init(&sfree[i], 1);
       mbar_init(&bfull[i], 1);
@@ -1814,7 +1814,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
   if (w == TC_CW) {  // ---------------- B loader
     if (L == 0)
       for (int s = 0; s < nsteps; ++s) {
-        const int st = s % TC_NS, k = s / TC_NS;
+        const int st = s % ns, k = s / ns;
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);
         const int fi = f0 + s / nch, c = s % nch;
         mbar_expect(&bfull[st], bbytes);
@@ -1824,7 +1824,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
     if (L == 0) {
       const uint32_t idesc = umma_idesc_tf32(128, npad), lboB = (uint32_t)(npad >> 3) * 128;
       for (int s = 0; s < nsteps; ++s) {
-        const int st = s % TC_NS, k = s / TC_NS, fl = s / nch, c = s % nch;
+        const int st = s % ns, k = s / ns, fl = s / nch, c = s % nch;
         mbar_wait(&afull[st], k & 1);
         mbar_wait(&bfull[st], k & 1);
         if (c == 0 && fl >= 2) mbar_wait(&zfree[fl & 1], ((fl - 2) >> 1) & 1);  // region read by epilogue(fl-2)
@@ -1855,7 +1855,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
       for (int q = tid; q < sa.nr; q += HT) side_params<float, EXACT>(kf, d0[g.T + sa.rs[q]], kr[q], br[q]);
       named_bar(1, HT);
       for (int c = 0; c < nch; ++c) {
-        const int s = fl * nch + c, st = s % TC_NS, k = s / TC_NS;
+        const int s = fl * nch + c, st = s % ns, k = s / ns;
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);  // MMAs of step s - NS released the stage
         unsigned char* Ast = sm + ly.a_off + st * 2 * TC_A_BYTES;
 #pragma unroll
@@ -2509,7 +2509,7 @@ bool use_tc_struct(const nf_plan* p, bool forward) {
     if (!p->tc_force && !p->tc_fwd) return false;
     return p->snr <= 256 && TcfLayout((p->snr + 15) / 16 * 16, p->snt + p->snr).bytes <= TC_SMEM_MAX;
   }
-  return TcLayout((2 * p->snt + 15) / 16 * 16, p->snt + p->snr).bytes <= TC_SMEM_MAX;
+  return TcLayout((2 * p->snt + 15) / 16 * 16, p->snt + p->snr, 2).bytes <= TC_SMEM_MAX;
 }
 
 template <typename Real>
@@ -2585,10 +2585,12 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
                                                                           (2 * p->g.ntiles)));
       fch = std::max(1, std::min(fch, p->adj_ch_cap / 2));
       a.CH = 2 * fch;
-      const uint32_t smem = TcLayout(npad, sa.nt + sa.nr).bytes;
+      int ns = TC_NS;  // as many pipeline stages as fit next to the table
+      while (ns > 2 && TcLayout(npad, sa.nt + sa.nr, ns).bytes > TC_SMEM_MAX) --ns;
+      const uint32_t smem = TcLayout(npad, sa.nt + sa.nr, ns).bytes;
       auto kern = p->exact ? adj_tc_kernel<PROX, true> : adj_tc_kernel<PROX, false>;
       CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kern<<<(unsigned)(p->g.ntiles * a.CH), TC_THREADS, smem, st>>>(a, sa, p->d_kd, p->d_bimg, npad, nch, fch);
+      kern<<<(unsigned)(p->g.ntiles * a.CH), TC_THREADS, smem, st>>>(a, sa, p->d_kd, p->d_bimg, npad, nch, fch, ns);
       CUDA_TRY(cudaGetLastError());
       p->launches += 3;
       if (PROX) {
