@@ -1633,7 +1633,7 @@ constexpr int TC_THREADS = TC_CT + 64;        // + B-loader warp + MMA warp
 constexpr int TC_SUB = TC_CT / 128;           // compute threads per voxel row
 constexpr int TC_RCH = 8;                     // receivers per pipeline step (K = 16 reals = two MMAs of K = 8)
 constexpr int TC_NS = 4;                      // adjoint pipeline stages (at most; fewer when the table is large)
-constexpr int TCF_NS = 5;                     // forward pipeline stages
+constexpr int TCF_NS = 2;                     // forward pipeline stages
 constexpr int TC_NMAX = 128;                  // max padded 2·n_t (TMEM: 2 regions × N ≤ 256 columns)
 constexpr uint32_t TC_A_BYTES = 128 * 2 * TC_RCH * 4;  // one of hi/lo: 8 KB
 constexpr uint32_t TC_SMEM_MAX = 227 * 1024;
@@ -1813,18 +1813,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
 
   if (w == TC_CW) {  // ---------------- B loader
     if (L == 0)
-      for (int s = 0; s < nsteps; ++s) {
-        const int st = s % ns, k = s / ns;
+      for (int s = 0, st = 0, k = 0, fi = f0, c = 0; s < nsteps; ++s) {  // stage st, its use k; batch row fi, chunk c
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);
-        const int fi = f0 + s / nch, c = s % nch;
         mbar_expect(&bfull[st], bbytes);
         bulk_g2s(sm + ly.b_off + st * bbytes, bimg + ((size_t)fi * nch + c) * (bbytes / 4), bbytes, &bfull[st]);
+        if (++st == ns) st = 0, ++k;
+        if (++c == nch) c = 0, ++fi;
       }
   } else if (w == TC_CW + 1) {  // ---------------- MMA issuer
     if (L == 0) {
       const uint32_t idesc = umma_idesc_tf32(128, npad), lboB = (uint32_t)(npad >> 3) * 128;
-      for (int s = 0; s < nsteps; ++s) {
-        const int st = s % ns, k = s / ns, fl = s / nch, c = s % nch;
+      for (int s = 0, st = 0, k = 0, fl = 0, c = 0; s < nsteps; ++s) {
         mbar_wait(&afull[st], k & 1);
         mbar_wait(&bfull[st], k & 1);
         if (c == 0 && fl >= 2) mbar_wait(&zfree[fl & 1], ((fl - 2) >> 1) & 1);  // region read by epilogue(fl-2)
@@ -1844,10 +1843,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
         }
         umma_commit(&sfree[st]);
         if (c == nch - 1) umma_commit(&zfull[fl & 1]);
+        if (++st == ns) st = 0, ++k;
+        if (++c == nch) c = 0, ++fl;
       }
     }
   } else if (w < TC_CW / 2) {  // ---------------- A generation: conj(V) of 8 receivers per step
     const int row = tid & 127, sub = tid >> 7;  // 2 threads per voxel row
+    int st = 0, k = 0;                          // pipeline stage and its use count
     for (int fl = 0; fl < nfl; ++fl) {
       float* kr = par + (fl & 1) * 512;
       float* br = kr + 256;
@@ -1855,7 +1857,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
       for (int q = tid; q < sa.nr; q += HT) side_params<float, EXACT>(kf, d0[g.T + sa.rs[q]], kr[q], br[q]);
       named_bar(1, HT);
       for (int c = 0; c < nch; ++c) {
-        const int s = fl * nch + c, st = s % ns, k = s / ns;
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);  // MMAs of step s - NS released the stage
         unsigned char* Ast = sm + ly.a_off + st * 2 * TC_A_BYTES;
 #pragma unroll
@@ -1880,6 +1881,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (L == 0) mbar_arrive(&afull[st]);
+        if (++st == ns) st = 0, ++k;
       }
     }
   } else {  // ---------------- epilogue: g += Σ_t conj(U_t)·z_t
@@ -1946,12 +1948,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
 // (the pair of lanes 2t, 2t+1 combined by a shuffle) into one partial per (half tile, channel),
 // warp 17 issues the MMAs; fwd_reduce1/2 finish the sum over the 2·tiles partial rows.
 
+constexpr int TCF_VPS = 16;                          // voxels per forward pipeline step
+constexpr int TCF_KPS = 2 * TCF_VPS;                 // reals of K per step (4 MMAs of K = 8)
+constexpr uint32_t TCF_A_BYTES = 128 * TCF_KPS * 4;  // one of hi/lo of an A stage
 struct TcfLayout {
   uint32_t a_off, b_off, b_stage, s_off, tab_off, d0_off, par_off, bar_off, bytes;
   __host__ __device__ TcfLayout(int npr, int nant) {
-    a_off = 0;                                  // [stage][hi, lo][128 x 16]
-    b_off = TCF_NS * 2 * 128 * 16 * 4;          // [stage][hi, lo][npr x 16]
-    b_stage = (uint32_t)npr * 16 * 4 * 2;
+    a_off = 0;                                  // [stage][hi, lo][128 x KPS]
+    b_off = TCF_NS * 2 * TCF_A_BYTES;           // [stage][hi, lo][npr x KPS]
+    b_stage = (uint32_t)npr * TCF_KPS * 4 * 2;
     s_off = b_off + TCF_NS * b_stage;           // s of the half tile: [128] complex
     tab_off = s_off + 128 * 8;                  // [voxel 128][slot, stride nant|1] (δ, 1/d)
     d0_off = tab_off + (uint32_t)(nant | 1) * 1024;
@@ -2007,10 +2012,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
     // zero the padding rows of every stage once (A rows >= 2 n_t, B rows >= n_r); generation never writes them
     for (int st = 0; st < TCF_NS; ++st)
       for (int hl = 0; hl < 2; ++hl) {
-        float* A0 = reinterpret_cast<float*>(sm + ly.a_off + (st * 2 + hl) * 8192);
-        for (int i = tid; i < (128 - mrows) * 16; i += TC_CT) A0[kmaj(mrows + i / 16, i % 16, 128) >> 2] = 0.f;
+        float* A0 = reinterpret_cast<float*>(sm + ly.a_off + (st * 2 + hl) * TCF_A_BYTES);
+        for (int i = tid; i < (128 - mrows) * TCF_KPS; i += TC_CT)
+          A0[kmaj(mrows + i / TCF_KPS, i % TCF_KPS, 128) >> 2] = 0.f;
         float* B0 = reinterpret_cast<float*>(sm + ly.b_off + st * ly.b_stage + hl * (ly.b_stage / 2));
-        for (int i = tid; i < (npr - sa.nr) * 16; i += TC_CT) B0[kmaj(sa.nr + i / 16, i % 16, npr) >> 2] = 0.f;
+        for (int i = tid; i < (npr - sa.nr) * TCF_KPS; i += TC_CT)
+          B0[kmaj(sa.nr + i / TCF_KPS, i % TCF_KPS, npr) >> 2] = 0.f;
       }
   }
   if (tid == 0) {
@@ -2037,7 +2044,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
   const int nwin = fb - fa;
   const int f0 = fa + (int)(((long long)nwin * fc) / fch), f1 = fa + (int)(((long long)nwin * (fc + 1)) / fch);
   const int nfl = f1 - f0;
-  constexpr int SPF = 128 / 8;  // pipeline steps per frequency (8 voxels each)
+  constexpr int SPF = 128 / TCF_VPS;  // pipeline steps per frequency
   const int nsteps = nfl * SPF;
 
   if (w == TC_CW + 1) {  // ---------------- MMA issuer
@@ -2049,14 +2056,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
         if (c == 0 && fl >= 2) mbar_wait(&zfree[fl & 1], ((fl - 2) >> 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)((fl & 1) * npr);
-        const uint32_t a0 = smem_u32(sm + ly.a_off + st * 2 * 8192);
+        const uint32_t a0 = smem_u32(sm + ly.a_off + st * 2 * TCF_A_BYTES);
         const uint32_t b0 = smem_u32(sm + ly.b_off + st * ly.b_stage);
 #pragma unroll
         for (int pass = 0; pass < 3; ++pass) {
           const int ah = pass == 2 ? 1 : 0, bh = pass == 1 ? 1 : 0;
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const uint64_t ad = umma_desc(a0 + ah * 8192 + ks * 2 * 2048, 2048, 128);
+          for (int ks = 0; ks < TCF_KPS / 8; ++ks) {
+            const uint64_t ad = umma_desc(a0 + ah * TCF_A_BYTES + ks * 2 * 2048, 2048, 128);
             const uint64_t bd = umma_desc(b0 + bh * (ly.b_stage / 2) + ks * 2 * lboB, lboB, 128);
             umma_tf32(d, ad, bd, idesc, (c > 0 || pass > 0 || ks > 0) ? 1u : 0u);
           }
@@ -2103,12 +2110,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
     // this thread's (at most two) generation items per step, decoded once. Items pair up on adjacent
     // lanes: U items (row m = 2t + c', voxel pair vp) compute voxel 2vp + (m & 1) and write row m;
     // W items (receiver r, voxel pair vp, e) compute voxel 2vp + e, and lane e = 0 / 1 writes hi / lo.
-    int icode[2];
-    uint32_t ioff[2];
+    constexpr int NIT = 4;  // items per thread per step (up to 2048 items)
+    int icode[NIT];
+    uint32_t ioff[NIT];
     {
-      const int nu = 4 * mrows, nw = 8 * sa.nr;
+      const int nu = (TCF_VPS / 2) * mrows, nw = TCF_VPS * sa.nr;
 #pragma unroll
-      for (int it = 0; it < 2; ++it) {
+      for (int it = 0; it < NIT; ++it) {
         const int j = tid + it * TC_CT;
         icode[it] = -1;
         ioff[it] = 0;
@@ -2118,7 +2126,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
           ioff[it] = kmaj(m, 4 * vp, 128);
         } else if (j < nu + nw) {
           const int jw = j - nu, pr = jw >> 1, e = jw & 1, r = pr % sa.nr, vp = pr / sa.nr;
-          icode[it] = (sa.nt + r) | ((2 * vp + e) << 10) | ((1 + e) << 13);
+          icode[it] = (sa.nt + r) | ((2 * vp + e) << 10) | ((1 + e) << 14);
           ioff[it] = kmaj(r, 4 * vp, npr);
         }
       }
@@ -2135,21 +2143,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
       for (int c = 0; c < SPF; ++c) {
         const int s = fl * SPF + c, st = s % TCF_NS, k = s / TCF_NS;
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);
-        unsigned char* Ast = sm + ly.a_off + st * 2 * 8192;
+        unsigned char* Ast = sm + ly.a_off + st * 2 * TCF_A_BYTES;
         unsigned char* Bst = sm + ly.b_off + st * ly.b_stage;
 #pragma unroll
-        for (int it = 0; it < 2; ++it) {
+        for (int it = 0; it < NIT; ++it) {
           const int code = icode[it];
           if (code < 0) continue;
-          const int slot = code & 0x3ff, vv = (code >> 10) & 7, kind = code >> 13;  // kind 0: U row, 1/2: W hi/lo
-          const float2 e = tv[(c * 8 + vv) * TS + slot];
+          const int slot = code & 0x3ff, vv = (code >> 10) & 15, kind = code >> 14;  // kind 0: U row, 1/2: W hi/lo
+          const float2 e = tv[(c * TCF_VPS + vv) * TS + slot];
           float pr_, pi_;
           if (kind == 0) {
             phasor1<EXACT>(kt[slot], bt[slot], e.x, e.y, -1.f, pr_, pi_);
           } else {
             float vr, vim;
             phasor1<EXACT>(kr[slot - sa.nt], br[slot - sa.nt], e.x, e.y, -1.f, vr, vim);
-            const float2 sv = ssm[c * 8 + vv];
+            const float2 sv = ssm[c * TCF_VPS + vv];
             pr_ = vr * sv.x - vim * sv.y;
             pi_ = vr * sv.y + vim * sv.x;
           }
@@ -2168,7 +2176,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
           const uint32_t off = ioff[it];
           if (kind == 0) {
             *reinterpret_cast<float4*>(base + off) = h;
-            *reinterpret_cast<float4*>(base + 8192 + off) = make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
+            *reinterpret_cast<float4*>(base + TCF_A_BYTES + off) =
+                make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
           } else if (kind == 1) {
             *reinterpret_cast<float4*>(base + off) = h;
           } else {
@@ -2505,8 +2514,9 @@ bool use_tc_struct(const nf_plan* p, bool forward) {
   // the tensor core pays off once the contraction dominates the phasor work: both antenna
   // counts >= 24 and enough frequencies per tile (tools/time_structured.py crossover)
   if (!p->tc_force && !(amin >= 24 && p->snf * amin >= 192)) return false;
-  if (forward) {  // the tcgen05 forward is not yet faster than the FFMA one: opt-in
-    if (!p->tc_force && !p->tc_fwd) return false;
+  if (forward) {  // the tcgen05 forward wins only on large batches: >= 40 antennas a side and
+                  // >= 12 frequencies (full set: -10% vs FFMA); NFGPU_TC_FWD=1 takes it for every eligible batch
+    if (!p->tc_force && !p->tc_fwd && !(amin >= 40 && p->snf >= 12)) return false;
     return p->snr <= 256 && TcfLayout((p->snr + 15) / 16 * 16, p->snt + p->snr).bytes <= TC_SMEM_MAX;
   }
   return TcLayout((2 * p->snt + 15) / 16 * 16, p->snt + p->snr, 2).bytes <= TC_SMEM_MAX;
