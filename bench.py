@@ -412,6 +412,11 @@ def structured_line(eng, w):
     out = {"composition": [comp.n_f, comp.n_tx, comp.n_rx], "batch": B, "structured": eng.plan.staged_structured,
            "value": 2.0 * B * N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "iters_per_s": 1e3 / ms,
            "sampler": "host numpy (reference sample_minibatch), indices uploaded every step"}
+    # the same compositions drawn on the device (nf_sample_structured), 2 steps per CUDA graph replay
+    g = eng.graph(configs.SEEDS["minibatch"], 0, pairs=1, composition=comp)
+    ms_g = timed(g.replay, 3, 50) / 2
+    out["device_sampler_cuda_graph"] = {"value": 2.0 * B * N / (ms_g * 1e-3), "unit": UNIT, "ms_per_step": ms_g,
+                                        "iters_per_s": 1e3 / ms_g}
     pf = DevicePlan(scn, dtype=w.dtype, device=eng.plan.device, max_batch=M)
     ef = SPGMEngine(pf, eng.y, eng.eta, eng.alpha, initial=eng.s)
     ef.stage(np.arange(M))

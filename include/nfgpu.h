@@ -11,6 +11,7 @@
  *                                   (phasor tables F×(T+R)×N are NOT built; a frequency-free
  *                                    per-(antenna, voxel) distance table is built instead)
  *   nf_batch_prepare      replaces  forward._subset_indices + _channel_groups  forward.py:227-258
+ *   nf_sample_structured  device counterpart of solver.sample_minibatch (solver.py:205-225)
  *   nf_batch_prepare_structured  replaces the same for the Cartesian subsets that
  *                                 solver.sample_minibatch draws (solver.py:205-225) and for the
  *                                 full channel set (forward.py:233-236); separable fast path
@@ -113,6 +114,15 @@ int nf_adjoint_prox(nf_plan* plan, const void* r_dev, const void* ymeas_dev, con
 #define NF_ITER_DEVICE 0xffffffffffffffffULL
 int nf_sample_flat(nf_plan* plan, uint64_t seed, uint64_t iter, int batch, int32_t* idx_dev,
                    void* stream);
+
+/* Structured sampler on the device: draws a Cartesian batch of n_f frequencies x n_tx
+ * transmitters x n_rx receivers (distinct, sorted; keyed Feistel permutations of each axis, the
+ * device counterpart of solver.sample_minibatch, solver.py:205-225, with its own RNG) and stages
+ * it as nf_batch_prepare_structured would. iter = NF_ITER_DEVICE reads and advances the plan's
+ * device iteration counter (capturable in a CUDA graph). lists (device, n_f + n_tx + n_rx), if
+ * not null, receives the drawn [fs | ts | rs]. */
+int nf_sample_structured(nf_plan* plan, uint64_t seed, uint64_t iter, int n_f, int n_tx, int n_rx,
+                         int32_t* lists_dev, void* stream);
 
 /* Set the plan's device iteration counter (stream-ordered). */
 int nf_plan_set_iter(nf_plan* plan, uint64_t iter, void* stream);

@@ -556,6 +556,41 @@ __global__ void sample_kernel(uint64_t seed, uint64_t iter, const unsigned long 
   idx[j] = (int)x;
 }
 __global__ void bump_kernel(unsigned long long* it) { *it += 1ULL; }
+
+// Structured (Cartesian) sampler on the device: k_a distinct sorted indices out of n_a for each axis
+// a in {frequency, tx, rx}, the first k_a images of a keyed Feistel permutation of [0, n_a)
+// (cycle-walking on the next even power of two), ranked into ascending order. One block of 256
+// threads; lists go to out = [F | T | R] (the plan's structured-batch lists). iter_dev: the
+// iteration number is read from (and then advanced in) device memory, so the call is capturable.
+__global__ void __launch_bounds__(256) struct_sample_kernel(uint64_t seed, uint64_t iter,
+                                                            unsigned long long* __restrict__ iter_dev, int F, int T,
+                                                            int R, int nf, int nt, int nr, int* __restrict__ out) {
+  __shared__ int vals[256];
+  const uint64_t key0 = sample_key(seed, iter_dev ? (uint64_t)*iter_dev : iter);
+  const int ns[3] = {F, T, R}, ks[3] = {nf, nt, nr}, offs[3] = {0, F, F + T};
+  for (int axis = 0; axis < 3; ++axis) {
+    const int n = ns[axis], k = ks[axis];
+    int bits = 2;
+    while ((1 << bits) < n) bits += 2;
+    const uint64_t key = key0 ^ (0x632BE59BD9B4E019ULL * (uint64_t)(axis + 1));
+    for (int i = threadIdx.x; i < k; i += 256) {
+      uint32_t x = (uint32_t)i;
+      do {
+        x = feistel(x, bits / 2, key);
+      } while (x >= (uint32_t)n);
+      vals[i] = (int)x;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += 256) {  // rank of vals[i] among the k distinct values
+      const int v = vals[i];
+      int pos = 0;
+      for (int j = 0; j < k; ++j) pos += vals[j] < v;
+      out[offs[axis] + pos] = v;
+    }
+    __syncthreads();
+  }
+  if (iter_dev && threadIdx.x == 0) *iter_dev += 1ULL;  // every thread has read it
+}
 __global__ void set_kernel(unsigned long long* it, unsigned long long v) { *it = v; }
 
 // ------------------------------------------------------------------ per-warp shared state
@@ -2903,6 +2938,35 @@ int nf_adjoint_prox(nf_plan* p, const void* r, const void* ymeas, const void* s_
   if (p->dtype == NF_C64)
     return launch_adjoint<float, true>(p, r, ymeas, nullptr, 0, s_in, s_out, eta_over_b, alpha, stats, st);
   return launch_adjoint<double, true>(p, r, ymeas, nullptr, 0, s_in, s_out, eta_over_b, alpha, stats, st);
+}
+
+int nf_sample_structured(nf_plan* p, uint64_t seed, uint64_t iter, int nf, int nt, int nr, int32_t* lists,
+                         void* stream) {
+  if (!p) return fail(NF_ERR_ARG, "null argument");
+  if (nf < 1 || nf > p->g.F || nt < 1 || nt > p->g.T || nr < 1 || nr > p->g.R)
+    return fail(NF_ERR_ARG, "composition must satisfy 1 <= n_f <= F, 1 <= n_tx <= T, 1 <= n_rx <= R");
+  const long long B = (long long)nf * nt * nr;
+  if (B > p->max_batch) return fail(NF_ERR_ARG, "batch larger than the plan's max_batch");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool dev = iter == NF_ITER_DEVICE;
+  struct_sample_kernel<<<1, 256, 0, st>>>(seed, iter, dev ? p->d_iter : nullptr, p->g.F, p->g.T, p->g.R, nf, nt, nr,
+                                          p->d_struct);
+  CUDA_TRY(cudaGetLastError());
+  p->snf = nf;
+  p->snt = nt;
+  p->snr = nr;
+  const StructArgs sa = struct_args(p);
+  struct_prep_kernel<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(sa, p->g.T, p->g.R, p->d_sm, p->d_spos, p->d_sf);
+  CUDA_TRY(cudaGetLastError());
+  p->launches += 2;
+  if (lists) {  // copy of the drawn lists, [fs | ts | rs]
+    CUDA_TRY(cudaMemcpyAsync(lists, sa.fs, sizeof(int) * nf, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(lists + nf, sa.ts, sizeof(int) * nt, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(lists + nf + nt, sa.rs, sizeof(int) * nr, cudaMemcpyDeviceToDevice, st));
+  }
+  p->B = (int)B;
+  p->structured = true;
+  return NF_OK;
 }
 
 int nf_sample_flat(nf_plan* p, uint64_t seed, uint64_t iter, int B, int32_t* idx, void* stream) {

@@ -255,6 +255,21 @@ class DevicePlan:
         )
         return out
 
+    def sample_structured(self, seed: int, it: int | None, n_f: int, n_tx: int, n_rx: int,
+                          lists: torch.Tensor | None = None) -> None:
+        """Device structured sampler: draw and stage an n_f x n_tx x n_rx Cartesian batch
+        (nf_sample_structured). ``it=None`` uses and advances the device iteration counter;
+        ``lists`` (int32 device, n_f + n_tx + n_rx) receives the drawn [fs | ts | rs]."""
+        itv = _lib.NF_ITER_DEVICE if it is None else int(it)
+        _lib.check(
+            self.lib.nf_sample_structured(self._h, int(seed) & (2**64 - 1), itv, int(n_f), int(n_tx), int(n_rx),
+                                          _ptr(lists), _stream(self.device)),
+            "nf_sample_structured",
+        )
+        self.B = int(n_f * n_tx * n_rx)
+        self._idx = None
+        self.staged_structured = True
+
     def set_iter(self, it: int) -> None:
         _lib.check(self.lib.nf_plan_set_iter(self._h, int(it), _stream(self.device)), "nf_plan_set_iter")
 

@@ -152,8 +152,8 @@ class SolverConfig:
             self.flat_batch = int(self.flat_batch)
         if int(self.check_every) < 1:
             raise ValueError("check_every must be >= 1")
-        if self.sampler == "device" and self.composition is not None:
-            raise ValueError("sampler='device' draws flat batches; use flat_batch, not composition")
+        if self.sampler == "device" and self.composition is None and self.flat_batch is None:
+            raise ValueError("sampler='device' needs flat_batch or composition")
         if self.sampler == "table":
             if self.index_table is None:
                 raise ValueError("sampler='table' needs index_table")
@@ -338,19 +338,32 @@ class SPGMEngine:
         self.plan.sample_flat(seed, it, batch, self.idx_dev)
         self.plan.prepare(self.idx_dev[:batch])
 
-    def graph(self, seed: int, batch: int, pairs: int = 1):
+    def sample_device_structured(self, seed: int, it: int | None, composition) -> None:
+        """Device structured sampler (a Cartesian n_f x n_tx x n_rx batch per iteration)."""
+        c = composition
+        self.plan.sample_structured(seed, it, c.n_f, c.n_tx, c.n_rx)
+
+    def graph(self, seed: int, batch: int, pairs: int = 1, composition=None):
         """Capture ``2·pairs`` device-sampled SPGM iterations in one CUDA graph (an even count,
         so the iterate ends in the buffer it started in). Replays draw fresh batches from the
-        plan's device iteration counter. With a process group the NCCL all-reduce of the
-        forward partials is captured into the graph as well."""
+        plan's device iteration counter: flat batches of ``batch`` channels, or Cartesian
+        ``composition`` batches. With a process group the NCCL all-reduce of the forward
+        partials is captured into the graph as well."""
+
+        def draw():
+            if composition is None:
+                self.sample_device(seed, None, batch)
+            else:
+                self.sample_device_structured(seed, None, composition)
+
         # one eager step outside capture so every kernel attribute is set (and NCCL is warm)
-        self.sample_device(seed, None, batch)
+        draw()
         self.step_staged()
         torch.cuda.synchronize(self.plan.device)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for _ in range(2 * pairs):
-                self.sample_device(seed, None, batch)
+                draw()
                 self.step_staged()
         return g
 
@@ -398,6 +411,9 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
                 staged_full = True
             return m
         if config.sampler == "device":
+            if config.composition is not None:
+                eng.sample_device_structured(config.rng_seed, k, config.composition)
+                return config.composition.batch_size
             eng.sample_device(config.rng_seed, k, config.flat_batch)
             return config.flat_batch
         if config.sampler == "table":
@@ -456,8 +472,12 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
                 staged_full = True
             B = m
         elif config.sampler == "device":
-            B = config.flat_batch
-            eng.sample_device(config.rng_seed, k, B)
+            if config.composition is not None:
+                B = config.composition.batch_size
+                eng.sample_device_structured(config.rng_seed, k, config.composition)
+            else:
+                B = config.flat_batch
+                eng.sample_device(config.rng_seed, k, B)
         elif config.sampler == "table":
             B = eng.stage(np.asarray(config.index_table[k - 1]))
         elif config.flat_batch is not None:

@@ -30,6 +30,7 @@ from paper_2509_00774_b200 import (
     spgm_solve,
 )
 from paper_2509_00774_b200.forward import get_plan
+from paper_2509_00774_b200.plan import DevicePlan
 from paper_2509_00774_b200.solver import SPGMEngine
 
 pytestmark = pytest.mark.gpu
@@ -316,3 +317,73 @@ def test_pipelined_solver_equals_serial_loop(small_scenario, rng):
     p1 = pgm_solve(y, small_scenario, SolverConfig(max_iters=15, tol=1e-300))
     p2 = pgm_solve(y, small_scenario, SolverConfig(max_iters=15, tol=1e-300), progress=lambda k, s: None)
     assert np.array_equal(p1.volume.values, p2.volume.values)
+
+
+def test_device_structured_sampler():
+    """nf_sample_structured: distinct sorted in-range lists per axis, deterministic in (seed, iter),
+    the device counter path equal to explicit iterations, and uniform per-axis selection."""
+    scn = configs.large_scenario()
+    plan = DevicePlan(scn, dtype="c64", max_batch=4096)
+    F, T, R = scn.frequencies.count, scn.array.n_tx, scn.array.n_rx
+    nf, nt, nr = 4, 32, 32
+    lists = torch.empty(nf + nt + nr, dtype=torch.int32, device=plan.device)
+    counts = np.zeros(F)
+    seen = set()
+    for it in range(600):
+        plan.sample_structured(7, it, nf, nt, nr, lists)
+        v = lists.cpu().numpy()
+        for part, n in ((v[:nf], F), (v[nf:nf + nt], T), (v[nf + nt:], R)):
+            assert np.all(np.diff(part) > 0) and part.min() >= 0 and part.max() < n
+        counts[v[:nf]] += 1
+        seen.add(tuple(v))
+        assert plan.B == nf * nt * nr and plan.staged_structured
+    assert len(seen) == 600
+    exp = 600 * nf / F
+    chi2 = float(np.sum((counts - exp) ** 2 / exp))
+    assert chi2 < 190  # 127 dof, p = 0.001 critical value ≈ 181 (+ margin)
+    plan.sample_structured(7, 5, nf, nt, nr, lists)
+    a = lists.cpu().numpy().copy()
+    plan.set_iter(5)
+    plan.sample_structured(7, None, nf, nt, nr, lists)
+    assert np.array_equal(lists.cpu().numpy(), a)
+    plan.sample_structured(7, None, nf, nt, nr, lists)  # the counter advanced to 6
+    plan2 = lists.cpu().numpy().copy()
+    plan.sample_structured(7, 6, nf, nt, nr, lists)
+    assert np.array_equal(lists.cpu().numpy(), plan2)
+    with pytest.raises(ValueError):
+        plan.sample_structured(7, 0, F + 1, 1, 1)
+
+
+def test_device_structured_steps_equal_host_staging_and_graph():
+    """SPGM steps on device-drawn Cartesian batches equal the same batches staged from the host
+    (same kernels, bitwise), and a captured graph of them equals the eager sequence."""
+    scn = configs.medium_scenario()
+    rng = np.random.default_rng(9)
+    y = rc(rng, scn.n_channels)
+    comp = MinibatchComposition(4, 12, 12)
+    n = comp.n_f + comp.n_tx + comp.n_rx
+    outs = []
+    for mode in ("device", "host", "graph"):
+        plan = DevicePlan(scn, dtype="c64", max_batch=comp.batch_size)
+        plan.set_iter(0)
+        eng = SPGMEngine(plan, y, eta=100.0, alpha=1e-6)
+        if mode == "graph":
+            g = eng.graph(seed=2, batch=0, pairs=2, composition=comp)  # one eager step + 4 captured
+            g.replay()
+        else:
+            lists = torch.empty(n, dtype=torch.int32, device=plan.device)
+            for _ in range(5):
+                if mode == "device":
+                    eng.sample_device_structured(2, None, comp)
+                else:
+                    probe = DevicePlan(scn, dtype="c64", max_batch=comp.batch_size) if _ == 0 else probe
+                    probe.sample_structured(2, _, comp.n_f, comp.n_tx, comp.n_rx, lists)
+                    v = lists.cpu().numpy()
+                    plan.prepare_structured(v[:comp.n_f], v[comp.n_f:comp.n_f + comp.n_tx], v[comp.n_f + comp.n_tx:])
+                eng.step_staged()
+        torch.cuda.synchronize()
+        outs.append(eng.volume())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    rep = spgm_solve(y, scn, SolverConfig(max_iters=6, tol=1e-300, composition=comp, sampler="device", rng_seed=2,
+                                          dtype="c64", eta=100.0, alpha=1e-6))
+    assert rep.iterations == 6 and [r.batch_size for r in rep.per_iteration] == [comp.batch_size] * 6
