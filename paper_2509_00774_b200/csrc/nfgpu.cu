@@ -93,6 +93,17 @@ static_assert(TBR == 8 || TBR == 16, "TBR must be 8 or 16");
 constexpr int A_MAX = 256;     // antennas (T + R) per plan
 constexpr int RED_THREADS = 300000;
 constexpr unsigned FULL = 0xffffffffu;
+
+// Programmatic dependent launch: kernels of the SPGM step are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs are scheduled while its
+// predecessor drains; each of them waits here before touching its predecessor's outputs.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// small kernels let their successor's CTAs be scheduled right away (they wait in pdl_wait());
+// the two big kernels keep the implicit trigger at exit so waiting CTAs do not take their SM slots
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 constexpr double PI = 3.14159265358979323846;
 constexpr double EXACT_FREE_REV = 12.0;  // largest |phase| (revolutions) fed to MUFU unreduced
 
@@ -431,6 +442,7 @@ __device__ __forceinline__ int4 chan_of_key(const KeyMap& k, int key) {  // {f, 
 }
 
 __global__ void mark_kernel(KeyMap km, const int* __restrict__ idx, int B, int* __restrict__ pos_of_key) {
+  pdl_wait_and_release();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < B) pos_of_key[key_of(km, idx[i])] = i;
 }
@@ -463,6 +475,7 @@ __device__ __forceinline__ int block_excl_scan_1024(int v, int* sh, int& total) 
 
 __global__ void __launch_bounds__(1024) count_kernel(const int* __restrict__ pos_of_key, int KS,
                                                       int* __restrict__ cnt) {
+  pdl_wait_and_release();
   const int key = blockIdx.x * 1024 + threadIdx.x;
   const int f = (key < KS && pos_of_key[key] >= 0) ? 1 : 0;
   const int c = __syncthreads_count(f);
@@ -470,6 +483,7 @@ __global__ void __launch_bounds__(1024) count_kernel(const int* __restrict__ pos
 }
 
 __global__ void __launch_bounds__(1024) scan_kernel(int* __restrict__ cnt, int n) {
+  pdl_wait_and_release();
   __shared__ int sh[32];
   int carry = 0;
   for (int base = 0; base < n; base += 1024) {
@@ -498,6 +512,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(KeyMap km, int* __restric
                                                         const int* __restrict__ off, int* __restrict__ sm,
                                                         int* __restrict__ spos, ChanRec* __restrict__ crec,
                                                         int* __restrict__ sf, const double* __restrict__ kd) {
+  pdl_wait_and_release();
   __shared__ int sh[32];
   const int key = blockIdx.x * 1024 + threadIdx.x;
   const int p = key < KS ? pos_of_key[key] : -1;
@@ -546,6 +561,7 @@ __host__ __device__ __forceinline__ uint64_t sample_key(uint64_t seed, uint64_t 
 // iter_dev != null: the iteration number is read from device memory (graph-capturable loop)
 __global__ void sample_kernel(uint64_t seed, uint64_t iter, const unsigned long long* __restrict__ iter_dev, int hb,
                               int M, int B, int* __restrict__ idx) {
+  pdl_wait_and_release();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= B) return;
   const uint64_t key = sample_key(seed, iter_dev ? (uint64_t)*iter_dev : iter);
@@ -555,7 +571,10 @@ __global__ void sample_kernel(uint64_t seed, uint64_t iter, const unsigned long 
   } while (x >= (uint32_t)M);
   idx[j] = (int)x;
 }
-__global__ void bump_kernel(unsigned long long* it) { *it += 1ULL; }
+__global__ void bump_kernel(unsigned long long* it) {
+  pdl_wait_and_release();
+  *it += 1ULL;
+}
 
 // Structured (Cartesian) sampler on the device: k_a distinct sorted indices out of n_a for each axis
 // a in {frequency, tx, rx}, the first k_a images of a keyed Feistel permutation of [0, n_a)
@@ -784,6 +803,7 @@ __global__ void __launch_bounds__(256) resid_kernel(const int* __restrict__ sm, 
                                                     const Real* __restrict__ r, const Real* __restrict__ ymeas,
                                                     const double* __restrict__ pulse, R2<Real>* __restrict__ wrec,
                                                     double* __restrict__ dpart) {
+  pdl_wait_and_release();
   __shared__ double sh[8];
   const int j = blockIdx.x * 256 + threadIdx.x;
   double e = 0;
@@ -902,6 +922,7 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
 
 template <typename Real, bool PROX, bool EXACT>
 __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(AdjArgs<Real> a) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
@@ -972,6 +993,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
 __global__ void __launch_bounds__(256) stats_reduce_kernel(const double* __restrict__ part, int n,
                                                            const double* __restrict__ dpart, int nd,
                                                            double* __restrict__ out) {
+  pdl_wait_and_release();
   __shared__ double sh[4][256];
   double acc[4] = {0, 0, 0, 0};
   for (int i = threadIdx.x; i < n; i += 256) {
@@ -1036,6 +1058,7 @@ __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __re
 // rows in L2.
 template <typename Real, bool EXACT>
 __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(FwdArgs<Real> a) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
@@ -2251,6 +2274,7 @@ __global__ void struct_prep_kernel(StructArgs sa, int T, int R, int* __restrict_
 template <typename Real>
 __global__ void fwd_reduce1_kernel(const Real* __restrict__ part, int nx, int span, int nseg,
                                    double2* __restrict__ tmp) {
+  pdl_wait_and_release();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int seg = blockIdx.y;
   if (j >= span) return;
@@ -2268,6 +2292,7 @@ template <typename Real>
 __global__ void fwd_reduce2_kernel(const double2* __restrict__ tmp, int span, int nseg, int w0,
                                    const int* __restrict__ sf, const int* __restrict__ spos,
                                    const double* __restrict__ pulse, Real* __restrict__ y) {
+  pdl_wait_and_release();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= span) return;
   double sr = 0, si = 0;
@@ -2378,6 +2403,7 @@ struct nf_plan {
   // tensor-core structured adjoint (c64): B images [batch frequency][K chunk][hi|lo][npad][16]
   bool use_tc = false;
   bool tc_force = false;  // NFGPU_TC=2: tensor-core kernels whenever eligible (tests)
+  bool use_pdl = true;    // programmatic dependent launch of the SPGM step kernels (env NFGPU_PDL=0 disables)
   bool tc_fwd = false;    // NFGPU_TC_FWD=1: route structured forwards to the tcgen05 forward
   float* d_bimg = nullptr;
   // tensor-core structured forward: per-(half tile, channel) partials, allocated on first use
@@ -2386,6 +2412,23 @@ struct nf_plan {
 };
 
 namespace {
+
+// launch with programmatic dependent launch when enabled (the kernel must begin with pdl_wait())
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 template <typename T>
 int dalloc(nf_plan* p, T** ptr, size_t bytes) {
@@ -2454,17 +2497,15 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.Q = channel_splits(p, span);
     a.part = (Real*)p->d_part;
     const long long units = (long long)p->g.ntiles * a.Q;
-    kern<<<(unsigned)((units + FWD_WARPS - 1) / FWD_WARPS), FWD_WARPS * 32, sm, st>>>(a);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_k(p->use_pdl, kern, dim3((unsigned)((units + FWD_WARPS - 1) / FWD_WARPS)), dim3(FWD_WARPS * 32),
+                      sm, st, a));
     // two-level reduce: ~sqrt(rows) segments so both levels have short serial sums
     int nseg = (int)std::ceil(std::sqrt((double)p->fwd_gridx));
     nseg = std::max(1, std::min({nseg, p->fwd_gridx, std::max(1, RED_THREADS / span)}));
-    fwd_reduce1_kernel<Real><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const Real*)p->d_part, p->fwd_gridx,
-                                                                             span, nseg, p->d_tmp);
-    CUDA_TRY(cudaGetLastError());
-    fwd_reduce2_kernel<Real><<<(span + 255) / 256, 256, 0, st>>>(p->d_tmp, span, nseg, w0, p->d_sf, p->d_spos,
-                                                                 p->d_pulse, (Real*)y);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_k(p->use_pdl, fwd_reduce1_kernel<Real>, dim3((span + 255) / 256, nseg), dim3(256), 0, st,
+                      (const Real*)p->d_part, p->fwd_gridx, span, nseg, p->d_tmp));
+    CUDA_TRY(launch_k(p->use_pdl, fwd_reduce2_kernel<Real>, dim3((span + 255) / 256), dim3(256), 0, st, p->d_tmp, span,
+                      nseg, w0, p->d_sf, p->d_spos, p->d_pulse, (Real*)y));
     p->launches += 3;
   }
   return NF_OK;
@@ -2598,9 +2639,8 @@ template <typename Real, bool PROX>
 int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, double scale, const void* s_in,
                    void* s_out, double eta_over_b, double alpha, double* stats, cudaStream_t st) {
   const int nblk = (p->B + 255) / 256;
-  resid_kernel<Real><<<nblk, 256, 0, st>>>(p->d_sm, p->d_spos, p->d_sf, p->B, (const Real*)r,
-                                            (const Real*)ymeas, p->d_pulse, (R2<Real>*)p->d_wrec, p->d_dpart);
-  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(launch_k(p->use_pdl, resid_kernel<Real>, dim3(nblk), dim3(256), 0, st, p->d_sm, p->d_spos, p->d_sf, p->B,
+                    (const Real*)r, (const Real*)ymeas, p->d_pulse, (R2<Real>*)p->d_wrec, p->d_dpart));
   AdjArgs<Real> a;
   a.g = p->g;
   a.tab = (const Real*)p->d_tab;
@@ -2662,13 +2702,13 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
     CUDA_TRY(
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     const int units = p->g.ntiles * a.CH;
-    kern<<<(units + ADJ_WARPS - 1) / ADJ_WARPS, ADJ_WARPS * 32, sm, st>>>(a);
+    CUDA_TRY(launch_k(p->use_pdl, kern, dim3((units + ADJ_WARPS - 1) / ADJ_WARPS), dim3(ADJ_WARPS * 32), sm, st, a));
   }
   CUDA_TRY(cudaGetLastError());
   p->launches += 2;
   if (PROX) {
-    stats_reduce_kernel<<<1, 256, 0, st>>>(p->d_stat_part, p->g.ntiles, p->d_dpart, nblk, stats);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_k(p->use_pdl, stats_reduce_kernel, dim3(1), dim3(256), 0, st, (const double*)p->d_stat_part,
+                      p->g.ntiles, (const double*)p->d_dpart, nblk, stats));
     p->launches += 1;
   }
   return NF_OK;
@@ -2797,6 +2837,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     p->tc_force = std::atoi(e) == 2;
   }
   if (const char* e = std::getenv("NFGPU_TC_FWD")) p->tc_fwd = std::atoi(e) != 0;
+  if (const char* e = std::getenv("NFGPU_PDL")) p->use_pdl = std::atoi(e) != 0;
   if (p->use_tc) {
     const size_t npad_max = (size_t)((2 * n_tx + 15) / 16) * 16;
     ALLOC(p->d_bimg, (size_t)n_f * ((n_rx + TC_RCH - 1) / TC_RCH) * npad_max * (2 * TC_RCH) * 4 * 2);
@@ -2859,12 +2900,13 @@ int nf_batch_prepare(nf_plan* p, const int32_t* idx, int B, void* stream) {
   if (B < 1) return fail(NF_ERR_ARG, "channel subset must be non-empty");
   if (B > p->max_batch) return fail(NF_ERR_ARG, "batch larger than the plan's max_batch");
   cudaStream_t st = (cudaStream_t)stream;
-  mark_kernel<<<(B + 255) / 256, 256, 0, st>>>(p->km, idx, B, p->d_pos_of_key);
-  count_kernel<<<p->ksblocks, 1024, 0, st>>>(p->d_pos_of_key, p->KS, p->d_cnt);
-  scan_kernel<<<1, 1024, 0, st>>>(p->d_cnt, p->ksblocks);
-  compact_kernel<<<p->ksblocks, 1024, 0, st>>>(p->km, p->d_pos_of_key, p->KS, p->d_cnt, p->d_sm, p->d_spos,
-                                               p->d_crec, p->d_sf, p->d_kd);
-  CUDA_TRY(cudaGetLastError());
+  const bool pdl = p->use_pdl;
+  CUDA_TRY(launch_k(pdl, mark_kernel, dim3((B + 255) / 256), dim3(256), 0, st, p->km, idx, B, p->d_pos_of_key));
+  CUDA_TRY(launch_k(pdl, count_kernel, dim3(p->ksblocks), dim3(1024), 0, st, (const int*)p->d_pos_of_key, p->KS,
+                    p->d_cnt));
+  CUDA_TRY(launch_k(pdl, scan_kernel, dim3(1), dim3(1024), 0, st, p->d_cnt, p->ksblocks));
+  CUDA_TRY(launch_k(pdl, compact_kernel, dim3(p->ksblocks), dim3(1024), 0, st, p->km, p->d_pos_of_key, p->KS,
+                    (const int*)p->d_cnt, p->d_sm, p->d_spos, p->d_crec, p->d_sf, (const double*)p->d_kd));
   p->launches += 4;
   p->B = B;
   p->structured = false;
@@ -2976,12 +3018,11 @@ int nf_sample_flat(nf_plan* p, uint64_t seed, uint64_t iter, int B, int32_t* idx
   while ((1LL << bits) < p->M) bits += 2;
   cudaStream_t st = (cudaStream_t)stream;
   const bool dev = iter == NF_ITER_DEVICE;
-  sample_kernel<<<(B + 255) / 256, 256, 0, st>>>(seed, iter, dev ? p->d_iter : nullptr, bits / 2, p->M, B, idx);
-  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(launch_k(p->use_pdl, sample_kernel, dim3((B + 255) / 256), dim3(256), 0, st, seed, iter,
+                    (const unsigned long long*)(dev ? p->d_iter : nullptr), bits / 2, p->M, B, idx));
   p->launches += 1;
   if (dev) {
-    bump_kernel<<<1, 1, 0, st>>>(p->d_iter);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_k(p->use_pdl, bump_kernel, dim3(1), dim3(1), 0, st, p->d_iter));
     p->launches += 1;
   }
   return NF_OK;
