@@ -1783,6 +1783,18 @@ __device__ __forceinline__ void phasor1(float k, float b, float dl, float amp, f
   im = amp * sgn * s;
 }
 
+// two phasors at once on packed pairs: amp·(cos x, sin x), x = b + k·δ (sgn +1)
+template <bool EXACT>
+__device__ __forceinline__ void phasor2(float2 k, float2 b, float2 dl, float2 amp, float2& re, float2& im) {
+  float2 x = fma2(k, dl, b);
+  if (EXACT) x = mul2(sub2(x, sub2(add2(x, bc(12582912.0f)), bc(12582912.0f))), bc(6.28318530717958647692f));
+  float2 sn, cs;
+  __sincosf(x.x, &sn.x, &cs.x);
+  __sincosf(x.y, &sn.y, &cs.y);
+  re = mul2(amp, cs);
+  im = mul2(amp, sn);
+}
+
 // B images of every (batch frequency, K chunk): [hi | lo] x [npad rows][32 k] in the smem layout
 __global__ void tc_bprep_kernel(StructArgs sa, const float2* __restrict__ wrec, int npad, int nch,
                                 float* __restrict__ out) {
@@ -1918,23 +1930,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);  // MMAs of step s - NS released the stage
         unsigned char* Ast = sm + ly.a_off + st * 2 * TC_A_BYTES;
 #pragma unroll
-        for (int qq = 0; qq < TC_RCH / 2; qq += 2) {  // two receivers = one 16-B chunk of the row
+        for (int qq = 0; qq < TC_RCH / 2; qq += 2) {  // two receivers (a packed pair) = one 16-B chunk of the row
           const int q = sub * (TC_RCH / 2) + qq;
-          float v4[4];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = c * TC_RCH + q + e;
-            v4[2 * e] = v4[2 * e + 1] = 0.f;
-            if (r < sa.nr) {
-              const float* rowp = tsm + (sa.nt + r) * 256 + row;
-              phasor1<EXACT>(kr[r], br[r], rowp[0], rowp[128], 1.f, v4[2 * e], v4[2 * e + 1]);
-            }
-          }
-          const float4 h = make_float4(tf32_round(v4[0]), tf32_round(v4[1]), tf32_round(v4[2]), tf32_round(v4[3]));
+          const int r0 = c * TC_RCH + q, r1 = r0 + 1;
+          const int c0 = min(r0, sa.nr - 1), c1 = min(r1, sa.nr - 1);  // out-of-range partners get amplitude 0
+          const float* p0 = tsm + (sa.nt + c0) * 256 + row;
+          const float* p1 = tsm + (sa.nt + c1) * 256 + row;
+          float2 re, im;
+          phasor2<EXACT>(make_float2(kr[c0], kr[c1]), make_float2(br[c0], br[c1]), make_float2(p0[0], p1[0]),
+                         make_float2(r0 < sa.nr ? p0[128] : 0.f, r1 < sa.nr ? p1[128] : 0.f), re, im);
+          const float4 h = make_float4(tf32_round(re.x), tf32_round(im.x), tf32_round(re.y), tf32_round(im.y));
+          const float2 l0 = sub2(make_float2(re.x, im.x), make_float2(h.x, h.y));
+          const float2 l1 = sub2(make_float2(re.y, im.y), make_float2(h.z, h.w));
           const uint32_t off = kmaj(row, 2 * q, 128);
           *reinterpret_cast<float4*>(Ast + off) = h;
-          *reinterpret_cast<float4*>(Ast + TC_A_BYTES + off) =
-              make_float4(v4[0] - h.x, v4[1] - h.y, v4[2] - h.z, v4[3] - h.w);
+          *reinterpret_cast<float4*>(Ast + TC_A_BYTES + off) = make_float4(l0.x, l0.y, l1.x, l1.y);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -1944,7 +1954,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
     }
   } else {  // ---------------- epilogue: g += Σ_t conj(U_t)·z_t
     const int et = tid - HT, row = et & 127, sub = et >> 7;  // 2 threads per voxel row
-    float gr = 0.f, gi = 0.f;
+    float2 g2r = make_float2(0.f, 0.f), g2i = g2r;          // even / odd transmitters, added at the end
     for (int fl = 0; fl < nfl; ++fl) {
       float* kt = par + 1024 + (fl & 1) * 128;
       float* bt = kt + 64;
@@ -1958,20 +1968,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
         float z[8];
         tmem_ld8(base + t4 * 8, z);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int t = t4 * 4 + j;
-          if (t < sa.nt) {
-            float ur, ui;
-            phasor1<EXACT>(kt[t], bt[t], tsm[t * 256 + row], tsm[t * 256 + 128 + row], 1.f, ur, ui);
-            gr = fmaf(ur, z[2 * j], fmaf(-ui, z[2 * j + 1], gr));
-            gi = fmaf(ur, z[2 * j + 1], fmaf(ui, z[2 * j], gi));
-          }
+        for (int j = 0; j < 4; j += 2) {  // transmitters t, t+1 as a packed pair
+          const int t0 = t4 * 4 + j, t1 = t0 + 1;
+          const int c0 = min(t0, sa.nt - 1), c1 = min(t1, sa.nt - 1);  // out-of-range partners get amplitude 0
+          float2 ur, ui;
+          phasor2<EXACT>(make_float2(kt[c0], kt[c1]), make_float2(bt[c0], bt[c1]),
+                         make_float2(tsm[c0 * 256 + row], tsm[c1 * 256 + row]),
+                         make_float2(t0 < sa.nt ? tsm[c0 * 256 + 128 + row] : 0.f,
+                                     t1 < sa.nt ? tsm[c1 * 256 + 128 + row] : 0.f),
+                         ur, ui);
+          const float2 zr = make_float2(z[2 * j], z[2 * j + 2]), zi = make_float2(z[2 * j + 1], z[2 * j + 3]);
+          g2r = fma2(ur, zr, fma2(make_float2(-ui.x, -ui.y), zi, g2r));
+          g2i = fma2(ur, zi, fma2(ui, zr, g2i));
         }
       }
       tc_fence_before();
       __syncwarp();
       if (L == 0) mbar_arrive(&zfree[fl & 1]);
     }
+    const float gr = g2r.x + g2r.y, gi = g2i.x + g2i.y;
     // combine the two sub-threads; every MMA is complete, so the A stages are free
     float* cb = reinterpret_cast<float*>(sm + ly.a_off);  // [2][128][2]
     cb[(sub * 128 + row) * 2] = gr;
