@@ -1853,7 +1853,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
                    : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    for (int i = tid; i < g.A; i += TC_CT) d0[i] = a.D0[(size_t)tile * g.A + i];
+    for (int i = tid; i < nant; i += TC_CT)  // fp64 anchors per batch slot: no global index loads later
+      d0[i] = a.D0[(size_t)tile * g.A + (i < sa.nt ? sa.ts[i] : g.T + sa.rs[i - sa.nt])];
   }
   if (tid == 0) {
     for (int i = 0; i < ns; ++i) {
@@ -1920,11 +1921,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
   } else if (w < TC_CW / 2) {  // ---------------- A generation: conj(V) of 8 receivers per step
     const int row = tid & 127, sub = tid >> 7;  // 2 threads per voxel row
     int st = 0, k = 0;                          // pipeline stage and its use count
+    double kfn = nfl > 0 ? kd[sa.fs[f0]] : 0.0;
     for (int fl = 0; fl < nfl; ++fl) {
       float* kr = par + (fl & 1) * 512;
       float* br = kr + 256;
-      const double kf = kd[sa.fs[f0 + fl]];
-      for (int q = tid; q < sa.nr; q += HT) side_params<float, EXACT>(kf, d0[g.T + sa.rs[q]], kr[q], br[q]);
+      const double kf = kfn;
+      if (fl + 1 < nfl) kfn = kd[sa.fs[f0 + fl + 1]];  // prefetch: lands while this frequency runs
+      for (int q = tid; q < sa.nr; q += HT) side_params<float, EXACT>(kf, d0[sa.nt + q], kr[q], br[q]);
       named_bar(1, HT);
       for (int c = 0; c < nch; ++c) {
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);  // MMAs of step s - NS released the stage
@@ -1955,11 +1958,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
   } else {  // ---------------- epilogue: g += Σ_t conj(U_t)·z_t
     const int et = tid - HT, row = et & 127, sub = et >> 7;  // 2 threads per voxel row
     float2 g2r = make_float2(0.f, 0.f), g2i = g2r;          // even / odd transmitters, added at the end
+    double kfn = nfl > 0 ? kd[sa.fs[f0]] : 0.0;
     for (int fl = 0; fl < nfl; ++fl) {
       float* kt = par + 1024 + (fl & 1) * 128;
       float* bt = kt + 64;
-      const double kf = kd[sa.fs[f0 + fl]];
-      for (int q = et; q < sa.nt; q += HT) side_params<float, EXACT>(kf, d0[sa.ts[q]], kt[q], bt[q]);
+      const double kf = kfn;
+      if (fl + 1 < nfl) kfn = kd[sa.fs[f0 + fl + 1]];
+      for (int q = et; q < sa.nt; q += HT) side_params<float, EXACT>(kf, d0[q], kt[q], bt[q]);
       named_bar(2, HT);
       mbar_wait(&zfull[fl & 1], (fl >> 1) & 1);
       tc_fence_after();
@@ -2067,7 +2072,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
       const float* src = tabt + (size_t)ant * TABW + vi;
       tv[vi * TS + sl] = make_float2(src[0], src[TILE]);
     }
-    for (int i = tid; i < g.A; i += TC_CT) d0[i] = a.D0[(size_t)tile * g.A + i];
+    for (int i = tid; i < sa.nt + sa.nr; i += TC_CT)  // fp64 anchors per batch slot
+      d0[i] = a.D0[(size_t)tile * g.A + (i < sa.nt ? sa.ts[i] : g.T + sa.rs[i - sa.nt])];
     if (tid < 128) {  // s at the half tile's table positions
       int tx, ty, tz;
       tile_coords(g, tile, tx, ty, tz);
@@ -2204,14 +2210,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
         }
       }
     }
+    double kfn = nfl > 0 ? kd[sa.fs[f0]] : 0.0;
     for (int fl = 0; fl < nfl; ++fl) {
       float* kt = par + (fl & 1) * 640;
       float* bt = kt + 64;
       float* kr = kt + 128;
       float* br = kt + 384;
-      const double kf = kd[sa.fs[f0 + fl]];
-      for (int q = tid; q < sa.nt; q += TC_CT) side_params<float, EXACT>(kf, d0[sa.ts[q]], kt[q], bt[q]);
-      for (int q = tid; q < sa.nr; q += TC_CT) side_params<float, EXACT>(kf, d0[g.T + sa.rs[q]], kr[q], br[q]);
+      const double kf = kfn;
+      if (fl + 1 < nfl) kfn = kd[sa.fs[f0 + fl + 1]];  // prefetch: lands while this frequency runs
+      for (int q = tid; q < sa.nt; q += TC_CT) side_params<float, EXACT>(kf, d0[q], kt[q], bt[q]);
+      for (int q = tid; q < sa.nr; q += TC_CT) side_params<float, EXACT>(kf, d0[sa.nt + q], kr[q], br[q]);
       named_bar(1, TC_CT);
       for (int c = 0; c < SPF; ++c) {
         const int s = fl * SPF + c, st = s % TCF_NS, k = s / TCF_NS;
