@@ -1692,6 +1692,8 @@ constexpr int TC_SUB = TC_CT / 128;           // compute threads per voxel row
 constexpr int TC_RCH = 8;                     // receivers per pipeline step (K = 16 reals = two MMAs of K = 8)
 constexpr int TC_NS = 4;                      // adjoint pipeline stages (at most; fewer when the table is large)
 constexpr int TCF_NS = 2;                     // forward pipeline stages
+constexpr int TCF_GW = 12;                    // forward generation warps (warps 12..15 drain TMEM)
+constexpr int TCF_NIT = 7;                    // generation items per thread and step: 8·(64 + 256) <= 7·384
 constexpr int TC_NMAX = 128;                  // max padded 2·n_t (TMEM: 2 regions × N ≤ 256 columns)
 constexpr uint32_t TC_A_BYTES = 128 * 2 * TC_RCH * 4;  // one of hi/lo: 8 KB
 constexpr uint32_t TC_SMEM_MAX = 227 * 1024;
@@ -1766,10 +1768,10 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, float (&v)[8]) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// round to the nearest tf32, ties away from zero (cvt.rna.tf32.f32 for finite x; ptxas expands that
+// instruction with an inf/nan check, this is two integer ops)
 __device__ __forceinline__ float tf32_round(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
 // amplitude-weighted one-sided phasor of one voxel: amp·(cos x, sgn·sin x), x = b + k·δ
@@ -2038,7 +2040,7 @@ struct TcfLayout {
     s_off = b_off + TCF_NS * b_stage;           // s of the half tile: [128] complex
     tab_off = s_off + 128 * 8;                  // [voxel 128][slot, stride nant|1] (δ, 1/d)
     d0_off = tab_off + (uint32_t)(nant | 1) * 1024;
-    par_off = d0_off + A_MAX * 8;               // [2][kt 64 | bt 64 | kr 256 | br 256]
+    par_off = d0_off + A_MAX * 8;               // [2][k of slot 320 | b of slot 320]
     bar_off = par_off + 2 * 640 * 4;
     bytes = bar_off + (2 * TCF_NS + 6) * 8;
   }
@@ -2066,12 +2068,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
   uint32_t tcols = 32;
   while (tcols < 2u * npr) tcols <<= 1;
   if (tid < TC_CT) {
-    for (int i = tid; i < nant * 128; i += TC_CT) {  // coalesced global reads, transposed into smem
+    for (int i = tid; i < nant * 128; i += TC_CT) {  // coalesced 4-byte async copies, transposed into smem
       const int sl = i >> 7, vi = i & 127;
       const int ant = sl < sa.nt ? sa.ts[sl] : g.T + sa.rs[sl - sa.nt];
       const float* src = tabt + (size_t)ant * TABW + vi;
-      tv[vi * TS + sl] = make_float2(src[0], src[TILE]);
+      const uint32_t dst = smem_u32(tv + vi * TS + sl);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4), "l"(src + TILE) : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     for (int i = tid; i < sa.nt + sa.nr; i += TC_CT)  // fp64 anchors per batch slot
       d0[i] = a.D0[(size_t)tile * g.A + (i < sa.nt ? sa.ts[i] : g.T + sa.rs[i - sa.nt])];
     if (tid < 128) {  // s at the half tile's table positions
@@ -2101,12 +2106,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
   }
   if (tid == 0) {
     for (int i = 0; i < TCF_NS; ++i) {
-      mbar_init(&afull[i], TC_CW);
+      mbar_init(&afull[i], TCF_GW);
       mbar_init(&sfree[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&zfull[i], 1);
-      mbar_init(&zfree[i], TC_CW);
+      mbar_init(&zfree[i], TC_CW - TCF_GW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -2151,19 +2156,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
         if (c == SPF - 1) umma_commit(&zfull[fl & 1]);
       }
     }
-  } else if (w < TC_CW) {  // ---------------- compute warps: generate U (A) and W = V·s (B); drain TMEM
+  } else if (w >= TCF_GW && w < TC_CW) {  // ---------------- epilogue: drain TMEM of each frequency
+    // rows 2t, 2t+1 (lane pair) -> one complex partial per (half tile, channel). The pair splits each
+    // 16-receiver chunk 8/8, so every lane stores 8 complex (64 contiguous bytes).
     const int span = a.w1 - a.w0;
     float2* out = part + (size_t)(2 * tile + hb) * span - a.w0;
-    // epilogue of local frequency fl: TMEM rows 2t, 2t+1 -> one complex partial per (half tile, channel);
-    // the four warps of a lane quarter take every fourth 16-receiver column chunk
-    auto epilogue = [&](int fl) {
+    const int q = w & 3, row = 32 * q + L, t = row >> 1, odd = row & 1;
+    for (int fl = 0; fl < nfl; ++fl) {
       mbar_wait(&zfull[fl & 1], (fl >> 1) & 1);
       tc_fence_after();
-      const int row = 32 * (w & 3) + L, t = row >> 1, cp = row & 1;
-      if (32 * (w & 3) < mrows) {
-        const uint32_t base = tmem + (uint32_t)((fl & 1) * npr) + ((uint32_t)(32 * (w & 3)) << 16);
+      if (32 * q < mrows) {
+        const uint32_t base = tmem + (uint32_t)((fl & 1) * npr) + ((uint32_t)(32 * q) << 16);
         const int jb = (f0 + fl) * sa.nt * sa.nr;
-        for (int r16 = w >> 2; r16 * 16 < sa.nr; r16 += TC_CW / 4) {
+        for (int r16 = 0; r16 * 16 < sa.nr; ++r16) {
           uint32_t rr[16];
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -2172,107 +2177,103 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
                 "=r"(rr[14]), "=r"(rr[15])
               : "r"(base + r16 * 16));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float2 o[8];  // even lane: receivers 0..7 of the chunk, odd lane: 8..15
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float v = __uint_as_float(rr[j]);
-            const float o = __shfl_xor_sync(FULL, v, 1);
-            const int r = r16 * 16 + j;
-            if (cp == 0 && t < sa.nt && r < sa.nr) out[jb + t * sa.nr + r] = make_float2(v, o);
+          for (int j = 0; j < 8; ++j) {
+            const float lo8 = __uint_as_float(rr[j]), hi8 = __uint_as_float(rr[j + 8]);
+            const float mine = odd ? hi8 : lo8;
+            const float other = __shfl_xor_sync(FULL, odd ? lo8 : hi8, 1);
+            o[j] = odd ? make_float2(other, mine) : make_float2(mine, other);
+          }
+          const int r0 = r16 * 16 + 8 * odd;
+          if (t < sa.nt) {
+            float2* dst = out + jb + t * sa.nr + r0;
+            if (r0 + 8 <= sa.nr && ((sa.nr & 1) == 0)) {
+#pragma unroll
+              for (int j = 0; j < 8; j += 2)
+                *reinterpret_cast<float4*>(dst + j) = make_float4(o[j].x, o[j].y, o[j + 1].x, o[j + 1].y);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (r0 + j < sa.nr) dst[j] = o[j];
+            }
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (L == 0) mbar_arrive(&zfree[fl & 1]);
-    };
-    constexpr int EPI_STEP = 4;  // drain frequency f-1 this many steps into f (its MMAs are done by then)
-    // this thread's (at most two) generation items per step, decoded once. Items pair up on adjacent
-    // lanes: U items (row m = 2t + c', voxel pair vp) compute voxel 2vp + (m & 1) and write row m;
-    // W items (receiver r, voxel pair vp, e) compute voxel 2vp + e, and lane e = 0 / 1 writes hi / lo.
-    constexpr int NIT = 4;  // items per thread per step (up to 2048 items)
-    int icode[NIT];
-    uint32_t ioff[NIT];
-    {
-      const int nu = (TCF_VPS / 2) * mrows, nw = TCF_VPS * sa.nr;
+    }
+  } else if (w < TCF_GW) {  // ---------------- generation: U (A operand) and W = V·s (B operand)
+    // One item = (antenna slot, voxel pair) of a step; the thread computes both voxels. U items
+    // (transmitters) come first, padded to whole warps, so a warp is all-U or all-W, and its lanes
+    // run over consecutive antennas (conflict-free table reads). A U item writes rows 2t, 2t+1 of A
+    // ([[Ur, -Ui], [Ui, Ur]] form), a W item row r of B; hi and lo of the 3xTF32 split.
+    constexpr int GT = TCF_GW * 32;
+    const int nu = sa.nt * (TCF_VPS / 2), nupad = (nu + 31) & ~31, nitems = nupad + sa.nr * (TCF_VPS / 2);
+    int icode[TCF_NIT];
+    uint32_t ioff[TCF_NIT];
 #pragma unroll
-      for (int it = 0; it < NIT; ++it) {
-        const int j = tid + it * TC_CT;
-        icode[it] = -1;
-        ioff[it] = 0;
-        if (j < nu) {
-          const int m = j % mrows, vp = j / mrows;
-          icode[it] = (m >> 1) | ((2 * vp + (m & 1)) << 10);
-          ioff[it] = kmaj(m, 4 * vp, 128);
-        } else if (j < nu + nw) {
-          const int jw = j - nu, pr = jw >> 1, e = jw & 1, r = pr % sa.nr, vp = pr / sa.nr;
-          icode[it] = (sa.nt + r) | ((2 * vp + e) << 10) | ((1 + e) << 14);
-          ioff[it] = kmaj(r, 4 * vp, npr);
-        }
+    for (int it = 0; it < TCF_NIT; ++it) {
+      const int i = tid + it * GT;
+      icode[it] = -1;
+      ioff[it] = 0;
+      if (i < nu) {
+        const int t = i % sa.nt, vp = i / sa.nt;
+        icode[it] = t | (vp << 10);
+        ioff[it] = kmaj(2 * t, 4 * vp, 128);
+      } else if (i >= nupad && i < nitems) {
+        const int j = i - nupad, r = j % sa.nr, vp = j / sa.nr;
+        icode[it] = (sa.nt + r) | (vp << 10) | (1 << 14);
+        ioff[it] = kmaj(r, 4 * vp, npr);
       }
     }
     double kfn = nfl > 0 ? kd[sa.fs[f0]] : 0.0;
     for (int fl = 0; fl < nfl; ++fl) {
-      float* kt = par + (fl & 1) * 640;
-      float* bt = kt + 64;
-      float* kr = kt + 128;
-      float* br = kt + 384;
+      float* kp = par + (fl & 1) * 640;  // [slot] k, then [slot] b at +320
       const double kf = kfn;
       if (fl + 1 < nfl) kfn = kd[sa.fs[f0 + fl + 1]];  // prefetch: lands while this frequency runs
-      for (int q = tid; q < sa.nt; q += TC_CT) side_params<float, EXACT>(kf, d0[q], kt[q], bt[q]);
-      for (int q = tid; q < sa.nr; q += TC_CT) side_params<float, EXACT>(kf, d0[sa.nt + q], kr[q], br[q]);
-      named_bar(1, TC_CT);
+      for (int q = tid; q < nant; q += GT) side_params<float, EXACT>(kf, d0[q], kp[q], kp[320 + q]);
+      named_bar(1, GT);
       for (int c = 0; c < SPF; ++c) {
         const int s = fl * SPF + c, st = s % TCF_NS, k = s / TCF_NS;
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);
         unsigned char* Ast = sm + ly.a_off + st * 2 * TCF_A_BYTES;
         unsigned char* Bst = sm + ly.b_off + st * ly.b_stage;
 #pragma unroll
-        for (int it = 0; it < NIT; ++it) {
+        for (int it = 0; it < TCF_NIT; ++it) {
           const int code = icode[it];
           if (code < 0) continue;
-          const int slot = code & 0x3ff, vv = (code >> 10) & 15, kind = code >> 14;  // kind 0: U row, 1/2: W hi/lo
-          const float2 e = tv[(c * TCF_VPS + vv) * TS + slot];
-          float pr_, pi_;
-          if (kind == 0) {
-            phasor1<EXACT>(kt[slot], bt[slot], e.x, e.y, -1.f, pr_, pi_);
-          } else {
-            float vr, vim;
-            phasor1<EXACT>(kr[slot - sa.nt], br[slot - sa.nt], e.x, e.y, -1.f, vr, vim);
-            const float2 sv = ssm[c * TCF_VPS + vv];
-            pr_ = vr * sv.x - vim * sv.y;
-            pi_ = vr * sv.y + vim * sv.x;
-          }
-          // the partner lane holds the other voxel of the pair (every pair is lane-adjacent)
-          const unsigned pm = __activemask();
-          const float qr = __shfl_xor_sync(pm, pr_, 1), qi = __shfl_xor_sync(pm, pi_, 1);
-          const bool odd = L & 1;
-          const float r0 = odd ? qr : pr_, i0 = odd ? qi : pi_, r1 = odd ? pr_ : qr, i1 = odd ? pi_ : qi;
-          float4 q;
-          if (kind == 0)
-            q = odd ? make_float4(i0, r0, i1, r1) : make_float4(r0, -i0, r1, -i1);  // rows 2t+1 / 2t
-          else
-            q = make_float4(r0, i0, r1, i1);
-          const float4 h = make_float4(tf32_round(q.x), tf32_round(q.y), tf32_round(q.z), tf32_round(q.w));
-          unsigned char* base = kind == 0 ? Ast : Bst;
-          const uint32_t off = ioff[it];
-          if (kind == 0) {
-            *reinterpret_cast<float4*>(base + off) = h;
-            *reinterpret_cast<float4*>(base + TCF_A_BYTES + off) =
-                make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
-          } else if (kind == 1) {
-            *reinterpret_cast<float4*>(base + off) = h;
-          } else {
-            *reinterpret_cast<float4*>(base + ly.b_stage / 2 + off) =
-                make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
+          const int slot = code & 0x3ff, vp = (code >> 10) & 15;
+          const int v0 = c * TCF_VPS + 2 * vp;
+          const float2 e0 = tv[v0 * TS + slot], e1 = tv[(v0 + 1) * TS + slot];
+          float2 re, im;  // amp·(cos x, sin x) of voxels v0, v0 + 1; the phasor is re − j·im
+          phasor2<EXACT>(bc(kp[slot]), bc(kp[320 + slot]), make_float2(e0.x, e1.x), make_float2(e0.y, e1.y), re, im);
+          if (!(code >> 14)) {  // U = re − j·im: row 2t (Ur, −Ui, ..) = (re, im, ..), row 2t+1 (Ui, Ur, ..)
+            const float4 r0 = make_float4(re.x, im.x, re.y, im.y), r1 = make_float4(-im.x, re.x, -im.y, re.y);
+            const float4 h0 = make_float4(tf32_round(r0.x), tf32_round(r0.y), tf32_round(r0.z), tf32_round(r0.w));
+            const float4 h1 = make_float4(-h0.y, h0.x, -h0.w, h0.z);
+            unsigned char* p0 = Ast + ioff[it];
+            *reinterpret_cast<float4*>(p0) = h0;
+            *reinterpret_cast<float4*>(p0 + 16) = h1;
+            *reinterpret_cast<float4*>(p0 + TCF_A_BYTES) = make_float4(r0.x - h0.x, r0.y - h0.y, r0.z - h0.z, r0.w - h0.w);
+            *reinterpret_cast<float4*>(p0 + TCF_A_BYTES + 16) =
+                make_float4(r1.x - h1.x, r1.y - h1.y, r1.z - h1.z, r1.w - h1.w);
+          } else {  // W = (re − j·im)·s
+            const float4 sv = *reinterpret_cast<const float4*>(ssm + v0);
+            const float4 q = make_float4(re.x * sv.x + im.x * sv.y, re.x * sv.y - im.x * sv.x,
+                                         re.y * sv.z + im.y * sv.w, re.y * sv.w - im.y * sv.z);
+            const float4 h = make_float4(tf32_round(q.x), tf32_round(q.y), tf32_round(q.z), tf32_round(q.w));
+            unsigned char* p0 = Bst + ioff[it];
+            *reinterpret_cast<float4*>(p0) = h;
+            *reinterpret_cast<float4*>(p0 + ly.b_stage / 2) = make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (L == 0) mbar_arrive(&afull[st]);
-        if (fl > 0 && c == EPI_STEP) epilogue(fl - 1);
       }
     }
-    if (nfl > 0) epilogue(nfl - 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -2565,6 +2566,8 @@ int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   // partial buffer: up to 2 GB, at least one frequency; windows of whole frequencies
   long long fwin = std::max(1LL, std::min<long long>(sa.nf, (2LL << 30) / (rows * 8 * per_f)));
   fwin = std::min<long long>(fwin, std::max(1LL, (long long)RED_THREADS / per_f));
+  const long long nwins = (sa.nf + fwin - 1) / fwin;
+  fwin = (sa.nf + nwins - 1) / nwins;  // balanced windows (16 = 8 + 8, not 14 + 2)
   const size_t need = (size_t)(rows * per_f * fwin);
   if (need > p->tcpart_elems) {
     cudaFree(p->d_tcpart);
