@@ -1691,9 +1691,14 @@ constexpr int TC_THREADS = TC_CT + 64;        // + B-loader warp + MMA warp
 constexpr int TC_SUB = TC_CT / 128;           // compute threads per voxel row
 constexpr int TC_RCH = 8;                     // receivers per pipeline step (K = 16 reals = two MMAs of K = 8)
 constexpr int TC_NS = 4;                      // adjoint pipeline stages (at most; fewer when the table is large)
-constexpr int TCF_NS = 2;                     // forward pipeline stages
+#ifndef NFGPU_TCF_NS
+#define NFGPU_TCF_NS 2
+#endif
+#ifndef NFGPU_TCF_VPS
+#define NFGPU_TCF_VPS 16
+#endif
+constexpr int TCF_NS = NFGPU_TCF_NS;          // forward pipeline stages
 constexpr int TCF_GW = 12;                    // forward generation warps (warps 12..15 drain TMEM)
-constexpr int TCF_NIT = 7;                    // generation items per thread and step: 8·(64 + 256) <= 7·384
 constexpr int TC_NMAX = 128;                  // max padded 2·n_t (TMEM: 2 regions × N ≤ 256 columns)
 constexpr uint32_t TC_A_BYTES = 128 * 2 * TC_RCH * 4;  // one of hi/lo: 8 KB
 constexpr uint32_t TC_SMEM_MAX = 227 * 1024;
@@ -2028,7 +2033,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
 // (the pair of lanes 2t, 2t+1 combined by a shuffle) into one partial per (half tile, channel),
 // warp 17 issues the MMAs; fwd_reduce1/2 finish the sum over the 2·tiles partial rows.
 
-constexpr int TCF_VPS = 16;                          // voxels per forward pipeline step
+constexpr int TCF_VPS = NFGPU_TCF_VPS;               // voxels per forward pipeline step
 constexpr int TCF_KPS = 2 * TCF_VPS;                 // reals of K per step (4 MMAs of K = 8)
 constexpr uint32_t TCF_A_BYTES = 128 * TCF_KPS * 4;  // one of hi/lo of an A stage
 struct TcfLayout {
@@ -2038,7 +2043,7 @@ struct TcfLayout {
     b_off = TCF_NS * 2 * TCF_A_BYTES;           // [stage][hi, lo][npr x KPS]
     b_stage = (uint32_t)npr * TCF_KPS * 4 * 2;
     s_off = b_off + TCF_NS * b_stage;           // s of the half tile: [128] complex
-    tab_off = s_off + 128 * 8;                  // [voxel 128][slot, stride nant|1] (δ, 1/d)
+    tab_off = s_off + 128 * 8;                  // [voxel pair 64][slot, stride nant|1] (δ δ, 1/d 1/d)
     d0_off = tab_off + (uint32_t)(nant | 1) * 1024;
     par_off = d0_off + A_MAX * 8;               // [2][k of slot 320 | b of slot 320]
     bar_off = par_off + 2 * 640 * 4;
@@ -2057,7 +2062,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
   const int tile = blockIdx.x / (2 * fch), rem = blockIdx.x - tile * 2 * fch, hb = rem / fch, fc = rem - hb * fch;
   float2* ssm = reinterpret_cast<float2*>(sm + ly.s_off);
   double* d0 = reinterpret_cast<double*>(sm + ly.d0_off);
-  float2* tv = reinterpret_cast<float2*>(sm + ly.tab_off);  // voxel-major: [vi * TS + slot] = (δ, 1/d)
+  // voxel-pair-major table: [vp * TS + slot] = (δ of voxels 2vp, 2vp+1 | 1/d of 2vp, 2vp+1)
+  float4* tv = reinterpret_cast<float4*>(sm + ly.tab_off);
   float* par = reinterpret_cast<float*>(sm + ly.par_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + ly.bar_off);
   uint64_t *afull = bars, *sfree = bars + TCF_NS, *zfull = bars + 2 * TCF_NS, *zfree = bars + 2 * TCF_NS + 2;
@@ -2072,9 +2078,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
       const int sl = i >> 7, vi = i & 127;
       const int ant = sl < sa.nt ? sa.ts[sl] : g.T + sa.rs[sl - sa.nt];
       const float* src = tabt + (size_t)ant * TABW + vi;
-      const uint32_t dst = smem_u32(tv + vi * TS + sl);
+      const uint32_t dst = smem_u32(tv + (vi >> 1) * TS + sl) + (vi & 1) * 4;
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4), "l"(src + TILE) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 8), "l"(src + TILE) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     for (int i = tid; i < sa.nt + sa.nr; i += TC_CT)  // fp64 anchors per batch slot
@@ -2205,68 +2211,78 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
       if (L == 0) mbar_arrive(&zfree[fl & 1]);
     }
   } else if (w < TCF_GW) {  // ---------------- generation: U (A operand) and W = V·s (B operand)
-    // One item = (antenna slot, voxel pair) of a step; the thread computes both voxels. U items
-    // (transmitters) come first, padded to whole warps, so a warp is all-U or all-W, and its lanes
-    // run over consecutive antennas (conflict-free table reads). A U item writes rows 2t, 2t+1 of A
+    // One item = (antenna, voxel pair) of a step; the thread computes both voxels. The first gu
+    // warps take the U items (transmitters), the others the W items (receivers), in proportion
+    // to n_t : n_r; lanes run over consecutive antennas (conflict-free table reads). Items go two
+    // at a time with clamped, branch-free loads and math so their latency chains interleave;
+    // only the stores of a padding item are skipped. A U item writes rows 2t, 2t+1 of A
     // ([[Ur, -Ui], [Ui, Ur]] form), a W item row r of B; hi and lo of the 3xTF32 split.
-    constexpr int GT = TCF_GW * 32;
-    const int nu = sa.nt * (TCF_VPS / 2), nupad = (nu + 31) & ~31, nitems = nupad + sa.nr * (TCF_VPS / 2);
-    int icode[TCF_NIT];
-    uint32_t ioff[TCF_NIT];
-#pragma unroll
-    for (int it = 0; it < TCF_NIT; ++it) {
-      const int i = tid + it * GT;
-      icode[it] = -1;
-      ioff[it] = 0;
-      if (i < nu) {
-        const int t = i % sa.nt, vp = i / sa.nt;
-        icode[it] = t | (vp << 10);
-        ioff[it] = kmaj(2 * t, 4 * vp, 128);
-      } else if (i >= nupad && i < nitems) {
-        const int j = i - nupad, r = j % sa.nr, vp = j / sa.nr;
-        icode[it] = (sa.nt + r) | (vp << 10) | (1 << 14);
-        ioff[it] = kmaj(r, 4 * vp, npr);
-      }
-    }
+    constexpr int VP = TCF_VPS / 2;
+    const int gu = min(TCF_GW - 1, max(1, (TCF_GW * sa.nt + (sa.nt + sa.nr) / 2) / (sa.nt + sa.nr)));
+    const bool isU = w < gu;
+    const int gthreads = 32 * (isU ? gu : TCF_GW - gu), gtid = isU ? tid : tid - 32 * gu;
+    const int nant_k = isU ? sa.nt : sa.nr, nk = nant_k * VP;  // items of this kind
+    const int slot0 = isU ? 0 : sa.nt;
+    // item i = vp · nant_k + a; a thread's items advance by gthreads: (a, vp) += (dr, dq) with carry
+    const int dq = gthreads / nant_k, dr = gthreads - dq * nant_k;
+    const int a_first = gtid % nant_k, vp_first = gtid / nant_k;
     double kfn = nfl > 0 ? kd[sa.fs[f0]] : 0.0;
     for (int fl = 0; fl < nfl; ++fl) {
       float* kp = par + (fl & 1) * 640;  // [slot] k, then [slot] b at +320
       const double kf = kfn;
       if (fl + 1 < nfl) kfn = kd[sa.fs[f0 + fl + 1]];  // prefetch: lands while this frequency runs
-      for (int q = tid; q < nant; q += GT) side_params<float, EXACT>(kf, d0[q], kp[q], kp[320 + q]);
-      named_bar(1, GT);
+      for (int q = tid; q < nant; q += TCF_GW * 32) side_params<float, EXACT>(kf, d0[q], kp[q], kp[320 + q]);
+      named_bar(1, TCF_GW * 32);
       for (int c = 0; c < SPF; ++c) {
         const int s = fl * SPF + c, st = s % TCF_NS, k = s / TCF_NS;
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);
         unsigned char* Ast = sm + ly.a_off + st * 2 * TCF_A_BYTES;
         unsigned char* Bst = sm + ly.b_off + st * ly.b_stage;
+        int an = a_first, vn = vp_first;
+        for (int i0 = gtid; i0 < nk; i0 += 2 * gthreads) {
+          int ai[2], vi[2];
+          bool ok[2];
+          float4 e[2];
+          float kk[2], bb[2];
 #pragma unroll
-        for (int it = 0; it < TCF_NIT; ++it) {
-          const int code = icode[it];
-          if (code < 0) continue;
-          const int slot = code & 0x3ff, vp = (code >> 10) & 15;
-          const int v0 = c * TCF_VPS + 2 * vp;
-          const float2 e0 = tv[v0 * TS + slot], e1 = tv[(v0 + 1) * TS + slot];
-          float2 re, im;  // amp·(cos x, sin x) of voxels v0, v0 + 1; the phasor is re − j·im
-          phasor2<EXACT>(bc(kp[slot]), bc(kp[320 + slot]), make_float2(e0.x, e1.x), make_float2(e0.y, e1.y), re, im);
-          if (!(code >> 14)) {  // U = re − j·im: row 2t (Ur, −Ui, ..) = (re, im, ..), row 2t+1 (Ui, Ur, ..)
-            const float4 r0 = make_float4(re.x, im.x, re.y, im.y), r1 = make_float4(-im.x, re.x, -im.y, re.y);
-            const float4 h0 = make_float4(tf32_round(r0.x), tf32_round(r0.y), tf32_round(r0.z), tf32_round(r0.w));
-            const float4 h1 = make_float4(-h0.y, h0.x, -h0.w, h0.z);
-            unsigned char* p0 = Ast + ioff[it];
-            *reinterpret_cast<float4*>(p0) = h0;
-            *reinterpret_cast<float4*>(p0 + 16) = h1;
-            *reinterpret_cast<float4*>(p0 + TCF_A_BYTES) = make_float4(r0.x - h0.x, r0.y - h0.y, r0.z - h0.z, r0.w - h0.w);
-            *reinterpret_cast<float4*>(p0 + TCF_A_BYTES + 16) =
-                make_float4(r1.x - h1.x, r1.y - h1.y, r1.z - h1.z, r1.w - h1.w);
-          } else {  // W = (re − j·im)·s
-            const float4 sv = *reinterpret_cast<const float4*>(ssm + v0);
-            const float4 q = make_float4(re.x * sv.x + im.x * sv.y, re.x * sv.y - im.x * sv.x,
-                                         re.y * sv.z + im.y * sv.w, re.y * sv.w - im.y * sv.z);
-            const float4 h = make_float4(tf32_round(q.x), tf32_round(q.y), tf32_round(q.z), tf32_round(q.w));
-            unsigned char* p0 = Bst + ioff[it];
-            *reinterpret_cast<float4*>(p0) = h;
-            *reinterpret_cast<float4*>(p0 + ly.b_stage / 2) = make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
+          for (int u = 0; u < 2; ++u) {
+            ok[u] = i0 + u * gthreads < nk;
+            ai[u] = ok[u] ? an : ai[0];  // a padding item recomputes item 0; its stores are skipped
+            vi[u] = ok[u] ? vn : vi[0];
+            an += dr;
+            vn += dq;
+            if (an >= nant_k) an -= nant_k, ++vn;
+            e[u] = tv[(c * VP + vi[u]) * TS + slot0 + ai[u]];
+            kk[u] = kp[slot0 + ai[u]];
+            bb[u] = kp[320 + slot0 + ai[u]];
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int a_ = ai[u], vp = vi[u];
+            float2 re, im;  // amp·(cos x, sin x) of voxels 2vp, 2vp+1; the phasor is re − j·im
+            phasor2<EXACT>(bc(kk[u]), bc(bb[u]), make_float2(e[u].x, e[u].y), make_float2(e[u].z, e[u].w), re, im);
+            if (isU) {  // U = re − j·im: row 2t (Ur, −Ui, ..) = (re, im, ..), row 2t+1 (Ui, Ur, ..)
+              const float4 r0 = make_float4(re.x, im.x, re.y, im.y);
+              const float4 h0 = make_float4(tf32_round(r0.x), tf32_round(r0.y), tf32_round(r0.z), tf32_round(r0.w));
+              const float4 l0 = make_float4(r0.x - h0.x, r0.y - h0.y, r0.z - h0.z, r0.w - h0.w);
+              if (ok[u]) {
+                unsigned char* p0 = Ast + kmaj(2 * a_, 4 * vp, 128);
+                *reinterpret_cast<float4*>(p0) = h0;
+                *reinterpret_cast<float4*>(p0 + 16) = make_float4(-h0.y, h0.x, -h0.w, h0.z);
+                *reinterpret_cast<float4*>(p0 + TCF_A_BYTES) = l0;
+                *reinterpret_cast<float4*>(p0 + TCF_A_BYTES + 16) = make_float4(-l0.y, l0.x, -l0.w, l0.z);
+              }
+            } else {  // W = (re − j·im)·s
+              const float4 sv = *reinterpret_cast<const float4*>(ssm + c * TCF_VPS + 2 * vp);
+              const float4 q = make_float4(re.x * sv.x + im.x * sv.y, re.x * sv.y - im.x * sv.x,
+                                           re.y * sv.z + im.y * sv.w, re.y * sv.w - im.y * sv.z);
+              const float4 h = make_float4(tf32_round(q.x), tf32_round(q.y), tf32_round(q.z), tf32_round(q.w));
+              if (ok[u]) {
+                unsigned char* p0 = Bst + kmaj(a_, 4 * vp, npr);
+                *reinterpret_cast<float4*>(p0) = h;
+                *reinterpret_cast<float4*>(p0 + ly.b_stage / 2) = make_float4(q.x - h.x, q.y - h.y, q.z - h.z, q.w - h.w);
+              }
+            }
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
