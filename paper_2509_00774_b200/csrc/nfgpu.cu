@@ -1694,6 +1694,9 @@ constexpr int TC_NS = 4;                      // adjoint pipeline stages (at mos
 #ifndef NFGPU_TCF_NS
 #define NFGPU_TCF_NS 2
 #endif
+#ifndef NFGPU_TCF_PROBE  // diagnostics only: 1 = skip the forward MMAs, 2 = skip the forward operand generation
+#define NFGPU_TCF_PROBE 0
+#endif
 #ifndef NFGPU_TCF_VPS
 #define NFGPU_TCF_VPS 16
 #endif
@@ -2037,33 +2040,38 @@ constexpr int TCF_VPS = NFGPU_TCF_VPS;               // voxels per forward pipel
 constexpr int TCF_KPS = 2 * TCF_VPS;                 // reals of K per step (4 MMAs of K = 8)
 constexpr uint32_t TCF_A_BYTES = 128 * TCF_KPS * 4;  // one of hi/lo of an A stage
 struct TcfLayout {
-  uint32_t a_off, b_off, b_stage, s_off, tab_off, d0_off, par_off, bar_off, bytes;
-  __host__ __device__ TcfLayout(int npr, int nant) {
+  uint32_t a_off, b_off, b_stage, s_off, tab_off, tab_buf, ant_off, d0_off, par_off, bar_off, bytes;
+  // stream = false: the half tile's whole table is staged once; true: one step's slice at a time
+  __host__ __device__ TcfLayout(int npr, int nant, bool stream) {
     a_off = 0;                                  // [stage][hi, lo][128 x KPS]
     b_off = TCF_NS * 2 * TCF_A_BYTES;           // [stage][hi, lo][npr x KPS]
     b_stage = (uint32_t)npr * TCF_KPS * 4 * 2;
     s_off = b_off + TCF_NS * b_stage;           // s of the half tile: [128] complex
-    tab_off = s_off + 128 * 8;                  // [voxel pair 64][slot, stride nant|1] (δ δ, 1/d 1/d)
-    d0_off = tab_off + (uint32_t)(nant | 1) * 1024;
+    tab_off = s_off + 128 * 8;                  // table [voxel pair][slot, stride nant|1] (δ δ, 1/d 1/d):
+    tab_buf = (uint32_t)(TCF_VPS / 2) * (nant | 1) * 16;  // whole half tile, or 2 x one step's slice
+    ant_off = tab_off + (stream ? 2 * tab_buf : (uint32_t)(nant | 1) * 1024);  // [slot] antenna index
+    d0_off = (ant_off + (uint32_t)nant * 4 + 7) & ~7u;
     par_off = d0_off + A_MAX * 8;               // [2][k of slot 320 | b of slot 320]
     bar_off = par_off + 2 * 640 * 4;
     bytes = bar_off + (2 * TCF_NS + 6) * 8;
   }
 };
 
-template <bool EXACT>
+template <bool EXACT, bool STREAM>
 __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a, StructArgs sa,
                                                                const double* __restrict__ kd, int npr, int fa, int fb,
                                                                int fch, float2* __restrict__ part) {
   extern __shared__ __align__(1024) unsigned char sm[];
-  const TcfLayout ly(npr, sa.nt + sa.nr);
+  const TcfLayout ly(npr, sa.nt + sa.nr, STREAM);
   const Geo& g = a.g;
   const int tid = threadIdx.x, w = tid >> 5, L = tid & 31;
   const int tile = blockIdx.x / (2 * fch), rem = blockIdx.x - tile * 2 * fch, hb = rem / fch, fc = rem - hb * fch;
   float2* ssm = reinterpret_cast<float2*>(sm + ly.s_off);
   double* d0 = reinterpret_cast<double*>(sm + ly.d0_off);
-  // voxel-pair-major table: [vp * TS + slot] = (δ of voxels 2vp, 2vp+1 | 1/d of 2vp, 2vp+1)
-  float4* tv = reinterpret_cast<float4*>(sm + ly.tab_off);
+  // table [vp * TS + slot] = (δ of voxels 2vp, 2vp+1 | 1/d of 2vp, 2vp+1): the half tile's whole
+  // table, staged once, or (STREAM) one pipeline step's slice, double-buffered, from L2 one step ahead
+  float4* tvb = reinterpret_cast<float4*>(sm + ly.tab_off);
+  int* antrow = reinterpret_cast<int*>(sm + ly.ant_off);
   float* par = reinterpret_cast<float*>(sm + ly.par_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + ly.bar_off);
   uint64_t *afull = bars, *sfree = bars + TCF_NS, *zfull = bars + 2 * TCF_NS, *zfree = bars + 2 * TCF_NS + 2;
@@ -2074,17 +2082,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
   uint32_t tcols = 32;
   while (tcols < 2u * npr) tcols <<= 1;
   if (tid < TC_CT) {
-    for (int i = tid; i < nant * 128; i += TC_CT) {  // coalesced 4-byte async copies, transposed into smem
-      const int sl = i >> 7, vi = i & 127;
-      const int ant = sl < sa.nt ? sa.ts[sl] : g.T + sa.rs[sl - sa.nt];
-      const float* src = tabt + (size_t)ant * TABW + vi;
-      const uint32_t dst = smem_u32(tv + (vi >> 1) * TS + sl) + (vi & 1) * 4;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 8), "l"(src + TILE) : "memory");
+    for (int i = tid; i < nant; i += TC_CT) {  // antenna of each batch slot; fp64 anchors per slot
+      const int ant = i < sa.nt ? sa.ts[i] : g.T + sa.rs[i - sa.nt];
+      antrow[i] = ant;
+      d0[i] = a.D0[(size_t)tile * g.A + ant];
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    for (int i = tid; i < sa.nt + sa.nr; i += TC_CT)  // fp64 anchors per batch slot
-      d0[i] = a.D0[(size_t)tile * g.A + (i < sa.nt ? sa.ts[i] : g.T + sa.rs[i - sa.nt])];
+    if (!STREAM)  // the whole table: (slot, voxel pair) as two 8-byte async copies (δ pair, 1/d pair)
+      for (int i = tid; i < nant * 64; i += TC_CT) {
+        const int sl = i >> 6, vp = i & 63;
+        const int ant = sl < sa.nt ? sa.ts[sl] : g.T + sa.rs[sl - sa.nt];
+        const float* src = tabt + (size_t)ant * TABW + 2 * vp;
+        const uint32_t d = smem_u32(tvb + vp * TS + sl);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d + 8), "l"(src + TILE) : "memory");
+      }
     if (tid < 128) {  // s at the half tile's table positions
       int tx, ty, tz;
       tile_coords(g, tile, tx, ty, tz);
@@ -2155,7 +2166,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
           for (int ks = 0; ks < TCF_KPS / 8; ++ks) {
             const uint64_t ad = umma_desc(a0 + ah * TCF_A_BYTES + ks * 2 * 2048, 2048, 128);
             const uint64_t bd = umma_desc(b0 + bh * (ly.b_stage / 2) + ks * 2 * lboB, lboB, 128);
+#if NFGPU_TCF_PROBE != 1
             umma_tf32(d, ad, bd, idesc, (c > 0 || pass > 0 || ks > 0) ? 1u : 0u);
+#endif
           }
         }
         umma_commit(&sfree[st]);
@@ -2226,20 +2239,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
     // item i = vp · nant_k + a; a thread's items advance by gthreads: (a, vp) += (dr, dq) with carry
     const int dq = gthreads / nant_k, dr = gthreads - dq * nant_k;
     const int a_first = gtid % nant_k, vp_first = gtid / nant_k;
+    // one step's table slice: (slot, voxel pair) as two 8-byte copies (δ pair, 1/d pair)
+    auto stage_slice = [&](int c, int buf) {
+      float4* dst = tvb + buf * (ly.tab_buf / 16);
+      for (int i = tid; i < nant * VP; i += TCF_GW * 32) {
+        const int sl = i / VP, vp = i - sl * VP;
+        const float* src = tabt + (size_t)antrow[sl] * TABW + c * TCF_VPS + 2 * vp;
+        const uint32_t d = smem_u32(dst + vp * TS + sl);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d + 8), "l"(src + TILE) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (STREAM && nfl > 0) stage_slice(0, 0);
     double kfn = nfl > 0 ? kd[sa.fs[f0]] : 0.0;
     for (int fl = 0; fl < nfl; ++fl) {
       float* kp = par + (fl & 1) * 640;  // [slot] k, then [slot] b at +320
       const double kf = kfn;
       if (fl + 1 < nfl) kfn = kd[sa.fs[f0 + fl + 1]];  // prefetch: lands while this frequency runs
       for (int q = tid; q < nant; q += TCF_GW * 32) side_params<float, EXACT>(kf, d0[q], kp[q], kp[320 + q]);
-      named_bar(1, TCF_GW * 32);
+      if (!STREAM) named_bar(1, TCF_GW * 32);
       for (int c = 0; c < SPF; ++c) {
         const int s = fl * SPF + c, st = s % TCF_NS, k = s / TCF_NS;
+        if (STREAM) {  // this step's slice has landed for every thread, and every thread is done with
+                       // step s-1 (its slice buffer and the previous frequency's parameters are free)
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          named_bar(1, TCF_GW * 32);
+          if (s + 1 < nsteps) stage_slice((c + 1) % SPF, (s + 1) & 1);
+        }
+        const float4* tv = STREAM ? tvb + (s & 1) * (ly.tab_buf / 16) : tvb + c * VP * TS;
         if (k > 0) mbar_wait(&sfree[st], (k - 1) & 1);
         unsigned char* Ast = sm + ly.a_off + st * 2 * TCF_A_BYTES;
         unsigned char* Bst = sm + ly.b_off + st * ly.b_stage;
         int an = a_first, vn = vp_first;
-        for (int i0 = gtid; i0 < nk; i0 += 2 * gthreads) {
+        for (int i0 = gtid; i0 < (NFGPU_TCF_PROBE == 2 ? 0 : nk); i0 += 2 * gthreads) {
           int ai[2], vi[2];
           bool ok[2];
           float4 e[2];
@@ -2252,7 +2285,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fwd_tc_kernel(FwdArgs<float> a,
             an += dr;
             vn += dq;
             if (an >= nant_k) an -= nant_k, ++vn;
-            e[u] = tv[(c * VP + vi[u]) * TS + slot0 + ai[u]];
+            e[u] = tv[vi[u] * TS + slot0 + ai[u]];
             kk[u] = kp[slot0 + ai[u]];
             bb[u] = kp[320 + slot0 + ai[u]];
           }
@@ -2593,8 +2626,10 @@ int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     if (rc) return rc;
     p->tcpart_elems = need;
   }
-  const uint32_t smem = TcfLayout(npr, sa.nt + sa.nr).bytes;
-  auto kern = p->exact ? fwd_tc_kernel<true> : fwd_tc_kernel<false>;
+  const bool stream = TcfLayout(npr, sa.nt + sa.nr, false).bytes > TC_SMEM_MAX;  // table too big to stage whole
+  const uint32_t smem = TcfLayout(npr, sa.nt + sa.nr, stream).bytes;
+  auto kern = stream ? (p->exact ? fwd_tc_kernel<true, true> : fwd_tc_kernel<false, true>)
+                     : (p->exact ? fwd_tc_kernel<true, false> : fwd_tc_kernel<false, false>);
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int fa = 0; fa < sa.nf; fa += (int)fwin) {
     const int fb = std::min(sa.nf, fa + (int)fwin);
@@ -2635,7 +2670,7 @@ bool use_tc_struct(const nf_plan* p, bool forward) {
   if (forward) {  // the tcgen05 forward wins only on large batches: >= 40 antennas a side and
                   // >= 12 frequencies (full set: -10% vs FFMA); NFGPU_TC_FWD=1 takes it for every eligible batch
     if (!p->tc_force && !p->tc_fwd && !(amin >= 40 && p->snf >= 12)) return false;
-    return p->snr <= 256 && TcfLayout((p->snr + 15) / 16 * 16, p->snt + p->snr).bytes <= TC_SMEM_MAX;
+    return p->snr <= 256 && TcfLayout((p->snr + 15) / 16 * 16, p->snt + p->snr, true).bytes <= TC_SMEM_MAX;
   }
   return TcLayout((2 * p->snt + 15) / 16 * 16, p->snt + p->snr, 2).bytes <= TC_SMEM_MAX;
 }
