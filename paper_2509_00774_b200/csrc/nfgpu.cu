@@ -72,6 +72,9 @@ namespace {
 #ifndef NFGPU_FWD_TREE
 #define NFGPU_FWD_TREE 0
 #endif
+#ifndef NFGPU_L2_TABLE_MB  // distance tables up to this size use chunk-major work units (nf_plan::chunk_order)
+#define NFGPU_L2_TABLE_MB 256
+#endif
 #ifndef NFGPU_FWD_PAIR
 #define NFGPU_FWD_PAIR 1
 #endif
@@ -785,7 +788,7 @@ __device__ __forceinline__ int chunk_bound(int n, int c, int C, int order) {
   return (int)((double)n * ((x - 0.375 * x * x) / 0.625));
 }
 // (tile, chunk) of a warp work unit: tile-major (a tile's chunks adjacent, sharing its table rows
-// in L2) or chunk-major (the default: with tapered chunks the launch ends on short units)
+// in L2) or chunk-major (tables that stay in L2: with tapered chunks the launch ends on short units)
 __device__ __forceinline__ void unit_coords(int unit, int ntiles, int C, int order, int& tile, int& chunk) {
   if (order == 0) {
     tile = unit / C;
@@ -1077,8 +1080,8 @@ __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __re
 // Forward: a warp owns (tile, channel chunk) like the adjoint. Per channel, each lane forms
 // the sum over its V voxels. Every 16 channels, a transpose through smem reduces over the
 // 32 lanes in a fixed order, and the tile's per-channel sum goes to part[tile][j].
-// Chunks of one tile are adjacent units, so they run together and share the tile's table
-// rows in L2.
+// With tile-major units (large tables), chunks of one tile are adjacent units, so they run
+// together and share the tile's table rows in L2.
 template <typename Real, bool EXACT>
 __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(FwdArgs<Real> a) {
   pdl_wait();
@@ -2463,11 +2466,10 @@ struct nf_plan {
   bool exact = true;  // explicit phase reduction (false when |x| <= EXACT_FREE_REV is guaranteed)
   double phase_bound_rev = 0;
   long long fwd_target = 148LL * 16 * 4;  // warp work units per forward launch (env NFGPU_FWD_TARGET)
-  long long adj_target = 148LL * 16 * 2;  // warp work units per adjoint launch (env NFGPU_ADJ_TARGET): two waves;
-                                          // its chunk combine favours fewer units (1/8 Large slab +2.4%)
+  long long adj_target = 148LL * 16 * 4;  // warp work units per adjoint launch (set with chunk_order; env NFGPU_ADJ_TARGET)
   long long struct_target = 148LL * 3 * 4;  // blocks per structured launch (env NFGPU_STRUCT_TARGET)
   int min_chunk = 64;                       // fewest channels per flat forward unit (env NFGPU_MIN_CHUNK)
-  int chunk_order = 1;                      // flat work-unit order (unit_coords / chunk_bound)
+  int chunk_order = 0;                      // flat work-unit order (unit_coords / chunk_bound)
   int adj_min_chunk = 128;                  // ... per flat adjoint unit: its chunk combine favours fewer, longer
                                             // chunks (Medium |B| = 512: 80.9 -> 72.7 us; env NFGPU_ADJ_MIN_CHUNK)
   size_t dev_bytes = 0;
@@ -2885,16 +2887,20 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     p->exact = dtype != NF_C64 || p->phase_bound_rev > EXACT_FREE_REV || std::getenv("NFGPU_FORCE_EXACT");
   }
   if (const char* e = std::getenv("NFGPU_FWD_TARGET")) p->fwd_target = std::max(1LL, std::atoll(e));
-  if (const char* e = std::getenv("NFGPU_ADJ_TARGET")) p->adj_target = std::max(1LL, std::atoll(e));
   if (const char* e = std::getenv("NFGPU_STRUCT_TARGET")) p->struct_target = std::max(1LL, std::atoll(e));
   if (const char* e = std::getenv("NFGPU_MIN_CHUNK")) p->min_chunk = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("NFGPU_ADJ_MIN_CHUNK")) p->adj_min_chunk = std::max(1, std::atoi(e));
   const size_t rs = real_size(p);
-  // chunk-major, tapered work units (chunk_bound): the last wave is made of the smallest chunks.
-  // Measured faster than tile-major equal chunks on every Large slab (1/8 slab +2.2%, full +0.9%),
-  // even when the table does not stay in L2. NFGPU_CHUNK_ORDER=0 restores tile-major order.
-  p->chunk_order = 1;
+  // Work-unit order (unit_coords / chunk_bound). Chunk-major with tapered chunks ends a launch on
+  // short units (1/8 Large slab +2.2%, 1/4 slab +2.3%), but a tile's chunks are then far apart,
+  // so its table rows are re-read from DRAM unless the table stays in L2 (full Large: 1.5 -> 5.3 GB
+  // per forward for +0.9%). Tile-major equal chunks above NFGPU_L2_TABLE_MB; env NFGPU_CHUNK_ORDER.
+  p->chunk_order = rs * (size_t)g.ntiles * g.A * TABW <= ((size_t)NFGPU_L2_TABLE_MB << 20) ? 1 : 0;
   if (const char* e = std::getenv("NFGPU_CHUNK_ORDER")) p->chunk_order = std::atoi(e) ? 1 : 0;
+  // adjoint units: two waves with chunk-major order, four with tile-major (its chunk combine favours
+  // fewer units; the tile-major full problem prefers three chunks per tile)
+  p->adj_target = p->chunk_order ? 148LL * 16 * 2 : 148LL * 16 * 4;
+  if (const char* e = std::getenv("NFGPU_ADJ_TARGET")) p->adj_target = std::max(1LL, std::atoll(e));
   {
     // bound the forward partial buffer to ~512 MB
     long long ch = (512LL << 20) / ((long long)p->fwd_gridx * 2 * rs);
