@@ -2562,6 +2562,12 @@ size_t adj_smem(const nf_plan* p) {
                                           : warp_smem_bytes<double>(p->g.Tg, p->g.A));
 }
 
+// Tapered chunk-major units pay off only with several waves of units: with fewer, the tapered
+// first chunk (1.6x the mean at 4 chunks) is the critical path (Medium: 135 -> 156 us per step).
+int unit_order(const nf_plan* p, long long units) {
+  return p->chunk_order && units >= 2LL * 148 * 16 ? 1 : 0;
+}
+
 int channel_splits(const nf_plan* p, int span) {
   // enough (tile, chunk) warp units for the target number of units; >= 64 channels per chunk
   const long long target = p->fwd_target;
@@ -2596,9 +2602,9 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.w0 = w0;
     a.w1 = w1;
     a.Q = channel_splits(p, span);
-    a.order = p->chunk_order;
     a.part = (Real*)p->d_part;
     const long long units = (long long)p->g.ntiles * a.Q;
+    a.order = unit_order(p, units);
     CUDA_TRY(launch_k(p->use_pdl, kern, dim3((unsigned)((units + FWD_WARPS - 1) / FWD_WARPS)), dim3(FWD_WARPS * 32),
                       sm, st, a));
     // two-level reduce: ~sqrt(rows) segments so both levels have short serial sums
@@ -2757,7 +2763,7 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   a.wrec = (const R2<Real>*)p->d_wrec;
   a.B = p->B;
   a.CH = adjoint_chunks(p);
-  a.order = p->structured ? 0 : p->chunk_order;
+  a.order = p->structured ? 0 : unit_order(p, (long long)p->g.ntiles * a.CH);
   a.gpart = (Real*)p->d_gpart;
   a.cnt = p->d_tilecnt;
   a.gout = (Real*)gout;
