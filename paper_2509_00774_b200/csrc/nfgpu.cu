@@ -207,6 +207,27 @@ __device__ __forceinline__ DV make_v(const double* x) {
   return q;
 }
 
+// fp64 cos/sin(2π·r) for r in [-½, ½] revolutions: (cos, sin) of the nearest 256th of a turn from a
+// table, times cos/sin of the remainder |2πδ| <= π/256 by short Taylor polynomials (truncation
+// below 1e-20), combined by angle addition. About 14 fp64 operations against ~35 for sincospi; error
+// a few ulp (c128 parity is 1e-10).
+__device__ double2 g_cis256[256];  // (cos, sin)(2π i / 256), filled by init_cis_kernel
+__global__ void init_cis_kernel() {
+  double s, c;
+  sincospi(threadIdx.x / 128.0, &s, &c);
+  g_cis256[threadIdx.x] = make_double2(c, s);
+}
+__device__ __forceinline__ void cis_rev(double r, double& s, double& c) {
+  const double q = rint(r * 256.0);
+  const double d = fma(q, -1.0 / 256.0, r) * 6.283185307179586476925;
+  const double d2 = d * d;
+  const double sd = d * fma(d2, fma(d2, fma(d2, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0), 1.0);
+  const double cd = fma(d2, fma(d2, fma(d2, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0);
+  const double2 t = g_cis256[(int)q & 255];
+  c = fma(t.x, cd, -t.y * sd);
+  s = fma(t.y, cd, t.x * sd);
+}
+
 // cos/sin(2π·x_v), x_v = base + k·(dT_v + dR_v), reduced exactly to [-½, ½] revolutions
 // (magic-number round-to-nearest, exact for |x| < 2^22) before MUFU.SIN/COS.
 //
@@ -215,7 +236,7 @@ __device__ __forceinline__ DV make_v(const double* x) {
 // precision and saves 3 packed FADDs per voxel pair.
 // With EXACT = false the channel record already holds 2π·k and 2π·base (radians), so x is
 // the phase in radians and no scaling multiply is needed before __sincosf.
-template <bool EXACT>
+template <bool EXACT, bool CIS_TABLE = true>
 __device__ __forceinline__ void phasorv(float k, float base, const FV& dT, const FV& dR, FV& c, FV& s) {
   const float2 M2 = bc(12582912.0f);
 #pragma unroll
@@ -227,12 +248,17 @@ __device__ __forceinline__ void phasorv(float k, float base, const FV& dT, const
     __sincosf(r.y, &s.p[i].y, &c.p[i].y);
   }
 }
-template <bool EXACT>
+// CIS_TABLE = false keeps sincospi: the flat forward is LSU-heavy already, and the table gather
+// costs it more than the fp64 it saves (c128 forward 3.0e11 -> 2.8e11 with it; adjoint 2.6e11 -> 3.0e11)
+template <bool EXACT, bool CIS_TABLE = true>
 __device__ __forceinline__ void phasorv(double k, double base, const DV& dT, const DV& dR, DV& c, DV& s) {
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const double x = fma(k, dT.v[v] + dR.v[v], base);
-    sincospi(2.0 * (x - rint(x)), &s.v[v], &c.v[v]);
+    if (CIS_TABLE)
+      cis_rev(x - rint(x), s.v[v], c.v[v]);
+    else
+      sincospi(2.0 * (x - rint(x)), &s.v[v], &c.v[v]);
   }
 }
 
@@ -1160,8 +1186,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const QV<Real> dT0 = ldv(tsl + o0), iT0 = ldv(tsl + o0 + TILE);
           const QV<Real> dT1 = ldv(tsl + o1), iT1 = ldv(tsl + o1 + TILE);
           QV<Real> cs0, sn0, cs1, sn1;
-          phasorv<EXACT>(q0.x, q0.y, dT0, dR, cs0, sn0);
-          phasorv<EXACT>(q1.x, q1.y, dT1, dR, cs1, sn1);
+          phasorv<EXACT, false>(q0.x, q0.y, dT0, dR, cs0, sn0);
+          phasorv<EXACT, false>(q1.x, q1.y, dT1, dR, cs1, sn1);
           if (stage_pending) {  // dR/iR are consumed: refill the single slot for the next run
             stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
             stage_pending = false;
@@ -1176,7 +1202,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const int off = bits_int(q.z);
           const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
           QV<Real> cs, sn;
-          phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
+          phasorv<EXACT, false>(q.x, q.y, dT, dR, cs, sn);
           if (stage_pending) {
             stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
             stage_pending = false;
@@ -1193,7 +1219,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const int offn = ws.rect[c + 1].x;
           const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
           QV<Real> cs, sn;
-          phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
+          phasorv<EXACT, false>(q.x, q.y, dT, dR, cs, sn);
           if (stage_pending) {  // dR/iR are consumed: refill the single slot for the next run
             stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
             stage_pending = false;
@@ -1349,7 +1375,7 @@ __device__ __forceinline__ void side_phasor(double k, double b, const DV& d, con
   for (int v = 0; v < V; ++v) {
     const double x = fma(k, d.v[v], b);
     double c, sn;
-    sincospi(2.0 * (x - rint(x)), &sn, &c);
+    cis_rev(x - rint(x), sn, c);
     re.v[v] = amp.v[v] * c;
     im.v[v] = amp.v[v] * sgn * sn;
   }
@@ -2990,6 +3016,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     build_table_kernel<float><<<grid, 32>>>(g, p->d_ant, (float*)p->d_tab, p->d_D0);
   else
     build_table_kernel<double><<<grid, 32>>>(g, p->d_ant, (double*)p->d_tab, p->d_D0);
+  init_cis_kernel<<<1, 256>>>();  // fp64 phasor table (cis_rev) of the c128 kernels
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
