@@ -69,14 +69,8 @@ namespace {
 #ifndef NFGPU_MINB_ADJ
 #define NFGPU_MINB_ADJ 4
 #endif
-#ifndef NFGPU_FWD_TREE
-#define NFGPU_FWD_TREE 0
-#endif
 #ifndef NFGPU_L2_TABLE_MB  // distance tables up to this size use chunk-major work units (nf_plan::chunk_order)
 #define NFGPU_L2_TABLE_MB 256
-#endif
-#ifndef NFGPU_FWD_PAIR
-#define NFGPU_FWD_PAIR 1
 #endif
 #ifndef NFGPU_EXACT_REDUCE
 #define NFGPU_EXACT_REDUCE 1
@@ -299,58 +293,43 @@ __device__ __forceinline__ void flush(const DV& iR, DV& hr, DV& hi, DV& gr, DV& 
   zero(hr);
   zero(hi);
 }
-// forward: ŝ = iR·s for the current rx run
-__device__ __forceinline__ void scale_s(const FV& iR, const FV& sr, const FV& si, FV& shr, FV& shi) {
+// forward: ŝ = iR·s for the current rx run, and −Re ŝ (the subtracted term of Im, kept per run)
+__device__ __forceinline__ void scale_s(const FV& iR, const FV& sr, const FV& si, FV& shr, FV& shi, FV& nshr) {
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
     shr.p[i] = mul2(iR.p[i], sr.p[i]);
     shi.p[i] = mul2(iR.p[i], si.p[i]);
+    nshr.p[i] = mul2(shr.p[i], bc(-1.f));
   }
 }
-__device__ __forceinline__ void scale_s(const DV& iR, const DV& sr, const DV& si, DV& shr, DV& shi) {
+__device__ __forceinline__ void scale_s(const DV& iR, const DV& sr, const DV& si, DV& shr, DV& shi, DV& nshr) {
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     shr.v[v] = iR.v[v] * sr.v[v];
     shi.v[v] = iR.v[v] * si.v[v];
+    nshr.v[v] = -shr.v[v];
   }
 }
 // forward: Σ_v iT·e^{-jθ}·ŝ over the lane's V voxels
-__device__ __forceinline__ float2 fwd_part(const FV& iT, const FV& c, const FV& s, const FV& shr, const FV& shi) {
-#if NFGPU_FWD_TREE
-  // per-pair products, then a pairwise tree (dependency depth 4 instead of 2·NP)
-  float2 pr[NP], pi[NP];
-#pragma unroll
-  for (int i = 0; i < NP; ++i) {
-    const float2 a = mul2(iT.p[i], c.p[i]), b = mul2(iT.p[i], s.p[i]);
-    pr[i] = fma2(b, shi.p[i], mul2(a, shr.p[i]));
-    pi[i] = fma2(b, make_float2(-shr.p[i].x, -shr.p[i].y), mul2(a, shi.p[i]));
-  }
-#pragma unroll
-  for (int w = 1; w < NP; w <<= 1)
-#pragma unroll
-    for (int i = 0; i + w < NP; i += 2 * w) {
-      pr[i] = add2(pr[i], pr[i + w]);
-      pi[i] = add2(pi[i], pi[i + w]);
-    }
-  return make_float2(pr[0].x + pr[0].y, pi[0].x + pi[0].y);
-#else
+__device__ __forceinline__ float2 fwd_part(const FV& iT, const FV& c, const FV& s, const FV& shr, const FV& shi,
+                                           const FV& nshr) {
   float2 pr = make_float2(0.f, 0.f), pi = make_float2(0.f, 0.f);
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
     const float2 a = mul2(iT.p[i], c.p[i]), b = mul2(iT.p[i], s.p[i]);
     pr = fma2(b, shi.p[i], fma2(a, shr.p[i], pr));
-    pi = fma2(b, make_float2(-shr.p[i].x, -shr.p[i].y), fma2(a, shi.p[i], pi));
+    pi = fma2(b, nshr.p[i], fma2(a, shi.p[i], pi));
   }
   return make_float2(pr.x + pr.y, pi.x + pi.y);
-#endif
 }
-__device__ __forceinline__ double2 fwd_part(const DV& iT, const DV& c, const DV& s, const DV& shr, const DV& shi) {
+__device__ __forceinline__ double2 fwd_part(const DV& iT, const DV& c, const DV& s, const DV& shr, const DV& shi,
+                                            const DV& nshr) {
   double pr = 0, pi = 0;
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const double a = iT.v[v] * c.v[v], b = iT.v[v] * s.v[v];
     pr = fma(b, shi.v[v], fma(a, shr.v[v], pr));
-    pi = fma(-b, shr.v[v], fma(a, shi.v[v], pi));
+    pi = fma(b, nshr.v[v], fma(a, shi.v[v], pi));
   }
   return make_double2(pr, pi);
 }
@@ -737,8 +716,11 @@ __device__ __forceinline__ int bits_int(double v) { return (int)__double_as_long
 
 // Build the 32 channel records of one batch (lane L <-> sorted position jb+L) from the
 // prefetched ChanRec/w in registers, and prefetch the next batch's. Returns the bitmask of
-// run starts (a run = maximal stretch with equal (rx, tx group)).
-template <typename Real, bool EXACT>
+// run starts (a run = maximal stretch with equal (rx, tx group)). rect[L] = {x, run key}, where
+// x is the tx-row offset in the group (adjoint) or, for the forward (FWD), the end of the run
+// that position L belongs to (the next run start after L, or nb), so the forward's segment loop
+// reads its bound with one shared load.
+template <typename Real, bool EXACT, bool FWD = false>
 __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<Real>& ws,
                                                   const ChanRec* __restrict__ crec,
                                                   const R2<Real>* __restrict__ wrec, int jb, int nb, int jend,
@@ -749,7 +731,7 @@ __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<R
     nxt = crec[jb + 32 + L];
     if (wrec) nxtw = wrec[jb + 32 + L];
   }
-  int key = -1;
+  int key = -1, toff = 0;
   if (L < nb) {
     const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = pk_tg(cr.pk);
     const double x = cr.kd * (ws.d0[t] + ws.d0[g.T + r]);
@@ -766,21 +748,29 @@ __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<R
       q.x = cr.kd;
       q.y = (Real)(x - rint(x));
     }
+    toff = (t - tg * g.Tg) * TABW;
     if (wrec) {
       q.z = w.x;
       q.w = w.y;
     } else {  // forward: the tx-row offset rides in .z as a bit pattern (one broadcast load per channel)
-      q.z = int_bits<Real>((t - tg * g.Tg) * TABW);
+      q.z = int_bits<Real>(toff);
       q.w = 0;
     }
     ws.rec[L] = q;
     key = r | (tg << 16);
-    ws.rect[L] = make_int2((t - tg * g.Tg) * TABW, key);
   }
   int prev = __shfl_up_sync(FULL, key, 1);
   if (L == 0) prev = carry;
   const unsigned starts = __ballot_sync(FULL, L < nb && key != prev);
   carry = __shfl_sync(FULL, key, nb - 1);
+  if (L < nb) {
+    int x = toff;
+    if (FWD) {
+      const unsigned later = L < 31 ? (starts >> (L + 1)) << (L + 1) : 0u;
+      x = later ? __ffs(later) - 1 : nb;
+    }
+    ws.rect[L] = make_int2(x, key);
+  }
   __syncwarp();
   return starts;
 }
@@ -1084,9 +1074,22 @@ __host__ __device__ constexpr size_t fwd_warp_bytes(int Tg, int A) {
   return warp_smem_bytes<Real>(Tg, A, 1) + (size_t)TBR * 33 * sizeof(R2<Real>);
 }
 
-// Forward variant with ONE staging slot: read the prefetched rows, and defer the prefetch
-// of the next receiver until the rows have been consumed by arithmetic (caller issues
-// stage_rx after the run's first entry). This keeps the slot free of write-after-read races.
+// Sum of one element from each of the four (c64) / eight (c128) shared loads of ldv(dR), ldv(iR):
+// consuming it makes an instruction wait until every load of the slot has returned its data.
+__device__ __forceinline__ float slot_guard(const FV& dR, const FV& iR) {
+  return (dR.p[0].x + dR.p[NP / 2].x) + (iR.p[0].x + iR.p[NP / 2].x);
+}
+__device__ __forceinline__ double slot_guard(const DV& dR, const DV& iR) {
+  double t = 0;
+#pragma unroll
+  for (int i = 0; i < V; i += 2) t += dR.v[i] + iR.v[i];
+  return t;
+}
+
+// Forward variant with ONE staging slot: read the prefetched rows of receiver rr into registers,
+// then start the prefetch of the next receiver into the same slot. The prefetch is predicated on
+// a value computed from every load of the slot (always true: table entries are finite), so it
+// cannot be issued before those loads have completed (no write-after-read race on the slot).
 template <typename Real>
 __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __restrict__ tabt,
                                                   const WarpSmem<Real>& ws, int rr, int& pf_r, int L, QV<Real>& dR,
@@ -1101,6 +1104,8 @@ __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __re
   dR = ldv(src);
   iR = ldv(src + TILE);
   pf_r = rr + 1 < g.R ? rr + 1 : 0;
+  const Real guard = slot_guard(dR, iR);
+  if (guard == guard) stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
 }
 
 // Forward: a warp owns (tile, channel chunk) like the adjoint. Per channel, each lane forms
@@ -1150,34 +1155,34 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   const QV<Real> sr = make_v(srv), si = make_v(siv);
   __syncwarp();
 
-  QV<Real> dR, iR, shr, shi;
+  QV<Real> dR, iR, shr, shi, nshr;
   zero(dR);
   zero(iR);
   zero(shr);
   zero(shi);
+  zero(nshr);
   int cur_tg = -1, pf_r = -1, carry = -1;
-  bool stage_pending = false;
+  R2<Real>* outl = out + L;
   for (int jb = c0; jb < c1; jb += 32) {
     const int nb = min(32, c1 - jb);
-    const unsigned starts = build_records<Real, EXACT>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
+    const unsigned starts =
+        build_records<Real, EXACT, true>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
     // sub-batches of TBR channels share one [TBR][33] transpose buffer
     for (int h0 = 0; h0 < nb; h0 += TBR) {
       const int h1 = min(nb, h0 + TBR);
       int c = h0;
       while (c < h1) {
-        const int e = min(run_end(starts, c, nb), h1);
-        if ((starts >> c) & 1u) {
-          const int key = ws.rect[c].y;
-          const int rr = key & 0xffff, tg = key >> 16;
+        const int2 rc = ws.rect[c];
+        const int e = min(rc.x, h1);
+        if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c
+          const int rr = rc.y & 0xffff, tg = rc.y >> 16;
           if (tg != cur_tg) {
             load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
             cur_tg = tg;
           }
           rx_run_rows_1slot<Real>(g, tabt, ws, rr, pf_r, L, dR, iR);
-          scale_s(iR, sr, si, shr, shi);
-          stage_pending = true;
+          scale_s(iR, sr, si, shr, shi, nshr);
         }
-#if NFGPU_FWD_PAIR
         // two channels per iteration, both results stored after both are computed, so the
         // compiler can overlap their dependency chains (a store in between would be a barrier)
         for (; c + 1 < e; c += 2) {
@@ -1188,12 +1193,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           QV<Real> cs0, sn0, cs1, sn1;
           phasorv<EXACT, false>(q0.x, q0.y, dT0, dR, cs0, sn0);
           phasorv<EXACT, false>(q1.x, q1.y, dT1, dR, cs1, sn1);
-          if (stage_pending) {  // dR/iR are consumed: refill the single slot for the next run
-            stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
-            stage_pending = false;
-          }
-          const R2<Real> p0 = fwd_part(iT0, cs0, sn0, shr, shi);
-          const R2<Real> p1 = fwd_part(iT1, cs1, sn1, shr, shi);
+          const R2<Real> p0 = fwd_part(iT0, cs0, sn0, shr, shi, nshr);
+          const R2<Real> p1 = fwd_part(iT1, cs1, sn1, shr, shi, nshr);
           tb[(c - h0) * 33 + L] = p0;
           tb[(c + 1 - h0) * 33 + L] = p1;
         }
@@ -1203,32 +1204,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
           QV<Real> cs, sn;
           phasorv<EXACT, false>(q.x, q.y, dT, dR, cs, sn);
-          if (stage_pending) {
-            stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
-            stage_pending = false;
-          }
-          tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi);
+          tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi, nshr);
           ++c;
         }
-#else
-        R4<Real> q = ws.rec[c];
-        int off = ws.rect[c].x;
-#pragma unroll UNROLL
-        for (; c < e; ++c) {
-          const R4<Real> qn = ws.rec[c + 1];
-          const int offn = ws.rect[c + 1].x;
-          const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
-          QV<Real> cs, sn;
-          phasorv<EXACT, false>(q.x, q.y, dT, dR, cs, sn);
-          if (stage_pending) {  // dR/iR are consumed: refill the single slot for the next run
-            stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
-            stage_pending = false;
-          }
-          tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi);
-          q = qn;
-          off = offn;
-        }
-#endif
       }
       __syncwarp();
       // transpose-reduce: 32/TBR lanes per row each sum a 32/(32/TBR) slice of row L % TBR,
@@ -1253,7 +1231,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
         S.x += __shfl_down_sync(FULL, S.x, o);
         S.y += __shfl_down_sync(FULL, S.y, o);
       }
-      if (L < h1 - h0) out[jb + h0 + L] = S;
+      if (L < h1 - h0) outl[jb + h0] = S;
       __syncwarp();
     }
   }
