@@ -280,9 +280,10 @@ __device__ __forceinline__ void flush(const FV& iR, FV& hr, FV& hi, FV& gr, FV& 
   for (int i = 0; i < NP; ++i) {
     gr.p[i] = fma2(iR.p[i], hr.p[i], gr.p[i]);
     gi.p[i] = fma2(iR.p[i], hi.p[i], gi.p[i]);
+    // h = 0 as one packed multiply per pair (h is finite; a literal 0 costs two 32-bit moves)
+    hr.p[i] = mul2(hr.p[i], bc(0.f));
+    hi.p[i] = mul2(hi.p[i], bc(0.f));
   }
-  zero(hr);
-  zero(hi);
 }
 __device__ __forceinline__ void flush(const DV& iR, DV& hr, DV& hi, DV& gr, DV& gi) {
 #pragma unroll
@@ -716,11 +717,10 @@ __device__ __forceinline__ int bits_int(double v) { return (int)__double_as_long
 
 // Build the 32 channel records of one batch (lane L <-> sorted position jb+L) from the
 // prefetched ChanRec/w in registers, and prefetch the next batch's. Returns the bitmask of
-// run starts (a run = maximal stretch with equal (rx, tx group)). rect[L] = {x, run key}, where
-// x is the tx-row offset in the group (adjoint) or, for the forward (FWD), the end of the run
-// that position L belongs to (the next run start after L, or nb), so the forward's segment loop
-// reads its bound with one shared load.
-template <typename Real, bool EXACT, bool FWD = false>
+// run starts (a run = maximal stretch with equal (rx, tx group)). rect[L] = {tx-row offset in the
+// group, rx | tx group << 16 | run end << 24}; the run end of position L is the next run start
+// after L (or nb), so the channel loops read their segment bound with the same shared load.
+template <typename Real, bool EXACT>
 __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<Real>& ws,
                                                   const ChanRec* __restrict__ crec,
                                                   const R2<Real>* __restrict__ wrec, int jb, int nb, int jend,
@@ -764,12 +764,9 @@ __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<R
   const unsigned starts = __ballot_sync(FULL, L < nb && key != prev);
   carry = __shfl_sync(FULL, key, nb - 1);
   if (L < nb) {
-    int x = toff;
-    if (FWD) {
-      const unsigned later = L < 31 ? (starts >> (L + 1)) << (L + 1) : 0u;
-      x = later ? __ffs(later) - 1 : nb;
-    }
-    ws.rect[L] = make_int2(x, key);
+    const unsigned later = L < 31 ? (starts >> (L + 1)) << (L + 1) : 0u;
+    const int end = later ? __ffs(later) - 1 : nb;
+    ws.rect[L] = make_int2(toff, key | (end << 24));
   }
   __syncwarp();
   return starts;
@@ -787,11 +784,6 @@ __device__ __forceinline__ void prefetch_first(const ChanRec* __restrict__ crec,
     nxt = crec[j0 + L];
     if (wrec) nxtw = wrec[j0 + L];
   }
-}
-
-__device__ __forceinline__ int run_end(unsigned starts, int c, int nb) {
-  const unsigned later = (c + 1 < 32) ? (starts >> (c + 1)) << (c + 1) : 0u;
-  return later ? __ffs(later) - 1 : nb;
 }
 
 // ------------------------------------------------------------------ adjoint (+prox)
@@ -996,10 +988,10 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
     const unsigned starts = build_records<Real, EXACT>(g, ws, a.crec, a.wrec, jb, nb, j1, L, carry, nxt, nxtw);
     int c = 0;
     while (c < nb) {
-      const int e = run_end(starts, c, nb);
+      const int key = ws.rect[c].y;
+      const int e = key >> 24;
       if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c
-        const int key = ws.rect[c].y;
-        const int rr = key & 0xffff, tg = key >> 16;
+        const int rr = key & 0xffff, tg = (key >> 16) & 0xff;
         if (tg != cur_tg) {
           load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
           cur_tg = tg;
@@ -1166,16 +1158,16 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   for (int jb = c0; jb < c1; jb += 32) {
     const int nb = min(32, c1 - jb);
     const unsigned starts =
-        build_records<Real, EXACT, true>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
+        build_records<Real, EXACT>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
     // sub-batches of TBR channels share one [TBR][33] transpose buffer
     for (int h0 = 0; h0 < nb; h0 += TBR) {
       const int h1 = min(nb, h0 + TBR);
       int c = h0;
       while (c < h1) {
-        const int2 rc = ws.rect[c];
-        const int e = min(rc.x, h1);
+        const int key = ws.rect[c].y;
+        const int e = min(key >> 24, h1);
         if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c
-          const int rr = rc.y & 0xffff, tg = rc.y >> 16;
+          const int rr = key & 0xffff, tg = (key >> 16) & 0xff;
           if (tg != cur_tg) {
             load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
             cur_tg = tg;
