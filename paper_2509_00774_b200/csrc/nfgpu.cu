@@ -2899,9 +2899,10 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   // per forward for +0.9%). Tile-major equal chunks above NFGPU_L2_TABLE_MB; env NFGPU_CHUNK_ORDER.
   p->chunk_order = rs * (size_t)g.ntiles * g.A * TABW <= ((size_t)NFGPU_L2_TABLE_MB << 20) ? 1 : 0;
   if (const char* e = std::getenv("NFGPU_CHUNK_ORDER")) p->chunk_order = std::atoi(e) ? 1 : 0;
-  // adjoint units: two waves with chunk-major order, four with tile-major (its chunk combine favours
-  // fewer units; the tile-major full problem prefers three chunks per tile)
-  p->adj_target = p->chunk_order ? 148LL * 16 * 2 : 148LL * 16 * 4;
+  // adjoint units: ~3.2 waves with chunk-major order (tools/sweep: 1/8 Large slab 15 chunks 0.327 ms vs
+  // 10 chunks 0.351 ms, 1/4 slab 8 chunks 0.610 vs 5 chunks 0.644), four with tile-major (its chunk
+  // combine favours fewer units; the tile-major full problem prefers three chunks per tile)
+  p->adj_target = p->chunk_order ? 148LL * 16 * 16 / 5 : 148LL * 16 * 4;
   if (const char* e = std::getenv("NFGPU_ADJ_TARGET")) p->adj_target = std::max(1LL, std::atoll(e));
   {
     // bound the forward partial buffer to ~512 MB
