@@ -52,7 +52,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-graph", action="store_true", help="launch steps eagerly instead of a CUDA graph")
     ap.add_argument("--no-extras", action="store_true", help="skip the Medium extra line")
-    ap.add_argument("--force-dist", action="store_true", help="use the NCCL path even at world size 1")
+    ap.add_argument("--force-dist", action="store_true", help="use the distributed path even at world size 1")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
+                    help="forward-partial all-reduce at N > 1: NCCL, or the fused NVLink peer all-reduce "
+                         "(nf_forward_allreduce; validated on one GPU by rank emulation, DESIGN.md §5)")
     return ap.parse_args()
 
 
@@ -204,7 +207,7 @@ def slab(nz: int, rank: int, world: int):
     return slab_range(nz, rank, world)
 
 
-def build_engine(workload, dev, rank, world, pg):
+def build_engine(workload, dev, rank, world, pg, collective="nccl"):
     """Setup (not timed): plan for this rank's slab, synthetic scene and measurements, the
     power-iteration Lipschitz constant (20 iterations, as BASELINE.json), λ and α."""
     from paper_2509_00774_b200 import configs
@@ -224,7 +227,7 @@ def build_engine(workload, dev, rank, world, pg):
     eta, alpha = 1.0 / L, lam / L
     setup.release()
     plan = DevicePlan(scn, dtype=w.dtype, device=dev, z_range=zr, max_batch=w.batch)
-    eng = SPGMEngine(plan, y, eta, alpha, process_group=pg)
+    eng = SPGMEngine(plan, y, eta, alpha, process_group=pg, collective=collective)
     return w, plan, eng, eta, alpha, time.perf_counter() - t0
 
 
@@ -291,7 +294,7 @@ def run_ours(args):
         os.environ.setdefault("MASTER_PORT", "29511")
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         pg = dist.group.WORLD
-    w, plan, eng, eta, alpha, setup_s = build_engine(args.workload, dev, rank, world, pg)
+    w, plan, eng, eta, alpha, setup_s = build_engine(args.workload, dev, rank, world, pg, args.collective)
     scn = w.scenario
     B, N, M = w.batch, scn.n_voxels, scn.n_channels
     use_graph = not args.no_graph
@@ -342,7 +345,7 @@ def run_ours(args):
             "data": "synthetic (seeded scene/array/noise with the BASELINE shapes; no dataset)",
             "iters_per_s": 1e3 / ms_step,
             "config": {"workload": args.workload, "M": M, "N": N, "batch": B, "sampler": "device flat (Feistel)",
-                       "parallelism": f"voxel-slab x{world}", "l2": "inputs larger than L2 (distance table "
+                       "parallelism": f"voxel-slab x{world}", "collective": eng.collective, "l2": "inputs larger than L2 (distance table "
                        f"{plan.info()['device_bytes'] / 2**30:.2f} GiB streamed per kernel)",
                        "cuda_graph": use_graph, "eta": eta, "alpha": alpha, "setup_s": setup_s},
             "roofline": roof, "clocks": clocks, "gpu_launches": per_step * steps, "launches_per_step": per_step,
@@ -456,9 +459,12 @@ def kernel_times(eng, plan, seed, k0, reps):
         b = torch.cuda.Event(enable_timing=True)
         c = torch.cuda.Event(enable_timing=True)
         a.record(st)
-        plan.forward(eng.s, out=yb)
+        if eng.collective == "peer":
+            plan.forward_allreduce(eng.s, out=yb)
+        else:
+            plan.forward(eng.s, out=yb)
         b.record(st)
-        if eng.pg is not None:
+        if eng.pg is not None and eng.collective != "peer":
             torch.distributed.all_reduce(torch.view_as_real(yb), group=eng.pg)
         c0 = torch.cuda.Event(enable_timing=True)
         c0.record(st)

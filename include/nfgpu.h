@@ -136,6 +136,27 @@ int nf_soft_threshold(int dtype, const void* v_dev, void* out_dev, int64_t n, do
 int nf_magnitude_change(int dtype, const void* a_dev, const void* b_dev, int64_t n,
                         double* stats_dev, void* stream);
 
+/* Peer all-reduce of the forward partials over NVLink/NVSwitch (multi-GPU voxel-slab sharding,
+ * SURVEY.md §8(e); the reference has no multi-GPU path, so nothing in it is replaced). One process per
+ * GPU, one plan per rank over its z-slab:
+ *   nf_comm_create        allocate this rank's receive slots and flags; write its CUDA IPC handle
+ *                         (NF_IPC_HANDLE_BYTES bytes) to handle_out
+ *   nf_comm_connect       map every peer's buffer; handles = world handles in rank order (the host
+ *                         exchanges them, e.g. torch.distributed.all_gather_object)
+ *   nf_forward_allreduce  nf_forward whose last reduce kernel pushes this rank's channel sums into every
+ *                         rank's slots and sums all ranks' slots in rank order: y_dev is the FULL A_B s on
+ *                         every rank (replaces nf_forward + an all-reduce of 2*B reals)
+ *   nf_comm_status        *timed_out = 1 if a peer flag wait gave up (a rank stopped participating)
+ *   nf_comm_emulate       test hook: `world` ranks emulated in one cooperative launch on the current GPU;
+ *                         tmp_host [epochs][world][nseg][span][2] level-1 sums, y_host [epochs][world][span][2] */
+#define NF_IPC_HANDLE_BYTES 64
+int nf_comm_create(nf_plan* plan, int rank, int world, void* handle_out);
+int nf_comm_connect(nf_plan* plan, const void* handles);
+int nf_forward_allreduce(nf_plan* plan, const void* s_dev, void* y_dev, void* stream);
+int nf_comm_status(nf_plan* plan, int* timed_out);
+int nf_comm_emulate(int dtype, int world, int span, int nseg, int epochs, const double* tmp_host,
+                    const int* sf_host, const int* spos_host, const double* pulse_host, int n_f, double* y_host);
+
 const char* nf_last_error(void);
 
 #ifdef __cplusplus

@@ -41,8 +41,14 @@ SIGNATURES = {
     "nf_plan_set_iter": (_I, [_P, ctypes.c_uint64, _P]),
     "nf_soft_threshold": (_I, [_I, _P, _P, ctypes.c_int64, _D, _P]),
     "nf_magnitude_change": (_I, [_I, _P, _P, ctypes.c_int64, _P, _P]),
+    "nf_comm_create": (_I, [_P, _I, _I, _P]),
+    "nf_comm_connect": (_I, [_P, _P]),
+    "nf_forward_allreduce": (_I, [_P, _P, _P, _P]),
+    "nf_comm_status": (_I, [_P, _IP]),
+    "nf_comm_emulate": (_I, [_I, _I, _I, _I, _I, _DP, _IP, _IP, _DP, _I, _DP]),
     "nf_last_error": (ctypes.c_char_p, []),
 }
+NF_IPC_HANDLE_BYTES = 64
 
 _lock = threading.Lock()
 _lib = None

@@ -2404,6 +2404,96 @@ __global__ void fwd_reduce2_kernel(const double2* __restrict__ tmp, int span, in
   y[2 * (size_t)k + 1] = (Real)(pr * si + pim * sr);
 }
 
+// ------------------------------------------------------------------ peer all-reduce of the forward partials
+//
+// Multi-GPU voxel-slab sharding: A_B s = Σ_p A_B[:, slab_p] s[slab_p].
+// Instead of the NCCL all-reduce of the 2·B forward reals that follows nf_forward, the last forward
+// reduce kernel pushes its (pre-pulse, fp64) channel sums straight into every rank's receive buffer
+// over NVLink/NVSwitch (CUDA IPC peer mappings), raises one flag per (source rank, block) on every
+// rank, waits for the flags of all source ranks for its own block, and sums the world slots in rank
+// order, so every rank gets the same bits and the result does not depend on arrival order.
+// Per-block epoch counters (advanced once per launch, in lockstep on all ranks) make the flags
+// monotone; the receive buffer is double-buffered on epoch parity, so a fast rank can run one
+// iteration ahead without overwriting slots a slow rank is still reading.
+// With gridDim.y > 1 the same kernel emulates gridDim.y ranks in one cooperative launch on one GPU
+// (tests: every block of every emulated rank is co-resident, no launch waits on another launch).
+constexpr int PEER_MAX = 8;
+constexpr long long PEER_SPIN_LIMIT = 1LL << 26;  // ~seconds of polling, then report instead of hanging
+struct PeerArgs {
+  int world, rank0;                    // rank of blockIdx.y == 0 (production: this rank, gridDim.y = 1)
+  int cap, nblk_cap;                   // receive slots per (parity, source) and flag slots per source
+  int blk_base;                        // flag/epoch slot of blockIdx.x == 0 in this launch
+  double2* recv[PEER_MAX];             // every rank's receive buffer as mapped here: [2][world][cap]
+  unsigned long long* flag[PEER_MAX];  // every rank's flags as mapped here: [world][nblk_cap]
+  const double2* tmp[PEER_MAX];        // per grid rank: level-1 segment sums [nseg][span]
+  void* y[PEER_MAX];                   // per grid rank: output, subset order
+  unsigned long long* epoch[PEER_MAX]; // per grid rank: per-block launch counters [nblk_cap]
+  int* err;                            // per grid rank 0: set to 1 if a wait timed out
+};
+__device__ __forceinline__ void st_release_sys(unsigned long long* a, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+template <typename Real>
+__global__ void __launch_bounds__(256) fwd_reduce2_peer_kernel(PeerArgs pa, int span, int nseg, int w0,
+                                                               const int* __restrict__ sf,
+                                                               const int* __restrict__ spos,
+                                                               const double* __restrict__ pulse) {
+  pdl_wait_and_release();
+  const int gr = blockIdx.y, rank = pa.rank0 + gr, W = pa.world;
+  const int b = pa.blk_base + blockIdx.x;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = j < span;
+  const unsigned long long e = pa.epoch[gr][b] + 1;
+  const int par = (int)(e & 1ULL);
+  double sr = 0, si = 0;
+  if (act)
+    for (int s = 0; s < nseg; ++s) {
+      const double2 v = pa.tmp[gr][(size_t)s * span + j];
+      sr += v.x;
+      si += v.y;
+    }
+  if (act)
+    for (int q = 0; q < W; ++q) pa.recv[q][((size_t)par * W + rank) * pa.cap + w0 + j] = make_double2(sr, si);
+  __syncthreads();  // the block's pushes happen before any of its flags
+  if (threadIdx.x < W) {
+    __threadfence_system();
+    st_release_sys(pa.flag[threadIdx.x] + (size_t)rank * pa.nblk_cap + b, e);
+  }
+  if (threadIdx.x < W) {  // thread q waits for source rank q's push of this block
+    const unsigned long long* f = pa.flag[rank] + (size_t)threadIdx.x * pa.nblk_cap + b;
+    long long spins = 0;
+    while (ld_acquire_sys(f) < e) {
+      if (++spins > PEER_SPIN_LIMIT) {
+        atomicExch(pa.err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  if (act) {
+    double tr = 0, ti = 0;
+    const double2* src = pa.recv[rank] + (size_t)par * W * pa.cap + w0 + j;
+    for (int q = 0; q < W; ++q) {  // fixed rank order: identical bits on every rank
+      const double2 v = __ldcg(src + (size_t)q * pa.cap);
+      tr += v.x;
+      ti += v.y;
+    }
+    const int f = sf[w0 + j];
+    const double pr = pulse[2 * f] / (4.0 * PI), pim = pulse[2 * f + 1] / (4.0 * PI);
+    const int k = spos[w0 + j];
+    Real* y = reinterpret_cast<Real*>(pa.y[gr]);
+    y[2 * (size_t)k] = (Real)(pr * tr - pim * ti);
+    y[2 * (size_t)k + 1] = (Real)(pr * ti + pim * tr);
+  }
+  if (threadIdx.x == 0) pa.epoch[gr][b] = e;
+}
+
 // ------------------------------------------------------------------ elementwise utilities
 template <typename Real>
 __global__ void soft_threshold_kernel(const Real* __restrict__ v, Real* __restrict__ out, int64_t n,
@@ -2506,6 +2596,16 @@ struct nf_plan {
   // tensor-core structured forward: per-(half tile, channel) partials, allocated on first use
   float2* d_tcpart = nullptr;
   size_t tcpart_elems = 0;
+  // peer all-reduce of the forward partials (nf_comm_*): own buffer = receive slots
+  // [2][world][comm_cap] double2, then flags [world][comm_nblk] u64; peers mapped by CUDA IPC
+  int comm_world = 0, comm_rank = -1, comm_cap = 0, comm_nblk = 0;
+  bool comm_connected = false;
+  void* comm_buf = nullptr;
+  void* comm_peer[PEER_MAX] = {};
+  unsigned long long* d_epoch = nullptr;
+  int* d_comm_err = nullptr;
+  bool comm_active = false;  // inside nf_forward_allreduce: the last reduce is the peer kernel
+  int comm_blk = 0;          // flag/epoch slot of the next peer-reduce block within one forward
 };
 
 namespace {
@@ -2543,6 +2643,11 @@ void free_plan(nf_plan* p) {
                   p->d_cnt,  p->d_sm,   p->d_spos,  p->d_crec,  p->d_sf, p->d_wrec, p->d_dpart,   p->d_part,
                   p->d_tmp,  p->d_gpart, p->d_tilecnt, p->d_stat_part, p->d_iter, p->d_struct, p->d_bimg, p->d_tcpart};
   for (void* q : ptrs) cudaFree(q);
+  for (int q = 0; q < p->comm_world; ++q)
+    if (q != p->comm_rank && p->comm_peer[q]) cudaIpcCloseMemHandle(p->comm_peer[q]);
+  cudaFree(p->comm_buf);
+  cudaFree(p->d_epoch);
+  cudaFree(p->d_comm_err);
   delete p;
 }
 
@@ -2580,6 +2685,40 @@ int adjoint_chunks(const nf_plan* p) {
   return (int)std::max(1LL, ch);
 }
 
+size_t comm_recv_bytes(const nf_plan* p) { return (size_t)2 * p->comm_world * p->comm_cap * sizeof(double2); }
+
+// Level 2 of the forward reduce: plain (scatter to y) or, inside nf_forward_allreduce, fused with the
+// peer all-reduce across the plan's voxel-slab ranks (fwd_reduce2_peer_kernel).
+template <typename Real>
+int launch_reduce2(nf_plan* p, int span, int nseg, int w0, void* y, cudaStream_t st, bool pdl) {
+  const int nblk = (span + 255) / 256;
+  if (!p->comm_active) {
+    CUDA_TRY(launch_k(pdl, fwd_reduce2_kernel<Real>, dim3(nblk), dim3(256), 0, st, (const double2*)p->d_tmp, span,
+                      nseg, w0, (const int*)p->d_sf, (const int*)p->d_spos, (const double*)p->d_pulse, (Real*)y));
+    return NF_OK;
+  }
+  if (p->comm_blk + nblk > p->comm_nblk) return fail(NF_ERR_STATE, "peer all-reduce: flag slots exhausted");
+  PeerArgs pa = {};
+  pa.world = p->comm_world;
+  pa.rank0 = p->comm_rank;
+  pa.cap = p->comm_cap;
+  pa.nblk_cap = p->comm_nblk;
+  pa.blk_base = p->comm_blk;
+  for (int q = 0; q < p->comm_world; ++q) {
+    char* base = (char*)p->comm_peer[q];
+    pa.recv[q] = (double2*)base;
+    pa.flag[q] = (unsigned long long*)(base + comm_recv_bytes(p));
+  }
+  pa.tmp[0] = p->d_tmp;
+  pa.y[0] = y;
+  pa.epoch[0] = p->d_epoch;
+  pa.err = p->d_comm_err;
+  CUDA_TRY(launch_k(pdl, fwd_reduce2_peer_kernel<Real>, dim3(nblk, 1), dim3(256), 0, st, pa, span, nseg, w0,
+                    (const int*)p->d_sf, (const int*)p->d_spos, (const double*)p->d_pulse));
+  p->comm_blk += nblk;
+  return NF_OK;
+}
+
 template <typename Real>
 int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const size_t sm = fwd_smem(p);
@@ -2608,8 +2747,7 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     nseg = std::max(1, std::min({nseg, p->fwd_gridx, std::max(1, RED_THREADS / span)}));
     CUDA_TRY(launch_k(p->use_pdl, fwd_reduce1_kernel<Real>, dim3((span + 255) / 256, nseg), dim3(256), 0, st,
                       (const Real*)p->d_part, p->fwd_gridx, span, nseg, p->d_tmp));
-    CUDA_TRY(launch_k(p->use_pdl, fwd_reduce2_kernel<Real>, dim3((span + 255) / 256), dim3(256), 0, st, p->d_tmp, span,
-                      nseg, w0, p->d_sf, p->d_spos, p->d_pulse, (Real*)y));
+    if (int rc = launch_reduce2<Real>(p, span, nseg, w0, y, st, p->use_pdl)) return rc;
     p->launches += 3;
   }
   return NF_OK;
@@ -2685,9 +2823,7 @@ int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     fwd_reduce1_kernel<float><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const float*)p->d_tcpart, (int)rows,
                                                                               span, nseg, p->d_tmp);
     CUDA_TRY(cudaGetLastError());
-    fwd_reduce2_kernel<float><<<(span + 255) / 256, 256, 0, st>>>(p->d_tmp, span, nseg, a.w0, p->d_sf, p->d_spos,
-                                                                  p->d_pulse, (float*)y);
-    CUDA_TRY(cudaGetLastError());
+    if (int rc = launch_reduce2<float>(p, span, nseg, a.w0, y, st, false)) return rc;
     p->launches += 3;
   }
   return NF_OK;
@@ -2737,9 +2873,7 @@ int launch_forward_struct(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     fwd_reduce1_kernel<Real><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const Real*)p->d_part, p->fwd_gridx,
                                                                              span, nseg, p->d_tmp);
     CUDA_TRY(cudaGetLastError());
-    fwd_reduce2_kernel<Real><<<(span + 255) / 256, 256, 0, st>>>(p->d_tmp, span, nseg, a.w0, p->d_sf, p->d_spos,
-                                                                 p->d_pulse, (Real*)y);
-    CUDA_TRY(cudaGetLastError());
+    if (int rc = launch_reduce2<Real>(p, span, nseg, a.w0, y, st, false)) return rc;
     p->launches += 3;
   }
   return NF_OK;
@@ -3081,6 +3215,148 @@ int nf_forward(nf_plan* p, const void* s, void* y, void* stream) {
   if (p->structured)
     return p->dtype == NF_C64 ? launch_forward_struct<float>(p, s, y, st) : launch_forward_struct<double>(p, s, y, st);
   return p->dtype == NF_C64 ? launch_forward<float>(p, s, y, st) : launch_forward<double>(p, s, y, st);
+}
+
+int nf_comm_create(nf_plan* p, int rank, int world, void* handle_out) {
+  if (!p || !handle_out) return fail(NF_ERR_ARG, "null argument");
+  if (world < 1 || world > PEER_MAX) return fail(NF_ERR_ARG, "world must be in [1, 8]");
+  if (rank < 0 || rank >= world) return fail(NF_ERR_ARG, "rank out of range");
+  if (p->comm_buf) return fail(NF_ERR_STATE, "communicator already created for this plan");
+  p->comm_world = world;
+  p->comm_rank = rank;
+  p->comm_cap = p->max_batch;
+  p->comm_nblk = (p->max_batch + 255) / 256 + 256;  // blocks of all windows of one forward
+  const size_t bytes = comm_recv_bytes(p) + (size_t)world * p->comm_nblk * sizeof(unsigned long long);
+  CUDA_TRY(cudaMalloc(&p->comm_buf, bytes));
+  CUDA_TRY(cudaMemset(p->comm_buf, 0, bytes));
+  CUDA_TRY(cudaMalloc((void**)&p->d_epoch, p->comm_nblk * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemset(p->d_epoch, 0, p->comm_nblk * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc((void**)&p->d_comm_err, sizeof(int)));
+  CUDA_TRY(cudaMemset(p->d_comm_err, 0, sizeof(int)));
+  p->dev_bytes += bytes + p->comm_nblk * sizeof(unsigned long long) + sizeof(int);
+  CUDA_TRY(cudaDeviceSynchronize());
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, p->comm_buf));
+  static_assert(sizeof(cudaIpcMemHandle_t) == NF_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle_out, &h, NF_IPC_HANDLE_BYTES);
+  p->comm_peer[rank] = p->comm_buf;
+  return NF_OK;
+}
+
+int nf_comm_connect(nf_plan* p, const void* handles) {
+  if (!p || !handles) return fail(NF_ERR_ARG, "null argument");
+  if (!p->comm_buf) return fail(NF_ERR_STATE, "nf_comm_create first");
+  if (p->comm_connected) return fail(NF_ERR_STATE, "communicator already connected");
+  for (int q = 0; q < p->comm_world; ++q) {
+    if (q == p->comm_rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, (const char*)handles + (size_t)q * NF_IPC_HANDLE_BYTES, NF_IPC_HANDLE_BYTES);
+    CUDA_TRY(cudaIpcOpenMemHandle(&p->comm_peer[q], h, cudaIpcMemLazyEnablePeerAccess));
+  }
+  p->comm_connected = true;
+  return NF_OK;
+}
+
+int nf_forward_allreduce(nf_plan* p, const void* s, void* y, void* stream) {
+  if (!p || !s || !y) return fail(NF_ERR_ARG, "null argument");
+  if (!p->comm_connected) return fail(NF_ERR_STATE, "peer all-reduce not connected (nf_comm_create/nf_comm_connect)");
+  p->comm_active = true;
+  p->comm_blk = 0;
+  const int rc = nf_forward(p, s, y, stream);
+  p->comm_active = false;
+  return rc;
+}
+
+int nf_comm_status(nf_plan* p, int* timed_out) {
+  if (!p || !timed_out) return fail(NF_ERR_ARG, "null argument");
+  *timed_out = 0;
+  if (!p->d_comm_err) return NF_OK;
+  CUDA_TRY(cudaMemcpy(timed_out, p->d_comm_err, sizeof(int), cudaMemcpyDeviceToHost));
+  return NF_OK;
+}
+
+int nf_comm_emulate(int dtype, int world, int span, int nseg, int epochs, const double* tmp_host,
+                    const int* sf_host, const int* spos_host, const double* pulse_host, int n_f, double* y_host) {
+  if (!tmp_host || !sf_host || !spos_host || !pulse_host || !y_host) return fail(NF_ERR_ARG, "null argument");
+  if (world < 1 || world > PEER_MAX || span < 1 || nseg < 1 || epochs < 1 || n_f < 1)
+    return fail(NF_ERR_ARG, "bad sizes");
+  if (dtype != NF_C64 && dtype != NF_C128) return fail(NF_ERR_ARG, "dtype must be NF_C64 or NF_C128");
+  const int nblk = (span + 255) / 256;
+  const size_t rs = dtype == NF_C64 ? sizeof(float) : sizeof(double);
+  const size_t recv_b = (size_t)2 * world * span * sizeof(double2), flag_b = (size_t)world * nblk * 8;
+  std::vector<void*> bufs;
+  auto dmal = [&](size_t b) -> void* {
+    void* q = nullptr;
+    if (cudaMalloc(&q, b) != cudaSuccess) return nullptr;
+    cudaMemset(q, 0, b);
+    bufs.push_back(q);
+    return q;
+  };
+  int rc = NF_OK;
+  PeerArgs pa = {};
+  pa.world = world;
+  pa.rank0 = 0;
+  pa.cap = span;
+  pa.nblk_cap = nblk;
+  pa.blk_base = 0;
+  int *sf = (int*)dmal(span * sizeof(int)), *sp = (int*)dmal(span * sizeof(int));
+  double* pulse = (double*)dmal(2 * n_f * sizeof(double));
+  pa.err = (int*)dmal(sizeof(int));
+  std::vector<double> tmpd((size_t)nseg * span * 2);
+  for (int q = 0; q < world && rc == NF_OK; ++q) {
+    char* b = (char*)dmal(recv_b + flag_b);
+    pa.tmp[q] = (const double2*)dmal(tmpd.size() * sizeof(double));
+    pa.y[q] = dmal(2 * span * rs);
+    pa.epoch[q] = (unsigned long long*)dmal(nblk * 8);
+    if (!b || !pa.tmp[q] || !pa.y[q] || !pa.epoch[q]) rc = fail(NF_ERR_CUDA, "cudaMalloc failed");
+    pa.recv[q] = (double2*)b;
+    pa.flag[q] = (unsigned long long*)(b + recv_b);
+  }
+  if (rc == NF_OK && (!sf || !sp || !pulse || !pa.err)) rc = fail(NF_ERR_CUDA, "cudaMalloc failed");
+  if (rc == NF_OK) {
+    cudaMemcpy(sf, sf_host, span * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(sp, spos_host, span * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(pulse, pulse_host, 2 * n_f * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  std::vector<char> yh(2 * span * rs);
+  for (int ep = 0; ep < epochs && rc == NF_OK; ++ep) {
+    for (int q = 0; q < world; ++q)
+      cudaMemcpy((void*)pa.tmp[q], tmp_host + ((size_t)ep * world + q) * nseg * span * 2,
+                 (size_t)nseg * span * 2 * sizeof(double), cudaMemcpyHostToDevice);
+    // one cooperative launch holds every emulated rank's blocks, so all of them are co-resident
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblk, world);
+    cfg.blockDim = dim3(256);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = dtype == NF_C64
+                        ? cudaLaunchKernelEx(&cfg, fwd_reduce2_peer_kernel<float>, pa, span, nseg, 0, (const int*)sf,
+                                             (const int*)sp, (const double*)pulse)
+                        : cudaLaunchKernelEx(&cfg, fwd_reduce2_peer_kernel<double>, pa, span, nseg, 0, (const int*)sf,
+                                             (const int*)sp, (const double*)pulse);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      rc = fail(NF_ERR_CUDA, std::string("peer emulation: ") + cudaGetErrorString(e));
+      break;
+    }
+    int err = 0;
+    cudaMemcpy(&err, pa.err, sizeof(int), cudaMemcpyDeviceToHost);
+    if (err) {
+      rc = fail(NF_ERR_STATE, "peer emulation: a flag wait timed out");
+      break;
+    }
+    for (int q = 0; q < world; ++q) {
+      cudaMemcpy(yh.data(), pa.y[q], yh.size(), cudaMemcpyDeviceToHost);
+      double* out = y_host + ((size_t)ep * world + q) * span * 2;
+      for (int i = 0; i < 2 * span; ++i)
+        out[i] = dtype == NF_C64 ? (double)((const float*)yh.data())[i] : ((const double*)yh.data())[i];
+    }
+  }
+  for (void* q : bufs) cudaFree(q);
+  return rc;
 }
 
 int nf_adjoint(nf_plan* p, const void* r, const void* ymeas, void* g, double scale, void* stream) {

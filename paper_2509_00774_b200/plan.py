@@ -224,6 +224,35 @@ class DevicePlan:
         _lib.check(self.lib.nf_forward(self._h, _ptr(s), _ptr(out), _stream(self.device)), "nf_forward")
         return out
 
+    # ---------------------------------------------------------------- peer all-reduce (multi-GPU)
+    def comm_create(self, rank: int, world: int) -> bytes:
+        """Allocate this rank's peer all-reduce slots; returns its CUDA IPC handle (64 bytes)."""
+        h = ctypes.create_string_buffer(_lib.NF_IPC_HANDLE_BYTES)
+        _lib.check(self.lib.nf_comm_create(self._h, int(rank), int(world), h), "nf_comm_create")
+        return h.raw
+
+    def comm_connect(self, handles: list[bytes]) -> None:
+        """Map every rank's slots (``handles`` in rank order, from comm_create on each rank)."""
+        if any(len(h) != _lib.NF_IPC_HANDLE_BYTES for h in handles):
+            raise ValueError("comm_connect: every handle must be 64 bytes")
+        buf = ctypes.create_string_buffer(b"".join(handles), len(handles) * _lib.NF_IPC_HANDLE_BYTES)
+        _lib.check(self.lib.nf_comm_connect(self._h, buf), "nf_comm_connect")
+
+    def forward_allreduce(self, s: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """forward() summed over every connected rank's slab by the fused peer all-reduce:
+        out is the full A_B s on every rank (bitwise the same on all of them)."""
+        if out is None:
+            out = self.vec(self.B)
+        _lib.check(self.lib.nf_forward_allreduce(self._h, _ptr(s), _ptr(out), _stream(self.device)),
+                   "nf_forward_allreduce")
+        return out
+
+    def comm_timed_out(self) -> bool:
+        """True if a peer flag wait gave up (synchronises with the device)."""
+        v = ctypes.c_int(0)
+        _lib.check(self.lib.nf_comm_status(self._h, ctypes.byref(v)), "nf_comm_status")
+        return bool(v.value)
+
     def adjoint(self, r: torch.Tensor, out: torch.Tensor | None = None, ymeas: torch.Tensor | None = None,
                 scale: float = 1.0) -> torch.Tensor:
         """out[n] = scale Σ_k conj(A[m_k, n]) (r[k] - ymeas[m_k])."""

@@ -37,6 +37,26 @@ def slab_range(nz: int, rank: int, world: int) -> tuple[int, int]:
     return lo * unit, (hi * unit if rank < world - 1 else nz)
 
 
+def connect_peer_allreduce(plan, process_group, create=None, connect=None) -> None:
+    """Set up the fused peer all-reduce of the forward partials (nf_comm_*) on
+    ``plan`` for the ranks of ``process_group``: every rank exports the CUDA IPC handle of its
+    receive slots, the handles are all-gathered in rank order over the group (any backend), and
+    every rank maps all of them. Ends with a barrier, so no rank pushes into an unmapped peer.
+    ``create``/``connect`` default to the plan's C-ABI calls (tests substitute host stand-ins)."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(process_group), dist.get_world_size(process_group)
+    create = create or plan.comm_create
+    connect = connect or plan.comm_connect
+    mine = create(rank, world)
+    handles: list = [None] * world
+    dist.all_gather_object(handles, mine, group=process_group)
+    if handles[rank] != mine:
+        raise RuntimeError("peer all-reduce: handle exchange returned a different handle for this rank")
+    connect(handles)
+    dist.barrier(group=process_group)
+
+
 def _allreduce(t: torch.Tensor, pg, op=None) -> torch.Tensor:
     if pg is not None:
         if t.is_complex():

@@ -303,11 +303,21 @@ class SPGMEngine:
     """
 
     def __init__(self, plan: DevicePlan, y: np.ndarray | torch.Tensor, eta: float, alpha: float,
-                 initial: np.ndarray | torch.Tensor | None = None, process_group=None):
+                 initial: np.ndarray | torch.Tensor | None = None, process_group=None,
+                 collective: str = "nccl"):
+        if collective not in ("nccl", "peer"):
+            raise ValueError("collective must be 'nccl' or 'peer'")
         self.plan = plan
         self.eta = float(eta)
         self.alpha = float(alpha)
         self.pg = process_group
+        # "peer": the forward's last reduce kernel all-reduces over NVLink itself (nf_forward_allreduce);
+        # "nccl": nf_forward, then torch.distributed.all_reduce of the 2·B reals
+        self.collective = collective if process_group is not None else "nccl"
+        if self.collective == "peer":
+            from .sharding import connect_peer_allreduce
+
+            connect_peer_allreduce(plan, process_group)
         dev = plan.device
         self.y = plan._as_dev(y, plan.M, "y")
         self.s = torch.zeros(plan.n_local, dtype=plan.torch_dtype, device=dev)
@@ -371,13 +381,18 @@ class SPGMEngine:
         """One iteration on the staged batch: forward, [allreduce], adjoint+prox, swap."""
         B = self.plan.B
         yb = self.ybuf[:B]
-        self.plan.forward(self.s, out=yb)
-        if self.pg is not None:
-            torch.distributed.all_reduce(torch.view_as_real(yb), group=self.pg)
+        if self.collective == "peer":
+            self.plan.forward_allreduce(self.s, out=yb)
+        else:
+            self.plan.forward(self.s, out=yb)
+            if self.pg is not None:
+                torch.distributed.all_reduce(torch.view_as_real(yb), group=self.pg)
         self.plan.adjoint_prox(yb, self.y, self.s, self.s_next, self.eta / B, self.alpha, self.stats)
         self.s, self.s_next = self.s_next, self.s
 
     def magnitude_change(self) -> float:
+        if self.collective == "peer" and self.plan.comm_timed_out():
+            raise RuntimeError("peer all-reduce: a rank stopped participating (flag wait timed out)")
         st = self.stats
         if self.pg is not None:
             st = st.clone()

@@ -102,3 +102,45 @@ def test_two_rank_sharded_step_matches_unsharded():
     st = out[0][4]
     change = np.sqrt(st[1]) / max(np.sqrt(st[0]), 1e-12)
     assert change == pytest.approx(O.relative_magnitude_change(s, s_next), rel=1e-10)
+
+
+def _peer_worker(rank: int, world: int, port: int, q):
+    from paper_2509_00774_b200.sharding import connect_peer_allreduce
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        got = {}
+
+        def create(r, w):  # stands in for nf_comm_create: a rank-specific 64-byte IPC handle
+            got["create"] = (r, w)
+            return bytes([r + 1]) * 64
+
+        def connect(handles):  # stands in for nf_comm_connect
+            got["handles"] = list(handles)
+
+        connect_peer_allreduce(None, dist.group.WORLD, create=create, connect=connect)
+        q.put((rank, got["create"], got["handles"]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_allreduce_handle_exchange(world):
+    """Host side of the fused peer all-reduce (sharding.connect_peer_allreduce): every rank
+    exports one handle, and every rank maps the full list in rank order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [bytes([r + 1]) * 64 for r in range(world)]
+    for rank, (r, w), handles in out:
+        assert (r, w) == (rank, world)
+        assert handles == want
