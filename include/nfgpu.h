@@ -148,7 +148,9 @@ int nf_magnitude_change(int dtype, const void* a_dev, const void* b_dev, int64_t
  *                         every rank (replaces nf_forward + an all-reduce of 2*B reals)
  *   nf_comm_status        *timed_out = 1 if a peer flag wait gave up (a rank stopped participating)
  *   nf_comm_emulate       test hook: `world` ranks emulated in one cooperative launch on the current GPU;
- *                         tmp_host [epochs][world][nseg][span][2] level-1 sums, y_host [epochs][world][span][2] */
+ *                         tmp_host [epochs][world][nseg][span][2] level-1 sums, y_host [epochs][world][span][2];
+ *                         nseg = 0 runs the one-shot variant (structured batches): tmp_host [epochs][world][span][2]
+ *                         is each rank's finished y */
 #define NF_IPC_HANDLE_BYTES 64
 int nf_comm_create(nf_plan* plan, int rank, int world, void* handle_out);
 int nf_comm_connect(nf_plan* plan, const void* handles);

@@ -2438,7 +2438,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
   return v;
 }
-template <typename Real>
+// FROM_Y = false: fused with level 2 of the forward reduce (flat batches; windows start at multiples of
+// 256 channels, so flag slot w0/256 + block is the same channel group on every rank whatever its window
+// split). FROM_Y = true: a one-shot all-reduce of a finished y (structured batches, whose window
+// boundaries depend on the slab): slots per 256 channels of y, no pulse, no scatter.
+template <typename Real, bool FROM_Y>
 __global__ void __launch_bounds__(256) fwd_reduce2_peer_kernel(PeerArgs pa, int span, int nseg, int w0,
                                                                const int* __restrict__ sf,
                                                                const int* __restrict__ spos,
@@ -2451,12 +2455,17 @@ __global__ void __launch_bounds__(256) fwd_reduce2_peer_kernel(PeerArgs pa, int 
   const unsigned long long e = pa.epoch[gr][b] + 1;
   const int par = (int)(e & 1ULL);
   double sr = 0, si = 0;
-  if (act)
+  if (act && FROM_Y) {
+    const Real* y = reinterpret_cast<const Real*>(pa.y[gr]);
+    sr = (double)y[2 * (size_t)(w0 + j)];
+    si = (double)y[2 * (size_t)(w0 + j) + 1];
+  } else if (act) {
     for (int s = 0; s < nseg; ++s) {
       const double2 v = pa.tmp[gr][(size_t)s * span + j];
       sr += v.x;
       si += v.y;
     }
+  }
   if (act)
     for (int q = 0; q < W; ++q) pa.recv[q][((size_t)par * W + rank) * pa.cap + w0 + j] = make_double2(sr, si);
   __syncthreads();  // the block's pushes happen before any of its flags
@@ -2476,14 +2485,21 @@ __global__ void __launch_bounds__(256) fwd_reduce2_peer_kernel(PeerArgs pa, int 
     }
   }
   __syncthreads();
+  double tr = 0, ti = 0;
   if (act) {
-    double tr = 0, ti = 0;
     const double2* src = pa.recv[rank] + (size_t)par * W * pa.cap + w0 + j;
     for (int q = 0; q < W; ++q) {  // fixed rank order: identical bits on every rank
       const double2 v = __ldcg(src + (size_t)q * pa.cap);
       tr += v.x;
       ti += v.y;
     }
+    if (FROM_Y) {
+      Real* y = reinterpret_cast<Real*>(pa.y[gr]);
+      y[2 * (size_t)(w0 + j)] = (Real)tr;
+      y[2 * (size_t)(w0 + j) + 1] = (Real)ti;
+    }
+  }
+  if (act && !FROM_Y) {
     const int f = sf[w0 + j];
     const double pr = pulse[2 * f] / (4.0 * PI), pim = pulse[2 * f + 1] / (4.0 * PI);
     const int k = spos[w0 + j];
@@ -2604,8 +2620,8 @@ struct nf_plan {
   void* comm_peer[PEER_MAX] = {};
   unsigned long long* d_epoch = nullptr;
   int* d_comm_err = nullptr;
-  bool comm_active = false;  // inside nf_forward_allreduce: the last reduce is the peer kernel
-  int comm_blk = 0;          // flag/epoch slot of the next peer-reduce block within one forward
+  bool comm_active = false;  // inside nf_forward_allreduce
+  bool comm_fused = false;   // ... and the flat forward's last reduce already did the all-reduce
 };
 
 namespace {
@@ -2687,35 +2703,40 @@ int adjoint_chunks(const nf_plan* p) {
 
 size_t comm_recv_bytes(const nf_plan* p) { return (size_t)2 * p->comm_world * p->comm_cap * sizeof(double2); }
 
-// Level 2 of the forward reduce: plain (scatter to y) or, inside nf_forward_allreduce, fused with the
-// peer all-reduce across the plan's voxel-slab ranks (fwd_reduce2_peer_kernel).
-template <typename Real>
-int launch_reduce2(nf_plan* p, int span, int nseg, int w0, void* y, cudaStream_t st, bool pdl) {
-  const int nblk = (span + 255) / 256;
-  if (!p->comm_active) {
-    CUDA_TRY(launch_k(pdl, fwd_reduce2_kernel<Real>, dim3(nblk), dim3(256), 0, st, (const double2*)p->d_tmp, span,
-                      nseg, w0, (const int*)p->d_sf, (const int*)p->d_spos, (const double*)p->d_pulse, (Real*)y));
-    return NF_OK;
-  }
-  if (p->comm_blk + nblk > p->comm_nblk) return fail(NF_ERR_STATE, "peer all-reduce: flag slots exhausted");
+PeerArgs peer_args(const nf_plan* p, int blk_base, const void* tmp, void* y) {
   PeerArgs pa = {};
   pa.world = p->comm_world;
   pa.rank0 = p->comm_rank;
   pa.cap = p->comm_cap;
   pa.nblk_cap = p->comm_nblk;
-  pa.blk_base = p->comm_blk;
+  pa.blk_base = blk_base;
   for (int q = 0; q < p->comm_world; ++q) {
     char* base = (char*)p->comm_peer[q];
     pa.recv[q] = (double2*)base;
     pa.flag[q] = (unsigned long long*)(base + comm_recv_bytes(p));
   }
-  pa.tmp[0] = p->d_tmp;
+  pa.tmp[0] = (const double2*)tmp;
   pa.y[0] = y;
   pa.epoch[0] = p->d_epoch;
   pa.err = p->d_comm_err;
-  CUDA_TRY(launch_k(pdl, fwd_reduce2_peer_kernel<Real>, dim3(nblk, 1), dim3(256), 0, st, pa, span, nseg, w0,
+  return pa;
+}
+
+// Level 2 of the forward reduce: plain (scatter to y) or, inside nf_forward_allreduce on a flat batch
+// (`fuse`), fused with the peer all-reduce across the plan's voxel-slab ranks (fwd_reduce2_peer_kernel).
+template <typename Real>
+int launch_reduce2(nf_plan* p, int span, int nseg, int w0, void* y, cudaStream_t st, bool pdl, bool fuse = false) {
+  const int nblk = (span + 255) / 256;
+  if (!(p->comm_active && fuse)) {
+    CUDA_TRY(launch_k(pdl, fwd_reduce2_kernel<Real>, dim3(nblk), dim3(256), 0, st, (const double2*)p->d_tmp, span,
+                      nseg, w0, (const int*)p->d_sf, (const int*)p->d_spos, (const double*)p->d_pulse, (Real*)y));
+    return NF_OK;
+  }
+  if (w0 % 256 || w0 / 256 + nblk > p->comm_nblk) return fail(NF_ERR_STATE, "peer all-reduce: unaligned window");
+  const PeerArgs pa = peer_args(p, w0 / 256, p->d_tmp, y);
+  CUDA_TRY(launch_k(pdl, fwd_reduce2_peer_kernel<Real, false>, dim3(nblk, 1), dim3(256), 0, st, pa, span, nseg, w0,
                     (const int*)p->d_sf, (const int*)p->d_spos, (const double*)p->d_pulse));
-  p->comm_blk += nblk;
+  p->comm_fused = true;
   return NF_OK;
 }
 
@@ -2747,7 +2768,7 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     nseg = std::max(1, std::min({nseg, p->fwd_gridx, std::max(1, RED_THREADS / span)}));
     CUDA_TRY(launch_k(p->use_pdl, fwd_reduce1_kernel<Real>, dim3((span + 255) / 256, nseg), dim3(256), 0, st,
                       (const Real*)p->d_part, p->fwd_gridx, span, nseg, p->d_tmp));
-    if (int rc = launch_reduce2<Real>(p, span, nseg, w0, y, st, p->use_pdl)) return rc;
+    if (int rc = launch_reduce2<Real>(p, span, nseg, w0, y, st, p->use_pdl, true)) return rc;
     p->launches += 3;
   }
   return NF_OK;
@@ -3041,7 +3062,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   {
     // bound the forward partial buffer to ~512 MB
     long long ch = (512LL << 20) / ((long long)p->fwd_gridx * 2 * rs);
-    ch = std::max<long long>(ch, 1024);
+    ch = std::max<long long>(ch, 1024) / 256 * 256;  // windows start at multiples of 256 channels (peer all-reduce)
     ch = std::min<long long>(ch, max_batch);
     p->fwd_chunk = (int)ch;
     // bound the adjoint chunk partials to ~256 MB
@@ -3225,7 +3246,7 @@ int nf_comm_create(nf_plan* p, int rank, int world, void* handle_out) {
   p->comm_world = world;
   p->comm_rank = rank;
   p->comm_cap = p->max_batch;
-  p->comm_nblk = (p->max_batch + 255) / 256 + 256;  // blocks of all windows of one forward
+  p->comm_nblk = (p->max_batch + 255) / 256;  // one flag/epoch slot per 256 channels of the batch
   const size_t bytes = comm_recv_bytes(p) + (size_t)world * p->comm_nblk * sizeof(unsigned long long);
   CUDA_TRY(cudaMalloc(&p->comm_buf, bytes));
   CUDA_TRY(cudaMemset(p->comm_buf, 0, bytes));
@@ -3261,9 +3282,22 @@ int nf_forward_allreduce(nf_plan* p, const void* s, void* y, void* stream) {
   if (!p || !s || !y) return fail(NF_ERR_ARG, "null argument");
   if (!p->comm_connected) return fail(NF_ERR_STATE, "peer all-reduce not connected (nf_comm_create/nf_comm_connect)");
   p->comm_active = true;
-  p->comm_blk = 0;
-  const int rc = nf_forward(p, s, y, stream);
+  p->comm_fused = false;
+  int rc = nf_forward(p, s, y, stream);
   p->comm_active = false;
+  if (rc == NF_OK && !p->comm_fused) {  // structured batches: one-shot peer all-reduce of the finished y
+    const int nblk = (p->B + 255) / 256;
+    const PeerArgs pa = peer_args(p, 0, nullptr, y);
+    cudaError_t e = p->dtype == NF_C64
+                        ? launch_k(false, fwd_reduce2_peer_kernel<float, true>, dim3(nblk, 1), dim3(256), 0,
+                                   (cudaStream_t)stream, pa, p->B, 0, 0, (const int*)nullptr, (const int*)nullptr,
+                                   (const double*)nullptr)
+                        : launch_k(false, fwd_reduce2_peer_kernel<double, true>, dim3(nblk, 1), dim3(256), 0,
+                                   (cudaStream_t)stream, pa, p->B, 0, 0, (const int*)nullptr, (const int*)nullptr,
+                                   (const double*)nullptr);
+    if (e != cudaSuccess) return fail(NF_ERR_CUDA, std::string("peer all-reduce: ") + cudaGetErrorString(e));
+    p->launches += 1;
+  }
   return rc;
 }
 
@@ -3278,7 +3312,7 @@ int nf_comm_status(nf_plan* p, int* timed_out) {
 int nf_comm_emulate(int dtype, int world, int span, int nseg, int epochs, const double* tmp_host,
                     const int* sf_host, const int* spos_host, const double* pulse_host, int n_f, double* y_host) {
   if (!tmp_host || !sf_host || !spos_host || !pulse_host || !y_host) return fail(NF_ERR_ARG, "null argument");
-  if (world < 1 || world > PEER_MAX || span < 1 || nseg < 1 || epochs < 1 || n_f < 1)
+  if (world < 1 || world > PEER_MAX || span < 1 || nseg < 0 || epochs < 1 || n_f < 1)
     return fail(NF_ERR_ARG, "bad sizes");
   if (dtype != NF_C64 && dtype != NF_C128) return fail(NF_ERR_ARG, "dtype must be NF_C64 or NF_C128");
   const int nblk = (span + 255) / 256;
@@ -3302,7 +3336,7 @@ int nf_comm_emulate(int dtype, int world, int span, int nseg, int epochs, const 
   int *sf = (int*)dmal(span * sizeof(int)), *sp = (int*)dmal(span * sizeof(int));
   double* pulse = (double*)dmal(2 * n_f * sizeof(double));
   pa.err = (int*)dmal(sizeof(int));
-  std::vector<double> tmpd((size_t)nseg * span * 2);
+  std::vector<double> tmpd((size_t)std::max(nseg, 1) * span * 2);
   for (int q = 0; q < world && rc == NF_OK; ++q) {
     char* b = (char*)dmal(recv_b + flag_b);
     pa.tmp[q] = (const double2*)dmal(tmpd.size() * sizeof(double));
@@ -3320,9 +3354,20 @@ int nf_comm_emulate(int dtype, int world, int span, int nseg, int epochs, const 
   }
   std::vector<char> yh(2 * span * rs);
   for (int ep = 0; ep < epochs && rc == NF_OK; ++ep) {
-    for (int q = 0; q < world; ++q)
-      cudaMemcpy((void*)pa.tmp[q], tmp_host + ((size_t)ep * world + q) * nseg * span * 2,
-                 (size_t)nseg * span * 2 * sizeof(double), cudaMemcpyHostToDevice);
+    for (int q = 0; q < world; ++q) {
+      const double* src = tmp_host + ((size_t)ep * world + q) * std::max(nseg, 1) * span * 2;
+      if (nseg > 0) {
+        cudaMemcpy((void*)pa.tmp[q], src, (size_t)nseg * span * 2 * sizeof(double), cudaMemcpyHostToDevice);
+      } else {  // nseg = 0: the input is y itself (the one-shot all-reduce of a finished y)
+        for (int i = 0; i < 2 * span; ++i) {
+          if (dtype == NF_C64)
+            ((float*)yh.data())[i] = (float)src[i];
+          else
+            ((double*)yh.data())[i] = src[i];
+        }
+        cudaMemcpy(pa.y[q], yh.data(), yh.size(), cudaMemcpyHostToDevice);
+      }
+    }
     // one cooperative launch holds every emulated rank's blocks, so all of them are co-resident
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblk, world);
@@ -3332,11 +3377,17 @@ int nf_comm_emulate(int dtype, int world, int span, int nseg, int epochs, const 
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = dtype == NF_C64
-                        ? cudaLaunchKernelEx(&cfg, fwd_reduce2_peer_kernel<float>, pa, span, nseg, 0, (const int*)sf,
-                                             (const int*)sp, (const double*)pulse)
-                        : cudaLaunchKernelEx(&cfg, fwd_reduce2_peer_kernel<double>, pa, span, nseg, 0, (const int*)sf,
-                                             (const int*)sp, (const double*)pulse);
+    cudaError_t e;
+    if (nseg > 0)
+      e = dtype == NF_C64 ? cudaLaunchKernelEx(&cfg, fwd_reduce2_peer_kernel<float, false>, pa, span, nseg, 0,
+                                               (const int*)sf, (const int*)sp, (const double*)pulse)
+                          : cudaLaunchKernelEx(&cfg, fwd_reduce2_peer_kernel<double, false>, pa, span, nseg, 0,
+                                               (const int*)sf, (const int*)sp, (const double*)pulse);
+    else
+      e = dtype == NF_C64 ? cudaLaunchKernelEx(&cfg, fwd_reduce2_peer_kernel<float, true>, pa, span, 0, 0,
+                                               (const int*)sf, (const int*)sp, (const double*)pulse)
+                          : cudaLaunchKernelEx(&cfg, fwd_reduce2_peer_kernel<double, true>, pa, span, 0, 0,
+                                               (const int*)sf, (const int*)sp, (const double*)pulse);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       rc = fail(NF_ERR_CUDA, std::string("peer emulation: ") + cudaGetErrorString(e));

@@ -26,7 +26,7 @@ def _emulate(dtype: int, world: int, span: int, nseg: int, epochs: int, seed: in
     lib = _lib.load()
     rng = np.random.default_rng(seed)
     n_f = 7
-    tmp = rng.standard_normal((epochs, world, nseg, span, 2))
+    tmp = rng.standard_normal((epochs, world, max(nseg, 1), span, 2))
     sf = rng.integers(0, n_f, span).astype(np.int32)
     spos = rng.permutation(span).astype(np.int32)
     pulse = rng.standard_normal((n_f, 2))
@@ -36,6 +36,12 @@ def _emulate(dtype: int, world: int, span: int, nseg: int, epochs: int, seed: in
     rc = lib.nf_comm_emulate(dtype, world, span, nseg, epochs, tmp.ctypes.data_as(dp), sf.ctypes.data_as(ip),
                              spos.ctypes.data_as(ip), pulse.ctypes.data_as(dp), n_f, y.ctypes.data_as(dp))
     _lib.check(rc, "nf_comm_emulate")
+    if nseg == 0:  # one-shot variant: each rank's input is its finished y (as stored in Real)
+        yin = tmp[:, :, 0].astype(np.float32 if dtype == _lib.NF_C64 else np.float64).astype(np.float64)
+        tot = np.zeros((epochs, span, 2))
+        for q in range(world):
+            tot += yin[:, q]
+        return y[..., 0] + 1j * y[..., 1], tot[..., 0] + 1j * tot[..., 1]
     # expected: per rank, segments summed in order; then ranks summed in order; times p_f/(4π)
     part = np.zeros((epochs, world, span, 2))
     for s in range(nseg):
@@ -71,6 +77,18 @@ def test_emulated_ranks_c64_many_epochs():
         assert np.array_equal(got[:, q], got[:, 0])
     err = np.linalg.norm(got[:, 0] - exp) / np.linalg.norm(exp)
     assert err <= 1e-7, err
+
+
+@pytest.mark.parametrize("world", [2, 5])
+def test_emulated_ranks_one_shot(world):
+    from paper_2509_00774_b200 import _lib
+
+    for dt, tol in ((_lib.NF_C128, 1e-15), (_lib.NF_C64, 1e-7)):
+        got, exp = _emulate(dt, world, span=777, nseg=0, epochs=4, seed=world)
+        for q in range(world):
+            assert np.array_equal(got[:, q], got[:, 0])
+        err = np.linalg.norm(got[:, 0] - exp) / np.linalg.norm(exp)
+        assert err <= tol, (dt, err)
 
 
 def _free_port() -> int:
@@ -137,3 +155,24 @@ def test_spgm_engine_peer_world1_matches_unsharded():
         assert e2.magnitude_change() == e1.magnitude_change()
     finally:
         dist.destroy_process_group()
+
+
+def test_forward_allreduce_world1_multiwindow_flat():
+    """Large, a flat batch of 40,000 channels: three forward windows (16,384-channel partial buffer),
+    each fused with the peer all-reduce at its 256-aligned channel offset."""
+    from paper_2509_00774_b200 import configs
+    from paper_2509_00774_b200.plan import DevicePlan
+
+    scn = configs.WORKLOADS["large"]().scenario
+    plan = DevicePlan(scn, dtype="c64", device="cuda:0", max_batch=40000, structured="never")
+    plan.comm_connect([plan.comm_create(0, 1)])
+    rng = np.random.default_rng(9)
+    s = plan._as_dev(rng.standard_normal(scn.n_voxels) + 1j * rng.standard_normal(scn.n_voxels), scn.n_voxels, "s")
+    idx = np.sort(rng.choice(scn.n_channels, 40000, replace=False))
+    plan.prepare(torch.from_numpy(idx.astype(np.int32)).cuda())
+    for _ in range(2):
+        a = plan.forward(s)
+        b = plan.forward_allreduce(s)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+    assert not plan.comm_timed_out()
