@@ -806,6 +806,28 @@ __device__ __forceinline__ void unit_coords(int unit, int ntiles, int C, int ord
     tile = unit - chunk * ntiles;
   }
 }
+// Units of a launch: chunk-major (order 1) as unit_coords, or tile-major with a split tail: tiles [0, t1)
+// in C chunks, tiles [t1, ntiles) in C2 (shorter) chunks, so the last wave of the launch is made of short
+// units while every tile's chunks stay adjacent (table rows reused from L2). Ct = chunk count of the tile.
+__device__ __forceinline__ void unit_map(int unit, int ntiles, int C, int t1, int C2, int order, int& tile, int& chunk,
+                                         int& Ct) {
+  if (order != 0) {
+    unit_coords(unit, ntiles, C, order, tile, chunk);
+    Ct = C;
+    return;
+  }
+  const int u1 = t1 * C;
+  if (unit < u1) {
+    tile = unit / C;
+    chunk = unit - tile * C;
+    Ct = C;
+  } else {
+    const int k = (unit - u1) / C2;
+    tile = t1 + k;
+    chunk = unit - u1 - k * C2;
+    Ct = C2;
+  }
+}
 
 template <typename Real>
 struct AdjArgs {
@@ -816,6 +838,7 @@ struct AdjArgs {
   const R2<Real>* __restrict__ wrec;
   int B, CH;
   int order;                 // unit order: 0 tile-major, equal chunks; 1 chunk-major, tapered (chunk_bound)
+  int t1, CH2;               // tile-major tail: tiles [t1, ntiles) in CH2 chunks (unit_map; t1 = ntiles: none)
   Real* __restrict__ gpart;  // [CH][ntiles][32][4] complex (CH > 1)
   int* __restrict__ cnt;     // [ntiles] arrival counters (zero between launches)
   // plain adjoint
@@ -870,7 +893,7 @@ __global__ void __launch_bounds__(256) resid_kernel(const int* __restrict__ sm, 
 // partial; the last of the tile's CH warps sums the partials in chunk order and writes
 // g (plain adjoint) or applies the prox and the termination statistics (SPGM step).
 template <typename Real, bool PROX>
-__device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, int chunk, int L, const QV<Real>& gr,
+__device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, int chunk, int C, int L, const QV<Real>& gr,
                                              const QV<Real>& gi) {
   const Geo& g = a.g;
   Real Gr[V], Gi[V];
@@ -879,7 +902,7 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
     Gr[v] = get(gr, v);
     Gi[v] = get(gi, v);
   }
-  if (a.CH > 1) {
+  if (C > 1) {
     // publish this chunk's partial; the last of the CH warps of this tile combines in chunk order
     Real* mine = a.gpart + (((size_t)chunk * g.ntiles + tile) * 32 + L) * (2 * V);
 #pragma unroll
@@ -889,13 +912,13 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
     }
     __threadfence();
     int last = 0;
-    if (L == 0) last = atomicAdd(a.cnt + tile, 1) == a.CH - 1;
+    if (L == 0) last = atomicAdd(a.cnt + tile, 1) == C - 1;
     last = __shfl_sync(FULL, last, 0);
     if (!last) return;
     __threadfence();
 #pragma unroll
     for (int v = 0; v < V; ++v) Gr[v] = Gi[v] = 0;
-    for (int ch = 0; ch < a.CH; ++ch) {
+    for (int ch = 0; ch < C; ++ch) {
       const Real* q = a.gpart + (((size_t)ch * g.ntiles + tile) * 32 + L) * (2 * V);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -959,12 +982,12 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
   const int unit = blockIdx.x * ADJ_WARPS + w;
-  if (unit >= g.ntiles * a.CH) return;  // warps are independent: no block barriers below
-  int tile, chunk;
-  unit_coords(unit, g.ntiles, a.CH, a.order, tile, chunk);
+  if (unit >= a.t1 * a.CH + (g.ntiles - a.t1) * a.CH2) return;  // warps are independent: no block barriers below
+  int tile, chunk, C;
+  unit_map(unit, g.ntiles, a.CH, a.t1, a.CH2, a.order, tile, chunk, C);
   const WarpSmem<Real> ws = carve<Real>(smem_raw + (size_t)w * warp_smem_bytes<Real>(g.Tg, g.A), g.Tg, g.A);
-  const int j0 = chunk_bound(a.B, chunk, a.CH, a.order);
-  const int j1 = chunk_bound(a.B, chunk + 1, a.CH, a.order);
+  const int j0 = chunk_bound(a.B, chunk, C, a.order);
+  const int j1 = chunk_bound(a.B, chunk + 1, C, a.order);
   ChanRec nxt;  // start-up loads issued together: first channel records, then the D0 row
   R2<Real> nxtw;
   prefetch_first<Real>(a.crec, a.wrec, j0, j1, L, nxt, nxtw);
@@ -1019,7 +1042,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   flush(iR, hr, hi, gr, gi);
   stage_wait();
 
-  adj_epilogue<Real, PROX>(a, tile, chunk, L, gr, gi);
+  adj_epilogue<Real, PROX>(a, tile, chunk, C, L, gr, gi);
 }
 
 // stats = {Σ_tile part[.][0], Σ part[.][1], ½ Σ_block dpart, Σ part[.][3]} in a fixed order
@@ -1058,6 +1081,7 @@ struct FwdArgs {
   int w0, w1;                  // sorted positions of this launch window
   int Q;                       // channel splits per tile
   int order;                   // unit order, as AdjArgs::order
+  int t1, Q2;                  // tile-major tail, as AdjArgs::t1/CH2
   Real* __restrict__ part;     // [gridDim.x][w1-w0] complex
 };
 
@@ -1112,17 +1136,17 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
   const int unit = blockIdx.x * FWD_WARPS + w;
-  if (unit >= g.ntiles * a.Q) return;  // warps are independent: no block barriers
-  int tile, chunk;
-  unit_coords(unit, g.ntiles, a.Q, a.order, tile, chunk);
+  if (unit >= a.t1 * a.Q + (g.ntiles - a.t1) * a.Q2) return;  // warps are independent: no block barriers
+  int tile, chunk, C;
+  unit_map(unit, g.ntiles, a.Q, a.t1, a.Q2, a.order, tile, chunk, C);
   unsigned char* wbase = smem_raw + (size_t)w * fwd_warp_bytes<Real>(g.Tg, g.A);
   const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A, 1);
   R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A, 1));  // [TBR][33]
 
   // start-up loads issued together: first channel records, the lane's s values, the D0 row
   const int span = a.w1 - a.w0;
-  const int c0 = a.w0 + chunk_bound(span, chunk, a.Q, a.order);
-  const int c1 = a.w0 + chunk_bound(span, chunk + 1, a.Q, a.order);
+  const int c0 = a.w0 + chunk_bound(span, chunk, C, a.order);
+  const int c1 = a.w0 + chunk_bound(span, chunk + 1, C, a.order);
   R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * span - a.w0;
   ChanRec nxt;
   R2<Real> nxtw;
@@ -1531,7 +1555,7 @@ __global__ void __launch_bounds__(SW * 32, NFGPU_MINB_STRUCT) adj_struct_kernel(
       Gi[v] += q[2 * v + 1];
     }
   }
-  adj_epilogue<Real, PROX>(a, tile, chunk, L, make_v(Gr), make_v(Gi));
+  adj_epilogue<Real, PROX>(a, tile, chunk, a.CH, L, make_v(Gr), make_v(Gi));
 }
 
 // Structured forward: y_ftr = p_f/(4π) Σ_n U_ft(n)·(V_fr(n) s_n). The block stages W_fr = V_fr·s;
@@ -2041,7 +2065,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
           Gi[v] = cb[p * 2 + 1] + cb[(128 + p) * 2 + 1];
         }
       }
-      adj_epilogue<float, PROX>(a, tile, hb * fch + fc, L, make_v(Gr), make_v(Gi));
+      adj_epilogue<float, PROX>(a, tile, hb * fch + fc, a.CH, L, make_v(Gr), make_v(Gi));
     }
   }
   tc_fence_before();
@@ -2572,6 +2596,9 @@ struct nf_plan {
   long long struct_target = 148LL * 3 * 4;  // blocks per structured launch (env NFGPU_STRUCT_TARGET)
   int min_chunk = 64;                       // fewest channels per flat forward unit (env NFGPU_MIN_CHUNK)
   int chunk_order = 0;                      // flat work-unit order (unit_coords / chunk_bound)
+  bool tail_split = true;                   // tile-major launches end on shorter units (unit_map; env NFGPU_TAIL=0)
+  int tail_factor = 4;                      // ... tail_factor x more chunks per tail tile (env NFGPU_TAIL_FACTOR)
+  double tail_waves = 1.0;                  // ... for about this many waves of warp slots (env NFGPU_TAIL_WAVES)
   int adj_min_chunk = 128;                  // ... per flat adjoint unit: its chunk combine favours fewer, longer
                                             // chunks (Medium |B| = 512: 80.9 -> 72.7 us; env NFGPU_ADJ_MIN_CHUNK)
   size_t dev_bytes = 0;
@@ -2685,6 +2712,20 @@ int unit_order(const nf_plan* p, long long units) {
   return p->chunk_order && units >= 2LL * 148 * 16 ? 1 : 0;
 }
 
+// Tile-major split tail (unit_map): the last tiles take 4x as many (so 4x shorter) chunks, enough of them for
+// about one wave of warp slots, so the launch does not end on a wave of long units. cmax bounds the chunk count.
+void tail_split(const nf_plan* p, int order, int C, long long cmax, int& t1, int& C2) {
+  t1 = p->g.ntiles;
+  C2 = C;
+  if (order != 0 || !p->tail_split) return;
+  const long long c2 = std::min<long long>((long long)p->tail_factor * C, cmax);
+  if (c2 <= C) return;
+  const long long slots = (long long)(148.0 * 16 * p->tail_waves);
+  const long long ntail = std::min<long long>(p->g.ntiles, (slots + c2 - 1) / c2);
+  t1 = p->g.ntiles - (int)ntail;
+  C2 = (int)c2;
+}
+
 int channel_splits(const nf_plan* p, int span) {
   // enough (tile, chunk) warp units for the target number of units; >= 64 channels per chunk
   const long long target = p->fwd_target;
@@ -2759,8 +2800,9 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.w1 = w1;
     a.Q = channel_splits(p, span);
     a.part = (Real*)p->d_part;
-    const long long units = (long long)p->g.ntiles * a.Q;
-    a.order = unit_order(p, units);
+    a.order = unit_order(p, (long long)p->g.ntiles * a.Q);
+    tail_split(p, a.order, a.Q, std::max(1, span / p->min_chunk), a.t1, a.Q2);
+    const long long units = (long long)a.t1 * a.Q + (long long)(p->g.ntiles - a.t1) * a.Q2;
     CUDA_TRY(launch_k(p->use_pdl, kern, dim3((unsigned)((units + FWD_WARPS - 1) / FWD_WARPS)), dim3(FWD_WARPS * 32),
                       sm, st, a));
     // two-level reduce: ~sqrt(rows) segments so both levels have short serial sums
@@ -2833,6 +2875,8 @@ int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.w1 = (int)(fb * per_f);
     a.Q = 1;
     a.order = 0;
+    a.t1 = p->g.ntiles;
+    a.Q2 = 1;
     a.part = nullptr;
     const int span = a.w1 - a.w0;
     // one CTA per SM, two per tile: split the window's frequencies for at least two waves
@@ -2886,6 +2930,8 @@ int launch_forward_struct(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     const int span = a.w1 - a.w0;
     a.Q = struct_splits(p->struct_target, p->g.ntiles, ub - ua);
     a.order = 0;
+    a.t1 = p->g.ntiles;
+    a.Q2 = a.Q;
     a.part = (Real*)p->d_part;
     kern<<<(unsigned)((long long)p->g.ntiles * a.Q), SW * 32, sm, st>>>(a, sa, p->d_kd);
     CUDA_TRY(cudaGetLastError());
@@ -2915,6 +2961,10 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   a.B = p->B;
   a.CH = adjoint_chunks(p);
   a.order = p->structured ? 0 : unit_order(p, (long long)p->g.ntiles * a.CH);
+  a.t1 = p->g.ntiles;
+  a.CH2 = a.CH;
+  if (!p->structured)
+    tail_split(p, a.order, a.CH, std::min<long long>(std::max(1, p->B / p->adj_min_chunk), p->adj_ch_cap), a.t1, a.CH2);
   a.gpart = (Real*)p->d_gpart;
   a.cnt = p->d_tilecnt;
   a.gout = (Real*)gout;
@@ -2967,7 +3017,7 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CUDA_TRY(
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-    const int units = p->g.ntiles * a.CH;
+    const int units = a.t1 * a.CH + (p->g.ntiles - a.t1) * a.CH2;
     CUDA_TRY(launch_k(p->use_pdl, kern, dim3((units + ADJ_WARPS - 1) / ADJ_WARPS), dim3(ADJ_WARPS * 32), sm, st, a));
   }
   CUDA_TRY(cudaGetLastError());
@@ -3054,6 +3104,9 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   // per forward for +0.9%). Tile-major equal chunks above NFGPU_L2_TABLE_MB; env NFGPU_CHUNK_ORDER.
   p->chunk_order = rs * (size_t)g.ntiles * g.A * TABW <= ((size_t)NFGPU_L2_TABLE_MB << 20) ? 1 : 0;
   if (const char* e = std::getenv("NFGPU_CHUNK_ORDER")) p->chunk_order = std::atoi(e) ? 1 : 0;
+  if (const char* e = std::getenv("NFGPU_TAIL")) p->tail_split = std::atoi(e) != 0;
+  if (const char* e = std::getenv("NFGPU_TAIL_FACTOR")) p->tail_factor = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("NFGPU_TAIL_WAVES")) p->tail_waves = std::max(0.0, std::atof(e));
   // adjoint units: ~3.2 waves with chunk-major order (tools/sweep: 1/8 Large slab 15 chunks 0.327 ms vs
   // 10 chunks 0.351 ms, 1/4 slab 8 chunks 0.610 vs 5 chunks 0.644), four with tile-major (its chunk
   // combine favours fewer units; the tile-major full problem prefers three chunks per tile)
