@@ -788,12 +788,12 @@ __device__ __forceinline__ void prefetch_first(const ChanRec* __restrict__ crec,
 
 // ------------------------------------------------------------------ adjoint (+prox)
 // Boundary c of C channel chunks over n channels. order 0: equal chunks. order 1: sizes fall
-// linearly to 1/4 of the first, g(x) = (x − 0.375x²)/0.625 (monotone, g(1) = 1), so that with
-// chunk-major unit order the last wave of a launch is made of the smallest chunks (short tail).
-__device__ __forceinline__ int chunk_bound(int n, int c, int C, int order) {
+// linearly, g(x) = (x − h·x²)/(1 − h) (monotone for h < ½, g(1) = 1; the last chunk is 1 − 2h of the
+// first), so that with chunk-major unit order the last wave of a launch is made of the smallest chunks.
+__device__ __forceinline__ int chunk_bound(int n, int c, int C, int order, float h) {
   if (order == 0 || c >= C) return (int)(((long long)n * c) / C);
   const double x = (double)c / C;
-  return (int)((double)n * ((x - 0.375 * x * x) / 0.625));
+  return (int)((double)n * ((x - h * x * x) / (1.0 - h)));
 }
 // (tile, chunk) of a warp work unit: tile-major (a tile's chunks adjacent, sharing its table rows
 // in L2) or chunk-major (tables that stay in L2: with tapered chunks the launch ends on short units)
@@ -839,6 +839,7 @@ struct AdjArgs {
   int B, CH;
   int order;                 // unit order: 0 tile-major, equal chunks; 1 chunk-major, tapered (chunk_bound)
   int t1, CH2;               // tile-major tail: tiles [t1, ntiles) in CH2 chunks (unit_map; t1 = ntiles: none)
+  float taper;               // chunk-major taper coefficient h (chunk_bound)
   Real* __restrict__ gpart;  // [CH][ntiles][32][4] complex (CH > 1)
   int* __restrict__ cnt;     // [ntiles] arrival counters (zero between launches)
   // plain adjoint
@@ -977,7 +978,6 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
 
 template <typename Real, bool PROX, bool EXACT>
 __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(AdjArgs<Real> a) {
-  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
@@ -986,13 +986,18 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   int tile, chunk, C;
   unit_map(unit, g.ntiles, a.CH, a.t1, a.CH2, a.order, tile, chunk, C);
   const WarpSmem<Real> ws = carve<Real>(smem_raw + (size_t)w * warp_smem_bytes<Real>(g.Tg, g.A), g.Tg, g.A);
-  const int j0 = chunk_bound(a.B, chunk, C, a.order);
-  const int j1 = chunk_bound(a.B, chunk + 1, C, a.order);
-  ChanRec nxt;  // start-up loads issued together: first channel records, then the D0 row
+  const int j0 = chunk_bound(a.B, chunk, C, a.order, a.taper);
+  const int j1 = chunk_bound(a.B, chunk + 1, C, a.order, a.taper);
+  // Start-up loads that do not depend on the predecessor kernel are issued before griddepcontrol.wait:
+  // the D0 row (plan data) and the channel records (written by nf_batch_prepare, whose kernels completed
+  // before the residual kernel, our predecessor, released us). The residual records w come after the wait.
+  ChanRec nxt;
   R2<Real> nxtw;
-  prefetch_first<Real>(a.crec, a.wrec, j0, j1, L, nxt, nxtw);
+  prefetch_first<Real>(a.crec, nullptr, j0, j1, L, nxt, nxtw);
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
+  pdl_wait();
+  if (j0 + L < j1) nxtw = a.wrec[j0 + L];
   __syncwarp();
   const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
   const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
@@ -1082,6 +1087,7 @@ struct FwdArgs {
   int Q;                       // channel splits per tile
   int order;                   // unit order, as AdjArgs::order
   int t1, Q2;                  // tile-major tail, as AdjArgs::t1/CH2
+  float taper;                 // as AdjArgs::taper
   Real* __restrict__ part;     // [gridDim.x][w1-w0] complex
 };
 
@@ -1131,7 +1137,6 @@ __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __re
 // together and share the tile's table rows in L2.
 template <typename Real, bool EXACT>
 __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(FwdArgs<Real> a) {
-  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
@@ -1143,14 +1148,15 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A, 1);
   R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A, 1));  // [TBR][33]
 
-  // start-up loads issued together: first channel records, the lane's s values, the D0 row
+  // Start-up loads: the lane's s values and the D0 row do not depend on the predecessor kernel (the
+  // last of nf_batch_prepare's kernels, which waited for everything before it), so they are issued
+  // before griddepcontrol.wait; the channel records it writes come after.
   const int span = a.w1 - a.w0;
-  const int c0 = a.w0 + chunk_bound(span, chunk, C, a.order);
-  const int c1 = a.w0 + chunk_bound(span, chunk + 1, C, a.order);
+  const int c0 = a.w0 + chunk_bound(span, chunk, C, a.order, a.taper);
+  const int c1 = a.w0 + chunk_bound(span, chunk + 1, C, a.order, a.taper);
   R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * span - a.w0;
   ChanRec nxt;
   R2<Real> nxtw;
-  prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
   int tx, ty, tz;
   tile_coords(g, tile, tx, ty, tz);
   int x0, y, z;
@@ -1166,6 +1172,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   }
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
+  pdl_wait();
+  prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
   const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
   const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
   const QV<Real> sr = make_v(srv), si = make_v(siv);
@@ -2599,6 +2607,8 @@ struct nf_plan {
   bool tail_split = true;                   // tile-major launches end on shorter units (unit_map; env NFGPU_TAIL=0)
   int tail_factor = 4;                      // ... tail_factor x more chunks per tail tile (env NFGPU_TAIL_FACTOR)
   double tail_waves = 1.0;                  // ... for about this many waves of warp slots (env NFGPU_TAIL_WAVES)
+  double taper = 0.375;                     // chunk-major adjoint taper h: last chunk 1 − 2h of the first (env NFGPU_TAPER)
+  double fwd_taper = 0.475;                 // ... forward (1/8 Large slab 0.3552 -> 0.3516 ms; env NFGPU_FWD_TAPER)
   int adj_min_chunk = 128;                  // ... per flat adjoint unit: its chunk combine favours fewer, longer
                                             // chunks (Medium |B| = 512: 80.9 -> 72.7 us; env NFGPU_ADJ_MIN_CHUNK)
   size_t dev_bytes = 0;
@@ -2802,6 +2812,7 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.part = (Real*)p->d_part;
     a.order = unit_order(p, (long long)p->g.ntiles * a.Q);
     tail_split(p, a.order, a.Q, std::max(1, span / p->min_chunk), a.t1, a.Q2);
+    a.taper = (float)p->fwd_taper;
     const long long units = (long long)a.t1 * a.Q + (long long)(p->g.ntiles - a.t1) * a.Q2;
     CUDA_TRY(launch_k(p->use_pdl, kern, dim3((unsigned)((units + FWD_WARPS - 1) / FWD_WARPS)), dim3(FWD_WARPS * 32),
                       sm, st, a));
@@ -2877,6 +2888,7 @@ int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.order = 0;
     a.t1 = p->g.ntiles;
     a.Q2 = 1;
+    a.taper = 0;
     a.part = nullptr;
     const int span = a.w1 - a.w0;
     // one CTA per SM, two per tile: split the window's frequencies for at least two waves
@@ -2932,6 +2944,7 @@ int launch_forward_struct(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.order = 0;
     a.t1 = p->g.ntiles;
     a.Q2 = a.Q;
+    a.taper = 0;
     a.part = (Real*)p->d_part;
     kern<<<(unsigned)((long long)p->g.ntiles * a.Q), SW * 32, sm, st>>>(a, sa, p->d_kd);
     CUDA_TRY(cudaGetLastError());
@@ -2963,6 +2976,7 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   a.order = p->structured ? 0 : unit_order(p, (long long)p->g.ntiles * a.CH);
   a.t1 = p->g.ntiles;
   a.CH2 = a.CH;
+  a.taper = (float)p->taper;
   if (!p->structured)
     tail_split(p, a.order, a.CH, std::min<long long>(std::max(1, p->B / p->adj_min_chunk), p->adj_ch_cap), a.t1, a.CH2);
   a.gpart = (Real*)p->d_gpart;
@@ -3107,6 +3121,8 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   if (const char* e = std::getenv("NFGPU_TAIL")) p->tail_split = std::atoi(e) != 0;
   if (const char* e = std::getenv("NFGPU_TAIL_FACTOR")) p->tail_factor = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("NFGPU_TAIL_WAVES")) p->tail_waves = std::max(0.0, std::atof(e));
+  if (const char* e = std::getenv("NFGPU_TAPER")) p->taper = std::min(0.49, std::max(0.0, std::atof(e)));
+  if (const char* e = std::getenv("NFGPU_FWD_TAPER")) p->fwd_taper = std::min(0.49, std::max(0.0, std::atof(e)));
   // adjoint units: ~3.2 waves with chunk-major order (tools/sweep: 1/8 Large slab 15 chunks 0.327 ms vs
   // 10 chunks 0.351 ms, 1/4 slab 8 chunks 0.610 vs 5 chunks 0.644), four with tile-major (its chunk
   // combine favours fewer units; the tile-major full problem prefers three chunks per tile)
