@@ -904,12 +904,18 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
     Gi[v] = get(gi, v);
   }
   if (C > 1) {
-    // publish this chunk's partial; the last of the CH warps of this tile combines in chunk order
-    Real* mine = a.gpart + (((size_t)chunk * g.ntiles + tile) * 32 + L) * (2 * V);
+    // publish this chunk's partial (the lane's 2V Reals, interleaved re/im, as 16-byte stores); the last of
+    // the C warps of this tile combines in chunk order, four chunks' loads in flight at a time
+    using U16 = typename std::conditional<std::is_same<Real, float>::value, float4, double2>::type;
+    constexpr int NU = 2 * V * (int)sizeof(Real) / 16;
+    constexpr int PU = 16 / (int)sizeof(Real);  // Reals per U16
+    U16* mine = reinterpret_cast<U16*>(a.gpart + (((size_t)chunk * g.ntiles + tile) * 32 + L) * (2 * V));
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      mine[2 * v] = Gr[v];
-      mine[2 * v + 1] = Gi[v];
+    for (int u = 0; u < NU; ++u) {
+      Real t[PU];
+#pragma unroll
+      for (int k = 0; k < PU; ++k) t[k] = ((u * PU + k) & 1) ? Gi[(u * PU + k) >> 1] : Gr[(u * PU + k) >> 1];
+      mine[u] = *reinterpret_cast<const U16*>(t);
     }
     __threadfence();
     int last = 0;
@@ -919,12 +925,21 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
     __threadfence();
 #pragma unroll
     for (int v = 0; v < V; ++v) Gr[v] = Gi[v] = 0;
+#pragma unroll 4
     for (int ch = 0; ch < C; ++ch) {
-      const Real* q = a.gpart + (((size_t)ch * g.ntiles + tile) * 32 + L) * (2 * V);
+      const U16* q = reinterpret_cast<const U16*>(a.gpart + (((size_t)ch * g.ntiles + tile) * 32 + L) * (2 * V));
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        Gr[v] += __ldcg(q + 2 * v);
-        Gi[v] += __ldcg(q + 2 * v + 1);
+      for (int u = 0; u < NU; ++u) {
+        const U16 w = __ldcg(q + u);
+        const Real* t = reinterpret_cast<const Real*>(&w);
+#pragma unroll
+        for (int k = 0; k < PU; ++k) {
+          const int e = u * PU + k;
+          if (e & 1)
+            Gi[e >> 1] += t[k];
+          else
+            Gr[e >> 1] += t[k];
+        }
       }
     }
     if (L == 0) a.cnt[tile] = 0;
