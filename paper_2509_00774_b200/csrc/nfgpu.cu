@@ -3101,7 +3101,14 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   g.nty = (g.ny + TILE_Y - 1) / TILE_Y;
   g.ntz = (g.nzs + TILE_Z - 1) / TILE_Z;
   g.ntiles = g.ntx * g.nty * g.ntz;
-  g.ng = (n_tx + TG_MAX - 1) / TG_MAX;
+  // tx-group size: c128 rows are twice as wide, so 2-transmitter groups keep 12 warps per SM instead of 8
+  // (Large c128 step 240 -> 280 Gentry/s, 1/8 slab 228 -> 259; Medium 189 -> 182; env NFGPU_TG_C128)
+  int tg_max = TG_MAX;
+  if (dtype == NF_C128) {
+    tg_max = std::min(2, TG_MAX);
+    if (const char* e = std::getenv("NFGPU_TG_C128")) tg_max = std::max(1, std::min(TG_MAX, std::atoi(e)));
+  }
+  g.ng = (n_tx + tg_max - 1) / tg_max;
   g.Tg = (n_tx + g.ng - 1) / g.ng;
   for (int i = 0; i < 3; ++i) {
     g.corner[i] = corner[i];

@@ -22,13 +22,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="large")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--zslab", type=int, default=0, help="time one rank's slab: the first Z z-planes (0 = all)")
+ap.add_argument("--dtype", default=None, help="c64 or c128 (default: the workload's)")
 a = ap.parse_args()
 w = configs.WORKLOADS[a.workload]()
 scn = w.scenario
 rng = np.random.default_rng(0)
 y = (rng.standard_normal(scn.n_channels) + 1j * rng.standard_normal(scn.n_channels)).astype(np.complex64)
 zr = (0, a.zslab) if a.zslab else None
-plan = DevicePlan(scn, dtype=w.dtype, device="cuda:0", max_batch=w.batch, z_range=zr)
+plan = DevicePlan(scn, dtype=a.dtype or w.dtype, device="cuda:0", max_batch=w.batch, z_range=zr)
 s0 = configs.make_scene(w)[plan.vox_offset:plan.vox_offset + plan.n_local]
 eng = SPGMEngine(plan, y, eta=1e-2, alpha=1e-6, initial=s0)
 st = torch.cuda.current_stream()
