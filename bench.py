@@ -354,7 +354,7 @@ def run_ours(args):
         if e2e is not None:
             out["e2e"] = e2e
         if world == 1 and not args.no_extras and args.workload == "large":
-            out["extra_workloads"] = {"medium": medium_line(args, dev),
+            out["extra_workloads"] = {"medium": medium_line(args, dev), "small": medium_line(args, dev, "small"),
                                       "large_structured": structured_line(eng, w)}
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args.workload, 30, args.cpu_seconds)
@@ -366,9 +366,10 @@ def run_ours(args):
     return 0
 
 
-def medium_line(args, dev):
-    """BASELINE config 1 (Medium, |B| = 512, c64) on the same GPU: entries/s and iterations/s."""
-    w, plan, eng, eta, alpha, setup_s = build_engine("medium", dev, 0, 1, None)
+def medium_line(args, dev, workload="medium"):
+    """BASELINE config 1 (Medium, |B| = 512, c64) -- or config 0 (Small, |B| = 32, c128) -- on the same GPU:
+    entries/s and iterations/s."""
+    w, plan, eng, eta, alpha, setup_s = build_engine(workload, dev, 0, 1, None)
     ms, per_step, steps = timed_steps(eng, plan, w, 200, 10, None, 0, not args.no_graph)
     N = w.scenario.n_voxels
     return {"value": 2.0 * w.batch * N / (ms / steps * 1e-3), "unit": UNIT, "ms_per_step": ms / steps,

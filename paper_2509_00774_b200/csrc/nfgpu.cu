@@ -2751,20 +2751,26 @@ void tail_split(const nf_plan* p, int order, int C, long long cmax, int& t1, int
   C2 = (int)c2;
 }
 
-int channel_splits(const nf_plan* p, int span) {
-  // enough (tile, chunk) warp units for the target number of units; >= 64 channels per chunk
-  const long long target = p->fwd_target;
+// Chunks per tile: enough (tile, chunk) warp units for the target, with at least min_chunk channels per
+// chunk -- unless that leaves less than a quarter wave of units (tiny problems such as BASELINE Small: 8 tiles,
+// 32 channels), where chunks go down to SMALL_CHUNK channels to put more warps on the latency-bound work.
+#ifndef NFGPU_SMALL_CHUNK
+#define NFGPU_SMALL_CHUNK 4
+#endif
+constexpr int SMALL_CHUNK = NFGPU_SMALL_CHUNK;
+long long chunks_for(const nf_plan* p, long long target, int n, int min_chunk) {
+  const long long slots = 148LL * 16;
   long long q = (target + p->g.ntiles - 1) / p->g.ntiles;
-  q = std::min<long long>(q, std::max(1, span / p->min_chunk));
-  return (int)std::max(1LL, q);
+  long long cap = std::max(1, n / min_chunk);
+  if ((long long)p->g.ntiles * cap < slots / 4)
+    cap = std::min<long long>((slots + p->g.ntiles - 1) / p->g.ntiles, std::max(1, n / SMALL_CHUNK));
+  return std::max(1LL, std::min(q, cap));
 }
 
+int channel_splits(const nf_plan* p, int span) { return (int)chunks_for(p, p->fwd_target, span, p->min_chunk); }
+
 int adjoint_chunks(const nf_plan* p) {
-  // enough (tile, chunk) units for the target number of units; at least 64 channels per chunk
-  long long ch = (p->adj_target + p->g.ntiles - 1) / p->g.ntiles;
-  ch = std::min<long long>(ch, std::max(1, p->B / p->adj_min_chunk));
-  ch = std::min<long long>(ch, p->adj_ch_cap);
-  return (int)std::max(1LL, ch);
+  return (int)std::min<long long>(chunks_for(p, p->adj_target, p->B, p->adj_min_chunk), p->adj_ch_cap);
 }
 
 size_t comm_recv_bytes(const nf_plan* p) { return (size_t)2 * p->comm_world * p->comm_cap * sizeof(double2); }
