@@ -327,6 +327,20 @@ class SPGMEngine:
         self.ybuf = torch.empty(plan.max_batch, dtype=plan.torch_dtype, device=dev)
         self.stats = torch.zeros(4, dtype=torch.float64, device=dev)
         self.idx_dev = torch.empty(plan.max_batch, dtype=torch.int32, device=dev)
+        # two persistent pinned staging buffers for host index lists (no per-call pinned allocation); a buffer is
+        # reused only after the event recorded behind its last H2D copy has completed
+        self._pinned = [None, None]
+        self._pinned_ev = [None, None]
+        self._pinned_next = 0
+
+    def _pinned_idx(self, n: int) -> tuple[torch.Tensor, int]:
+        k = self._pinned_next
+        self._pinned_next ^= 1
+        if self._pinned_ev[k] is not None:
+            self._pinned_ev[k].synchronize()
+        if self._pinned[k] is None or self._pinned[k].numel() < n:
+            self._pinned[k] = torch.empty(max(n, self.plan.max_batch), dtype=torch.int32).pin_memory()
+        return self._pinned[k][:n], k
 
     def stage(self, idx) -> int:
         """Stage a host (numpy) or device index list; returns B."""
@@ -335,10 +349,14 @@ class SPGMEngine:
         elif self.plan.try_structured(np.asarray(idx)):
             return self.plan.B
         else:
-            t = torch.from_numpy(np.ascontiguousarray(np.asarray(idx, dtype=np.int32)))
-            t = t.pin_memory() if not t.is_pinned() else t
-            B = t.numel()
-            self.idx_dev[:B].copy_(t, non_blocking=True)
+            arr = np.asarray(idx)
+            B = int(arr.size)
+            buf, k = self._pinned_idx(B)
+            buf.numpy()[:] = arr.reshape(-1)  # int32 cast on the copy
+            self.idx_dev[:B].copy_(buf, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.plan.device))
+            self._pinned_ev[k] = ev
             t = self.idx_dev[:B]
         self.plan.prepare(t)
         return int(t.numel())
