@@ -3135,7 +3135,6 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     p->phase_bound_rev = 0.5 + fmax / c * 2.0 * std::sqrt(hx * hx + hy * hy + hz * hz);
     p->exact = dtype != NF_C64 || p->phase_bound_rev > EXACT_FREE_REV || std::getenv("NFGPU_FORCE_EXACT");
   }
-  if (const char* e = std::getenv("NFGPU_FWD_TARGET")) p->fwd_target = std::max(1LL, std::atoll(e));
   if (const char* e = std::getenv("NFGPU_STRUCT_TARGET")) p->struct_target = std::max(1LL, std::atoll(e));
   if (const char* e = std::getenv("NFGPU_MIN_CHUNK")) p->min_chunk = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("NFGPU_ADJ_MIN_CHUNK")) p->adj_min_chunk = std::max(1, std::atoi(e));
@@ -3151,10 +3150,13 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   if (const char* e = std::getenv("NFGPU_TAIL_WAVES")) p->tail_waves = std::max(0.0, std::atof(e));
   if (const char* e = std::getenv("NFGPU_TAPER")) p->taper = std::min(0.49, std::max(0.0, std::atof(e)));
   if (const char* e = std::getenv("NFGPU_FWD_TAPER")) p->fwd_taper = std::min(0.49, std::max(0.0, std::atof(e)));
-  // adjoint units: ~3.2 waves with chunk-major order (tools/sweep: 1/8 Large slab 15 chunks 0.327 ms vs
-  // 10 chunks 0.351 ms, 1/4 slab 8 chunks 0.610 vs 5 chunks 0.644), four with tile-major (its chunk
-  // combine favours fewer units; the tile-major full problem prefers three chunks per tile)
-  p->adj_target = p->chunk_order ? 148LL * 16 * 16 / 5 : 148LL * 16 * 4;
+  // Warp units per launch. Chunk-major (L2-resident tables): forward four waves, adjoint ~3.2 waves (1/8 Large
+  // slab 15 chunks 0.327 ms vs 10 chunks 0.351 ms, 1/4 slab 8 chunks 0.610 vs 5 chunks 0.644). Tile-major:
+  // 12288 units (~5.2 waves) for both, i.e. 3 chunks per tile on full Large and 6 on the 1/2 slab (forward
+  // 1.278 -> 1.262 ms, adjoint 1.148 -> 1.139 ms vs 5 chunks; the full problem is flat between 3 and 4).
+  p->fwd_target = p->chunk_order ? 148LL * 16 * 4 : 12288;
+  p->adj_target = p->chunk_order ? 148LL * 16 * 16 / 5 : 12288;
+  if (const char* e = std::getenv("NFGPU_FWD_TARGET")) p->fwd_target = std::max(1LL, std::atoll(e));
   if (const char* e = std::getenv("NFGPU_ADJ_TARGET")) p->adj_target = std::max(1LL, std::atoll(e));
   {
     // bound the forward partial buffer to ~512 MB
