@@ -236,6 +236,35 @@ def test_medium_spgm_c64_tracks_c128_and_oracle():
     assert rel_l2(s_gpu, s_or) <= 1e-4
 
 
+def test_large_spgm_500_iterations_c64_tracks_c128():
+    """BASELINE config 2 (Large: 48 + 48 antennas, 128 f, 128x128x64 voxels, |B| = 4096, 500 iterations): the c64
+    reconstruction after the full iteration count against the c128 GPU path (the proxy oracle of SURVEY.md §8(c):
+    the reference's tables would need 206 GB), same eta, alpha and the host numpy index sequence of the
+    reference's sampler. North-star bar: 1e-4 relative L2."""
+    from paper_2509_00774_b200.sharding import ShardedSetup
+
+    w = configs.WORKLOADS["large"]()
+    scn = w.scenario
+    setup = ShardedSetup(scn, dtype="c64", device="cuda:0", z_range=None)
+    clean = setup.forward_full(configs.make_scene(w))
+    y = configs.add_noise(clean, configs.noise_sigma(clean, w.snr_db))
+    L = setup.lipschitz(n_iters=20, rng_seed=configs.SEEDS["power"])
+    lam = 1e-3 * setup.max_abs_adjoint(y) / scn.n_channels
+    setup.release()
+    eta, alpha = 1.0 / L, lam / L
+    table = np.stack(O.flat_index_sequence(scn.n_channels, w.batch, w.iters, configs.SEEDS["minibatch"])).astype(np.int32)
+    assert table.shape == (500, 4096)
+    res = {}
+    for dtype in ("c128", "c64"):
+        cfg = SolverConfig(eta=eta, alpha=alpha, max_iters=w.iters, tol=1e-300, dtype=dtype, sampler="table",
+                           index_table=table, check_every=100)
+        rep = spgm_solve(y, scn, cfg)
+        assert rep.iterations == 500
+        res[dtype] = rep.volume.values
+    err = rel_l2(res["c64"], res["c128"])
+    assert err <= 1e-4, err
+
+
 def test_device_sampler_distinct_uniform():
     scn = configs.small_scenario()
     plan = get_plan(scn, "c64")
