@@ -9,25 +9,27 @@
 // distance table (8 B per pair in c64) and two MUFU ops (sin, cos).
 //
 // Work decomposition:
-//   * voxels are cut into warp tiles of 8×4×4 = 128 voxels. Lane L owns 4 voxels
-//     that are consecutive in x, stored as two fp32x2 pairs so the per-entry
-//     arithmetic runs on packed FADD2/FFMA2/FMUL2 (sm_100a).
+//   * voxels are cut into warp tiles of 8×8×4 = 256 voxels (NFGPU_V = 8). Lane L owns 8 voxels
+//     that are consecutive in x, held as four fp32x2 pairs so the per-entry arithmetic runs on
+//     packed FADD2/FFMA2/FMUL2 (sm_100a).
 //   * each tile has an fp64 anchor (its centre). The table stores δ = d − D0(tile, antenna)
 //     in fp32, plus 1/d. The per-(channel, tile) phase offset frac(f/c·(D0_T + D0_R))
-//     is computed once per channel and tile in fp64. Per entry the phase in
-//     revolutions is x = base + (f/c)·(δT+δR), |x| ≲ 8. It is reduced exactly to
-//     [-½, ½] before MUFU.SIN/COS. That holds the phase error to ~1e-6 rad at
+//     is computed once per channel and tile in fp64. Per entry the phase is
+//     x = base + (f/c)·(δT+δR) (|x| ≲ 12 revolutions), fed to MUFU.SIN/COS directly when the plan
+//     proves that bound and reduced exactly to [-½, ½] first otherwise: ~1e-6 rad phase error at
 //     phases of ~2e3 rad.
 //   * the channel batch is sorted on the device by (tx-group, rx, tx, f). Per rx
 //     run, a warp keeps the rx-side table entries of its voxels in registers
-//     (prefetched one run ahead). Per tx group, the tx-side entries sit in the warp's
+//     (staged one run ahead with cp.async). Per tx group, the tx-side entries sit in the warp's
 //     shared memory. Each entry then costs one conflict-free 16-byte shared load per 4 voxels.
-//   * adjoint (+prox): a warp owns (tile, channel chunk). Chunks of a tile are
-//     combined in fixed order by the last-arriving warp, which also applies the
-//     complex soft-threshold prox (solver.py:228-241) and writes the termination
-//     statistics (solver.py:244-251). The result is deterministic, with no float atomics.
-//   * forward: per-channel lane partials → warp transpose-reduce through smem →
-//     CTA combine → two-level deterministic fp64 column reduce.
+//   * work units are (tile, channel chunk) warps: tile-major with a split tail of shorter chunks
+//     when the distance table streams from DRAM, chunk-major with tapered chunks when it stays in L2.
+//   * adjoint (+prox): chunks of a tile are combined in fixed order by the last-arriving warp,
+//     which also applies the complex soft-threshold prox (solver.py:228-241) and writes the
+//     termination statistics (solver.py:244-251). Deterministic, with no float atomics.
+//   * forward: per-channel lane partials → warp transpose-reduce through smem every 8 channels →
+//     two-level deterministic fp64 column reduce over tiles (or, with a peer communicator, the
+//     second level fused with the NVLink all-reduce across voxel-slab ranks).
 #include <cuda_runtime.h>
 
 #include <algorithm>
