@@ -53,9 +53,10 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="launch steps eagerly instead of a CUDA graph")
     ap.add_argument("--no-extras", action="store_true", help="skip the Medium extra line")
     ap.add_argument("--force-dist", action="store_true", help="use the distributed path even at world size 1")
-    ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
-                    help="forward-partial all-reduce at N > 1: NCCL, or the fused NVLink peer all-reduce "
-                         "(nf_forward_allreduce; validated on one GPU by rank emulation, DESIGN.md §5)")
+    ap.add_argument("--collective", default="auto", choices=["auto", "nccl", "peer"],
+                    help="forward-partial all-reduce at N > 1: the fused NVLink peer all-reduce "
+                         "(nf_forward_allreduce, DESIGN.md §5), NCCL, or auto = peer when its start-up check "
+                         "against NCCL passes on every rank, else NCCL")
     return ap.parse_args()
 
 

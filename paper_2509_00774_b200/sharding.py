@@ -57,6 +57,29 @@ def connect_peer_allreduce(plan, process_group, create=None, connect=None) -> No
     dist.barrier(group=process_group)
 
 
+def peer_allreduce_self_check(plan, process_group, n: int = 1024, rtol: float = 1e-5) -> bool:
+    """Start-up check of a connected peer all-reduce on the real ranks: a forward of a fixed random
+    iterate over the first min(n, max_batch) channels through nf_forward_allreduce must match nf_forward +
+    an all-reduce over the process group (rtol; the two sum in different orders and precisions), with no
+    flag wait timing out. The verdict is agreed over the group (all ranks pass or all fall back)."""
+    import torch.distributed as dist
+
+    dev = plan.device
+    B = int(min(n, plan.max_batch, plan.M))
+    gen = torch.Generator(device="cpu").manual_seed(1234)  # the same on every rank
+    s = torch.randn(plan.n_local, dtype=plan.torch_dtype, generator=gen).to(dev)
+    plan.prepare(torch.arange(B, dtype=torch.int32, device=dev))
+    ref = plan.forward(s)
+    dist.all_reduce(torch.view_as_real(ref), group=process_group)
+    got = plan.forward_allreduce(s)
+    torch.cuda.synchronize(dev)
+    err = float(torch.linalg.vector_norm(got - ref) / torch.clamp(torch.linalg.vector_norm(ref), min=1e-300))
+    ok = (not plan.comm_timed_out()) and err <= rtol
+    flag = torch.tensor([1.0 if ok else 0.0], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=process_group)
+    return bool(flag.item() == 1.0)
+
+
 def _allreduce(t: torch.Tensor, pg, op=None) -> torch.Tensor:
     if pg is not None:
         if t.is_complex():

@@ -305,19 +305,35 @@ class SPGMEngine:
     def __init__(self, plan: DevicePlan, y: np.ndarray | torch.Tensor, eta: float, alpha: float,
                  initial: np.ndarray | torch.Tensor | None = None, process_group=None,
                  collective: str = "nccl"):
-        if collective not in ("nccl", "peer"):
-            raise ValueError("collective must be 'nccl' or 'peer'")
+        if collective not in ("nccl", "peer", "auto"):
+            raise ValueError("collective must be 'nccl', 'peer' or 'auto'")
         self.plan = plan
         self.eta = float(eta)
         self.alpha = float(alpha)
         self.pg = process_group
         # "peer": the forward's last reduce kernel all-reduces over NVLink itself (nf_forward_allreduce);
-        # "nccl": nf_forward, then torch.distributed.all_reduce of the 2·B reals
+        # "nccl": nf_forward, then torch.distributed.all_reduce of the 2·B reals;
+        # "auto": peer if its start-up check against NCCL passes on every rank, else NCCL
         self.collective = collective if process_group is not None else "nccl"
-        if self.collective == "peer":
-            from .sharding import connect_peer_allreduce
+        if self.collective in ("peer", "auto"):
+            from .sharding import connect_peer_allreduce, peer_allreduce_self_check
 
-            connect_peer_allreduce(plan, process_group)
+            ok = False
+            try:
+                connect_peer_allreduce(plan, process_group)
+                ok = peer_allreduce_self_check(plan, process_group)
+            except Exception as exc:  # an unusable peer mapping: fall back in "auto", report in "peer"
+                if self.collective == "peer":
+                    raise
+                import warnings
+
+                warnings.warn(f"peer all-reduce unavailable ({exc}); using NCCL")
+            if not ok:
+                if self.collective == "peer":
+                    raise RuntimeError("peer all-reduce failed its start-up check against NCCL")
+                self.collective = "nccl"
+            else:
+                self.collective = "peer"
         dev = plan.device
         self.y = plan._as_dev(y, plan.M, "y")
         self.s = torch.zeros(plan.n_local, dtype=plan.torch_dtype, device=dev)
