@@ -37,47 +37,70 @@ def slab_range(nz: int, rank: int, world: int) -> tuple[int, int]:
     return lo * unit, (hi * unit if rank < world - 1 else nz)
 
 
-def connect_peer_allreduce(plan, process_group, create=None, connect=None) -> None:
+def connect_peer_allreduce(plan, process_group, create=None, connect=None) -> bool:
     """Set up the fused peer all-reduce of the forward partials (nf_comm_*) on
     ``plan`` for the ranks of ``process_group``: every rank exports the CUDA IPC handle of its
     receive slots, the handles are all-gathered in rank order over the group (any backend), and
-    every rank maps all of them. Ends with a barrier, so no rank pushes into an unmapped peer.
-    ``create``/``connect`` default to the plan's C-ABI calls (tests substitute host stand-ins)."""
+    every rank maps all of them. Every rank runs the same collectives whatever fails locally, and
+    the result (True = connected everywhere) is agreed over the group, so no rank can be left
+    waiting in a collective the others skipped. Ends with a barrier, so no rank pushes into an
+    unmapped peer. ``create``/``connect`` default to the plan's C-ABI calls (tests substitute
+    host stand-ins)."""
     import torch.distributed as dist
 
     rank, world = dist.get_rank(process_group), dist.get_world_size(process_group)
     create = create or plan.comm_create
     connect = connect or plan.comm_connect
-    mine = create(rank, world)
+    try:
+        mine = create(rank, world)
+    except Exception:
+        mine = None
     handles: list = [None] * world
     dist.all_gather_object(handles, mine, group=process_group)
-    if handles[rank] != mine:
-        raise RuntimeError("peer all-reduce: handle exchange returned a different handle for this rank")
-    connect(handles)
+    ok = mine is not None and all(h is not None for h in handles) and handles[rank] == mine
+    if ok:
+        try:
+            connect(handles)
+        except Exception:
+            ok = False
+    votes: list = [None] * world
+    dist.all_gather_object(votes, bool(ok), group=process_group)
     dist.barrier(group=process_group)
+    return all(votes)
 
 
 def peer_allreduce_self_check(plan, process_group, n: int = 1024, rtol: float = 1e-5) -> bool:
     """Start-up check of a connected peer all-reduce on the real ranks: a forward of a fixed random
     iterate over the first min(n, max_batch) channels through nf_forward_allreduce must match nf_forward +
     an all-reduce over the process group (rtol; the two sum in different orders and precisions), with no
-    flag wait timing out. The verdict is agreed over the group (all ranks pass or all fall back)."""
+    flag wait timing out. Local failures are caught so that every rank runs the same collectives, and the
+    verdict is agreed over the group (all ranks pass or all fall back)."""
     import torch.distributed as dist
 
     dev = plan.device
     B = int(min(n, plan.max_batch, plan.M))
-    gen = torch.Generator(device="cpu").manual_seed(1234)  # the same on every rank
-    s = torch.randn(plan.n_local, dtype=plan.torch_dtype, generator=gen).to(dev)
-    plan.prepare(torch.arange(B, dtype=torch.int32, device=dev))
-    ref = plan.forward(s)
+    ok = True
+    try:
+        gen = torch.Generator(device="cpu").manual_seed(1234)  # the same on every rank
+        s = torch.randn(plan.n_local, dtype=plan.torch_dtype, generator=gen).to(dev)
+        plan.prepare(torch.arange(B, dtype=torch.int32, device=dev))
+        ref = plan.forward(s)
+    except Exception:
+        ok = False
+        ref = torch.zeros(B, dtype=plan.torch_dtype, device=dev)
     dist.all_reduce(torch.view_as_real(ref), group=process_group)
-    got = plan.forward_allreduce(s)
-    torch.cuda.synchronize(dev)
-    err = float(torch.linalg.vector_norm(got - ref) / torch.clamp(torch.linalg.vector_norm(ref), min=1e-300))
-    ok = (not plan.comm_timed_out()) and err <= rtol
-    flag = torch.tensor([1.0 if ok else 0.0], device=dev)
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=process_group)
-    return bool(flag.item() == 1.0)
+    if ok:
+        try:
+            got = plan.forward_allreduce(s)
+            torch.cuda.synchronize(dev)
+            den = torch.clamp(torch.linalg.vector_norm(ref), min=1e-300)
+            err = float(torch.linalg.vector_norm(got - ref) / den)
+            ok = (not plan.comm_timed_out()) and err <= rtol
+        except Exception:
+            ok = False
+    votes: list = [None] * dist.get_world_size(process_group)
+    dist.all_gather_object(votes, bool(ok), group=process_group)
+    return all(votes)
 
 
 def _allreduce(t: torch.Tensor, pg, op=None) -> torch.Tensor:

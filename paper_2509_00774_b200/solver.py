@@ -318,19 +318,15 @@ class SPGMEngine:
         if self.collective in ("peer", "auto"):
             from .sharding import connect_peer_allreduce, peer_allreduce_self_check
 
-            ok = False
-            try:
-                connect_peer_allreduce(plan, process_group)
-                ok = peer_allreduce_self_check(plan, process_group)
-            except Exception as exc:  # an unusable peer mapping: fall back in "auto", report in "peer"
-                if self.collective == "peer":
-                    raise
-                import warnings
-
-                warnings.warn(f"peer all-reduce unavailable ({exc}); using NCCL")
+            # both steps run the same collectives on every rank and agree on their verdict over the group
+            ok = connect_peer_allreduce(plan, process_group)
+            ok = ok and peer_allreduce_self_check(plan, process_group)
             if not ok:
                 if self.collective == "peer":
-                    raise RuntimeError("peer all-reduce failed its start-up check against NCCL")
+                    raise RuntimeError("peer all-reduce could not be connected or failed its start-up check")
+                import warnings
+
+                warnings.warn("peer all-reduce unavailable on this group; using NCCL")
                 self.collective = "nccl"
             else:
                 self.collective = "peer"

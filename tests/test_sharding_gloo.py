@@ -120,8 +120,17 @@ def _peer_worker(rank: int, world: int, port: int, q):
         def connect(handles):  # stands in for nf_comm_connect
             got["handles"] = list(handles)
 
-        connect_peer_allreduce(None, dist.group.WORLD, create=create, connect=connect)
-        q.put((rank, got["create"], got["handles"]))
+        ok = connect_peer_allreduce(None, dist.group.WORLD, create=create, connect=connect)
+        assert ok
+
+        def create_fails_on_1(r, w):  # a rank that cannot export: every rank must learn it, none may hang
+            if r == 1:
+                raise RuntimeError("no IPC")
+            return bytes([r + 1]) * 64
+
+        calls = []
+        ok2 = connect_peer_allreduce(None, dist.group.WORLD, create=create_fails_on_1, connect=calls.append)
+        q.put((rank, got["create"], got["handles"], ok2, len(calls)))
     finally:
         dist.destroy_process_group()
 
@@ -141,6 +150,7 @@ def test_peer_allreduce_handle_exchange(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     want = [bytes([r + 1]) * 64 for r in range(world)]
-    for rank, (r, w), handles in out:
+    for rank, (r, w), handles, ok2, ncalls in out:
         assert (r, w) == (rank, world)
         assert handles == want
+        assert ok2 is False and ncalls == 0  # the failure reached every rank, and nobody mapped anything
