@@ -952,29 +952,61 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
   int x0, y, z;
   lane_voxel(tx, ty, tz, L, x0, y, z);
   double st0 = 0, st1 = 0, st3 = 0;
+  // The lane's V voxels are consecutive in x: when all are inside the grid (and 16-byte aligned), its
+  // iterate is read and its new iterate (or gradient) written as 16-byte vectors, else voxel by voxel.
+  using U16 = typename std::conditional<std::is_same<Real, float>::value, float4, double2>::type;
+  constexpr int NU = 2 * V * (int)sizeof(Real) / 16;
+  const bool full = x0 + V <= g.nx && y < g.ny && z < g.nzs && (sizeof(Real) == 8 || (g.nx & 1) == 0);
+  const size_t n0 = ((size_t)z * g.ny + y) * g.nx + x0;
+  Real io[2 * V];  // interleaved (re, im): s_in in, s_out (or g) out
+  if (PROX) {
+    if (full) {
+#pragma unroll
+      for (int u = 0; u < NU; ++u) *reinterpret_cast<U16*>(io + u * (16 / sizeof(Real))) =
+          reinterpret_cast<const U16*>(a.s_in + 2 * n0)[u];
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const bool in = x0 + v < g.nx && y < g.ny && z < g.nzs;
+        io[2 * v] = in ? a.s_in[2 * (n0 + v)] : Real(0);
+        io[2 * v + 1] = in ? a.s_in[2 * (n0 + v) + 1] : Real(0);
+      }
+    }
+  }
 #pragma unroll
   for (int v = 0; v < V; ++v) {
-    const int x = x0 + v;
-    if (!(x < g.nx && y < g.ny && z < g.nzs)) continue;
-    const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
+    if (!(x0 + v < g.nx && y < g.ny && z < g.nzs)) continue;
     if (!PROX) {
-      a.gout[2 * n] = (Real)(a.scale * Gr[v]);
-      a.gout[2 * n + 1] = (Real)(a.scale * Gi[v]);
+      io[2 * v] = (Real)(a.scale * Gr[v]);
+      io[2 * v + 1] = (Real)(a.scale * Gi[v]);
     } else {
-      const Real s_r = a.s_in[2 * n], s_i = a.s_in[2 * n + 1];
+      const Real s_r = io[2 * v], s_i = io[2 * v + 1];
       const Real ur = s_r - (Real)a.eta_over_b * Gr[v];
       const Real ui = s_i - (Real)a.eta_over_b * Gi[v];
       const Real mag = sqrt(ur * ur + ui * ui);
       const Real al = (Real)a.alpha;
       const Real sc = mag > al ? (mag - al) / mag : Real(0);
       const Real o_r = ur * sc, o_i = ui * sc;
-      a.s_out[2 * n] = o_r;
-      a.s_out[2 * n + 1] = o_i;
+      io[2 * v] = o_r;
+      io[2 * v + 1] = o_i;
       const double m0 = sqrt((double)s_r * s_r + (double)s_i * s_i);
       const double m1 = sqrt((double)o_r * o_r + (double)o_i * o_i);
       st0 += m0 * m0;
       st1 += (m1 - m0) * (m1 - m0);
       st3 += m1;
+    }
+  }
+  Real* dst = PROX ? a.s_out : a.gout;
+  if (full) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+      reinterpret_cast<U16*>(dst + 2 * n0)[u] = *reinterpret_cast<const U16*>(io + u * (16 / sizeof(Real)));
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (!(x0 + v < g.nx && y < g.ny && z < g.nzs)) continue;
+      dst[2 * (n0 + v)] = io[2 * v];
+      dst[2 * (n0 + v) + 1] = io[2 * v + 1];
     }
   }
   if (PROX) {
@@ -1179,13 +1211,29 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   int x0, y, z;
   lane_voxel(tx, ty, tz, L, x0, y, z);
   Real srv[V], siv[V];
+  {  // the lane's V voxels (consecutive in x): 16-byte vector loads when all are inside and aligned
+    using U16 = typename std::conditional<std::is_same<Real, float>::value, float4, double2>::type;
+    constexpr int NU = 2 * V * (int)sizeof(Real) / 16, PU = 16 / (int)sizeof(Real);
+    const size_t n0 = ((size_t)z * g.ny + y) * g.nx + x0;
+    if (x0 + V <= g.nx && y < g.ny && z < g.nzs && (sizeof(Real) == 8 || (g.nx & 1) == 0)) {
 #pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int x = x0 + v;
-    const bool ok = x < g.nx && y < g.ny && z < g.nzs;
-    const size_t n = ((size_t)z * g.ny + y) * g.nx + x;
-    srv[v] = ok ? a.s[2 * n] : Real(0);
-    siv[v] = ok ? a.s[2 * n + 1] : Real(0);
+      for (int u = 0; u < NU; ++u) {
+        const U16 w = reinterpret_cast<const U16*>(a.s + 2 * n0)[u];
+        const Real* t = reinterpret_cast<const Real*>(&w);
+#pragma unroll
+        for (int k = 0; k < PU; k += 2) {
+          srv[(u * PU + k) >> 1] = t[k];
+          siv[(u * PU + k) >> 1] = t[k + 1];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const bool ok = x0 + v < g.nx && y < g.ny && z < g.nzs;
+        srv[v] = ok ? a.s[2 * (n0 + v)] : Real(0);
+        siv[v] = ok ? a.s[2 * (n0 + v) + 1] : Real(0);
+      }
+    }
   }
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
