@@ -1045,11 +1045,12 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   prefetch_first<Real>(a.crec, nullptr, j0, j1, L, nxt, nxtw);
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
+  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
+  int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
   pdl_wait();
   if (j0 + L < j1) nxtw = a.wrec[j0 + L];
   __syncwarp();
-  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
-  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
 
   QV<Real> gr, gi, hr, hi, dR, iR;
   zero(gr);
@@ -1058,7 +1059,6 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   zero(hi);
   zero(dR);
   zero(iR);
-  int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
 
   for (int jb = j0; jb < j1; jb += 32) {
     const int nb = min(32, j1 - jb);
@@ -1242,6 +1242,14 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
   const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
   const QV<Real> sr = make_v(srv), si = make_v(siv);
+  int cur_tg = -1, pf_r = -1, carry = -1;
+  if (c0 < c1) {  // stage the first run's tx group and rx rows as soon as the first record is in
+    const int pk0 = __shfl_sync(FULL, nxt.pk, 0);
+    cur_tg = pk_tg(pk0);
+    pf_r = pk_r(pk0);
+    load_tgroup_async<Real>(g, tabt, ws.tside, cur_tg, L);
+    stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
+  }
   __syncwarp();
 
   QV<Real> dR, iR, shr, shi, nshr;
@@ -1250,7 +1258,6 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   zero(shr);
   zero(shi);
   zero(nshr);
-  int cur_tg = -1, pf_r = -1, carry = -1;
   R2<Real>* outl = out + L;
   for (int jb = c0; jb < c1; jb += 32) {
     const int nb = min(32, c1 - jb);
