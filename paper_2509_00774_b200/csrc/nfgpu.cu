@@ -1045,12 +1045,11 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   prefetch_first<Real>(a.crec, nullptr, j0, j1, L, nxt, nxtw);
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
-  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
-  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
-  int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
   pdl_wait();
   if (j0 + L < j1) nxtw = a.wrec[j0 + L];
   __syncwarp();
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
+  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
 
   QV<Real> gr, gi, hr, hi, dR, iR;
   zero(gr);
@@ -1059,6 +1058,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   zero(hi);
   zero(dR);
   zero(iR);
+  int cur_tg = -1, pf_r = -1, carry = -1, rslot = 0;
 
   for (int jb = j0; jb < j1; jb += 32) {
     const int nb = min(32, j1 - jb);
