@@ -71,6 +71,9 @@ namespace {
 #ifndef NFGPU_MINB_ADJ
 #define NFGPU_MINB_ADJ 4
 #endif
+#ifndef NFGPU_FWD_CIS  // c128 forward: 1 = table-based cis_rev, 0 = sincospi (the c64 path ignores it)
+#define NFGPU_FWD_CIS false
+#endif
 #ifndef NFGPU_L2_TABLE_MB  // distance tables up to this size use chunk-major work units (nf_plan::chunk_order)
 #define NFGPU_L2_TABLE_MB 256
 #endif
@@ -1287,8 +1290,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const QV<Real> dT0 = ldv(tsl + o0), iT0 = ldv(tsl + o0 + TILE);
           const QV<Real> dT1 = ldv(tsl + o1), iT1 = ldv(tsl + o1 + TILE);
           QV<Real> cs0, sn0, cs1, sn1;
-          phasorv<EXACT, false>(q0.x, q0.y, dT0, dR, cs0, sn0);
-          phasorv<EXACT, false>(q1.x, q1.y, dT1, dR, cs1, sn1);
+          phasorv<EXACT, NFGPU_FWD_CIS>(q0.x, q0.y, dT0, dR, cs0, sn0);
+          phasorv<EXACT, NFGPU_FWD_CIS>(q1.x, q1.y, dT1, dR, cs1, sn1);
           const R2<Real> p0 = fwd_part(iT0, cs0, sn0, shr, shi, nshr);
           const R2<Real> p1 = fwd_part(iT1, cs1, sn1, shr, shi, nshr);
           tb[(c - h0) * 33 + L] = p0;
@@ -1299,7 +1302,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
           const int off = bits_int(q.z);
           const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
           QV<Real> cs, sn;
-          phasorv<EXACT, false>(q.x, q.y, dT, dR, cs, sn);
+          phasorv<EXACT, NFGPU_FWD_CIS>(q.x, q.y, dT, dR, cs, sn);
           tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi, nshr);
           ++c;
         }
