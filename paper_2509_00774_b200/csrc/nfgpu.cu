@@ -720,6 +720,13 @@ __device__ __forceinline__ double int_bits<double>(int v) { return __longlong_as
 __device__ __forceinline__ int bits_int(float v) { return __float_as_int(v); }
 __device__ __forceinline__ int bits_int(double v) { return (int)__double_as_longlong(v); }
 
+__device__ __forceinline__ float with_low2(float v, int k) { return __int_as_float((__float_as_int(v) & ~3) | k); }
+__device__ __forceinline__ double with_low2(double v, int k) {
+  return __longlong_as_double((__double_as_longlong(v) & ~3LL) | k);
+}
+__device__ __forceinline__ int low2(float v) { return __float_as_int(v) & 3; }
+__device__ __forceinline__ int low2(double v) { return (int)(__double_as_longlong(v) & 3LL); }
+
 // Build the 32 channel records of one batch (lane L <-> sorted position jb+L) from the
 // prefetched ChanRec/w in registers, and prefetch the next batch's. Returns the bitmask of
 // run starts (a run = maximal stretch with equal (rx, tx group)). rect[L] = {tx-row offset in the
@@ -757,6 +764,9 @@ __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<R
     if (wrec) {
       q.z = w.x;
       q.w = w.y;
+      // adjoint: the tx index within the group (< TG_MAX = 4) rides in the 2 low bits of the phase offset
+      // (≤ 3 ulp of |base| ≤ π: < 1e-6 rad), so one broadcast load per channel brings the whole record
+      q.y = with_low2(q.y, t - tg * g.Tg);
     } else {  // forward: the tx-row offset rides in .z as a bit pattern (one broadcast load per channel)
       q.z = int_bits<Real>(toff);
       q.w = 0;
@@ -1081,11 +1091,11 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
       }
       // software pipeline: channel c+1's record loads while c computes
       R4<Real> q = ws.rec[c];
-      int off = ws.rect[c].x;
+      int off = low2(q.y) * TABW;
 #pragma unroll UNROLL
       for (; c < e; ++c) {
         const R4<Real> qn = ws.rec[c + 1];
-        const int offn = ws.rect[c + 1].x;
+        const int offn = low2(qn.y) * TABW;
         const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
         QV<Real> cs, sn;
         phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
