@@ -92,8 +92,9 @@ constexpr int TG_MAX = NFGPU_TG;  // tx per shared-memory group
 constexpr int UNROLL = NFGPU_UNROLL;
 constexpr int TBR = NFGPU_TBR;  // forward transpose depth (channels per lane-reduction)
 static_assert(TBR == 8 || TBR == 16, "TBR must be 8 or 16");
-constexpr int A_MAX = 256;     // antennas (T + R) per plan
-constexpr int RED_THREADS = 300000;
+// antenna limits per plan (no cap on T + R itself): receivers fit 15 bits of the run key, tx groups 9 bits
+constexpr int R_MAX = 32767;
+constexpr int TGROUPS_MAX = 511;
 constexpr unsigned FULL = 0xffffffffu;
 
 // Programmatic dependent launch: kernels of the SPGM step are launched with
@@ -511,15 +512,14 @@ __global__ void __launch_bounds__(1024) scan_kernel(int* __restrict__ cnt, int n
 }
 
 // Per sorted position: everything a warp needs about a channel except its tile-dependent
-// phase offset. pk = t | r << 8 | tg << 16 (T, R <= 255 since T + R <= A_MAX).
+// phase offset. pk = t | r << 16 (T <= 65535, R <= R_MAX); the tx group is t / Tg.
 struct ChanRec {
   double kd;  // f / c (fp64, for the anchor phase)
   float kf;   // f / c (fp32, per-entry slope)
   int pk;
 };
-__device__ __forceinline__ int pk_t(int pk) { return pk & 0xff; }
-__device__ __forceinline__ int pk_r(int pk) { return (pk >> 8) & 0xff; }
-__device__ __forceinline__ int pk_tg(int pk) { return pk >> 16; }
+__device__ __forceinline__ int pk_t(int pk) { return pk & 0xffff; }
+__device__ __forceinline__ int pk_r(int pk) { return pk >> 16; }
 
 // sorted position j <- key order; crec[j], sf[j] = f
 __global__ void __launch_bounds__(1024) compact_kernel(KeyMap km, int* __restrict__ pos_of_key, int KS,
@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(KeyMap km, int* __restric
     ChanRec q;
     q.kd = kd[c.x];
     q.kf = (float)q.kd;
-    q.pk = c.y | (c.z << 8) | (c.w << 16);
+    q.pk = c.y | (c.z << 16);
     crec[j] = q;
     sf[j] = c.x;
     pos_of_key[key] = -1;
@@ -745,7 +745,7 @@ __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<R
   }
   int key = -1, toff = 0;
   if (L < nb) {
-    const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = pk_tg(cr.pk);
+    const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = t / g.Tg;
     const double x = cr.kd * (ws.d0[t] + ws.d0[g.T + r]);
     R4<Real> q;
     if constexpr (std::is_same<Real, float>::value) {
@@ -772,7 +772,7 @@ __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<R
       q.w = 0;
     }
     ws.rec[L] = q;
-    key = r | (tg << 16);
+    key = r | (tg << 15);  // run key: rx (15 bits) | tx group (9 bits); the run end rides in bits 24-29
   }
   int prev = __shfl_up_sync(FULL, key, 1);
   if (L == 0) prev = carry;
@@ -996,14 +996,14 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
       const Real s_r = io[2 * v], s_i = io[2 * v + 1];
       const Real ur = s_r - (Real)a.eta_over_b * Gr[v];
       const Real ui = s_i - (Real)a.eta_over_b * Gi[v];
-      const Real mag = sqrt(ur * ur + ui * ui);
+      const Real mag = hypot(ur, ui);  // |u| as np.abs (no overflow / underflow of the squares)
       const Real al = (Real)a.alpha;
       const Real sc = mag > al ? (mag - al) / mag : Real(0);
       const Real o_r = ur * sc, o_i = ui * sc;
       io[2 * v] = o_r;
       io[2 * v + 1] = o_i;
-      const double m0 = sqrt((double)s_r * s_r + (double)s_i * s_i);
-      const double m1 = sqrt((double)o_r * o_r + (double)o_i * o_i);
+      const double m0 = hypot((double)s_r, (double)s_i);
+      const double m1 = hypot((double)o_r, (double)o_i);
       st0 += m0 * m0;
       st1 += (m1 - m0) * (m1 - m0);
       st3 += m1;
@@ -1081,7 +1081,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
       const int key = ws.rect[c].y;
       const int e = key >> 24;
       if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c
-        const int rr = key & 0xffff, tg = (key >> 16) & 0xff;
+        const int rr = key & 0x7fff, tg = (key >> 15) & 0x1ff;
         if (tg != cur_tg) {
           load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
           cur_tg = tg;
@@ -1258,7 +1258,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   int cur_tg = -1, pf_r = -1, carry = -1;
   if (c0 < c1) {  // stage the first run's tx group and rx rows as soon as the first record is in
     const int pk0 = __shfl_sync(FULL, nxt.pk, 0);
-    cur_tg = pk_tg(pk0);
+    cur_tg = pk_t(pk0) / g.Tg;
     pf_r = pk_r(pk0);
     load_tgroup_async<Real>(g, tabt, ws.tside, cur_tg, L);
     stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
@@ -1284,7 +1284,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
         const int key = ws.rect[c].y;
         const int e = min(key >> 24, h1);
         if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c
-          const int rr = key & 0xffff, tg = (key >> 16) & 0xff;
+          const int rr = key & 0x7fff, tg = (key >> 15) & 0x1ff;
           if (tg != cur_tg) {
             load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
             cur_tg = tg;
@@ -1845,6 +1845,8 @@ constexpr int TCF_GW = 12;                    // forward generation warps (warps
 constexpr int TC_NMAX = 128;                  // max padded 2·n_t (TMEM: 2 regions × N ≤ 256 columns)
 constexpr uint32_t TC_A_BYTES = 128 * 2 * TC_RCH * 4;  // one of hi/lo: 8 KB
 constexpr uint32_t TC_SMEM_MAX = 227 * 1024;
+constexpr int TC_RX_MAX = 256;                     // receivers of a tensor-core batch (phase parameter slots)
+constexpr int TC_ANT_MAX = TC_NMAX / 2 + TC_RX_MAX;  // batch antennas (tx <= TC_NMAX / 2 = 64)
 
 // dynamic shared-memory layout of adj_tc_kernel (bytes), from the batch shape
 struct TcLayout {
@@ -1854,8 +1856,8 @@ struct TcLayout {
     b_off = ns * 2 * TC_A_BYTES;                 // [stage][hi, lo][npad x 16]
     b_stage = (uint32_t)npad * 2 * TC_RCH * 4 * 2;
     tab_off = b_off + ns * b_stage;              // [antenna slot][δ 128 | 1/d 128]
-    d0_off = tab_off + (uint32_t)nant * 1024;    // [A_MAX] fp64
-    par_off = d0_off + A_MAX * 8;                // rx [2][kr 256 | br 256], tx [2][kt 64 | bt 64]
+    d0_off = tab_off + (uint32_t)nant * 1024;    // [TC_ANT_MAX] fp64 (batch antennas)
+    par_off = d0_off + TC_ANT_MAX * 8;           // rx [2][kr 256 | br 256], tx [2][kt 64 | bt 64]
     bar_off = par_off + (1024 + 256) * 4;        // 3·NS + 4 mbarriers + TMEM base
     bytes = bar_off + (3 * TC_NS + 6) * 8;
   }
@@ -2191,7 +2193,7 @@ struct TcfLayout {
     tab_buf = (uint32_t)(TCF_VPS / 2) * (nant | 1) * 16;  // whole half tile, or 2 x one step's slice
     ant_off = tab_off + (stream ? 2 * tab_buf : (uint32_t)(nant | 1) * 1024);  // [slot] antenna index
     d0_off = (ant_off + (uint32_t)nant * 4 + 7) & ~7u;
-    par_off = d0_off + A_MAX * 8;               // [2][k of slot 320 | b of slot 320]
+    par_off = d0_off + TC_ANT_MAX * 8;          // [2][k of slot 320 | b of slot 320]
     bar_off = par_off + 2 * 640 * 4;
     bytes = bar_off + (2 * TCF_NS + 6) * 8;
   }
@@ -2634,7 +2636,7 @@ __global__ void soft_threshold_kernel(const Real* __restrict__ v, Real* __restri
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double vr = v[2 * i], vi = v[2 * i + 1];
-  const double mag = sqrt(vr * vr + vi * vi);
+  const double mag = hypot(vr, vi);  // np.abs: no overflow / underflow of the squares (solver.py:237)
   const double sc = mag > alpha ? (mag - alpha) / mag : 0.0;
   out[2 * i] = (Real)(vr * sc);
   out[2 * i + 1] = (Real)(vi * sc);
@@ -2647,8 +2649,8 @@ __global__ void __launch_bounds__(1024) magchange_kernel(const Real* __restrict_
   __shared__ double sh[2][1024];
   double s0 = 0, s1 = 0;
   for (int64_t i = threadIdx.x; i < n; i += 1024) {
-    const double ma = sqrt((double)a[2 * i] * a[2 * i] + (double)a[2 * i + 1] * a[2 * i + 1]);
-    const double mb = sqrt((double)b[2 * i] * b[2 * i] + (double)b[2 * i + 1] * b[2 * i + 1]);
+    const double ma = hypot((double)a[2 * i], (double)a[2 * i + 1]);
+    const double mb = hypot((double)b[2 * i], (double)b[2 * i + 1]);
     s0 += ma * ma;
     s1 += (mb - ma) * (mb - ma);
   }
@@ -2680,7 +2682,9 @@ struct nf_plan {
   double c;
   int64_t nvox;
   int fwd_gridx;
+  int fwd_nseg;        // level-1 segments of the forward reduce: a function of the plan only (bit-exact subsets)
   int fwd_chunk;
+  size_t tmp_elems = 0;  // d_tmp capacity (double2)
   int adj_ch_cap;
   bool exact = true;  // explicit phase reduction (false when |x| <= EXACT_FREE_REV is guaranteed)
   double phase_bound_rev = 0;
@@ -2787,6 +2791,12 @@ void free_plan(nf_plan* p) {
   cudaFree(p->d_epoch);
   cudaFree(p->d_comm_err);
   delete p;
+}
+
+// level-1 segments of the two-level forward reduce over `rows` partial rows: ~sqrt(rows), so both levels
+// have short serial sums; a function of the row count only
+int reduce_segments(int rows) {
+  return std::max(1, std::min(rows, (int)std::ceil(std::sqrt((double)rows))));
 }
 
 size_t real_size(const nf_plan* p) { return p->dtype == NF_C64 ? sizeof(float) : sizeof(double); }
@@ -2907,9 +2917,10 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     const long long units = (long long)a.t1 * a.Q + (long long)(p->g.ntiles - a.t1) * a.Q2;
     CUDA_TRY(launch_k(p->use_pdl, kern, dim3((unsigned)((units + FWD_WARPS - 1) / FWD_WARPS)), dim3(FWD_WARPS * 32),
                       sm, st, a));
-    // two-level reduce: ~sqrt(rows) segments so both levels have short serial sums
-    int nseg = (int)std::ceil(std::sqrt((double)p->fwd_gridx));
-    nseg = std::max(1, std::min({nseg, p->fwd_gridx, std::max(1, RED_THREADS / span)}));
+    // two-level reduce: ~sqrt(rows) segments so both levels have short serial sums. The segment count
+    // depends on the plan only, never on the span, so a channel's summation tree is the same in every
+    // batch: forward_apply(s, subset=sub) == forward_apply(s)[sub] bit for bit (forward.py:17-18).
+    const int nseg = p->fwd_nseg;
     CUDA_TRY(launch_k(p->use_pdl, fwd_reduce1_kernel<Real>, dim3((span + 255) / 256, nseg), dim3(256), 0, st,
                       (const Real*)p->d_part, p->fwd_gridx, span, nseg, p->d_tmp));
     if (int rc = launch_reduce2<Real>(p, span, nseg, w0, y, st, p->use_pdl, true)) return rc;
@@ -2948,10 +2959,18 @@ int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const long long rows = 2LL * p->g.ntiles, per_f = (long long)sa.nt * sa.nr;
   // partial buffer: up to 2 GB, at least one frequency; windows of whole frequencies
   long long fwin = std::max(1LL, std::min<long long>(sa.nf, (2LL << 30) / (rows * 8 * per_f)));
-  fwin = std::min<long long>(fwin, std::max(1LL, (long long)RED_THREADS / per_f));
+  const int nseg = reduce_segments((int)rows);
   const long long nwins = (sa.nf + fwin - 1) / fwin;
   fwin = (sa.nf + nwins - 1) / nwins;  // balanced windows (16 = 8 + 8, not 14 + 2)
   const size_t need = (size_t)(rows * per_f * fwin);
+  if ((size_t)nseg * per_f * fwin > p->tmp_elems) {  // one frequency's level-1 sums exceed the reduce buffer
+    cudaFree(p->d_tmp);
+    p->d_tmp = nullptr;
+    p->tmp_elems = 0;
+    int rc = dalloc(p, &p->d_tmp, (size_t)nseg * per_f * fwin * sizeof(double2));
+    if (rc) return rc;
+    p->tmp_elems = (size_t)nseg * per_f * fwin;
+  }
   if (need > p->tcpart_elems) {
     cudaFree(p->d_tcpart);
     p->d_tcpart = nullptr;
@@ -2986,8 +3005,6 @@ int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     const int fch = (int)std::min<long long>(fb - fa, std::max<long long>(1, (2LL * 148 + rows - 1) / rows));
     kern<<<(unsigned)(rows * fch), TC_THREADS, smem, st>>>(a, sa, p->d_kd, npr, fa, fb, fch, p->d_tcpart);
     CUDA_TRY(cudaGetLastError());
-    int nseg = (int)std::ceil(std::sqrt((double)rows));
-    nseg = std::max(1, std::min({nseg, (int)rows, std::max(1, RED_THREADS / span)}));
     fwd_reduce1_kernel<float><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const float*)p->d_tcpart, (int)rows,
                                                                               span, nseg, p->d_tmp);
     CUDA_TRY(cudaGetLastError());
@@ -2998,7 +3015,7 @@ int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
 }
 
 bool use_tc_struct(const nf_plan* p, bool forward) {
-  if (!p->structured || !p->use_tc || 2 * p->snt > TC_NMAX) return false;
+  if (!p->structured || !p->use_tc || 2 * p->snt > TC_NMAX || p->snr > TC_RX_MAX) return false;
   const int amin = std::min(p->snt, p->snr);
   // the tensor core pays off once the contraction dominates the phasor work: both antenna
   // counts >= 24 and enough frequencies per tile (tools/time_structured.py crossover)
@@ -3039,8 +3056,7 @@ int launch_forward_struct(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     a.part = (Real*)p->d_part;
     kern<<<(unsigned)((long long)p->g.ntiles * a.Q), SW * 32, sm, st>>>(a, sa, p->d_kd);
     CUDA_TRY(cudaGetLastError());
-    int nseg = (int)std::ceil(std::sqrt((double)p->fwd_gridx));
-    nseg = std::max(1, std::min({nseg, p->fwd_gridx, std::max(1, RED_THREADS / span)}));
+    const int nseg = p->fwd_nseg;
     fwd_reduce1_kernel<Real><<<dim3((span + 255) / 256, nseg), 256, 0, st>>>((const Real*)p->d_part, p->fwd_gridx,
                                                                              span, nseg, p->d_tmp);
     CUDA_TRY(cudaGetLastError());
@@ -3150,7 +3166,8 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   if (!tx_xyz || !rx_xyz || !freq_hz || !pulse_reim || !corner || !spacing || !dims)
     return fail(NF_ERR_ARG, "null geometry pointer");
   if (n_tx < 1 || n_rx < 1 || n_f < 1) return fail(NF_ERR_ARG, "n_tx, n_rx, n_f must be >= 1");
-  if (n_tx + n_rx > A_MAX) return fail(NF_ERR_ARG, "at most 256 antennas (n_tx + n_rx) per plan");
+  if (n_rx > R_MAX) return fail(NF_ERR_ARG, "at most 32767 receivers per plan");
+  if (n_tx > TGROUPS_MAX * 2) return fail(NF_ERR_ARG, "at most 1022 transmitters per plan");
   if (!(c > 0) || !std::isfinite(c)) return fail(NF_ERR_ARG, "speed of light must be positive and finite");
   if (dtype != NF_C64 && dtype != NF_C128) return fail(NF_ERR_ARG, "dtype must be NF_C64 or NF_C128");
   for (int i = 0; i < 3; ++i)
@@ -3186,15 +3203,31 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   }
   g.ng = (n_tx + tg_max - 1) / tg_max;
   g.Tg = (n_tx + g.ng - 1) / g.ng;
+  if (g.ng > TGROUPS_MAX) {
+    delete p;
+    return fail(NF_ERR_ARG, "too many transmitter groups");
+  }
   for (int i = 0; i < 3; ++i) {
     g.corner[i] = corner[i];
     g.sp[i] = spacing[i];
   }
   p->nvox = (int64_t)g.nx * g.ny * g.nzs;
+  {  // every kernel keeps the tile's anchor distances of all T + R antennas in shared memory
+    const size_t lim = 227 * 1024;
+    const size_t need = std::max({fwd_smem(p), adj_smem(p),
+                                  dtype == NF_C64 ? struct_smem<float, true>(p) : struct_smem<double, true>(p),
+                                  dtype == NF_C64 ? struct_smem<float, false>(p) : struct_smem<double, false>(p)});
+    if (need > lim) {
+      delete p;
+      return fail(NF_ERR_ARG, "too many antennas for the kernels' shared-memory layout (" + std::to_string(need) +
+                                  " bytes per block)");
+    }
+  }
   p->km = KeyMap{g.T, g.R, g.F, g.Tg};
   p->KS = g.ng * g.R * g.Tg * g.F;
   p->ksblocks = (p->KS + 1023) / 1024;
   p->fwd_gridx = g.ntiles;  // rows of the forward partial buffer (one per tile)
+  p->fwd_nseg = reduce_segments(p->fwd_gridx);
   {
     // |x| = |base + (f/c)(δT + δR)| <= 1/2 + (f_max/c) * 2 * (tile half-diagonal), since |δ| <= distance
     // from the tile centre to the voxel (triangle inequality).
@@ -3249,7 +3282,10 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
     kd[i] = freq_hz[i] / c;
     kf32[i] = (float)kd[i];
   }
-  const size_t nred = (size_t)std::max(RED_THREADS, p->fwd_chunk) + 1024;
+  // level-1 sums of one forward window: fwd_nseg rows of fwd_chunk channels (the tensor-core forward grows
+  // it for its frequency windows on first use)
+  p->tmp_elems = (size_t)p->fwd_nseg * p->fwd_chunk;
+  const size_t nred = p->tmp_elems;
 #define ALLOC(ptr, bytes)                  \
   if ((rc = dalloc(p, &(ptr), (bytes)))) { \
     free_plan(p);                          \

@@ -131,6 +131,9 @@ class DevicePlan:
         self.B = 0
         self._idx = None  # keeps the staged index tensor alive
         self.staged_structured = False
+        # bumped by every staging call: a caller that keeps a batch staged across calls it does not
+        # control (the solver's full-batch PGM loop around a progress callback) re-stages on a change
+        self.stage_gen = 0
 
     # ---------------------------------------------------------------- lifecycle
     def __del__(self):
@@ -176,6 +179,7 @@ class DevicePlan:
         self.B = B
         self._idx = idx
         self.staged_structured = False
+        self.stage_gen += 1
 
     def prepare_structured(self, fs, ts, rs) -> None:
         """Stage the Cartesian subset fs × ts × rs (sorted host index lists; the C ABI validates)."""
@@ -189,6 +193,7 @@ class DevicePlan:
         self.B = int(arrs[0].size * arrs[1].size * arrs[2].size)
         self._idx = None
         self.staged_structured = True
+        self.stage_gen += 1
 
     def prepare_full(self) -> None:
         """Stage all M channels (a Cartesian product; structured unless the policy is "never")."""
@@ -298,6 +303,7 @@ class DevicePlan:
         self.B = int(n_f * n_tx * n_rx)
         self._idx = None
         self.staged_structured = True
+        self.stage_gen += 1
 
     def set_iter(self, it: int) -> None:
         _lib.check(self.lib.nf_plan_set_iter(self._h, int(it), _stream(self.device)), "nf_plan_set_iter")

@@ -446,14 +446,14 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
     records: list[IterationRecord] = []
     termination = TERMINATION_MAX_ITERS
     iterations = 0
-    staged_full = False
+    staged_full = -1  # plan.stage_gen right after the full batch was staged
 
     def stage_iteration(k):  # host side of iteration k: draw (or reuse) its batch and stage it; returns B
         nonlocal staged_full
         if not stochastic:
-            if not staged_full:
+            if staged_full != plan.stage_gen:
                 eng.stage(full_idx)
-                staged_full = True
+                staged_full = plan.stage_gen
             return m
         if config.sampler == "device":
             if config.composition is not None:
@@ -512,9 +512,11 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
     for k in range(1, config.max_iters + 1):
         t_iter = time.perf_counter()
         if not stochastic:
-            if not staged_full:
+            # the plan is shared (cached per scenario): a progress callback that evaluates the operator
+            # on the same scenario re-stages it, so the full batch is staged again whenever that happened
+            if staged_full != plan.stage_gen:
                 eng.stage(full_idx)
-                staged_full = True
+                staged_full = plan.stage_gen
             B = m
         elif config.sampler == "device":
             if config.composition is not None:

@@ -48,9 +48,15 @@ def to_ref(scn) -> "ref.ImagingScenario":
             extent=scn.voxels.extent,
             dims=scn.voxels.dims,
         ),
-        pulse=ref.ConstantPulse(scn.pulse.value),
+        pulse=_ref_pulse(scn.pulse),
         c=scn.c,
     )
+
+
+def _ref_pulse(p):
+    if hasattr(p, "frequencies_hz"):
+        return ref.TabulatedPulse(tuple(p.frequencies_hz), tuple(p.values))
+    return ref.ConstantPulse(p.value)
 
 
 def rc(rng, n):
@@ -173,6 +179,139 @@ def gen_medium_ops():
     )
 
 
+def gen_baseline_medium():
+    """BASELINE config 1 ('Medium') end to end with the reference's operator: scene, noise, L (20 power
+    iterations), lambda, and the 300-iteration flat SPGM loop through ref.minibatch_gradient and
+    ref.soft_threshold (solver.py:181-183, 228-241), the index table drawn as the reference's
+    sampler would (one default_rng(0) across iterations). The reference run holds the 4.3 GB tables."""
+    w = configs.WORKLOADS["medium"]()
+    scn = to_ref(w.scenario)
+    threads = os.cpu_count() or 1
+    t0 = time.time()
+    s_true = configs.make_scene(w)
+    clean = ref.forward_apply(s_true, scn, threads=threads)
+    sigma = configs.noise_sigma(clean, w.snr_db)
+    y = ref.simulate_measurements(s_true, scn, noise_sigma=sigma, rng_seed=configs.SEEDS["noise"],
+                                  threads=threads).values
+    L = ref.lipschitz_estimate(scn, n_iters=20, rng_seed=configs.SEEDS["power"], threads=threads)
+    M = scn.n_channels
+    lam = 1e-3 * float(np.max(np.abs(ref.adjoint_apply(y, scn, threads=threads)))) / M
+    eta = 1.0 / L
+    alpha = eta * lam
+    print(f"medium setup: {time.time() - t0:.1f}s  L={L:.6e}")
+    rng = np.random.default_rng(configs.SEEDS["minibatch"])
+    table = np.stack([np.sort(rng.choice(M, w.batch, replace=False)) for _ in range(w.iters)])
+    s = np.zeros(scn.n_voxels, dtype=np.complex128)
+    changes = []
+    for idx in table:
+        g = ref.minibatch_gradient(s, y, scn, idx, threads=threads)
+        s_next = ref.soft_threshold(s - eta * g, alpha)
+        changes.append(ref.relative_magnitude_change(s, s_next))
+        s = s_next
+    print(f"medium 300 iterations done: {time.time() - t0:.1f}s")
+    np.savez_compressed(
+        OUT / "baseline_medium.npz",
+        fingerprint=np.frombuffer(ref.scenario_fingerprint(scn), dtype=np.uint8),
+        sigma=np.array(sigma), y=y, L=np.array(L), lam=np.array(lam), eta=np.array(eta), alpha=np.array(alpha),
+        index_table=table.astype(np.int32), s_final=s, changes=np.array(changes),
+    )
+
+
+def _sparse(v):
+    nz = np.flatnonzero(v)
+    return nz.astype(np.int32), v[nz]
+
+
+def gen_paper_v():
+    """The paper-v study of the reference's acceptance suite (test_acceptance.py:69-106, 201-308) run
+    by the reference itself: the converged PGM reconstruction at 30 dB, three seeded SPGM(4,4,3) runs
+    and their PSNR against it (criterion 6), and the single-scatterer localisation (criterion 9).
+    Volumes are stored sparse (the l1 prox zeroes most voxels)."""
+    paper = ref.preset_scenario("paper-v")
+    out = {"fingerprint": np.frombuffer(ref.scenario_fingerprint(paper), dtype=np.uint8)}
+    t0 = time.time()
+    phantom = ref.make_phantom("points:5", paper.voxels, rng_seed=42)
+    clean = ref.forward_apply(phantom, paper)
+    sigma = float(np.sqrt(np.mean(np.abs(clean) ** 2) * 10 ** (-30 / 10)))
+    y = ref.simulate_measurements(phantom, paper, noise_sigma=sigma, rng_seed=7).values
+    out["y"] = y
+    out["sigma"] = np.array(sigma)
+    pgm = ref.pgm_solve(y, paper, ref.SolverConfig(eta=1e-3, alpha=4e-5, tol=1e-3, max_iters=2000))
+    print(f"paper-v PGM: {pgm.iterations} iterations, {pgm.termination}, {time.time() - t0:.1f}s")
+    out["pgm_iterations"] = np.array(pgm.iterations)
+    out["pgm_changes"] = np.array([r.magnitude_change for r in pgm.per_iteration])
+    out["pgm_nz"], out["pgm_val"] = _sparse(pgm.volume.values)
+    for seed in (1, 2, 3):
+        rep = ref.spgm_solve(y, paper, ref.SolverConfig(eta=1e-3, alpha=4e-5, tol=1e-3, max_iters=4000,
+                                                        composition=ref.MinibatchComposition(4, 4, 3),
+                                                        rng_seed=seed))
+        psnr = ref.psnr_vs_reference(rep.volume, pgm.volume).psnr_db
+        print(f"paper-v SPGM seed {seed}: {rep.iterations} iterations, PSNR {psnr:.3f} dB, {time.time() - t0:.1f}s")
+        out[f"spgm{seed}_iterations"] = np.array(rep.iterations)
+        out[f"spgm{seed}_psnr"] = np.array(psnr)
+        out[f"spgm{seed}_changes"] = np.array([r.magnitude_change for r in rep.per_iteration])
+        out[f"spgm{seed}_nz"], out[f"spgm{seed}_val"] = _sparse(rep.volume.values)
+    truth = ref.make_phantom("points:1", paper.voxels, rng_seed=13)
+    y1 = ref.simulate_measurements(truth, paper, noise_sigma=0.0).values
+    rep = ref.pgm_solve(y1, paper, ref.SolverConfig(eta=1e-3, alpha=4e-5, tol=1e-3, max_iters=150))
+    out["loc_true_voxel"] = np.array(int(np.argmax(np.abs(truth.values))))
+    out["loc_found_voxel"] = np.array(int(np.argmax(np.abs(rep.volume.values))))
+    out["loc_iterations"] = np.array(rep.iterations)
+    out["loc_nz"], out["loc_val"] = _sparse(rep.volume.values)
+    print(f"paper-v localisation: {int(out['loc_found_voxel'])} vs {int(out['loc_true_voxel'])}, "
+          f"{time.time() - t0:.1f}s")
+    np.savez_compressed(OUT / "paper_v_study.npz", **out)
+
+
+def gen_pulse():
+    """Frequency-dependent complex pulse (TabulatedPulse, geometry.py:239-269) through the reference's
+    forward (p_f, forward.py:283-284), adjoint (conj p_f, :315-325) and a structured SPGM run."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import pulse_cases
+
+    out = {}
+    for name, build in pulse_cases.CASES.items():
+        scn = to_ref(build())
+        M, N = scn.n_channels, scn.n_voxels
+        rng = np.random.default_rng(31)
+        s = rc(rng, N)
+        threads = os.cpu_count() or 1
+        out[f"{name}_fingerprint"] = np.frombuffer(ref.scenario_fingerprint(scn), dtype=np.uint8)
+        if name != "medium":  # Medium's s is regenerated from default_rng(31) by the test (2 MB)
+            out[f"{name}_s"] = s
+        if name == "medium":
+            idx = np.sort(rng.choice(M, 512, replace=False))
+            r = rc(rng, idx.size)
+            out["medium_idx"] = idx.astype(np.int32)
+            out["medium_r"] = r
+            out["medium_fwd_sub"] = ref.forward_apply(s, scn, subset=idx, threads=threads)
+            adj = ref.adjoint_apply(r, scn, subset=idx, threads=threads)
+            probe = np.sort(rng.choice(N, 4096, replace=False))
+            out["medium_adj_probe_voxels"] = probe.astype(np.int64)
+            out["medium_adj_sub_probe"] = adj[probe]
+            continue
+        r = rc(rng, M)
+        sub = np.sort(rng.choice(M, max(1, M // 3), replace=False))
+        out[f"{name}_r"] = r
+        out[f"{name}_sub"] = sub
+        out[f"{name}_fwd"] = ref.forward_apply(s, scn)
+        out[f"{name}_fwd_sub"] = ref.forward_apply(s, scn, subset=sub)
+        out[f"{name}_adj"] = ref.adjoint_apply(r, scn)
+        out[f"{name}_adj_sub"] = ref.adjoint_apply(r[: sub.size], scn, subset=sub)
+        y = rc(np.random.default_rng(32), M)
+        out[f"{name}_y"] = y
+        T, R, F = scn.array.n_tx, scn.array.n_rx, scn.frequencies.count
+        comp = ref.MinibatchComposition(max(1, F // 2), max(1, T - 1), max(1, R - 1))
+        out[f"{name}_comp"] = np.array([comp.n_f, comp.n_tx, comp.n_rx])
+        eta = 0.9 / ref.lipschitz_estimate(scn, n_iters=200, tol=1e-12)
+        alpha = 0.05 * eta * float(np.max(np.abs(ref.adjoint_apply(y, scn)))) / M
+        out[f"{name}_eta_alpha"] = np.array([eta, alpha])
+        rep = ref.spgm_solve(y, scn, ref.SolverConfig(eta=eta, alpha=alpha, max_iters=10, tol=1e-300,
+                                                      composition=comp, rng_seed=4))
+        out[f"{name}_spgm"] = rep.volume.values
+    np.savez_compressed(OUT / "pulse_scenarios.npz", **out)
+
+
 def gen_known_answers():
     """The reference tests' scalar known answers, evaluated by the reference itself."""
     c = ref.SPEED_OF_LIGHT
@@ -205,4 +344,10 @@ if __name__ == "__main__":
         gen_baseline_small()
     if "medium" in which:
         gen_medium_ops()
+    if "medium_spgm" in which:
+        gen_baseline_medium()
+    if "paper_v" in which:
+        gen_paper_v()
+    if "pulse" in which:
+        gen_pulse()
     print("fixtures written to", OUT)

@@ -127,3 +127,50 @@ def test_flat_sequence_is_sorted_distinct():
     seq = O.flat_index_sequence(1000, 64, 5, 0)
     for idx in seq:
         assert np.all(np.diff(idx) > 0) and idx.min() >= 0 and idx.max() < 1000
+
+
+@pytest.mark.parametrize("name", ["tiny", "ragged"])
+def test_oracle_with_tabulated_pulse_matches_reference(name):
+    """The oracle's table restatement and direct formula carry p(f) as the reference does (p_f in the
+    forward, forward.py:283-284; conj p_f in the adjoint, :315-325): bit-exact table restatement and
+    1e-12 direct formula against the reference's outputs (tests/golden/pulse_scenarios.npz)."""
+    import pulse_cases
+    from paper_2509_00774_b200.geometry import scenario_fingerprint
+
+    g = golden("pulse_scenarios")
+    scn = pulse_cases.CASES[name]()
+    assert scenario_fingerprint(scn) == bytes(g[f"{name}_fingerprint"])
+    geo = O.geom_from_scenario(scn)
+    assert np.ptp(np.angle(geo.pulse)) > 0.1  # genuinely frequency dependent and complex
+    s, r, sub = g[f"{name}_s"], g[f"{name}_r"], g[f"{name}_sub"]
+    op = O.TableOperator(geo)
+    full = np.arange(geo.M)
+    assert np.array_equal(op.forward(s, full), g[f"{name}_fwd"])
+    assert np.array_equal(op.forward(s, sub), g[f"{name}_fwd_sub"])
+    assert rel_l2(op.adjoint(r, full), g[f"{name}_adj"]) <= 1e-14
+    assert rel_l2(O.direct_forward(geo, s, full), g[f"{name}_fwd"]) <= 1e-12
+    assert rel_l2(O.direct_adjoint(geo, r[: sub.size], sub), g[f"{name}_adj_sub"]) <= 1e-12
+
+
+def test_baseline_medium_fixture_is_the_reference_sampler():
+    """The Medium reconstruction fixture (reference run, make_golden.py gen_baseline_medium): its index
+    table is the reference sampler's numpy call sequence, as the oracle restates it, and its step size
+    and threshold follow the BASELINE recipe (eta = 1/L, alpha = eta * 1e-3 max|A^H y| / M)."""
+    b = golden("baseline_medium")
+    w = configs.WORKLOADS["medium"]()
+    M = w.scenario.n_channels
+    table = np.stack(O.flat_index_sequence(M, w.batch, w.iters, configs.SEEDS["minibatch"]))
+    assert np.array_equal(table, b["index_table"])
+    assert float(b["eta"]) == pytest.approx(1.0 / float(b["L"]), rel=1e-15)
+    assert float(b["alpha"]) == pytest.approx(float(b["eta"]) * float(b["lam"]), rel=1e-15)
+    assert b["s_final"].shape == (w.scenario.n_voxels,) and b["changes"].shape == (w.iters,)
+
+
+def test_paper_v_fixture_matches_recorded_reference_run():
+    """The paper-v study fixture agrees with the reference's own recorded acceptance run
+    (pkg/test_output.txt:221-225): PGM converges in 590 iterations, SPGM(4,4,3) PSNR 44.9 / 45.0 /
+    45.4 dB for seeds 1-3, argmax voxel 70010."""
+    g = golden("paper_v_study")
+    assert int(g["pgm_iterations"]) == 590
+    assert [round(float(g[f"spgm{k}_psnr"]), 1) for k in (1, 2, 3)] == [44.9, 45.0, 45.4]
+    assert int(g["loc_found_voxel"]) == int(g["loc_true_voxel"]) == 70010
