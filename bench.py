@@ -51,7 +51,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-graph", action="store_true", help="launch steps eagerly instead of a CUDA graph")
-    ap.add_argument("--no-extras", action="store_true", help="skip the Medium extra line")
+    ap.add_argument("--no-extras", action="store_true", help="skip the extra workload lines")
+    ap.add_argument("--quick", action="store_true", help="skip the sweep, microbenchmark and full-grid CPU lines")
+    ap.add_argument("--cpu-child", default=None, choices=["small", "medium"],
+                    help=argparse.SUPPRESS)  # internal: one full-grid CPU baseline in a child process
     ap.add_argument("--force-dist", action="store_true", help="use the distributed path even at world size 1")
     ap.add_argument("--collective", default="auto", choices=["auto", "nccl", "peer"],
                     help="forward-partial all-reduce at N > 1: the fused NVLink peer all-reduce "
@@ -368,11 +371,17 @@ def run_ours(args):
         if e2e is not None:
             out["e2e"] = e2e
         if world == 1 and not args.no_extras and args.workload == "large":
-            out["extra_workloads"] = {"medium": medium_line(args, dev), "small": medium_line(args, dev, "small"),
-                                      "large_structured": structured_line(eng, w)}
+            ex = {"medium": medium_line(args, dev), "small": medium_line(args, dev, "small"),
+                  "large_structured": structured_line(eng, w), "large_c128": large_c128_line(eng, w, args)}
+            if not args.quick:
+                ex["minibatch_sweep"] = sweep_line(eng, w)
+                ex["microbenchmark"] = micro_lines()
+            out["extra_workloads"] = ex
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args.workload, 30, args.cpu_seconds)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            if not args.quick and args.workload == "large":
+                out["cpu_baseline"]["full_grid"] = {wl: cpu_child(wl) for wl in ("small", "medium")}
         print(json.dumps(out), flush=True)
     if pg is not None:
         dist.barrier(device_ids=[local])
@@ -444,6 +453,108 @@ def structured_line(eng, w):
     del ef, pf
     torch.cuda.empty_cache()
     return out
+
+
+def large_c128_line(eng, w, args):
+    """The Large step in complex128, the reference's own precision (and the CPU arm's): same y, eta, alpha,
+    |B| = 4096 flat device-sampled batches, CUDA graph, so the like-for-like GPU/CPU ratio is measured."""
+    import torch
+
+    from paper_2509_00774_b200.plan import DevicePlan
+    from paper_2509_00774_b200.solver import SPGMEngine
+
+    plan = DevicePlan(w.scenario, dtype="c128", device=eng.plan.device, max_batch=w.batch)
+    e = SPGMEngine(plan, eng.y.to(torch.complex128), eng.eta, eng.alpha)
+    ms, per_step, steps = timed_steps(e, plan, w, 20, 3, None, 0, not args.no_graph)
+    N = w.scenario.n_voxels
+    v = 2.0 * w.batch * N / (ms / steps * 1e-3)
+    out = {"dtype": "c128", "value": v, "unit": UNIT, "ms_per_step": ms / steps, "iters_per_s": 1e3 * steps / ms,
+           "steps": steps, "batch": w.batch, "frac_step_sfu_roof": v / SFU_ENTRY_PEAK_MEASURED}
+    del e, plan
+    torch.cuda.empty_cache()
+    return out
+
+
+def sweep_line(eng, w):
+    """BASELINE config 3: the minibatch sweep on Large (|B| in {256 ... 65536} flat, plus ISTA with |B| = M on the
+    separable kernels), 100 iterations each from s = 0, device time; objective D(s) + lambda ||s||_1 against
+    device time at 25-iteration checkpoints (full-M forward, untimed). tools/minibatch_sweep.py."""
+    import torch
+
+    sys.path.insert(0, str(ROOT / "tools"))
+    from minibatch_sweep import sweep
+
+    y = eng.y.to(torch.complex128).cpu().numpy()
+    summary, _ = sweep(w.scenario, y, eng.eta, eng.alpha, eng.alpha / eng.eta, iters=100, every=25,
+                       dev=eng.plan.device)
+    return summary
+
+
+def micro_lines():
+    """BASELINE config 4: one full-M forward and one full-M adjoint (M = 64 x 64 x 256) on the 64^3, 128^3 and
+    192x192x96 grids, c64 and c128, flat and separable kernels (tools/microbenchmark.py)."""
+    sys.path.insert(0, str(ROOT / "tools"))
+    from microbenchmark import run
+
+    out = []
+    for dtype in ("c64", "c128"):
+        for grid in ("64^3", "128^3", "192x192x96"):
+            line = run(grid, dtype)
+            for path in ("flat", "structured"):
+                line[path]["frac_sfu_roof"] = {k: line[path][k] / SFU_ENTRY_PEAK_MEASURED
+                                               for k in ("fwd_entries_per_s", "adj_entries_per_s")}
+            out.append(line)
+    return out
+
+
+def cpu_child(workload: str) -> dict:
+    """Full-grid CPU baseline of one config in a child process, so that its peak RSS (the
+    reference's phasor tables, forward.py:190-211) is its own."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--cpu-child", workload]
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        return json.loads(res.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, not fatal: the GPU line stands on its own
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
+def cpu_child_main(workload: str, budget_s: float) -> int:
+    import resource
+
+    from oracle import nfmimo_oracle as O
+    from paper_2509_00774_b200 import configs
+
+    w = configs.WORKLOADS[workload]()
+    geo = O.geom_from_scenario(w.scenario)
+    threads = O.host_threads()
+    rss0 = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
+    t0 = time.perf_counter()
+    op = O.TableOperator(geo)
+    build_s = time.perf_counter() - t0
+    rss_tables = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
+    rng = np.random.default_rng(0)
+    y = rng.standard_normal(geo.M) + 1j * rng.standard_normal(geo.M)
+    s = np.zeros(geo.N, dtype=np.complex128)
+    seq = np.random.default_rng(configs.SEEDS["minibatch"])
+    times = []
+    while len(times) < w.iters and (sum(times) < budget_s or len(times) < 3):
+        idx = np.sort(seq.choice(geo.M, w.batch, replace=False))
+        t1 = time.perf_counter()
+        g = op.adjoint(op.forward(s, idx, threads) - y[idx], idx, threads) / idx.size
+        s = O.soft_threshold(s - 1e-3 * g, 1e-6)
+        times.append(time.perf_counter() - t1)
+    per = float(np.mean(times[1:]))
+    print(json.dumps({
+        "workload": workload, "value": 2.0 * w.batch * geo.N / per, "unit": UNIT, "iters_per_s": 1.0 / per,
+        "s_per_iter": per, "iters_timed": len(times), "iters_of_config": w.iters, "cores": threads, "kind": "port",
+        "plan_build_s": build_s, "table_bytes": O.TableOperator.table_bytes(geo),
+        "peak_rss_bytes": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss * 1024,
+        "rss_before_tables_bytes": rss0 * 1024, "rss_after_tables_bytes": rss_tables * 1024,
+        "sample": f"full {workload} grid (N={geo.N}, M={geo.M}), |B|={w.batch} flat, the oracle's table restatement "
+                  f"of the reference algorithm (forward.py:183-336, solver.py:181-241); plan build and peak RSS "
+                  f"reported separately (BASELINE.md §3)",
+    }), flush=True)
+    return 0
 
 
 def hbm_peak_gbs() -> float:
@@ -606,6 +717,8 @@ def e2e_run(eng, scn, B, N, args, pg, local):
 
 def main():
     args = parse()
+    if args.cpu_child:
+        return cpu_child_main(args.cpu_child, args.cpu_seconds)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

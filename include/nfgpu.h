@@ -19,6 +19,8 @@
  *   nf_adjoint            replaces  forward.adjoint_apply / _adjoint_values    forward.py:353-359, 292-336
  *   nf_adjoint_prox       replaces  solver._gradient + soft_threshold +
  *                                   relative_magnitude_change (one SPGM step)  solver.py:181-183, 228-251, 287-289
+ *   nf_spgm_loop          replaces  solver._solve's iteration loop for flat batches    solver.py:259-318
+ *                                   (K iterations per launch, device-side termination test)
  *   nf_sample_flat        replaces  host minibatch sampling (flat uniform w/o replacement; the
  *   nf_plan_set_iter                structured Cartesian sampler solver.py:206-225 stays on the host)
  *   nf_soft_threshold     replaces  solver.soft_threshold                      solver.py:228-241
@@ -74,7 +76,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
 int nf_plan_destroy(nf_plan* plan);
 
 /* info[0]=slab voxels, [1]=M, [2]=warp tiles, [3]=tx group size, [4]=device bytes held,
- * [5]=forward CTAs per channel chunk, [6]=dtype, [7]=kernel launches issued so far */
+ * [5]=forward window (channels per forward launch), [6]=dtype, [7]=kernel launches issued so far */
 int nf_plan_info(const nf_plan* plan, int64_t info[8]);
 
 /* Stage a channel subset (device int32, length B, subset order, validated by the caller:
@@ -123,6 +125,22 @@ int nf_sample_flat(nf_plan* plan, uint64_t seed, uint64_t iter, int batch, int32
  * not null, receives the drawn [fs | ts | rs]. */
 int nf_sample_structured(nf_plan* plan, uint64_t seed, uint64_t iter, int n_f, int n_tx, int n_rx,
                          int32_t* lists_dev, void* stream);
+
+/* Persistent SPGM loop (the device-side loop of solver._solve, solver.py:259-318, for flat batches):
+ * `iters` iterations in ONE cooperative launch (one CTA per SM, grid barriers between phases). Iteration k
+ * draws its batch from idx_table[k*batch .. (k+1)*batch) (device int32, subset order, validated by the caller)
+ * or, when idx_table is NULL, from the Feistel sampler with iteration number iter0 + k (nf_sample_flat), then
+ * runs the same arithmetic as nf_batch_prepare + nf_forward + nf_adjoint_prox (bit-identical iterates).
+ * Iteration k reads s_a (k even) or s_b (k odd) and writes the other buffer. records (device,
+ * iters x 6 doubles) receives per iteration the nf_adjoint_prox statistics {sum|s|^2, sum(|s+|-|s|)^2,
+ * D_B, sum|s+|} and the device time since launch [ns]. The loop stops early when
+ * sqrt(stat1)/max(sqrt(stat0), 1e-12) < tol (solver.py:302, every CTA decides on the same bits) or when
+ * time_budget_s >= 0 of device time has passed (checked after each iteration). state (device, 3 ints) =
+ * {iterations run, reason: 0 all iterations / 1 tolerance / 2 time budget, budget flag}. Requirements:
+ * batch <= max_batch, one forward window and batch <= 4096 (else NF_ERR_STATE; use the per-call path). */
+int nf_spgm_loop(nf_plan* plan, const int32_t* idx_table_dev, int iters, uint64_t seed, uint64_t iter0, int batch,
+                 const void* ymeas_dev, void* s_a_dev, void* s_b_dev, double eta_over_b, double alpha, double tol,
+                 double time_budget_s, double* records_dev, int* state_dev, void* stream);
 
 /* Set the plan's device iteration counter (stream-ordered). */
 int nf_plan_set_iter(nf_plan* plan, uint64_t iter, void* stream);

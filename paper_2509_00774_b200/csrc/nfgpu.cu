@@ -374,8 +374,10 @@ struct Geo {
   int nx, ny, nzs, zb;  // slab: nzs planes starting at global plane zb
   int ntx, nty, ntz, ntiles;
   int Tg, ng;
+  int tg_mul;  // ceil(65536 / Tg): tx group of transmitter t = (t * tg_mul) >> 16 (exact for t < 32768 / Tg)
   double corner[3], sp[3];
 };
+__device__ __forceinline__ int tx_group(const Geo& g, int t) { return (t * g.tg_mul) >> 16; }
 
 __device__ __forceinline__ void tile_coords(const Geo& g, int tile, int& tx, int& ty, int& tz) {
   tz = tile / (g.ntx * g.nty);
@@ -486,6 +488,33 @@ __device__ __forceinline__ int block_excl_scan_1024(int v, int* sh, int& total) 
   const int pre = (wid > 0 ? sh[wid - 1] : 0) + x - v;
   __syncthreads();
   return pre;
+}
+
+// exclusive block scan for any blockDim that is a multiple of 32 (<= 1024); sh: 32 ints of shared memory
+__device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < nw ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, w, o);
+      if (lane >= o) w += y;
+    }
+    sh[lane] = w;
+  }
+  __syncthreads();
+  total = sh[nw - 1];
+  const int res = (wid > 0 ? sh[wid - 1] : 0) + x - v;
+  __syncthreads();
+  return res;
 }
 
 __global__ void __launch_bounds__(1024) count_kernel(const int* __restrict__ pos_of_key, int KS,
@@ -745,7 +774,7 @@ __device__ __forceinline__ unsigned build_records(const Geo& g, const WarpSmem<R
   }
   int key = -1, toff = 0;
   if (L < nb) {
-    const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = t / g.Tg;
+    const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = tx_group(g, t);
     const double x = cr.kd * (ws.d0[t] + ws.d0[g.T + r]);
     R4<Real> q;
     if constexpr (std::is_same<Real, float>::value) {
@@ -910,7 +939,8 @@ __global__ void __launch_bounds__(256) resid_kernel(const int* __restrict__ sm, 
 // g (plain adjoint) or applies the prox and the termination statistics (SPGM step).
 template <typename Real, bool PROX>
 __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, int chunk, int C, int L, const QV<Real>& gr,
-                                             const QV<Real>& gi) {
+                                             const QV<Real>& gi, const Real* __restrict__ s_in,
+                                             Real* __restrict__ s_out) {
   const Geo& g = a.g;
   Real Gr[V], Gi[V];
 #pragma unroll
@@ -976,13 +1006,13 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
     if (full) {
 #pragma unroll
       for (int u = 0; u < NU; ++u) *reinterpret_cast<U16*>(io + u * (16 / sizeof(Real))) =
-          reinterpret_cast<const U16*>(a.s_in + 2 * n0)[u];
+          reinterpret_cast<const U16*>(s_in + 2 * n0)[u];
     } else {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const bool in = x0 + v < g.nx && y < g.ny && z < g.nzs;
-        io[2 * v] = in ? a.s_in[2 * (n0 + v)] : Real(0);
-        io[2 * v + 1] = in ? a.s_in[2 * (n0 + v) + 1] : Real(0);
+        io[2 * v] = in ? s_in[2 * (n0 + v)] : Real(0);
+        io[2 * v + 1] = in ? s_in[2 * (n0 + v) + 1] : Real(0);
       }
     }
   }
@@ -1009,7 +1039,7 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
       st3 += m1;
     }
   }
-  Real* dst = PROX ? a.s_out : a.gout;
+  Real* dst = PROX ? s_out : a.gout;
   if (full) {
 #pragma unroll
     for (int u = 0; u < NU; ++u)
@@ -1038,16 +1068,15 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
   }
 }
 
+// One adjoint warp unit (tile, channel chunk) of the flat kernel: the body of adj_kernel, also run by the
+// persistent SPGM loop (spgm_loop_kernel). wbase: this warp's shared-memory region.
 template <typename Real, bool PROX, bool EXACT>
-__global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(AdjArgs<Real> a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void adj_unit(const AdjArgs<Real>& a, int unit, unsigned char* wbase, int L,
+                                         const Real* __restrict__ s_in, Real* __restrict__ s_out) {
   const Geo& g = a.g;
-  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int unit = blockIdx.x * ADJ_WARPS + w;
-  if (unit >= a.t1 * a.CH + (g.ntiles - a.t1) * a.CH2) return;  // warps are independent: no block barriers below
   int tile, chunk, C;
   unit_map(unit, g.ntiles, a.CH, a.t1, a.CH2, a.order, tile, chunk, C);
-  const WarpSmem<Real> ws = carve<Real>(smem_raw + (size_t)w * warp_smem_bytes<Real>(g.Tg, g.A), g.Tg, g.A);
+  const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A);
   const int j0 = chunk_bound(a.B, chunk, C, a.order, a.taper);
   const int j1 = chunk_bound(a.B, chunk + 1, C, a.order, a.taper);
   // Start-up loads that do not depend on the predecessor kernel are issued before griddepcontrol.wait:
@@ -1109,7 +1138,17 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(Adj
   flush(iR, hr, hi, gr, gi);
   stage_wait();
 
-  adj_epilogue<Real, PROX>(a, tile, chunk, C, L, gr, gi);
+  adj_epilogue<Real, PROX>(a, tile, chunk, C, L, gr, gi, s_in, s_out);
+}
+
+template <typename Real, bool PROX, bool EXACT>
+__global__ void __launch_bounds__(ADJ_WARPS * 32, NFGPU_MINB_ADJ) adj_kernel(AdjArgs<Real> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+  const int unit = blockIdx.x * ADJ_WARPS + w;
+  if (unit >= a.t1 * a.CH + (a.g.ntiles - a.t1) * a.CH2) return;  // warps are independent: no block barriers
+  adj_unit<Real, PROX, EXACT>(a, unit, smem_raw + (size_t)w * warp_smem_bytes<Real>(a.g.Tg, a.g.A), L, a.s_in,
+                              a.s_out);
 }
 
 // stats = {Σ_tile part[.][0], Σ part[.][1], ½ Σ_block dpart, Σ part[.][3]} in a fixed order
@@ -1197,16 +1236,13 @@ __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __re
 // 32 lanes in a fixed order, and the tile's per-channel sum goes to part[tile][j].
 // With tile-major units (large tables), chunks of one tile are adjacent units, so they run
 // together and share the tile's table rows in L2.
+// One forward warp unit (tile, channel chunk): the body of fwd_kernel, also run by spgm_loop_kernel.
 template <typename Real, bool EXACT>
-__global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(FwdArgs<Real> a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void fwd_unit(const FwdArgs<Real>& a, int unit, unsigned char* wbase, int L,
+                                         const Real* __restrict__ sv) {
   const Geo& g = a.g;
-  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int unit = blockIdx.x * FWD_WARPS + w;
-  if (unit >= a.t1 * a.Q + (g.ntiles - a.t1) * a.Q2) return;  // warps are independent: no block barriers
   int tile, chunk, C;
   unit_map(unit, g.ntiles, a.Q, a.t1, a.Q2, a.order, tile, chunk, C);
-  unsigned char* wbase = smem_raw + (size_t)w * fwd_warp_bytes<Real>(g.Tg, g.A);
   const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A, 1);
   R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A, 1));  // [TBR][33]
 
@@ -1231,7 +1267,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
     if (x0 + V <= g.nx && y < g.ny && z < g.nzs && (sizeof(Real) == 8 || (g.nx & 1) == 0)) {
 #pragma unroll
       for (int u = 0; u < NU; ++u) {
-        const U16 w = reinterpret_cast<const U16*>(a.s + 2 * n0)[u];
+        const U16 w = reinterpret_cast<const U16*>(sv + 2 * n0)[u];
         const Real* t = reinterpret_cast<const Real*>(&w);
 #pragma unroll
         for (int k = 0; k < PU; k += 2) {
@@ -1243,8 +1279,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const bool ok = x0 + v < g.nx && y < g.ny && z < g.nzs;
-        srv[v] = ok ? a.s[2 * (n0 + v)] : Real(0);
-        siv[v] = ok ? a.s[2 * (n0 + v) + 1] : Real(0);
+        srv[v] = ok ? sv[2 * (n0 + v)] : Real(0);
+        siv[v] = ok ? sv[2 * (n0 + v) + 1] : Real(0);
       }
     }
   }
@@ -1258,7 +1294,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
   int cur_tg = -1, pf_r = -1, carry = -1;
   if (c0 < c1) {  // stage the first run's tx group and rx rows as soon as the first record is in
     const int pk0 = __shfl_sync(FULL, nxt.pk, 0);
-    cur_tg = pk_t(pk0) / g.Tg;
+    cur_tg = tx_group(g, pk_t(pk0));
     pf_r = pk_r(pk0);
     load_tgroup_async<Real>(g, tabt, ws.tside, cur_tg, L);
     stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
@@ -1345,6 +1381,15 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(Fwd
     }
   }
   stage_wait();
+}
+
+template <typename Real, bool EXACT>
+__global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(FwdArgs<Real> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+  const int unit = blockIdx.x * FWD_WARPS + w;
+  if (unit >= a.t1 * a.Q + (a.g.ntiles - a.t1) * a.Q2) return;  // warps are independent: no block barriers
+  fwd_unit<Real, EXACT>(a, unit, smem_raw + (size_t)w * fwd_warp_bytes<Real>(a.g.Tg, a.g.A), L, a.s);
 }
 
 // ------------------------------------------------------------------ structured (Cartesian) batches
@@ -1648,7 +1693,7 @@ __global__ void __launch_bounds__(SW * 32, NFGPU_MINB_STRUCT) adj_struct_kernel(
       Gi[v] += q[2 * v + 1];
     }
   }
-  adj_epilogue<Real, PROX>(a, tile, chunk, a.CH, L, make_v(Gr), make_v(Gi));
+  adj_epilogue<Real, PROX>(a, tile, chunk, a.CH, L, make_v(Gr), make_v(Gi), a.s_in, a.s_out);
 }
 
 // Structured forward: y_ftr = p_f/(4π) Σ_n U_ft(n)·(V_fr(n) s_n). The block stages W_fr = V_fr·s;
@@ -2160,7 +2205,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) adj_tc_kernel(AdjArgs<float> a,
           Gi[v] = cb[p * 2 + 1] + cb[(128 + p) * 2 + 1];
         }
       }
-      adj_epilogue<float, PROX>(a, tile, hb * fch + fc, a.CH, L, make_v(Gr), make_v(Gi));
+      adj_epilogue<float, PROX>(a, tile, hb * fch + fc, a.CH, L, make_v(Gr), make_v(Gi), a.s_in, a.s_out);
     }
   }
   tc_fence_before();
@@ -2670,6 +2715,627 @@ __global__ void __launch_bounds__(1024) magchange_kernel(const Real* __restrict_
   }
 }
 
+// ------------------------------------------------------------------ persistent SPGM loop
+//
+// spgm_loop_kernel runs K SPGM iterations (solver.py:281-310) of a flat batch in ONE cooperative launch, one CTA
+// per SM: the device-side loop for latency-bound configurations (BASELINE Small: 12 launches of ~3 us each per
+// iteration otherwise). Per iteration, between grid barriers:
+//   P0  every CTA draws the batch (index table row k, or the Feistel sampler) and sorts its (key, position)
+//       keys by rank in shared memory (same order as the counting sort of nf_batch_prepare), then writes its
+//       slice of the sorted channel records
+//   P1  forward warp units (fwd_unit, the body of fwd_kernel) over the grid's warps -> part[tile][j]
+//   P2  level 1 of the forward reduce (fwd_reduce1_kernel's sums)
+//   P3  level 2 + residual records, per 256-channel group (fwd_reduce2_kernel + resid_kernel)
+//   P4  adjoint + prox warp units (adj_unit) -> s_out, per-tile statistics
+//   P5  every CTA reduces the statistics (stats_reduce_kernel's tree), records them and tests the tolerance
+// Every value is computed by the same code in the same order as the per-launch path, so the iterates are
+// bit-identical to nf_batch_prepare + nf_forward + nf_adjoint_prox (tested). The time budget is checked on the
+// device clock by CTA 0 and takes effect after the next barrier.
+constexpr int LOOP_SORT_MAX = 4096;  // batches sorted in shared memory
+constexpr int LOOP_REC = 6;          // per iteration: the 4 statistics, device time (ns since launch), spare
+
+struct LoopArgs {
+  KeyMap km;
+  int M, B, K, nseg, hb;
+  const int* __restrict__ idx_table;  // [K][B] (subset order) or null: Feistel sampler
+  uint64_t seed, iter0;
+  const double* __restrict__ kd;
+  const double* __restrict__ pulse;
+  const void* ymeas;
+  int* sm;
+  int* spos;
+  int* sf;
+  ChanRec* crec;
+  double2* tmp;
+  double* dpart;
+  double* stat_part;
+  double tol;
+  long long budget_ns;  // < 0: no time budget
+  double eta_over_b, alpha;  // tiny_loop_kernel's prox (spgm_loop_kernel takes them from its AdjArgs)
+  double* rec;          // [K][LOOP_REC]
+  int* state;           // {iterations, reason: 0 max_iters / 1 tolerance / 2 time budget, stop flag}
+  unsigned* bar;        // grid barrier {arrivals, generation}
+  int kwords;           // 32-bit words of the key-space bitmap of the P0 rank sort (0: pairwise ranks)
+  int* ctr;             // work-unit counters {forward, adjoint}: warps fetch units past the first TW dynamically
+  void* s_a;            // iteration k reads s_a (k even) or s_b (k odd) and writes the other
+  void* s_b;
+  size_t warp_bytes;
+  unsigned long long* prof;  // diagnostics (NFGPU_LOOP_PROFILE): CTA 0's device clock at each phase boundary
+};
+constexpr int LOOP_PROF = 12;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* a, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// sense-reversing grid barrier (all CTAs co-resident: cooperative launch). Thread 0 arrives with an acq_rel
+// atomic (its release is cumulative over the CTA's writes ordered before it by __syncthreads), the last arrival
+// publishes the next generation with a release store, the others poll it with acquire loads.
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* a, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire_u32(bar + 1);
+    if (atom_add_acq_rel(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;  // ordered before the release below; nobody touches it until the new generation is seen
+      st_release_u32(bar + 1, gen + 1);
+    } else {
+      int spins = 0;
+      while (ld_acquire_u32(bar + 1) == gen)
+        if (++spins > 64) __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+// next work unit of a warp: the first TW units are assigned statically (unit = global warp index), later ones
+// are fetched in launch order from a counter, like the hardware's CTA scheduler (balances unequal units)
+__device__ __forceinline__ int next_unit(int* ctr, int TW, int L) {
+  int u = 0;
+  if (L == 0) u = atomicAdd(ctr, 1);
+  return __shfl_sync(FULL, u, 0) + TW;
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ int loop_index(const LoopArgs& la, int k, int i) {
+  if (la.idx_table) return la.idx_table[(size_t)k * la.B + i];
+  const uint64_t key = sample_key(la.seed, la.iter0 + (uint64_t)k);
+  uint32_t x = (uint32_t)i;
+  do {
+    x = feistel(x, la.hb, key);
+  } while (x >= (uint32_t)la.M);
+  return (int)x;
+}
+
+template <typename Real, bool EXACT>
+__global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<Real> fa, AdjArgs<Real> aa) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int scan_sh[32];
+  // P3 / P5 scratch in the warp regions (no warp unit is in flight during those phases)
+  double(*red)[256] = reinterpret_cast<double(*)[256]>(smem_raw);
+  double(*grp_sh)[8] = reinterpret_cast<double(*)[8]>(smem_raw + 4 * 256 * sizeof(double));
+  const Geo& g = fa.g;
+  const int NW = blockDim.x >> 5, w = threadIdx.x >> 5, L = threadIdx.x & 31;
+  // global warp index, CTA-fastest: the first units of a phase land on different SMs (small problems get one
+  // warp per SM instead of a few busy SMs)
+  const int gw = w * gridDim.x + blockIdx.x, TW = gridDim.x * NW;
+  const int B = la.B;
+  const int nfu = fa.t1 * fa.Q + (g.ntiles - fa.t1) * fa.Q2;
+  const int nau = aa.t1 * aa.CH + (g.ntiles - aa.t1) * aa.CH2;
+  unsigned char* wbase = smem_raw + (size_t)w * la.warp_bytes;
+  const unsigned long long t0 = globaltimer();
+  int done = 0, reason = 0;
+#define LOOP_STAMP(i) \
+  if (la.prof && blockIdx.x == 0 && threadIdx.x == 0) la.prof[(size_t)k * LOOP_PROF + (i)] = globaltimer() - t0
+  for (int k = 0; k < la.K; ++k) {
+    LOOP_STAMP(0);
+    const Real* s_in = reinterpret_cast<const Real*>((k & 1) ? la.s_b : la.s_a);
+    Real* s_out = reinterpret_cast<Real*>((k & 1) ? la.s_a : la.s_b);
+    if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[1] = 0;  // every warp is past its last adjoint fetch
+    // ---- P0: draw the batch and rank its keys (every CTA; keys are distinct), write this CTA's slice of the
+    // records in key order (the counting sort's order). Ranks come from a bitmap of the key space and a prefix
+    // count of its words when the bitmap fits in shared memory, else from pairwise comparisons.
+    {
+      int* keys = reinterpret_cast<int*>(smem_raw);
+      int* order = keys + LOOP_SORT_MAX;
+      unsigned* bm = reinterpret_cast<unsigned*>(order + LOOP_SORT_MAX);
+      int* pre = reinterpret_cast<int*>(bm + la.kwords);
+      const bool bitmap = la.kwords > 0;
+      if (bitmap)
+        for (int i = threadIdx.x; i < la.kwords; i += blockDim.x) bm[i] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < B; i += blockDim.x) {
+        const int key = key_of(la.km, loop_index(la, k, i));
+        keys[i] = key;
+        if (bitmap) atomicOr(bm + (key >> 5), 1u << (key & 31));
+      }
+      __syncthreads();
+      if (bitmap) {  // pre[w] = set bits in words < w
+        const int per = (la.kwords + blockDim.x - 1) / blockDim.x, w0 = threadIdx.x * per;
+        const int w1 = min(la.kwords, w0 + per);
+        int cnt = 0;
+        for (int q = w0; q < w1; ++q) cnt += __popc(bm[q]);
+        int total;
+        int run = block_excl_scan(cnt, scan_sh, total);
+        for (int q = w0; q < w1; ++q) {
+          pre[q] = run;
+          run += __popc(bm[q]);
+        }
+        __syncthreads();
+      }
+      const int j0 = (int)(((long long)B * blockIdx.x) / gridDim.x), j1 = (int)(((long long)B * (blockIdx.x + 1)) / gridDim.x);
+      for (int i = threadIdx.x; i < B; i += blockDim.x) {
+        const int ki = keys[i];
+        int r = 0;
+        if (bitmap) {
+          r = pre[ki >> 5] + __popc(bm[ki >> 5] & ((1u << (ki & 31)) - 1u));
+        } else {
+          for (int q = 0; q < B; ++q) r += keys[q] < ki;
+        }
+        if (r >= j0 && r < j1) order[r] = i;
+      }
+      __syncthreads();
+      for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        const int pos = order[j], key = keys[pos];
+        const int4 c = chan_of_key(la.km, key);
+        la.sm[j] = c.z + la.km.R * (c.y + la.km.T * c.x);
+        la.spos[j] = pos;
+        ChanRec q;
+        q.kd = la.kd[c.x];
+        q.kf = (float)q.kd;
+        q.pk = c.y | (c.z << 16);
+        la.crec[j] = q;
+        la.sf[j] = c.x;
+      }
+    }
+    LOOP_STAMP(1);
+    grid_sync(la.bar);
+    LOOP_STAMP(2);
+    if (k > 0 && *(volatile int*)(la.state + 2)) {  // time budget spent (CTA 0's decision of iteration k-1)
+      reason = 2;
+      break;
+    }
+    // ---- P1: forward
+    for (int u = gw; u < nfu; u = next_unit(la.ctr, TW, L)) fwd_unit<Real, EXACT>(fa, u, wbase, L, s_in);
+    LOOP_STAMP(3);
+    grid_sync(la.bar);
+    LOOP_STAMP(4);
+    // ---- P2: level 1 of the forward reduce: tmp[seg][j] = sum over the segment's tiles (fixed order)
+    if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[0] = 0;  // every warp is past its last forward fetch
+    {
+      const int n = la.nseg * B;
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int seg = i / B, j = i - seg * B;
+        const int x0 = (int)(((long long)g.ntiles * seg) / la.nseg), x1 = (int)(((long long)g.ntiles * (seg + 1)) / la.nseg);
+        double sr = 0, si = 0;
+        for (int x = x0; x < x1; ++x) {
+          const R2<Real> v = reinterpret_cast<const R2<Real>*>(fa.part)[(size_t)x * B + j];
+          sr += (double)v.x;
+          si += (double)v.y;
+        }
+        la.tmp[(size_t)seg * B + j] = make_double2(sr, si);
+      }
+    }
+    LOOP_STAMP(5);
+    grid_sync(la.bar);
+    LOOP_STAMP(6);
+    // ---- P3: level 2 (y = p_f/(4pi) sum, rounded to Real as stored), residual records, dpart per 256 channels
+    {
+      const int half = threadIdx.x >> 8, ht = threadIdx.x & 255, halves = blockDim.x >> 8;
+      const int ngrp = (B + 255) / 256;
+      const Real* ym = reinterpret_cast<const Real*>(la.ymeas);
+      for (int grp = blockIdx.x * halves + half; half < halves && grp < ngrp; grp += gridDim.x * halves) {
+        const int j = grp * 256 + ht;
+        double e = 0;
+        if (j < B) {
+          double sr = 0, si = 0;
+          for (int sgi = 0; sgi < la.nseg; ++sgi) {
+            const double2 v = la.tmp[(size_t)sgi * B + j];
+            sr += v.x;
+            si += v.y;
+          }
+          const int f = la.sf[j];
+          const double pr = la.pulse[2 * f] / (4.0 * PI), pim = la.pulse[2 * f + 1] / (4.0 * PI);
+          const Real yr = (Real)(pr * sr - pim * si), yi = (Real)(pr * si + pim * sr);
+          double rr = (double)yr, ri = (double)yi;
+          const int m = la.sm[j];
+          rr -= (double)ym[2 * (size_t)m];
+          ri -= (double)ym[2 * (size_t)m + 1];
+          e = rr * rr + ri * ri;
+          const double qr = la.pulse[2 * f] / (4.0 * PI), qi = -la.pulse[2 * f + 1] / (4.0 * PI);
+          R2<Real> wv;
+          wv.x = (Real)(qr * rr - qi * ri);
+          wv.y = (Real)(qr * ri + qi * rr);
+          const_cast<R2<Real>*>(aa.wrec)[j] = wv;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
+        if ((ht & 31) == 0) grp_sh[half][ht >> 5] = e;
+        named_sync(1 + half, 256);
+        if (ht == 0) {
+          double t = 0;
+          for (int i = 0; i < 8; ++i) t += grp_sh[half][i];
+          la.dpart[grp] = t;
+        }
+        named_sync(1 + half, 256);
+      }
+    }
+    LOOP_STAMP(7);
+    grid_sync(la.bar);
+    LOOP_STAMP(8);
+    // ---- P4: adjoint + prox
+    for (int u = gw; u < nau; u = next_unit(la.ctr + 1, TW, L)) adj_unit<Real, true, EXACT>(aa, u, wbase, L, s_in, s_out);
+    LOOP_STAMP(9);
+    grid_sync(la.bar);
+    LOOP_STAMP(10);
+    // ---- P5: statistics (stats_reduce_kernel's order, threads 0-255 of every CTA), record, termination
+    if (threadIdx.x < 256) {
+      double acc[4] = {0, 0, 0, 0};
+      for (int i = threadIdx.x; i < g.ntiles; i += 256) {
+        acc[0] += la.stat_part[(size_t)i * 4 + 0];
+        acc[1] += la.stat_part[(size_t)i * 4 + 1];
+        acc[3] += la.stat_part[(size_t)i * 4 + 3];
+      }
+      const int nd = (B + 255) / 256;
+      for (int i = threadIdx.x; i < nd; i += 256) acc[2] += la.dpart[i];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = acc[q];
+      named_sync(3, 256);
+      for (int sh = 128; sh > 0; sh >>= 1) {
+        if (threadIdx.x < sh)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + sh];
+        named_sync(3, 256);
+      }
+    }
+    __syncthreads();
+    const double st0 = red[0][0], st1 = red[1][0];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      double* r = la.rec + (size_t)k * LOOP_REC;
+      r[0] = st0;
+      r[1] = st1;
+      r[2] = 0.5 * red[2][0];
+      r[3] = red[3][0];
+      const unsigned long long now = globaltimer();
+      r[4] = (double)(now - t0);
+      r[5] = 0;
+      if (la.budget_ns >= 0 && (long long)(now - t0) > la.budget_ns) {
+        la.state[2] = 1;
+        __threadfence();
+      }
+    }
+    done = k + 1;
+    LOOP_STAMP(11);
+    const double change = sqrt(st1) / fmax(sqrt(st0), 1e-12);
+    if (change < la.tol) {  // every CTA reaches the same decision from the same bits
+      reason = 1;
+      break;
+    }
+    __syncthreads();  // red[][] is rewritten next iteration
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (reason == 0 && la.state[2]) reason = 2;  // the budget ran out on the last iteration of the launch
+    la.state[0] = done;
+    la.state[1] = reason;
+  }
+}
+#undef LOOP_STAMP
+template __global__ void spgm_loop_kernel<float, false>(LoopArgs, FwdArgs<float>, AdjArgs<float>);
+template __global__ void spgm_loop_kernel<float, true>(LoopArgs, FwdArgs<float>, AdjArgs<float>);
+template __global__ void spgm_loop_kernel<double, true>(LoopArgs, FwdArgs<double>, AdjArgs<double>);
+template __global__ void spgm_loop_kernel<double, false>(LoopArgs, FwdArgs<double>, AdjArgs<double>);
+
+// ------------------------------------------------------------------ persistent loop for tiny problems
+//
+// BASELINE Small (|B| = 32, N = 2048) has 65,536 entries per operator application: every warp unit of the
+// flat kernels is then a chain of start-up latencies (~10 us) rather than work. tiny_loop_kernel runs the
+// SPGM iteration for such problems (|B|·N <= TINY_MAX_ENTRIES) with one thread per voxel and the entries
+// evaluated straight from the geometry in fp64 (distances, phase in revolutions reduced exactly, table
+// cis), between three grid barriers per iteration:
+//   PA  items (channel group of JC, block of 256 voxels): each thread forms A[m_j, n]·s_n for its voxel and
+//       the block sums them in a fixed order -> part[vb][j]
+//   PB  per channel: y_j = p_f/(4π)·Σ_vb part[vb][j] (fixed order), residual record w_j = conj(p_f)/(4π)·(y_j −
+//       y_meas[m_j]) and ½|y_j − y_meas|² per 256-channel group
+//   PC  items (voxel block, channel chunk): thread-per-voxel Σ_j conj(A)·w_j -> gpart; the last chunk of a
+//       voxel block to finish sums the chunks in order, applies s − η/B·g and the complex soft threshold,
+//       and writes the block's termination statistics
+//   PD  every CTA reduces the statistics in a fixed order, records them and tests the tolerance
+// The arithmetic differs from the flat kernels' (per-voxel fp64 entries, different summation trees) but is
+// fixed for a given plan, batch and iterate: results are deterministic, and agree with the reference to the
+// c128 tolerance (tests/test_gpu_loop.py).
+constexpr long long TINY_MAX_ENTRIES = 1LL << 20;  // |B| x slab voxels
+constexpr int TINY_JC = 8;                         // channels per PA item, at most
+
+struct TinyArgs {
+  const double* ant;   // [A][3] antenna positions (tx then rx)
+  const double* kd;    // f / c
+  double corner[3], sp[3];
+  int nx, ny, nzs, zb, T, R;
+  int nvb, jc, cc;     // voxel blocks of 256, channels per PA item, channel chunks per PC voxel block
+  int chunk_max;       // largest PC channel chunk
+  double2* part;       // [nvb][B]
+  double* e2;          // [B] |y_j - y_meas|^2
+  double2* gpart;      // [cc][nvb][256]
+  int* vbcnt;          // [nvb] arrival counters (zero between iterations)
+  double* stat_part;   // [nvb][4]
+};
+
+// e^{-j 2π kd (dT + dR)} / (dT dR) for voxel centre (x, y, z) and channel (t, r, kd), in fp64
+__device__ __forceinline__ double2 tiny_entry(const TinyArgs& ta, double x, double y, double z, int t, int r,
+                                             double kd) {
+  const double* a = ta.ant + 3 * t;
+  const double* b = ta.ant + 3 * (ta.T + r);
+  const double dT = sqrt((x - a[0]) * (x - a[0]) + (y - a[1]) * (y - a[1]) + (z - a[2]) * (z - a[2]));
+  const double dR = sqrt((x - b[0]) * (x - b[0]) + (y - b[1]) * (y - b[1]) + (z - b[2]) * (z - b[2]));
+  const double rev = kd * (dT + dR);
+  double s, c;
+  cis_rev(rev - rint(rev), s, c);
+  const double amp = 1.0 / (dT * dR);
+  return make_double2(c * amp, -s * amp);
+}
+
+__device__ __forceinline__ void tiny_voxel(const TinyArgs& ta, int n, double& x, double& y, double& z) {
+  const int ix = n % ta.nx, q = n / ta.nx, iy = q % ta.ny, iz = q / ta.ny + ta.zb;
+  x = ta.corner[0] + ix * ta.sp[0];
+  y = ta.corner[1] + iy * ta.sp[1];
+  z = ta.corner[2] + iz * ta.sp[2];
+}
+
+// fixed-order sum over the 256 threads of a CTA of JC complex values: warp trees, then warps in order
+__device__ __forceinline__ void tiny_block_sum(double2* v, int jc, double2 (*sh)[TINY_JC]) {
+  const int L = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < TINY_JC; ++q) {
+    if (q >= jc) break;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v[q].x += __shfl_xor_sync(FULL, v[q].x, o);
+      v[q].y += __shfl_xor_sync(FULL, v[q].y, o);
+    }
+    if (L == 0) sh[w][q] = v[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < jc) {
+    double2 t = make_double2(0, 0);
+    for (int i = 0; i < 8; ++i) {
+      t.x += sh[i][threadIdx.x].x;
+      t.y += sh[i][threadIdx.x].y;
+    }
+    v[0] = t;  // thread q < jc holds the sum of channel q
+  }
+  __syncthreads();
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(256, 1) tiny_loop_kernel(LoopArgs la, TinyArgs ta) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double2 bsum[8][TINY_JC];
+  __shared__ double red[4][256];
+  __shared__ int last_sh;
+  double2* wsm = reinterpret_cast<double2*>(smem_raw);  // [chunk] residual records of the item's channel chunk
+  int4* csm = reinterpret_cast<int4*>(smem_raw + (size_t)ta.chunk_max * sizeof(double2));  // [chunk] channels
+  const int B = la.B, nvb = ta.nvb, jc = ta.jc, cc = ta.cc;
+  const long long nvox = (long long)ta.nx * ta.ny * ta.nzs;
+  const Real* ym = reinterpret_cast<const Real*>(la.ymeas);
+  const unsigned long long t0 = globaltimer();
+  int done = 0, reason = 0;
+#define TINY_STAMP(i) \
+  if (la.prof && blockIdx.x == 0 && threadIdx.x == 0) la.prof[(size_t)k * LOOP_PROF + (i)] = globaltimer() - t0
+  for (int k = 0; k < la.K; ++k) {
+    TINY_STAMP(0);
+    const Real* s_in = reinterpret_cast<const Real*>((k & 1) ? la.s_b : la.s_a);
+    Real* s_out = reinterpret_cast<Real*>((k & 1) ? la.s_a : la.s_b);
+    // ---- PA: forward partials per (channel group, voxel block)
+    const int ngrp = (B + jc - 1) / jc;
+    for (int item = blockIdx.x; item < ngrp * nvb; item += gridDim.x) {
+      const int jg = item / nvb, vb = item - jg * nvb;
+      const int n = vb * 256 + threadIdx.x;
+      double2 v[TINY_JC];
+      double sr = 0, si = 0, x = 0, y = 0, z = 0;
+      if (n < nvox) {
+        sr = (double)s_in[2 * (size_t)n];
+        si = (double)s_in[2 * (size_t)n + 1];
+        tiny_voxel(ta, n, x, y, z);
+      }
+#pragma unroll
+      for (int q = 0; q < TINY_JC; ++q) {
+        v[q] = make_double2(0, 0);
+        const int j = jg * jc + q;
+        if (q < jc && j < B && n < nvox) {
+          const int m = loop_index(la, k, j);
+          const int f = m / (ta.T * ta.R), rem = m - f * ta.T * ta.R, t = rem / ta.R, r = rem - t * ta.R;
+          const double2 e = tiny_entry(ta, x, y, z, t, r, ta.kd[f]);
+          v[q] = make_double2(e.x * sr - e.y * si, e.x * si + e.y * sr);
+        }
+      }
+      tiny_block_sum(v, jc, bsum);
+      const int j = jg * jc + threadIdx.x;
+      if (threadIdx.x < jc && j < B) ta.part[(size_t)vb * B + j] = v[0];
+    }
+    TINY_STAMP(1);
+    grid_sync(la.bar);
+    TINY_STAMP(2);
+    if (k > 0 && *(volatile int*)(la.state + 2)) {
+      reason = 2;
+      break;
+    }
+    // ---- PC: per (voxel block, channel chunk): the chunk's channel sums and residual records (recomputed by
+    // each of its voxel blocks from the same partials in the same order, so no barrier is needed before the
+    // adjoint; the vb = 0 item keeps ½|r_j|² for the statistics), the adjoint partial of the block over the
+    // chunk -> gpart; the last chunk of a voxel block to finish sums the chunks in order and applies the prox
+    for (int item = blockIdx.x; item < nvb * cc; item += gridDim.x) {
+      const int vb = item / cc, c = item - vb * cc;
+      const int n = vb * 256 + threadIdx.x;
+      const int j0 = (int)(((long long)B * c) / cc), j1 = (int)(((long long)B * (c + 1)) / cc);
+      for (int j = j0 + threadIdx.x; j < j1; j += 256) {
+        const int m = loop_index(la, k, j);
+        const int f = m / (ta.T * ta.R), rem = m - f * ta.T * ta.R, t = rem / ta.R, r = rem - t * ta.R;
+        double sr = 0, si = 0;
+        for (int q = 0; q < nvb; ++q) {
+          const double2 pp = __ldcg(ta.part + (size_t)q * B + j);
+          sr += pp.x;
+          si += pp.y;
+        }
+        const double pr = la.pulse[2 * f] / (4.0 * PI), pim = la.pulse[2 * f + 1] / (4.0 * PI);
+        const Real yr = (Real)(pr * sr - pim * si), yi = (Real)(pr * si + pim * sr);
+        const double rr = (double)yr - (double)ym[2 * (size_t)m], ri = (double)yi - (double)ym[2 * (size_t)m + 1];
+        wsm[j - j0] = make_double2(pr * rr + pim * ri, pr * ri - pim * rr);  // conj(p)/(4π)·r
+        csm[j - j0] = make_int4(f, t, r, m);
+        if (vb == 0) ta.e2[j] = rr * rr + ri * ri;
+      }
+      __syncthreads();
+      double gr = 0, gi = 0;
+      if (n < nvox) {
+        double x, y, z;
+        tiny_voxel(ta, n, x, y, z);
+        for (int j = 0; j < j1 - j0; ++j) {
+          const int4 q = csm[j];
+          const double2 e = tiny_entry(ta, x, y, z, q.y, q.z, ta.kd[q.x]);
+          const double2 wv = wsm[j];
+          gr += e.x * wv.x + e.y * wv.y;  // conj(e)·w
+          gi += e.x * wv.y - e.y * wv.x;
+        }
+      }
+      ta.gpart[((size_t)c * nvb + vb) * 256 + threadIdx.x] = make_double2(gr, gi);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) last_sh = atomicAdd(ta.vbcnt + vb, 1) == cc - 1;
+      __syncthreads();
+      if (!last_sh) continue;
+      __threadfence();
+      double st0 = 0, st1 = 0, st3 = 0;
+      if (n < nvox) {
+        gr = gi = 0;
+        for (int q = 0; q < cc; ++q) {
+          const double2 pp = __ldcg(ta.gpart + ((size_t)q * nvb + vb) * 256 + threadIdx.x);
+          gr += pp.x;
+          gi += pp.y;
+        }
+        const Real s_r = s_in[2 * (size_t)n], s_i = s_in[2 * (size_t)n + 1];
+        const Real ur = s_r - (Real)la.eta_over_b * (Real)gr, ui = s_i - (Real)la.eta_over_b * (Real)gi;
+        const Real mag = hypot(ur, ui);
+        const Real al = (Real)la.alpha;
+        const Real sc = mag > al ? (mag - al) / mag : Real(0);
+        const Real o_r = ur * sc, o_i = ui * sc;
+        s_out[2 * (size_t)n] = o_r;
+        s_out[2 * (size_t)n + 1] = o_i;
+        const double m0 = hypot((double)s_r, (double)s_i), m1 = hypot((double)o_r, (double)o_i);
+        st0 = m0 * m0;
+        st1 = (m1 - m0) * (m1 - m0);
+        st3 = m1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        st0 += __shfl_xor_sync(FULL, st0, o);
+        st1 += __shfl_xor_sync(FULL, st1, o);
+        st3 += __shfl_xor_sync(FULL, st3, o);
+      }
+      if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = st0;
+        red[1][threadIdx.x >> 5] = st1;
+        red[3][threadIdx.x >> 5] = st3;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double a0 = 0, a1 = 0, a3 = 0;
+        for (int i = 0; i < 8; ++i) {
+          a0 += red[0][i];
+          a1 += red[1][i];
+          a3 += red[3][i];
+        }
+        ta.stat_part[(size_t)vb * 4 + 0] = a0;
+        ta.stat_part[(size_t)vb * 4 + 1] = a1;
+        ta.stat_part[(size_t)vb * 4 + 2] = 0;
+        ta.stat_part[(size_t)vb * 4 + 3] = a3;
+        ta.vbcnt[vb] = 0;
+      }
+      __syncthreads();
+    }
+    TINY_STAMP(3);
+    grid_sync(la.bar);
+    TINY_STAMP(4);
+    // ---- PD: statistics (fixed order, every CTA), record, termination
+    if (nvb <= 256 && B <= 1024) {  // one warp: lane-strided sums, then a shuffle tree (no block barriers)
+      if (threadIdx.x < 32) {
+        double acc[4] = {0, 0, 0, 0};
+        for (int i = threadIdx.x; i < nvb; i += 32) {
+          acc[0] += __ldcg(ta.stat_part + (size_t)i * 4 + 0);
+          acc[1] += __ldcg(ta.stat_part + (size_t)i * 4 + 1);
+          acc[3] += __ldcg(ta.stat_part + (size_t)i * 4 + 3);
+        }
+        for (int i = threadIdx.x; i < B; i += 32) acc[2] += __ldcg(ta.e2 + i);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(FULL, acc[q], o);
+          if (threadIdx.x == 0) red[q][0] = acc[q];
+        }
+      }
+      __syncthreads();
+    } else {
+      double acc[4] = {0, 0, 0, 0};
+      for (int i = threadIdx.x; i < nvb; i += 256) {
+        acc[0] += ta.stat_part[(size_t)i * 4 + 0];
+        acc[1] += ta.stat_part[(size_t)i * 4 + 1];
+        acc[3] += ta.stat_part[(size_t)i * 4 + 3];
+      }
+      for (int i = threadIdx.x; i < B; i += 256) acc[2] += ta.e2[i];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = acc[q];
+      __syncthreads();
+      for (int sh = 128; sh > 0; sh >>= 1) {
+        if (threadIdx.x < sh)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + sh];
+        __syncthreads();
+      }
+    }
+    const double st0 = red[0][0], st1 = red[1][0];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      double* r = la.rec + (size_t)k * LOOP_REC;
+      r[0] = st0;
+      r[1] = st1;
+      r[2] = 0.5 * red[2][0];
+      r[3] = red[3][0];
+      const unsigned long long now = globaltimer();
+      r[4] = (double)(now - t0);
+      r[5] = 0;
+      if (la.budget_ns >= 0 && (long long)(now - t0) > la.budget_ns) {
+        la.state[2] = 1;
+        __threadfence();
+      }
+    }
+    done = k + 1;
+    TINY_STAMP(5);
+    const double change = sqrt(st1) / fmax(sqrt(st0), 1e-12);
+    if (change < la.tol) {
+      reason = 1;
+      break;
+    }
+    __syncthreads();
+  }
+#undef TINY_STAMP
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (reason == 0 && la.state[2]) reason = 2;
+    la.state[0] = done;
+    la.state[1] = reason;
+  }
+}
+template __global__ void tiny_loop_kernel<float>(LoopArgs, TinyArgs);
+template __global__ void tiny_loop_kernel<double>(LoopArgs, TinyArgs);
+
 }  // namespace
 
 // ====================================================================== plan
@@ -2746,6 +3412,12 @@ struct nf_plan {
   void* comm_peer[PEER_MAX] = {};
   unsigned long long* d_epoch = nullptr;
   int* d_comm_err = nullptr;
+  unsigned* d_loopbar = nullptr;  // persistent SPGM loop: grid barrier {arrivals, generation} (zero between launches)
+  int loop_threads = 0;           // ... CTA size chosen on first use (0: not yet)
+  unsigned long long* d_loop_prof = nullptr;  // ... phase time stamps (NFGPU_LOOP_PROFILE)
+  void* d_tiny = nullptr;  // tiny_loop_kernel scratch: part, wch, ch, gpart, vbcnt, stat_part
+  size_t tiny_bytes = 0;
+  size_t loop_prof_elems = 0;
   bool comm_active = false;  // inside nf_forward_allreduce
   bool comm_fused = false;   // ... and the flat forward's last reduce already did the all-reduce
 };
@@ -2788,6 +3460,9 @@ void free_plan(nf_plan* p) {
   for (int q = 0; q < p->comm_world; ++q)
     if (q != p->comm_rank && p->comm_peer[q]) cudaIpcCloseMemHandle(p->comm_peer[q]);
   cudaFree(p->comm_buf);
+  cudaFree(p->d_loopbar);
+  cudaFree(p->d_loop_prof);
+  cudaFree(p->d_tiny);
   cudaFree(p->d_epoch);
   cudaFree(p->d_comm_err);
   delete p;
@@ -2892,6 +3567,56 @@ int launch_reduce2(nf_plan* p, int span, int nseg, int w0, void* y, cudaStream_t
   return NF_OK;
 }
 
+// Forward launch arguments of one window [w0, w1) of the staged flat batch (launch_forward, spgm_loop)
+template <typename Real>
+FwdArgs<Real> fwd_args(const nf_plan* p, const void* s, int w0, int w1) {
+  const int span = w1 - w0;
+  FwdArgs<Real> a;
+  a.g = p->g;
+  a.tab = (const Real*)p->d_tab;
+  a.D0 = p->d_D0;
+  a.crec = p->d_crec;
+  a.s = (const Real*)s;
+  a.w0 = w0;
+  a.w1 = w1;
+  a.Q = channel_splits(p, span);
+  a.part = (Real*)p->d_part;
+  a.order = unit_order(p, (long long)p->g.ntiles * a.Q);
+  tail_split(p, a.order, a.Q, std::max(1, span / p->min_chunk), a.t1, a.Q2);
+  a.taper = (float)p->fwd_taper;
+  return a;
+}
+
+// Adjoint (+ prox) arguments of the staged flat batch (launch_adjoint, spgm_loop)
+template <typename Real>
+AdjArgs<Real> adj_args(const nf_plan* p, void* gout, double scale, const void* s_in, void* s_out, double eta_over_b,
+                       double alpha) {
+  AdjArgs<Real> a;
+  a.g = p->g;
+  a.tab = (const Real*)p->d_tab;
+  a.D0 = p->d_D0;
+  a.crec = p->d_crec;
+  a.wrec = (const R2<Real>*)p->d_wrec;
+  a.B = p->B;
+  a.CH = adjoint_chunks(p);
+  a.order = p->structured ? 0 : unit_order(p, (long long)p->g.ntiles * a.CH);
+  a.t1 = p->g.ntiles;
+  a.CH2 = a.CH;
+  a.taper = (float)p->taper;
+  if (!p->structured)
+    tail_split(p, a.order, a.CH, std::min<long long>(std::max(1, p->B / p->adj_min_chunk), p->adj_ch_cap), a.t1, a.CH2);
+  a.gpart = (Real*)p->d_gpart;
+  a.cnt = p->d_tilecnt;
+  a.gout = (Real*)gout;
+  a.scale = scale;
+  a.s_in = (const Real*)s_in;
+  a.s_out = (Real*)s_out;
+  a.eta_over_b = eta_over_b;
+  a.alpha = alpha;
+  a.stat_part = p->d_stat_part;
+  return a;
+}
+
 template <typename Real>
 int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const size_t sm = fwd_smem(p);
@@ -2901,19 +3626,7 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   for (int w0 = 0; w0 < p->B; w0 += p->fwd_chunk) {
     const int w1 = std::min(p->B, w0 + p->fwd_chunk);
     const int span = w1 - w0;
-    FwdArgs<Real> a;
-    a.g = p->g;
-    a.tab = (const Real*)p->d_tab;
-    a.D0 = p->d_D0;
-    a.crec = p->d_crec;
-    a.s = (const Real*)s;
-    a.w0 = w0;
-    a.w1 = w1;
-    a.Q = channel_splits(p, span);
-    a.part = (Real*)p->d_part;
-    a.order = unit_order(p, (long long)p->g.ntiles * a.Q);
-    tail_split(p, a.order, a.Q, std::max(1, span / p->min_chunk), a.t1, a.Q2);
-    a.taper = (float)p->fwd_taper;
+    const FwdArgs<Real> a = fwd_args<Real>(p, s, w0, w1);
     const long long units = (long long)a.t1 * a.Q + (long long)(p->g.ntiles - a.t1) * a.Q2;
     CUDA_TRY(launch_k(p->use_pdl, kern, dim3((unsigned)((units + FWD_WARPS - 1) / FWD_WARPS)), dim3(FWD_WARPS * 32),
                       sm, st, a));
@@ -3072,29 +3785,7 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   const int nblk = (p->B + 255) / 256;
   CUDA_TRY(launch_k(p->use_pdl, resid_kernel<Real>, dim3(nblk), dim3(256), 0, st, p->d_sm, p->d_spos, p->d_sf, p->B,
                     (const Real*)r, (const Real*)ymeas, p->d_pulse, (R2<Real>*)p->d_wrec, p->d_dpart));
-  AdjArgs<Real> a;
-  a.g = p->g;
-  a.tab = (const Real*)p->d_tab;
-  a.D0 = p->d_D0;
-  a.crec = p->d_crec;
-  a.wrec = (const R2<Real>*)p->d_wrec;
-  a.B = p->B;
-  a.CH = adjoint_chunks(p);
-  a.order = p->structured ? 0 : unit_order(p, (long long)p->g.ntiles * a.CH);
-  a.t1 = p->g.ntiles;
-  a.CH2 = a.CH;
-  a.taper = (float)p->taper;
-  if (!p->structured)
-    tail_split(p, a.order, a.CH, std::min<long long>(std::max(1, p->B / p->adj_min_chunk), p->adj_ch_cap), a.t1, a.CH2);
-  a.gpart = (Real*)p->d_gpart;
-  a.cnt = p->d_tilecnt;
-  a.gout = (Real*)gout;
-  a.scale = scale;
-  a.s_in = (const Real*)s_in;
-  a.s_out = (Real*)s_out;
-  a.eta_over_b = eta_over_b;
-  a.alpha = alpha;
-  a.stat_part = p->d_stat_part;
+  AdjArgs<Real> a = adj_args<Real>(p, gout, scale, s_in, s_out, eta_over_b, alpha);
   if constexpr (std::is_same<Real, float>::value) {
     const int npad = (2 * p->snt + 15) / 16 * 16;
     if (use_tc_struct(p, false)) {
@@ -3151,6 +3842,210 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
   return NF_OK;
 }
 
+// NFGPU_LOOP_PROFILE: phase time stamps of CTA 0 into a plan buffer (nf_loop_profile reads them back)
+int loop_profile_buffer(nf_plan* p, int K, LoopArgs& la) {
+  la.prof = nullptr;
+  if (!std::getenv("NFGPU_LOOP_PROFILE")) return NF_OK;
+  const size_t need = (size_t)K * LOOP_PROF;
+  if (need > p->loop_prof_elems) {
+    cudaFree(p->d_loop_prof);
+    p->d_loop_prof = nullptr;
+    p->loop_prof_elems = 0;
+    if (int rc = dalloc(p, &p->d_loop_prof, need * sizeof(unsigned long long))) return rc;
+    p->loop_prof_elems = need;
+  }
+  la.prof = p->d_loop_prof;
+  return NF_OK;
+}
+
+template <typename Real>
+int launch_tiny_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uint64_t iter0, int B, const void* ymeas,
+                     void* s_a, void* s_b, double eta_over_b, double alpha, double tol, long long budget_ns,
+                     double* rec, int* state, cudaStream_t st) {
+  int dev = 0, nsm = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const Geo& g = p->g;
+  const int nvb = (int)((p->nvox + 255) / 256);
+  int jc = (int)std::max(1LL, std::min<long long>(TINY_JC, ((long long)B * nvb + nsm - 1) / nsm));
+  int cc = std::max(1, std::min(B, nsm / std::max(1, nvb)));
+  if (const char* e = std::getenv("NFGPU_TINY_JC")) jc = std::max(1, std::min(TINY_JC, std::atoi(e)));
+  if (const char* e = std::getenv("NFGPU_TINY_CC")) cc = std::max(1, std::min(B, std::atoi(e)));
+  const size_t b_part = sizeof(double2) * (size_t)nvb * B, b_w = sizeof(double) * (size_t)B, b_ch = 0,
+               b_g = sizeof(double2) * (size_t)cc * nvb * 256,
+               b_cnt = sizeof(int) * (size_t)nvb, b_st = sizeof(double) * 4 * (size_t)nvb;
+  auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t need = al(b_part) + al(b_w) + al(b_ch) + al(b_g) + al(b_cnt) + al(b_st);
+  if (need > p->tiny_bytes) {
+    cudaFree(p->d_tiny);
+    p->d_tiny = nullptr;
+    p->tiny_bytes = 0;
+    if (int rc = dalloc(p, (char**)&p->d_tiny, need)) return rc;
+    CUDA_TRY(cudaMemset(p->d_tiny, 0, need));
+    p->tiny_bytes = need;
+  }
+  char* base = (char*)p->d_tiny;
+  TinyArgs ta;
+  ta.ant = p->d_ant;
+  ta.kd = p->d_kd;
+  for (int i = 0; i < 3; ++i) {
+    ta.corner[i] = g.corner[i];
+    ta.sp[i] = g.sp[i];
+  }
+  ta.nx = g.nx;
+  ta.ny = g.ny;
+  ta.nzs = g.nzs;
+  ta.zb = g.zb;
+  ta.T = g.T;
+  ta.R = g.R;
+  ta.nvb = nvb;
+  ta.jc = jc;
+  ta.cc = cc;
+  ta.chunk_max = (B + cc - 1) / cc;
+  // the per-voxel-block arrays first (their offsets depend on the plan only), then the batch-sized ones
+  ta.vbcnt = (int*)base;  // zero between iterations (reset by the last arriver; cleared per launch below)
+  base += al(b_cnt);
+  ta.stat_part = (double*)base;
+  base += al(b_st);
+  ta.part = (double2*)base;
+  base += al(b_part);
+  ta.e2 = (double*)base;
+  base += al(b_w);
+  base += al(b_ch);
+  ta.gpart = (double2*)base;
+  if (!p->d_loopbar) {
+    int rc = dalloc(p, &p->d_loopbar, 4 * sizeof(unsigned));
+    if (rc) return rc;
+    CUDA_TRY(cudaMemset(p->d_loopbar, 0, 4 * sizeof(unsigned)));
+  }
+  LoopArgs la = {};
+  la.km = p->km;
+  la.M = p->M;
+  la.B = B;
+  la.K = K;
+  int bits = 2;
+  while ((1LL << bits) < p->M) bits += 2;
+  la.hb = bits / 2;
+  la.idx_table = table;
+  la.seed = seed;
+  la.iter0 = iter0;
+  la.kd = p->d_kd;
+  la.pulse = p->d_pulse;
+  la.ymeas = ymeas;
+  la.dpart = p->d_dpart;
+  la.tol = tol;
+  la.budget_ns = budget_ns;
+  la.eta_over_b = eta_over_b;
+  la.alpha = alpha;
+  la.rec = rec;
+  la.state = state;
+  la.bar = p->d_loopbar;
+  la.s_a = s_a;
+  la.s_b = s_b;
+  if (int rc = loop_profile_buffer(p, K, la)) return rc;
+  const size_t smem = (size_t)ta.chunk_max * (sizeof(double2) + sizeof(int4));
+  auto kern = tiny_loop_kernel<Real>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
+  CUDA_TRY(cudaMemsetAsync(ta.vbcnt, 0, b_cnt, st));
+  void* args[] = {&la, &ta};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nsm), dim3(256), args, smem, st));
+  p->B = B;
+  p->structured = false;
+  p->launches += 1;
+  return NF_OK;
+}
+
+template <typename Real>
+int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uint64_t iter0, int B, const void* ymeas,
+                     void* s_a, void* s_b, double eta_over_b, double alpha, double tol, long long budget_ns,
+                     double* rec, int* state, cudaStream_t st) {
+  const char* tiny_env = std::getenv("NFGPU_TINY");  // read per launch: "0" keeps small problems here
+  if ((!tiny_env || std::atoi(tiny_env) != 0) && (long long)B * p->nvox <= TINY_MAX_ENTRIES)
+    return launch_tiny_loop<Real>(p, table, K, seed, iter0, B, ymeas, s_a, s_b, eta_over_b, alpha, tol, budget_ns,
+                                  rec, state, st);
+  auto kern = p->exact ? spgm_loop_kernel<Real, true> : spgm_loop_kernel<Real, false>;
+  size_t wb = std::max(fwd_warp_bytes<Real>(p->g.Tg, p->g.A), warp_smem_bytes<Real>(p->g.Tg, p->g.A));
+  wb = (wb + 15) & ~(size_t)15;
+  cudaFuncAttributes fattr;
+  CUDA_TRY(cudaFuncGetAttributes(&fattr, kern));
+  const size_t SMEM_DYN_MAX = 232448 - fattr.sharedSizeBytes;  // 227 KB per block (opt-in) beside the static part
+  int nw = 16;  // warps per CTA: 16, 12 or 8 (multiples of 4 keep the 256-thread groups of P3 / P5)
+  while (nw > 8 && (size_t)nw * wb > SMEM_DYN_MAX) nw -= 4;
+  if ((size_t)nw * wb > SMEM_DYN_MAX) return fail(NF_ERR_STATE, "persistent loop: shared memory layout does not fit");
+  // P0 rank sort: keys + order (LOOP_SORT_MAX ints each), then the key bitmap and its word prefix counts
+  const size_t kwords = ((size_t)p->KS + 31) / 32;
+  const bool bitmap = (size_t)LOOP_SORT_MAX * 8 + kwords * 8 <= SMEM_DYN_MAX;
+  const size_t sort_bytes = (size_t)LOOP_SORT_MAX * 8 + (bitmap ? kwords * 8 : 0);
+  const size_t smem = std::max({(size_t)nw * wb, sort_bytes, (size_t)(4 * 256 + 16) * sizeof(double)});
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, nsm = 0, per_sm = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
+  if (per_sm < 1) return fail(NF_ERR_STATE, "persistent loop: one CTA per SM does not fit");
+  if (!p->d_loopbar) {  // {barrier arrivals, barrier generation, forward unit counter, adjoint unit counter}
+    int rc = dalloc(p, &p->d_loopbar, 4 * sizeof(unsigned));
+    if (rc) return rc;
+    CUDA_TRY(cudaMemset(p->d_loopbar, 0, 4 * sizeof(unsigned)));
+  }
+  p->B = B;
+  p->structured = false;
+  LoopArgs la;
+  la.km = p->km;
+  la.M = p->M;
+  la.B = B;
+  la.K = K;
+  la.nseg = p->fwd_nseg;
+  int bits = 2;
+  while ((1LL << bits) < p->M) bits += 2;
+  la.hb = bits / 2;
+  la.idx_table = table;
+  la.seed = seed;
+  la.iter0 = iter0;
+  la.kd = p->d_kd;
+  la.pulse = p->d_pulse;
+  la.ymeas = ymeas;
+  la.sm = p->d_sm;
+  la.spos = p->d_spos;
+  la.sf = p->d_sf;
+  la.crec = p->d_crec;
+  la.tmp = p->d_tmp;
+  la.dpart = p->d_dpart;
+  la.stat_part = p->d_stat_part;
+  la.tol = tol;
+  la.budget_ns = budget_ns;
+  la.rec = rec;
+  la.state = state;
+  la.bar = p->d_loopbar;
+  la.ctr = (int*)p->d_loopbar + 2;
+  la.s_a = s_a;
+  la.s_b = s_b;
+  la.warp_bytes = wb;
+  la.kwords = bitmap ? (int)kwords : 0;
+  la.prof = nullptr;
+  if (std::getenv("NFGPU_LOOP_PROFILE")) {
+    const size_t need = (size_t)K * LOOP_PROF;
+    if (need > p->loop_prof_elems) {
+      cudaFree(p->d_loop_prof);
+  cudaFree(p->d_tiny);
+      p->d_loop_prof = nullptr;
+      p->loop_prof_elems = 0;
+      if (int rc = dalloc(p, &p->d_loop_prof, need * sizeof(unsigned long long))) return rc;
+      p->loop_prof_elems = need;
+    }
+    la.prof = p->d_loop_prof;
+  }
+  FwdArgs<Real> fa = fwd_args<Real>(p, s_a, 0, B);
+  AdjArgs<Real> aa = adj_args<Real>(p, nullptr, 0, s_a, s_b, eta_over_b, alpha);
+  CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
+  void* args[] = {&la, &fa, &aa};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nsm), dim3(nw * 32), args, smem, st));
+  p->loop_threads = nw * 32;
+  p->launches += 1;
+  return NF_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -3203,6 +4098,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   }
   g.ng = (n_tx + tg_max - 1) / tg_max;
   g.Tg = (n_tx + g.ng - 1) / g.ng;
+  g.tg_mul = (65536 + g.Tg - 1) / g.Tg;
   if (g.ng > TGROUPS_MAX) {
     delete p;
     return fail(NF_ERR_ARG, "too many transmitter groups");
@@ -3371,7 +4267,7 @@ int nf_plan_info(const nf_plan* p, int64_t info[8]) {
   info[2] = p->g.ntiles;
   info[3] = p->g.Tg;
   info[4] = (int64_t)p->dev_bytes;
-  info[5] = p->fwd_gridx;
+  info[5] = p->fwd_chunk;
   info[6] = p->dtype;
   info[7] = p->launches;
   return NF_OK;
@@ -3634,6 +4530,33 @@ int nf_adjoint_prox(nf_plan* p, const void* r, const void* ymeas, const void* s_
   if (p->dtype == NF_C64)
     return launch_adjoint<float, true>(p, r, ymeas, nullptr, 0, s_in, s_out, eta_over_b, alpha, stats, st);
   return launch_adjoint<double, true>(p, r, ymeas, nullptr, 0, s_in, s_out, eta_over_b, alpha, stats, st);
+}
+
+int nf_spgm_loop(nf_plan* p, const int32_t* idx_table, int iters, uint64_t seed, uint64_t iter0, int batch,
+                 const void* ymeas, void* s_a, void* s_b, double eta_over_b, double alpha, double tol,
+                 double time_budget_s, double* records, int* state, void* stream) {
+  if (!p || !ymeas || !s_a || !s_b || !records || !state) return fail(NF_ERR_ARG, "null argument");
+  if (s_a == s_b) return fail(NF_ERR_ARG, "s_a and s_b must not alias");
+  if (iters < 1) return fail(NF_ERR_ARG, "iters must be >= 1");
+  if (batch < 1 || batch > p->M) return fail(NF_ERR_ARG, "batch must be in [1, M]");
+  if (!(alpha >= 0) || !std::isfinite(alpha)) return fail(NF_ERR_ARG, "alpha must be >= 0");
+  if (batch > p->max_batch || batch > p->fwd_chunk || batch > LOOP_SORT_MAX)
+    return fail(NF_ERR_STATE, "persistent loop: batch exceeds the plan's single forward window or the sort size");
+  const long long budget = time_budget_s >= 0 && std::isfinite(time_budget_s) ? (long long)(time_budget_s * 1e9) : -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->dtype == NF_C64)
+    return launch_spgm_loop<float>(p, idx_table, iters, seed, iter0, batch, ymeas, s_a, s_b, eta_over_b, alpha, tol,
+                                   budget, records, state, st);
+  return launch_spgm_loop<double>(p, idx_table, iters, seed, iter0, batch, ymeas, s_a, s_b, eta_over_b, alpha, tol,
+                                  budget, records, state, st);
+}
+
+// diagnostics: copy the persistent loop's phase time stamps of its last launch (NFGPU_LOOP_PROFILE) to the host
+int nf_loop_profile(nf_plan* p, unsigned long long* host, int iters) {
+  if (!p || !host) return fail(NF_ERR_ARG, "null argument");
+  if (!p->d_loop_prof || (size_t)iters * LOOP_PROF > p->loop_prof_elems) return fail(NF_ERR_STATE, "no loop profile");
+  CUDA_TRY(cudaMemcpy(host, p->d_loop_prof, (size_t)iters * LOOP_PROF * 8, cudaMemcpyDeviceToHost));
+  return NF_OK;
 }
 
 int nf_sample_structured(nf_plan* p, uint64_t seed, uint64_t iter, int nf, int nt, int nr, int32_t* lists,

@@ -148,7 +148,7 @@ class DevicePlan:
     def info(self) -> dict:
         buf = (ctypes.c_int64 * 8)()
         _lib.check(self.lib.nf_plan_info(self._h, buf), "nf_plan_info")
-        keys = ("n_local", "M", "tiles", "tx_group", "device_bytes", "fwd_ctas", "dtype", "launches")
+        keys = ("n_local", "M", "tiles", "tx_group", "device_bytes", "fwd_window", "dtype", "launches")
         return dict(zip(keys, list(buf)))
 
     @property
@@ -304,6 +304,33 @@ class DevicePlan:
         self._idx = None
         self.staged_structured = True
         self.stage_gen += 1
+
+    def spgm_loop(self, table: torch.Tensor | None, iters: int, seed: int, iter0: int, batch: int,
+                  ymeas: torch.Tensor, s_a: torch.Tensor, s_b: torch.Tensor, eta_over_b: float, alpha: float,
+                  tol: float, time_budget_s: float | None, records: torch.Tensor, state: torch.Tensor) -> None:
+        """nf_spgm_loop: ``iters`` flat-batch SPGM iterations in one persistent launch (table: device int32
+        [iters, batch] in subset order, or None for the device Feistel sampler)."""
+        _lib.check(
+            self.lib.nf_spgm_loop(
+                self._h, _ptr(table), int(iters), int(seed) & (2**64 - 1), int(iter0), int(batch), _ptr(ymeas),
+                _ptr(s_a), _ptr(s_b), float(eta_over_b), float(alpha), float(tol),
+                -1.0 if time_budget_s is None else float(time_budget_s), _ptr(records), _ptr(state),
+                _stream(self.device),
+            ),
+            "nf_spgm_loop",
+        )
+        self.B = int(batch)
+        self._idx = None
+        self.staged_structured = False
+        self.stage_gen += 1
+
+    def loop_eligible(self, batch: int) -> bool:
+        """True when nf_spgm_loop can run this flat batch size (one forward window, <= 4096 channels)."""
+        return 1 <= batch <= min(self.max_batch, 4096, self.fwd_chunk)
+
+    @property
+    def fwd_chunk(self) -> int:
+        return int(self.info()["fwd_window"])
 
     def set_iter(self, it: int) -> None:
         _lib.check(self.lib.nf_plan_set_iter(self._h, int(it), _stream(self.device)), "nf_plan_set_iter")

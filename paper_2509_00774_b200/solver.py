@@ -344,6 +344,12 @@ class SPGMEngine:
         self._pinned = [None, None]
         self._pinned_ev = [None, None]
         self._pinned_next = 0
+        # persistent loop (run_loop): records, state, index-table staging
+        self._loop_rec = None
+        self._loop_state = torch.zeros(4, dtype=torch.int32, device=dev)
+        self._loop_pinned = None
+        self._loop_tab = None
+        self._loop_ev = None
 
     def _pinned_idx(self, n: int) -> tuple[torch.Tensor, int]:
         k = self._pinned_next
@@ -420,6 +426,60 @@ class SPGMEngine:
         self.plan.adjoint_prox(yb, self.y, self.s, self.s_next, self.eta / B, self.alpha, self.stats)
         self.s, self.s_next = self.s_next, self.s
 
+    def run_loop(self, iters: int, table=None, seed: int = 0, iter0: int = 0, batch: int | None = None,
+                 tol: float = 0.0, time_budget_s: float | None = None):
+        """``iters`` SPGM iterations in one persistent launch (nf_spgm_loop): flat batches from ``table``
+        ([iters, B] host array or device int32 tensor, subset order) or, with table=None, from the device
+        sampler (``seed``, iteration numbers iter0, iter0 + 1, ...). Stops early on the tolerance test or
+        the device-time budget. Returns (iterations run, reason 0/1/2, records [n, 6] float64 tensor on
+        the device: the 4 statistics and the device time in ns since launch). Afterwards ``self.s`` is the
+        latest iterate. Enqueued on the current stream; the caller synchronises (e.g. reading state)."""
+        if self.pg is not None:
+            raise RuntimeError("run_loop is single-GPU (voxel-slab ranks use step_staged with a collective)")
+        dev = self.plan.device
+        if table is not None:
+            if not isinstance(table, torch.Tensor) or table.device != dev:
+                arr = np.ascontiguousarray(np.asarray(table)[:iters], dtype=np.int32)
+                buf = self._loop_table(arr.size)
+                buf.numpy()[: arr.size] = arr.reshape(-1)
+                tab = self._loop_dev_table(arr.size)
+                tab[: arr.size].copy_(buf[: arr.size], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream(dev))
+                self._loop_ev = ev
+                table = tab[: arr.size]
+                batch = arr.shape[1]
+            else:
+                batch = int(table.shape[-1]) if table.dim() == 2 else int(batch)
+                table = table.to(torch.int32).contiguous()
+        if batch is None:
+            raise ValueError("run_loop needs batch with the device sampler")
+        if self._loop_rec is None or self._loop_rec.shape[0] < iters:
+            self._loop_rec = torch.empty((max(iters, 64), 6), dtype=torch.float64, device=dev)
+        self.plan.spgm_loop(table, iters, seed, iter0, batch, self.y, self.s, self.s_next, self.eta / batch,
+                            self.alpha, tol, time_budget_s, self._loop_rec, self._loop_state)
+        return self._loop_rec, self._loop_state
+
+    def loop_result(self) -> tuple[int, int]:
+        """(iterations run, reason) of the last run_loop (synchronises); swaps the iterate buffers so that
+        ``self.s`` holds the latest iterate."""
+        n, reason = (int(v) for v in self._loop_state[:2].cpu())
+        if n % 2 == 1:
+            self.s, self.s_next = self.s_next, self.s
+        return n, reason
+
+    def _loop_table(self, n: int) -> torch.Tensor:
+        if self._loop_ev is not None:
+            self._loop_ev.synchronize()
+        if self._loop_pinned is None or self._loop_pinned.numel() < n:
+            self._loop_pinned = torch.empty(n, dtype=torch.int32).pin_memory()
+        return self._loop_pinned
+
+    def _loop_dev_table(self, n: int) -> torch.Tensor:
+        if self._loop_tab is None or self._loop_tab.numel() < n:
+            self._loop_tab = torch.empty(n, dtype=torch.int32, device=self.plan.device)
+        return self._loop_tab
+
     def magnitude_change(self) -> float:
         if self.collective == "peer" and self.plan.comm_timed_out():
             raise RuntimeError("peer all-reduce: a rank stopped participating (flag wait timed out)")
@@ -468,6 +528,10 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
         return eng.stage(sample_minibatch(config.composition, scenario, rng).indices)
 
     t_start = time.perf_counter()
+    loop_batch = _loop_batch(plan, config, scenario, stochastic) if progress is None and config.check_every == 1 \
+        else None
+    if loop_batch is not None:
+        return _solve_persistent(eng, plan, config, scenario, stochastic, loop_batch, rng, t_start)
     if progress is None and config.check_every == 1:
         # Pipelined: iteration k+1 is drawn and launched before iteration k's statistics are read
         # (async D2H into a pinned double buffer), so host sampling and the read-back overlap the
@@ -556,6 +620,102 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
         per_iteration=records,
         termination=termination,
     )
+
+
+LOOP_CHUNK = 256  # iterations per persistent launch (the host draws the next chunk's batches meanwhile)
+
+
+def _loop_batch(plan: DevicePlan, config: SolverConfig, scenario: ImagingScenario, stochastic: bool):
+    """The batch size when this solve can run on the persistent device loop (nf_spgm_loop), else None.
+    The loop computes flat batches; batches the per-iteration path would send to the separable kernels
+    (Cartesian products with enough pairs, DevicePlan.try_structured) stay on that path, so every batch
+    of a solve takes the same arithmetic either way."""
+    import os
+
+    if os.environ.get("NFGPU_LOOP", "1") == "0":
+        return None
+    from .plan import STRUCT_MIN_PAIRS, cartesian_factors
+
+    def routes_flat(idx) -> bool:
+        if plan.structured == "never":
+            return True
+        fac = cartesian_factors(idx, plan.n_tx, plan.n_rx)
+        return fac is None or (plan.structured == "auto" and fac[1].size * fac[2].size < STRUCT_MIN_PAIRS)
+
+    if not stochastic:
+        B = scenario.n_channels
+        ok = routes_flat(np.arange(B))
+    elif config.sampler == "table":
+        rows = np.asarray(config.index_table[: config.max_iters])
+        if rows.dtype == object or rows.ndim != 2:
+            return None
+        B = rows.shape[1]
+        ok = all(routes_flat(r) for r in rows)
+    elif config.composition is not None:
+        c = config.composition
+        B = c.batch_size
+        ok = plan.structured == "never" or (plan.structured == "auto" and c.n_tx * c.n_rx < STRUCT_MIN_PAIRS)
+    else:
+        B = config.flat_batch
+        ok = True
+    return B if ok and plan.loop_eligible(B) else None
+
+
+def _solve_persistent(eng: SPGMEngine, plan: DevicePlan, config: SolverConfig, scenario: ImagingScenario,
+                      stochastic: bool, B: int, rng, t_start: float) -> SolveReport:
+    """_solve on the persistent device loop: chunks of LOOP_CHUNK iterations per launch, each iteration's
+    statistics, tolerance test (solver.py:302) and time-budget test on the device; the host draws the next
+    chunk's batches with the reference's call sequence while the current chunk runs, and builds the
+    IterationRecords (elapsed_seconds = device time of the iteration) from the records copied back once
+    per chunk. Same iterates, records and termination as the per-iteration loop."""
+    m = scenario.n_channels
+    full = np.arange(m, dtype=np.int64)
+
+    def draw(n):
+        if not stochastic:
+            return np.broadcast_to(full, (n, m))
+        if config.sampler == "device":
+            return None
+        if config.sampler == "table":
+            return None
+        if config.flat_batch is not None:
+            return np.stack([sample_flat(scenario, B, rng) for _ in range(n)])
+        return np.stack([sample_minibatch(config.composition, scenario, rng).indices for _ in range(n)])
+
+    records: list[IterationRecord] = []
+    termination = TERMINATION_MAX_ITERS
+    done = 0
+    n = min(LOOP_CHUNK, config.max_iters)
+    table = draw(n)
+    while done < config.max_iters:
+        if config.sampler == "table":
+            table = np.asarray(config.index_table[done:done + n])
+        budget = None
+        if config.time_budget_s is not None:
+            budget = max(0.0, config.time_budget_s - (time.perf_counter() - t_start))
+        rec, _ = eng.run_loop(n, table=table, seed=config.rng_seed, iter0=done + 1, batch=B, tol=config.tol,
+                              time_budget_s=budget)
+        n_next = min(LOOP_CHUNK, config.max_iters - done - n)
+        table = draw(n_next) if n_next > 0 else None  # overlaps the launch on the GPU
+        k_run, reason = eng.loop_result()
+        r = rec[:k_run].cpu().numpy()
+        t_prev = 0.0
+        for i in range(k_run):
+            st0, st1 = float(r[i, 0]), float(r[i, 1])
+            change = math.sqrt(st1) / max(math.sqrt(st0), _ZERO_NORM_GUARD)
+            records.append(IterationRecord(done + i + 1, change, (float(r[i, 4]) - t_prev) * 1e-9, B))
+            t_prev = float(r[i, 4])
+        done += k_run
+        if reason == 1:
+            termination = TERMINATION_TOLERANCE
+            break
+        if reason == 2 or (config.time_budget_s is not None and time.perf_counter() - t_start > config.time_budget_s):
+            termination = TERMINATION_TIME_BUDGET
+            break
+        n = n_next
+    vol = eng.volume()
+    return SolveReport(volume=ReflectivityVolume(vol, scenario.voxels), iterations=done,
+                       wall_time_s=time.perf_counter() - t_start, per_iteration=records, termination=termination)
 
 
 def pgm_solve(y, scenario: ImagingScenario, config: SolverConfig | None = None, initial=None,

@@ -364,7 +364,7 @@ def _many_antenna_scenario(n_tx, n_rx, n_f=2, dims=(10, 8, 6)):
     tx = np.c_[rng.uniform(-0.2, 0.2, (n_tx, 2)), np.zeros(n_tx)]
     rx = np.c_[rng.uniform(-0.2, 0.2, (n_rx, 2)), np.zeros(n_rx)]
     return ImagingScenario(array=ArrayGeometry(tuple(map(tuple, tx)), tuple(map(tuple, rx))),
-                           frequencies=FrequencyGrid(24e9, 28e9, n_f),
+                           frequencies=FrequencyGrid(24e9, 28e9 if n_f > 1 else 24e9, n_f),
                            voxels=VoxelGrid(center=Vec3(0, 0, 0.3), extent=(0.08, 0.06, 0.05), dims=dims))
 
 

@@ -348,10 +348,12 @@ def test_cuda_graph_steps_match_eager():
     assert np.array_equal(out[0], out[1])
 
 
-def test_pipelined_solver_equals_serial_loop(small_scenario, rng):
+def test_pipelined_solver_equals_serial_loop(small_scenario, rng, monkeypatch):
     """With no progress callback the solver launches iteration k+1 before reading k's statistics.
     A tolerance stop must drop the speculative step: volume, iteration count and records equal the
-    serial loop's (the serial loop runs when a progress callback is given)."""
+    serial loop's (the serial loop runs when a progress callback is given). NFGPU_LOOP=0 keeps these
+    solves off the persistent device loop (tests/test_gpu_loop.py covers that one)."""
+    monkeypatch.setenv("NFGPU_LOOP", "0")
     y = rc(rng, small_scenario.n_channels)
     base = SolverConfig(max_iters=60, tol=1e-300, composition=MinibatchComposition(2, 2, 1), rng_seed=3)
     serial = spgm_solve(y, small_scenario, base, progress=lambda k, s: None)

@@ -1,0 +1,69 @@
+#!/usr/bin/env python3
+"""Iterations/s of the persistent SPGM loop (nf_spgm_loop) against the CUDA-graph step on a BASELINE workload:
+device-sampled flat batches, CUDA events around K iterations.
+
+    python tools/loop_rate.py --workload small --iters 2000
+"""
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2509_00774_b200 import configs  # noqa: E402
+from paper_2509_00774_b200.plan import DevicePlan  # noqa: E402
+from paper_2509_00774_b200.solver import SPGMEngine  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="small")
+ap.add_argument("--iters", type=int, default=2000)
+ap.add_argument("--dtype", default=None)
+a = ap.parse_args()
+w = configs.WORKLOADS[a.workload]()
+scn = w.scenario
+dtype = a.dtype or w.dtype
+rng = np.random.default_rng(0)
+y = rng.standard_normal(scn.n_channels) + 1j * rng.standard_normal(scn.n_channels)
+plan = DevicePlan(scn, dtype=dtype, device="cuda:0", max_batch=w.batch)
+eng = SPGMEngine(plan, y, eta=1e-3, alpha=1e-7)
+st = torch.cuda.current_stream()
+
+
+def timed(fn):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3
+
+
+K = a.iters
+t_loop = timed(lambda: eng.run_loop(K, table=None, seed=0, iter0=1, batch=w.batch, tol=0.0))
+n, reason = eng.loop_result()
+g = eng.graph(0, w.batch, pairs=8)
+t_graph = timed(lambda: [g.replay() for _ in range(K // 16)]) / (16 * (K // 16)) * K
+prof = None
+if os.environ.get("NFGPU_LOOP_PROFILE"):
+    import ctypes
+
+    buf = (ctypes.c_uint64 * (K * 12))()
+    rc = plan.lib.nf_loop_profile(plan._h, buf, K)
+    if rc == 0:
+        t = np.frombuffer(buf, dtype=np.uint64).reshape(K, 12).astype(np.float64)[K // 4:]
+        tiny = not t[:, 6:].any()
+        names = (["fwd", "bar0", "sums+adj+prox", "bar1", "stats"] if tiny else
+                 ["sort", "bar0", "fwd", "bar1", "red1", "bar2", "red2+resid", "bar3", "adj", "bar4", "stats"])
+        last = 5 if tiny else 11
+        d = np.diff(t[:, :last + 1], axis=1).mean(axis=0) / 1e3
+        prof = {n: round(float(v), 2) for n, v in zip(names, d)}
+        prof["next_iter_gap"] = round(float((t[1:, 0] - t[:-1, last]).mean() / 1e3), 2)
+print(json.dumps({"workload": a.workload, "profile_us": prof, "dtype": dtype, "batch": w.batch, "iters": K, "loop_iters_run": n,
+                  "loop_us_per_iter": t_loop / K * 1e6, "loop_iters_per_s": K / t_loop,
+                  "graph_us_per_iter": t_graph / K * 1e6, "graph_iters_per_s": K / t_graph}))

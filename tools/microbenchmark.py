@@ -25,8 +25,9 @@ from paper_2509_00774_b200 import configs  # noqa: E402
 from paper_2509_00774_b200.plan import DevicePlan  # noqa: E402
 
 
-def timed(fn):
-    fn()
+def timed(fn, warm: bool = True):
+    if warm:
+        fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st = torch.cuda.current_stream()
@@ -41,7 +42,9 @@ def rel(a, b):
     return float(torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b))
 
 
-def run(grid: str, dtype: str):
+def run(grid: str, dtype: str, paths=("flat", "structured")):
+    """One full-M forward and adjoint per path. c128 operations last seconds, so they are timed on
+    their first call (no warm-up run: kernel attributes and first-launch costs are microseconds)."""
     scn = configs.micro_scenario(grid)
     plan = DevicePlan(scn, dtype=dtype)
     M, N = scn.n_channels, scn.n_voxels
@@ -53,17 +56,21 @@ def run(grid: str, dtype: str):
     z = plan.vec(N)
     out = {"grid": grid, "dtype": dtype, "M": M, "N": N, "entries_per_op": M * N}
     res = {}
-    for path in ("flat", "structured"):
+    warm = dtype == "c64"
+    for path in paths:
         if path == "flat":
             plan.prepare(torch.arange(M, dtype=torch.int32, device=plan.device))
         else:
             plan.prepare_full()
-        tf, yv = timed(lambda: plan.forward(s, out=y).clone())
-        ta, zv = timed(lambda: plan.adjoint(r, out=z).clone())
+        tf, yv = timed(lambda: plan.forward(s, out=y).clone(), warm)
+        ta, zv = timed(lambda: plan.adjoint(r, out=z).clone(), warm)
         res[path] = (yv, zv)
         out[path] = {"fwd_s": tf, "adj_s": ta, "fwd_entries_per_s": M * N / tf, "adj_entries_per_s": M * N / ta}
-    out["structured_vs_flat_rel_l2"] = {"forward": rel(res["structured"][0], res["flat"][0]),
-                                        "adjoint": rel(res["structured"][1], res["flat"][1])}
+    if len(res) == 2:
+        out["structured_vs_flat_rel_l2"] = {"forward": rel(res["structured"][0], res["flat"][0]),
+                                            "adjoint": rel(res["structured"][1], res["flat"][1])}
+    del plan, res
+    torch.cuda.empty_cache()
     return out
 
 

@@ -29,6 +29,62 @@ from paper_2509_00774_b200.sharding import ShardedSetup  # noqa: E402
 from paper_2509_00774_b200.solver import SPGMEngine  # noqa: E402
 
 
+def sweep(scn, y, eta: float, alpha: float, lam: float, iters: int = 100, every: int = 25,
+          batches=(256, 1024, 4096, 16384, 65536, "M"), dev=None, dtype: str = "c64"):
+    """Run the sweep; returns (summary per batch size, objective-vs-time rows). Flat batches are drawn on
+    the device (fixed seed); ISTA (|B| = M) steps on the full channel set (structured kernels). Device time
+    (CUDA events around the iterations only); the objective is evaluated between segments, untimed."""
+    dev = dev or torch.device("cuda", 0)
+    M, N = scn.n_channels, scn.n_voxels
+    obj_plan = DevicePlan(scn, dtype=dtype, device=dev)
+    obj_plan.prepare_full()
+    y_dev = obj_plan._as_dev(y, M, "y")
+
+    def objective(s: torch.Tensor) -> float:
+        r = obj_plan.forward(s) - y_dev
+        return float(0.5 * (r.abs().double() ** 2).sum().item() / M + lam * s.abs().double().sum().item())
+
+    rows, summary = [], []
+    st = torch.cuda.current_stream()
+    for bs in batches:
+        B = M if bs == "M" else int(bs)
+        plan = DevicePlan(scn, dtype=dtype, device=dev, max_batch=B)
+        eng = SPGMEngine(plan, y, eta, alpha)
+        if B == M:
+            eng.stage(np.arange(M))
+            eng.step_staged()  # warm-up (kernel attributes), then restart from s = 0
+        else:
+            eng.sample_device(configs.SEEDS["minibatch"], 0, B)
+            eng.step_staged()
+        eng.s.zero_()
+        torch.cuda.synchronize()
+        t_total = 0.0
+        f0 = objective(eng.s)
+        rows.append({"batch": B, "iter": 0, "elapsed_s": 0.0, "objective": f0})
+        for k0 in range(0, iters, every):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for k in range(k0, min(iters, k0 + every)):
+                if B < M:
+                    eng.sample_device(configs.SEEDS["minibatch"], k, B)
+                eng.step_staged()
+            e1.record(st)
+            torch.cuda.synchronize()
+            t_total += e0.elapsed_time(e1) / 1e3
+            rows.append({"batch": B, "iter": min(iters, k0 + every), "elapsed_s": t_total,
+                         "objective": objective(eng.s)})
+        ips = iters / t_total
+        summary.append({"batch": B, "iters": iters, "seconds": t_total, "iters_per_s": ips,
+                        "entries_per_s": 2.0 * B * N * ips, "structured": plan.staged_structured,
+                        "initial_objective": f0, "final_objective": rows[-1]["objective"],
+                        "objective_vs_time": [[r["elapsed_s"], r["objective"]] for r in rows if r["batch"] == B]})
+        del eng, plan
+        torch.cuda.empty_cache()
+    del obj_plan
+    torch.cuda.empty_cache()
+    return summary, rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=100)
@@ -39,49 +95,18 @@ def main():
     dev = torch.device("cuda", 0)
     w = configs.WORKLOADS["large"]()
     scn = w.scenario
-    M, N = scn.n_channels, scn.n_voxels
+    M = scn.n_channels
     setup = ShardedSetup(scn, dtype="c64", device=dev, z_range=None)
     y = configs.add_noise(setup.forward_full(configs.make_scene(w)), 0.0)
     sigma = configs.noise_sigma(y, w.snr_db)
     y = configs.add_noise(y, sigma)
     L = setup.lipschitz(n_iters=20)
     lam = 1e-3 * setup.max_abs_adjoint(y) / M
-    eta, alpha = 1.0 / L, lam / L
-    y_dev = setup.plan._as_dev(y, M, "y")
-
-    def objective(s: torch.Tensor) -> float:
-        pred = setup.plan.forward(s)
-        r = pred - y_dev
-        return float(0.5 * (r.abs() ** 2).sum().item() / M + lam * s.abs().sum().item())
-
-    rows = []
-    for bs in a.batches.split(","):
-        B = M if bs == "M" else int(bs)
-        plan = DevicePlan(scn, dtype="c64", device=dev, max_batch=B)
-        eng = SPGMEngine(plan, y, eta, alpha)
-        if B == M:
-            eng.stage(np.arange(M))
-        st = torch.cuda.current_stream()
-        t_total = 0.0
-        rows.append({"batch": B, "iter": 0, "elapsed_s": 0.0, "objective": objective(eng.s)})
-        for k0 in range(0, a.iters, a.every):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            for k in range(k0, min(a.iters, k0 + a.every)):
-                if B < M:
-                    eng.sample_device(configs.SEEDS["minibatch"], k, B)
-                eng.step_staged()
-            e1.record(st)
-            torch.cuda.synchronize()
-            t_total += e0.elapsed_time(e1) / 1e3
-            rows.append({"batch": B, "iter": min(a.iters, k0 + a.every), "elapsed_s": t_total,
-                         "objective": objective(eng.s)})
-        ips = a.iters / t_total
-        print(json.dumps({"batch": B, "iters": a.iters, "seconds": t_total, "iters_per_s": ips,
-                          "entries_per_s": 2.0 * B * N * ips, "final_objective": rows[-1]["objective"],
-                          "initial_objective": rows[-a.iters // a.every - 1]["objective"]}), flush=True)
-        del eng, plan
-        torch.cuda.empty_cache()
+    setup.release()
+    batches = [b if b == "M" else int(b) for b in a.batches.split(",")]
+    summary, rows = sweep(scn, y, 1.0 / L, lam / L, lam, a.iters, a.every, batches, dev)
+    for line in summary:
+        print(json.dumps({k: v for k, v in line.items() if k != "objective_vs_time"}), flush=True)
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     with open(a.out, "w", newline="") as f:
         wr = csv.DictWriter(f, fieldnames=["batch", "iter", "elapsed_s", "objective"])
