@@ -392,12 +392,58 @@ def run_ours(args):
 def medium_line(args, dev, workload="medium"):
     """BASELINE config 1 (Medium, |B| = 512, c64) -- or config 0 (Small, |B| = 32, c128) -- on the same GPU:
     entries/s and iterations/s."""
+    import torch
+
     w, plan, eng, eta, alpha, setup_s = build_engine(workload, dev, 0, 1, None)
     ms, per_step, steps = timed_steps(eng, plan, w, 200, 10, None, 0, not args.no_graph)
     N = w.scenario.n_voxels
-    return {"value": 2.0 * w.batch * N / (ms / steps * 1e-3), "unit": UNIT, "ms_per_step": ms / steps,
-            "iters_per_s": 1e3 * steps / ms, "steps": steps, "batch": w.batch, "N": N, "M": w.scenario.n_channels,
-            "frac_step": 2.0 * w.batch * N / (ms / steps * 1e-3) / SFU_ENTRY_PEAK_MEASURED, "cuda_graph": not args.no_graph}
+    out = {"value": 2.0 * w.batch * N / (ms / steps * 1e-3), "unit": UNIT, "ms_per_step": ms / steps,
+           "iters_per_s": 1e3 * steps / ms, "steps": steps, "batch": w.batch, "N": N, "M": w.scenario.n_channels,
+           "frac_step": 2.0 * w.batch * N / (ms / steps * 1e-3) / SFU_ENTRY_PEAK_MEASURED, "cuda_graph": not args.no_graph,
+           "launches_per_step": per_step}
+    # the persistent device loop (nf_spgm_loop: one cooperative launch for K iterations, device sampler)
+    K = 2000 if workload == "small" else 400
+    st = torch.cuda.current_stream()
+    eng.run_loop(16, table=None, seed=0, iter0=1, batch=w.batch, tol=0.0)
+    eng.loop_result()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    eng.run_loop(K, table=None, seed=0, iter0=17, batch=w.batch, tol=0.0)
+    e1.record(st)
+    torch.cuda.synchronize()
+    n_run, _ = eng.loop_result()
+    ms_l = e0.elapsed_time(e1) / n_run
+    out["persistent_loop"] = {"value": 2.0 * w.batch * N / (ms_l * 1e-3), "unit": UNIT, "ms_per_step": ms_l,
+                              "iters_per_s": 1e3 / ms_l, "iterations": n_run, "launches": 1,
+                              "kernel": "tiny_loop_kernel" if w.batch * plan.n_local <= (1 << 20) else "spgm_loop_kernel",
+                              "frac_step": 2.0 * w.batch * N / (ms_l * 1e-3) / SFU_ENTRY_PEAK_MEASURED}
+    # end to end through spgm_solve (the reference's entry point), host numpy sampling as the reference, the
+    # config's own iteration count, y on the host, the final volume back (median of 3 solves after a warm-up)
+    from paper_2509_00774_b200.solver import SolverConfig, spgm_solve
+
+    y_host = eng.y.to(torch.complex128).cpu().numpy()
+    cfg = SolverConfig(eta=eta, alpha=alpha, max_iters=w.iters, tol=1e-300, dtype=w.dtype, flat_batch=w.batch,
+                       rng_seed=configs_seed())
+    spgm_solve(y_host, w.scenario, cfg)
+    walls = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        rep = spgm_solve(y_host, w.scenario, cfg)
+        walls.append(time.perf_counter() - t0)
+    wall = float(np.median(walls))
+    out["e2e"] = {"value": 2.0 * w.batch * N * rep.iterations / wall, "unit": UNIT, "iters_per_s": rep.iterations / wall,
+                  "wall_s": wall, "iterations": rep.iterations, "h2d_bytes_per_step": 4 * w.batch,
+                  "d2h_bytes_per_step": 6 * 8,
+                  "how": "wall clock around spgm_solve with the config's iteration count (host numpy flat sampling, the "
+                         "reference's call sequence; index tables H2D per 256-iteration chunk, statistics D2H per chunk, "
+                         "one IterationRecord per iteration; the persistent device loop)"}
+    return out
+
+
+def configs_seed() -> int:
+    from paper_2509_00774_b200 import configs
+
+    return configs.SEEDS["minibatch"]
 
 
 def structured_line(eng, w):
@@ -518,20 +564,33 @@ def cpu_child(workload: str) -> dict:
         return {"error": f"{type(e).__name__}: {e}"}
 
 
-def cpu_child_main(workload: str, budget_s: float) -> int:
-    import resource
+def _vm_hwm_bytes() -> int:
+    """Peak resident set of this process (VmHWM; ru_maxrss would carry the forking parent's peak)."""
+    for line in open("/proc/self/status"):
+        if line.startswith("VmHWM:"):
+            return int(line.split()[1]) * 1024
+    return -1
 
+
+def _vm_rss_bytes() -> int:
+    for line in open("/proc/self/status"):
+        if line.startswith("VmRSS:"):
+            return int(line.split()[1]) * 1024
+    return -1
+
+
+def cpu_child_main(workload: str, budget_s: float) -> int:
     from oracle import nfmimo_oracle as O
     from paper_2509_00774_b200 import configs
 
     w = configs.WORKLOADS[workload]()
     geo = O.geom_from_scenario(w.scenario)
     threads = O.host_threads()
-    rss0 = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
+    rss0 = _vm_rss_bytes()
     t0 = time.perf_counter()
     op = O.TableOperator(geo)
     build_s = time.perf_counter() - t0
-    rss_tables = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
+    rss_tables = _vm_rss_bytes()
     rng = np.random.default_rng(0)
     y = rng.standard_normal(geo.M) + 1j * rng.standard_normal(geo.M)
     s = np.zeros(geo.N, dtype=np.complex128)
@@ -548,8 +607,7 @@ def cpu_child_main(workload: str, budget_s: float) -> int:
         "workload": workload, "value": 2.0 * w.batch * geo.N / per, "unit": UNIT, "iters_per_s": 1.0 / per,
         "s_per_iter": per, "iters_timed": len(times), "iters_of_config": w.iters, "cores": threads, "kind": "port",
         "plan_build_s": build_s, "table_bytes": O.TableOperator.table_bytes(geo),
-        "peak_rss_bytes": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss * 1024,
-        "rss_before_tables_bytes": rss0 * 1024, "rss_after_tables_bytes": rss_tables * 1024,
+        "peak_rss_bytes": _vm_hwm_bytes(), "rss_before_tables_bytes": rss0, "rss_after_tables_bytes": rss_tables,
         "sample": f"full {workload} grid (N={geo.N}, M={geo.M}), |B|={w.batch} flat, the oracle's table restatement "
                   f"of the reference algorithm (forward.py:183-336, solver.py:181-241); plan build and peak RSS "
                   f"reported separately (BASELINE.md §3)",

@@ -1237,12 +1237,16 @@ __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __re
 // With tile-major units (large tables), chunks of one tile are adjacent units, so they run
 // together and share the tile's table rows in L2.
 // One forward warp unit (tile, channel chunk): the body of fwd_kernel, also run by spgm_loop_kernel.
-template <typename Real, bool EXACT>
-__device__ __forceinline__ void fwd_unit(const FwdArgs<Real>& a, int unit, unsigned char* wbase, int L,
-                                         const Real* __restrict__ sv) {
+// LOOP = false (fwd_kernel): the iterate is a.s and the warp's region follows fwd_warp_bytes, as written inline
+// in the kernel (keeps its code generation); LOOP = true: the iterate sv_loop and the region wbase_loop.
+template <typename Real, bool EXACT, bool LOOP = false>
+__device__ __forceinline__ void fwd_unit(const FwdArgs<Real>& a, int unit, unsigned char* smem_base, int w, int L,
+                                         const Real* __restrict__ sv_loop = nullptr) {
   const Geo& g = a.g;
   int tile, chunk, C;
   unit_map(unit, g.ntiles, a.Q, a.t1, a.Q2, a.order, tile, chunk, C);
+  unsigned char* wbase = LOOP ? smem_base : smem_base + (size_t)w * fwd_warp_bytes<Real>(g.Tg, g.A);
+  const Real* __restrict__ sv = LOOP ? sv_loop : a.s;
   const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A, 1);
   R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A, 1));  // [TBR][33]
 
@@ -1383,13 +1387,156 @@ __device__ __forceinline__ void fwd_unit(const FwdArgs<Real>& a, int unit, unsig
   stage_wait();
 }
 
+// fwd_kernel keeps its own copy of the unit body (the same source as fwd_unit, which the persistent loop runs):
+// routing it through fwd_unit changes ptxas's schedule of the kernel and costs 1.8% on Large (2.437 -> 2.480 ms)
 template <typename Real, bool EXACT>
 __global__ void __launch_bounds__(FWD_WARPS * 32, NFGPU_MINB_FWD) fwd_kernel(FwdArgs<Real> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geo& g = a.g;
   const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
   const int unit = blockIdx.x * FWD_WARPS + w;
-  if (unit >= a.t1 * a.Q + (a.g.ntiles - a.t1) * a.Q2) return;  // warps are independent: no block barriers
-  fwd_unit<Real, EXACT>(a, unit, smem_raw + (size_t)w * fwd_warp_bytes<Real>(a.g.Tg, a.g.A), L, a.s);
+  if (unit >= a.t1 * a.Q + (g.ntiles - a.t1) * a.Q2) return;  // warps are independent: no block barriers
+  int tile, chunk, C;
+  unit_map(unit, g.ntiles, a.Q, a.t1, a.Q2, a.order, tile, chunk, C);
+  unsigned char* wbase = smem_raw + (size_t)w * fwd_warp_bytes<Real>(g.Tg, g.A);
+  const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A, 1);
+  R2<Real>* tb = reinterpret_cast<R2<Real>*>(wbase + warp_smem_bytes<Real>(g.Tg, g.A, 1));  // [TBR][33]
+
+  // Start-up loads: the lane's s values and the D0 row do not depend on the predecessor kernel (the
+  // last of nf_batch_prepare's kernels, which waited for everything before it), so they are issued
+  // before griddepcontrol.wait; the channel records it writes come after.
+  const int span = a.w1 - a.w0;
+  const int c0 = a.w0 + chunk_bound(span, chunk, C, a.order, a.taper);
+  const int c1 = a.w0 + chunk_bound(span, chunk + 1, C, a.order, a.taper);
+  R2<Real>* out = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * span - a.w0;
+  ChanRec nxt;
+  R2<Real> nxtw;
+  int tx, ty, tz;
+  tile_coords(g, tile, tx, ty, tz);
+  int x0, y, z;
+  lane_voxel(tx, ty, tz, L, x0, y, z);
+  Real srv[V], siv[V];
+  {  // the lane's V voxels (consecutive in x): 16-byte vector loads when all are inside and aligned
+    using U16 = typename std::conditional<std::is_same<Real, float>::value, float4, double2>::type;
+    constexpr int NU = 2 * V * (int)sizeof(Real) / 16, PU = 16 / (int)sizeof(Real);
+    const size_t n0 = ((size_t)z * g.ny + y) * g.nx + x0;
+    if (x0 + V <= g.nx && y < g.ny && z < g.nzs && (sizeof(Real) == 8 || (g.nx & 1) == 0)) {
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        const U16 w = reinterpret_cast<const U16*>(a.s + 2 * n0)[u];
+        const Real* t = reinterpret_cast<const Real*>(&w);
+#pragma unroll
+        for (int k = 0; k < PU; k += 2) {
+          srv[(u * PU + k) >> 1] = t[k];
+          siv[(u * PU + k) >> 1] = t[k + 1];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const bool ok = x0 + v < g.nx && y < g.ny && z < g.nzs;
+        srv[v] = ok ? a.s[2 * (n0 + v)] : Real(0);
+        siv[v] = ok ? a.s[2 * (n0 + v) + 1] : Real(0);
+      }
+    }
+  }
+  for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
+  for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
+  pdl_wait();
+  prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
+  const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
+  const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
+  const QV<Real> sr = make_v(srv), si = make_v(siv);
+  int cur_tg = -1, pf_r = -1, carry = -1;
+  if (c0 < c1) {  // stage the first run's tx group and rx rows as soon as the first record is in
+    const int pk0 = __shfl_sync(FULL, nxt.pk, 0);
+    cur_tg = tx_group(g, pk_t(pk0));
+    pf_r = pk_r(pk0);
+    load_tgroup_async<Real>(g, tabt, ws.tside, cur_tg, L);
+    stage_rx<Real>(g, tabt, pf_r, ws.rslot, L);
+  }
+  __syncwarp();
+
+  QV<Real> dR, iR, shr, shi, nshr;
+  zero(dR);
+  zero(iR);
+  zero(shr);
+  zero(shi);
+  zero(nshr);
+  R2<Real>* outl = out + L;
+  for (int jb = c0; jb < c1; jb += 32) {
+    const int nb = min(32, c1 - jb);
+    const unsigned starts =
+        build_records<Real, EXACT>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
+    // sub-batches of TBR channels share one [TBR][33] transpose buffer
+    for (int h0 = 0; h0 < nb; h0 += TBR) {
+      const int h1 = min(nb, h0 + TBR);
+      int c = h0;
+      while (c < h1) {
+        const int key = ws.rect[c].y;
+        const int e = min(key >> 24, h1);
+        if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c
+          const int rr = key & 0x7fff, tg = (key >> 15) & 0x1ff;
+          if (tg != cur_tg) {
+            load_tgroup_async<Real>(g, tabt, ws.tside, tg, L);
+            cur_tg = tg;
+          }
+          rx_run_rows_1slot<Real>(g, tabt, ws, rr, pf_r, L, dR, iR);
+          scale_s(iR, sr, si, shr, shi, nshr);
+        }
+        // two channels per iteration, both results stored after both are computed, so the
+        // compiler can overlap their dependency chains (a store in between would be a barrier)
+        for (; c + 1 < e; c += 2) {
+          const R4<Real> q0 = ws.rec[c], q1 = ws.rec[c + 1];
+          const int o0 = bits_int(q0.z), o1 = bits_int(q1.z);
+          const QV<Real> dT0 = ldv(tsl + o0), iT0 = ldv(tsl + o0 + TILE);
+          const QV<Real> dT1 = ldv(tsl + o1), iT1 = ldv(tsl + o1 + TILE);
+          QV<Real> cs0, sn0, cs1, sn1;
+          phasorv<EXACT, NFGPU_FWD_CIS>(q0.x, q0.y, dT0, dR, cs0, sn0);
+          phasorv<EXACT, NFGPU_FWD_CIS>(q1.x, q1.y, dT1, dR, cs1, sn1);
+          const R2<Real> p0 = fwd_part(iT0, cs0, sn0, shr, shi, nshr);
+          const R2<Real> p1 = fwd_part(iT1, cs1, sn1, shr, shi, nshr);
+          tb[(c - h0) * 33 + L] = p0;
+          tb[(c + 1 - h0) * 33 + L] = p1;
+        }
+        if (c < e) {
+          const R4<Real> q = ws.rec[c];
+          const int off = bits_int(q.z);
+          const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
+          QV<Real> cs, sn;
+          phasorv<EXACT, NFGPU_FWD_CIS>(q.x, q.y, dT, dR, cs, sn);
+          tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi, nshr);
+          ++c;
+        }
+      }
+      __syncwarp();
+      // transpose-reduce: 32/TBR lanes per row each sum a 32/(32/TBR) slice of row L % TBR,
+      // then combine with shuffles (fixed order)
+      constexpr int PER = 32 / TBR, SL = 32 / PER;
+      const int row = L % TBR, part = L / TBR;
+      R2<Real> S;
+      S.x = 0;
+      S.y = 0;
+#pragma unroll 8
+      for (int l = 0; l < SL; ++l) {
+        const R2<Real> t = tb[row * 33 + part * SL + l];
+        if constexpr (std::is_same<Real, float>::value) {
+          S = add2(S, t);
+        } else {
+          S.x += t.x;
+          S.y += t.y;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= TBR; o >>= 1) {
+        S.x += __shfl_down_sync(FULL, S.x, o);
+        S.y += __shfl_down_sync(FULL, S.y, o);
+      }
+      if (L < h1 - h0) outl[jb + h0] = S;
+      __syncwarp();
+    }
+  }
+  stage_wait();
 }
 
 // ------------------------------------------------------------------ structured (Cartesian) batches
@@ -2908,7 +3055,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
       break;
     }
     // ---- P1: forward
-    for (int u = gw; u < nfu; u = next_unit(la.ctr, TW, L)) fwd_unit<Real, EXACT>(fa, u, wbase, L, s_in);
+    for (int u = gw; u < nfu; u = next_unit(la.ctr, TW, L)) fwd_unit<Real, EXACT, true>(fa, u, wbase, 0, L, s_in);
     LOOP_STAMP(3);
     grid_sync(la.bar);
     LOOP_STAMP(4);
@@ -3077,12 +3224,13 @@ __device__ __forceinline__ double2 tiny_entry(const TinyArgs& ta, double x, doub
                                              double kd) {
   const double* a = ta.ant + 3 * t;
   const double* b = ta.ant + 3 * (ta.T + r);
-  const double dT = sqrt((x - a[0]) * (x - a[0]) + (y - a[1]) * (y - a[1]) + (z - a[2]) * (z - a[2]));
-  const double dR = sqrt((x - b[0]) * (x - b[0]) + (y - b[1]) * (y - b[1]) + (z - b[2]) * (z - b[2]));
-  const double rev = kd * (dT + dR);
+  const double qT = (x - a[0]) * (x - a[0]) + (y - a[1]) * (y - a[1]) + (z - a[2]) * (z - a[2]);
+  const double qR = (x - b[0]) * (x - b[0]) + (y - b[1]) * (y - b[1]) + (z - b[2]) * (z - b[2]);
+  const double iT = rsqrt(qT), iR = rsqrt(qR);  // 1/d within 1 ulp; d = q/sqrt(q) within 2 ulp
+  const double rev = kd * fma(qT, iT, qR * iR);
   double s, c;
   cis_rev(rev - rint(rev), s, c);
-  const double amp = 1.0 / (dT * dR);
+  const double amp = iT * iR;
   return make_double2(c * amp, -s * amp);
 }
 

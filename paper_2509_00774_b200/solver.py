@@ -623,6 +623,7 @@ def _solve(y, scenario: ImagingScenario, config: SolverConfig, initial, progress
 
 
 LOOP_CHUNK = 256  # iterations per persistent launch (the host draws the next chunk's batches meanwhile)
+LOOP_FIRST_CHUNK = 4
 
 
 def _loop_batch(plan: DevicePlan, config: SolverConfig, scenario: ImagingScenario, stochastic: bool):
@@ -685,7 +686,9 @@ def _solve_persistent(eng: SPGMEngine, plan: DevicePlan, config: SolverConfig, s
     records: list[IterationRecord] = []
     termination = TERMINATION_MAX_ITERS
     done = 0
-    n = min(LOOP_CHUNK, config.max_iters)
+    # chunks grow geometrically from LOOP_FIRST_CHUNK: the host draws only a few batches before the first
+    # launch, then each chunk's batches are drawn while the previous chunk runs
+    n = min(LOOP_FIRST_CHUNK, LOOP_CHUNK, config.max_iters)
     table = draw(n)
     while done < config.max_iters:
         if config.sampler == "table":
@@ -695,7 +698,7 @@ def _solve_persistent(eng: SPGMEngine, plan: DevicePlan, config: SolverConfig, s
             budget = max(0.0, config.time_budget_s - (time.perf_counter() - t_start))
         rec, _ = eng.run_loop(n, table=table, seed=config.rng_seed, iter0=done + 1, batch=B, tol=config.tol,
                               time_budget_s=budget)
-        n_next = min(LOOP_CHUNK, config.max_iters - done - n)
+        n_next = min(2 * n, LOOP_CHUNK, config.max_iters - done - n)
         table = draw(n_next) if n_next > 0 else None  # overlaps the launch on the GPU
         k_run, reason = eng.loop_result()
         r = rec[:k_run].cpu().numpy()
