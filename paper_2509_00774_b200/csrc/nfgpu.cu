@@ -3509,6 +3509,11 @@ struct nf_plan {
   int chunk_order = 0;                      // flat work-unit order (unit_coords / chunk_bound)
   bool tail_split = true;                   // tile-major launches end on shorter units (unit_map; env NFGPU_TAIL=0)
   int tail_factor = 4;                      // ... tail_factor x more chunks per tail tile (env NFGPU_TAIL_FACTOR)
+  // wave_fit: bit 0 forward, bit 1 adjoint. Per-launch kernels: the adjoint only (Medium step 119.5 -> 116.0 us;
+  // the hardware's CTA scheduler already balances the forward); the persistent loop, whose warps fetch units
+  // themselves: both (Medium loop 126.4 -> 121.5 us with the forward). Env NFGPU_WAVE_FIT / NFGPU_LOOP_WAVE_FIT.
+  int wave_fit = 2;
+  int loop_wave_fit = 3;
   double tail_waves = 1.0;                  // ... for about this many waves of warp slots (env NFGPU_TAIL_WAVES)
   double taper = 0.375;                     // chunk-major adjoint taper h: last chunk 1 − 2h of the first (env NFGPU_TAPER)
   double fwd_taper = 0.475;                 // ... forward (1/8 Large slab 0.3552 -> 0.3516 ms; env NFGPU_FWD_TAPER)
@@ -3654,6 +3659,22 @@ void tail_split(const nf_plan* p, int order, int C, long long cmax, int& t1, int
   C2 = (int)c2;
 }
 
+// Wave fit for tile-major launches without a split tail (Medium-sized problems, whose equal units leave the last
+// wave partly empty: BASELINE Medium's 4096 forward units fill 1.73 waves of the 2368 warp slots): tiles
+// [0, t1) take C chunks and tiles [t1, ntiles) C + 1, so the unit count is exactly k waves. cmax bounds the
+// chunk count (channels per tile for the forward, the partial-buffer cap for the adjoint).
+void wave_fit(const nf_plan* p, int order, int cmax, int& C, int& t1, int& C2) {
+  if (order != 0 || t1 != p->g.ntiles || C2 != C) return;  // chunk-major or already split
+  const long long slots = 148LL * 16, nt = p->g.ntiles, units = nt * C;
+  if (units < slots / 2 || units > 4 * slots) return;
+  const long long target = (units + slots - 1) / slots * slots;
+  const long long c = target / nt;
+  if (c < 1 || c + 1 > cmax) return;
+  t1 = (int)(nt * (c + 1) - target);
+  C = (int)c;
+  C2 = (int)c + 1;
+}
+
 // Chunks per tile: enough (tile, chunk) warp units for the target, with at least min_chunk channels per
 // chunk -- unless that leaves less than a quarter wave of units (tiny problems such as BASELINE Small: 8 tiles,
 // 32 channels), where chunks go down to SMALL_CHUNK channels to put more warps on the latency-bound work.
@@ -3717,7 +3738,7 @@ int launch_reduce2(nf_plan* p, int span, int nseg, int w0, void* y, cudaStream_t
 
 // Forward launch arguments of one window [w0, w1) of the staged flat batch (launch_forward, spgm_loop)
 template <typename Real>
-FwdArgs<Real> fwd_args(const nf_plan* p, const void* s, int w0, int w1) {
+FwdArgs<Real> fwd_args(const nf_plan* p, const void* s, int w0, int w1, bool loop = false) {
   const int span = w1 - w0;
   FwdArgs<Real> a;
   a.g = p->g;
@@ -3731,6 +3752,7 @@ FwdArgs<Real> fwd_args(const nf_plan* p, const void* s, int w0, int w1) {
   a.part = (Real*)p->d_part;
   a.order = unit_order(p, (long long)p->g.ntiles * a.Q);
   tail_split(p, a.order, a.Q, std::max(1, span / p->min_chunk), a.t1, a.Q2);
+  if ((loop ? p->loop_wave_fit : p->wave_fit) & 1) wave_fit(p, a.order, span, a.Q, a.t1, a.Q2);
   a.taper = (float)p->fwd_taper;
   return a;
 }
@@ -3738,7 +3760,7 @@ FwdArgs<Real> fwd_args(const nf_plan* p, const void* s, int w0, int w1) {
 // Adjoint (+ prox) arguments of the staged flat batch (launch_adjoint, spgm_loop)
 template <typename Real>
 AdjArgs<Real> adj_args(const nf_plan* p, void* gout, double scale, const void* s_in, void* s_out, double eta_over_b,
-                       double alpha) {
+                       double alpha, bool loop = false) {
   AdjArgs<Real> a;
   a.g = p->g;
   a.tab = (const Real*)p->d_tab;
@@ -3751,8 +3773,10 @@ AdjArgs<Real> adj_args(const nf_plan* p, void* gout, double scale, const void* s
   a.t1 = p->g.ntiles;
   a.CH2 = a.CH;
   a.taper = (float)p->taper;
-  if (!p->structured)
+  if (!p->structured) {
     tail_split(p, a.order, a.CH, std::min<long long>(std::max(1, p->B / p->adj_min_chunk), p->adj_ch_cap), a.t1, a.CH2);
+    if ((loop ? p->loop_wave_fit : p->wave_fit) & 2) wave_fit(p, a.order, std::min(p->B, p->adj_ch_cap), a.CH, a.t1, a.CH2);
+  }
   a.gpart = (Real*)p->d_gpart;
   a.cnt = p->d_tilecnt;
   a.gout = (Real*)gout;
@@ -4184,8 +4208,8 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
     }
     la.prof = p->d_loop_prof;
   }
-  FwdArgs<Real> fa = fwd_args<Real>(p, s_a, 0, B);
-  AdjArgs<Real> aa = adj_args<Real>(p, nullptr, 0, s_a, s_b, eta_over_b, alpha);
+  FwdArgs<Real> fa = fwd_args<Real>(p, s_a, 0, B, true);
+  AdjArgs<Real> aa = adj_args<Real>(p, nullptr, 0, s_a, s_b, eta_over_b, alpha, true);
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
   void* args[] = {&la, &fa, &aa};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nsm), dim3(nw * 32), args, smem, st));
@@ -4293,6 +4317,8 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   p->chunk_order = rs * (size_t)g.ntiles * g.A * TABW <= ((size_t)NFGPU_L2_TABLE_MB << 20) ? 1 : 0;
   if (const char* e = std::getenv("NFGPU_CHUNK_ORDER")) p->chunk_order = std::atoi(e) ? 1 : 0;
   if (const char* e = std::getenv("NFGPU_TAIL")) p->tail_split = std::atoi(e) != 0;
+  if (const char* e = std::getenv("NFGPU_WAVE_FIT")) p->wave_fit = std::atoi(e);
+  if (const char* e = std::getenv("NFGPU_LOOP_WAVE_FIT")) p->loop_wave_fit = std::atoi(e);
   if (const char* e = std::getenv("NFGPU_TAIL_FACTOR")) p->tail_factor = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("NFGPU_TAIL_WAVES")) p->tail_waves = std::max(0.0, std::atof(e));
   if (const char* e = std::getenv("NFGPU_TAPER")) p->taper = std::min(0.49, std::max(0.0, std::atof(e)));

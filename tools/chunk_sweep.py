@@ -25,16 +25,21 @@ ap.add_argument("--fwd", default="64")
 ap.add_argument("--adj", default="128")
 ap.add_argument("--reps", type=int, default=30)
 ap.add_argument("--graph", action="store_true", help="also time whole steps in a CUDA graph")
+ap.add_argument("--fit", default="", help="NFGPU_WAVE_FIT values to sweep (default: leave unset)")
 a = ap.parse_args()
 w = configs.WORKLOADS[a.workload]()
 scn = w.scenario
 rng = np.random.default_rng(0)
 y = (rng.standard_normal(scn.n_channels) + 1j * rng.standard_normal(scn.n_channels)).astype(np.complex64)
 st = torch.cuda.current_stream()
-for fm in a.fwd.split(","):
-    for am in a.adj.split(","):
+import itertools
+
+for fm, am, fit in itertools.product(a.fwd.split(","), a.adj.split(","), a.fit.split(",")):
+    if True:
         os.environ["NFGPU_MIN_CHUNK"] = fm
         os.environ["NFGPU_ADJ_MIN_CHUNK"] = am
+        if fit:
+            os.environ["NFGPU_WAVE_FIT"] = fit
         plan = DevicePlan(scn, dtype=w.dtype, device="cuda:0", max_batch=w.batch)
         eng = SPGMEngine(plan, y, eta=1e-2, alpha=1e-6, initial=configs.make_scene(w))
         f_ms, a_ms = [], []
@@ -52,7 +57,7 @@ for fm in a.fwd.split(","):
             if i >= 3:
                 f_ms.append(e0.elapsed_time(e1))
                 a_ms.append(e1.elapsed_time(e2))
-        out = {"workload": a.workload, "fwd_min_chunk": int(fm), "adj_min_chunk": int(am),
+        out = {"workload": a.workload, "fwd_min_chunk": int(fm), "adj_min_chunk": int(am), "wave_fit": fit,
                "fwd_ms": float(np.median(f_ms)), "adj_ms": float(np.median(a_ms))}
         if a.graph:
             g = eng.graph(0, w.batch, pairs=4)
