@@ -107,6 +107,14 @@ __device__ __forceinline__ void pdl_wait_and_release() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* a, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
 constexpr double PI = 3.14159265358979323846;
 constexpr double EXACT_FREE_REV = 12.0;  // largest |phase| (revolutions) fed to MUFU unreduced
 
@@ -937,7 +945,8 @@ __global__ void __launch_bounds__(256) resid_kernel(const int* __restrict__ sm, 
 // Adjoint epilogue shared by the flat and structured kernels: publish this (tile, chunk)
 // partial; the last of the tile's CH warps sums the partials in chunk order and writes
 // g (plain adjoint) or applies the prox and the termination statistics (SPGM step).
-template <typename Real, bool PROX>
+// LOOP (spgm_loop_kernel): the iterate is read through L2 (another SM wrote it an iteration ago)
+template <typename Real, bool PROX, bool LOOP = false>
 __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, int chunk, int C, int L, const QV<Real>& gr,
                                              const QV<Real>& gi, const Real* __restrict__ s_in,
                                              Real* __restrict__ s_out) {
@@ -1005,14 +1014,23 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
   if (PROX) {
     if (full) {
 #pragma unroll
-      for (int u = 0; u < NU; ++u) *reinterpret_cast<U16*>(io + u * (16 / sizeof(Real))) =
-          reinterpret_cast<const U16*>(s_in + 2 * n0)[u];
+      for (int u = 0; u < NU; ++u) {
+        if constexpr (LOOP)
+          *reinterpret_cast<U16*>(io + u * (16 / sizeof(Real))) = __ldcg(reinterpret_cast<const U16*>(s_in + 2 * n0) + u);
+        else
+          *reinterpret_cast<U16*>(io + u * (16 / sizeof(Real))) = reinterpret_cast<const U16*>(s_in + 2 * n0)[u];
+      }
     } else {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const bool in = x0 + v < g.nx && y < g.ny && z < g.nzs;
-        io[2 * v] = in ? s_in[2 * (n0 + v)] : Real(0);
-        io[2 * v + 1] = in ? s_in[2 * (n0 + v) + 1] : Real(0);
+        if constexpr (LOOP) {
+          io[2 * v] = in ? __ldcg(s_in + 2 * (n0 + v)) : Real(0);
+          io[2 * v + 1] = in ? __ldcg(s_in + 2 * (n0 + v) + 1) : Real(0);
+        } else {
+          io[2 * v] = in ? s_in[2 * (n0 + v)] : Real(0);
+          io[2 * v + 1] = in ? s_in[2 * (n0 + v) + 1] : Real(0);
+        }
       }
     }
   }
@@ -1070,9 +1088,10 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
 
 // One adjoint warp unit (tile, channel chunk) of the flat kernel: the body of adj_kernel, also run by the
 // persistent SPGM loop (spgm_loop_kernel). wbase: this warp's shared-memory region.
-template <typename Real, bool PROX, bool EXACT>
+template <typename Real, bool PROX, bool EXACT, bool LOOP = false>
 __device__ __forceinline__ void adj_unit(const AdjArgs<Real>& a, int unit, unsigned char* wbase, int L,
-                                         const Real* __restrict__ s_in, Real* __restrict__ s_out) {
+                                         const Real* __restrict__ s_in, Real* __restrict__ s_out,
+                                         const ChanRec* __restrict__ crec_loop = nullptr) {
   const Geo& g = a.g;
   int tile, chunk, C;
   unit_map(unit, g.ntiles, a.CH, a.t1, a.CH2, a.order, tile, chunk, C);
@@ -1084,7 +1103,7 @@ __device__ __forceinline__ void adj_unit(const AdjArgs<Real>& a, int unit, unsig
   // before the residual kernel, our predecessor, released us). The residual records w come after the wait.
   ChanRec nxt;
   R2<Real> nxtw;
-  prefetch_first<Real>(a.crec, nullptr, j0, j1, L, nxt, nxtw);
+  prefetch_first<Real>(LOOP ? crec_loop : a.crec, nullptr, j0, j1, L, nxt, nxtw);
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
   pdl_wait();
@@ -1104,7 +1123,8 @@ __device__ __forceinline__ void adj_unit(const AdjArgs<Real>& a, int unit, unsig
 
   for (int jb = j0; jb < j1; jb += 32) {
     const int nb = min(32, j1 - jb);
-    const unsigned starts = build_records<Real, EXACT>(g, ws, a.crec, a.wrec, jb, nb, j1, L, carry, nxt, nxtw);
+    const unsigned starts = build_records<Real, EXACT>(g, ws, LOOP ? crec_loop : a.crec, a.wrec, jb, nb, j1, L, carry, nxt,
+                                                             nxtw);
     int c = 0;
     while (c < nb) {
       const int key = ws.rect[c].y;
@@ -1138,7 +1158,7 @@ __device__ __forceinline__ void adj_unit(const AdjArgs<Real>& a, int unit, unsig
   flush(iR, hr, hi, gr, gi);
   stage_wait();
 
-  adj_epilogue<Real, PROX>(a, tile, chunk, C, L, gr, gi, s_in, s_out);
+  adj_epilogue<Real, PROX, LOOP>(a, tile, chunk, C, L, gr, gi, s_in, s_out);
 }
 
 template <typename Real, bool PROX, bool EXACT>
@@ -1241,10 +1261,12 @@ __device__ __forceinline__ void rx_run_rows_1slot(const Geo& g, const Real* __re
 // in the kernel (keeps its code generation); LOOP = true: the iterate sv_loop and the region wbase_loop.
 template <typename Real, bool EXACT, bool LOOP = false>
 __device__ __forceinline__ void fwd_unit(const FwdArgs<Real>& a, int unit, unsigned char* smem_base, int w, int L,
-                                         const Real* __restrict__ sv_loop = nullptr) {
+                                         const Real* __restrict__ sv_loop = nullptr,
+                                         const ChanRec* __restrict__ crec_loop = nullptr) {
   const Geo& g = a.g;
   int tile, chunk, C;
   unit_map(unit, g.ntiles, a.Q, a.t1, a.Q2, a.order, tile, chunk, C);
+  const ChanRec* __restrict__ crec = LOOP ? crec_loop : a.crec;
   unsigned char* wbase = LOOP ? smem_base : smem_base + (size_t)w * fwd_warp_bytes<Real>(g.Tg, g.A);
   const Real* __restrict__ sv = LOOP ? sv_loop : a.s;
   const WarpSmem<Real> ws = carve<Real>(wbase, g.Tg, g.A, 1);
@@ -1271,7 +1293,8 @@ __device__ __forceinline__ void fwd_unit(const FwdArgs<Real>& a, int unit, unsig
     if (x0 + V <= g.nx && y < g.ny && z < g.nzs && (sizeof(Real) == 8 || (g.nx & 1) == 0)) {
 #pragma unroll
       for (int u = 0; u < NU; ++u) {
-        const U16 w = reinterpret_cast<const U16*>(sv + 2 * n0)[u];
+        const U16 w = LOOP ? __ldcg(reinterpret_cast<const U16*>(sv + 2 * n0) + u)
+                           : reinterpret_cast<const U16*>(sv + 2 * n0)[u];
         const Real* t = reinterpret_cast<const Real*>(&w);
 #pragma unroll
         for (int k = 0; k < PU; k += 2) {
@@ -1283,15 +1306,15 @@ __device__ __forceinline__ void fwd_unit(const FwdArgs<Real>& a, int unit, unsig
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const bool ok = x0 + v < g.nx && y < g.ny && z < g.nzs;
-        srv[v] = ok ? sv[2 * (n0 + v)] : Real(0);
-        siv[v] = ok ? sv[2 * (n0 + v) + 1] : Real(0);
+        srv[v] = ok ? (LOOP ? __ldcg(sv + 2 * (n0 + v)) : sv[2 * (n0 + v)]) : Real(0);
+        siv[v] = ok ? (LOOP ? __ldcg(sv + 2 * (n0 + v) + 1) : sv[2 * (n0 + v) + 1]) : Real(0);
       }
     }
   }
   for (int i = L; i < g.A; i += 32) ws.d0[i] = a.D0[(size_t)tile * g.A + i];
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
   pdl_wait();
-  prefetch_first<Real>(a.crec, nullptr, c0, c1, L, nxt, nxtw);
+  prefetch_first<Real>(crec, nullptr, c0, c1, L, nxt, nxtw);
   const Real* tabt = a.tab + (size_t)tile * g.A * TABW;
   const Real* tsl = ws.tside + L * (16 / (int)sizeof(Real));
   const QV<Real> sr = make_v(srv), si = make_v(siv);
@@ -1315,7 +1338,7 @@ __device__ __forceinline__ void fwd_unit(const FwdArgs<Real>& a, int unit, unsig
   for (int jb = c0; jb < c1; jb += 32) {
     const int nb = min(32, c1 - jb);
     const unsigned starts =
-        build_records<Real, EXACT>(g, ws, a.crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
+        build_records<Real, EXACT>(g, ws, crec, nullptr, jb, nb, c1, L, carry, nxt, nxtw);
     // sub-batches of TBR channels share one [TBR][33] transpose buffer
     for (int h0 = 0; h0 < nb; h0 += TBR) {
       const int h1 = min(nb, h0 + TBR);
@@ -2889,7 +2912,7 @@ struct LoopArgs {
   const double* __restrict__ kd;
   const double* __restrict__ pulse;
   const void* ymeas;
-  int* sm;
+  int* sm;              // spgm_loop_kernel: per-CTA private records [2 parities][CTAs][B]
   int* spos;
   int* sf;
   ChanRec* crec;
@@ -2911,14 +2934,6 @@ struct LoopArgs {
 };
 constexpr int LOOP_PROF = 12;
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* a, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -2966,11 +2981,113 @@ __device__ __forceinline__ int loop_index(const LoopArgs& la, int k, int i) {
   return (int)x;
 }
 
+// P0 of an iteration: draw its batch and rank the keys (every CTA; keys are distinct) in shared memory, then
+// write ALL B channel records in key order (the counting sort's order) to this CTA's private copy. Ranks come
+// from a bitmap of the key space and a prefix count of its words when the bitmap fits, else pairwise.
+__device__ __forceinline__ void loop_sort(const LoopArgs& la, int k, int* scan_sh, unsigned char* smem_raw) {
+  const int B = la.B;
+  int* keys = reinterpret_cast<int*>(smem_raw);
+  int* order = keys + LOOP_SORT_MAX;
+  unsigned* bm = reinterpret_cast<unsigned*>(order + LOOP_SORT_MAX);
+  int* pre = reinterpret_cast<int*>(bm + la.kwords);
+  const bool bitmap = la.kwords > 0;
+  if (bitmap)
+    for (int i = threadIdx.x; i < la.kwords; i += blockDim.x) bm[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    const int key = key_of(la.km, loop_index(la, k, i));
+    keys[i] = key;
+    if (bitmap) atomicOr(bm + (key >> 5), 1u << (key & 31));
+  }
+  __syncthreads();
+  if (bitmap) {  // pre[w] = set bits in words < w
+    const int per = (la.kwords + blockDim.x - 1) / blockDim.x, w0 = threadIdx.x * per;
+    const int w1 = min(la.kwords, w0 + per);
+    int cnt = 0;
+    for (int q = w0; q < w1; ++q) cnt += __popc(bm[q]);
+    int total;
+    int run = block_excl_scan(cnt, scan_sh, total);
+    for (int q = w0; q < w1; ++q) {
+      pre[q] = run;
+      run += __popc(bm[q]);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    const int ki = keys[i];
+    int r = 0;
+    if (bitmap) {
+      r = pre[ki >> 5] + __popc(bm[ki >> 5] & ((1u << (ki & 31)) - 1u));
+    } else {
+      for (int q = 0; q < B; ++q) r += keys[q] < ki;
+    }
+    order[r] = i;
+  }
+  __syncthreads();
+  const size_t base = ((size_t)(k & 1) * gridDim.x + blockIdx.x) * B;
+  for (int j = threadIdx.x; j < B; j += blockDim.x) {
+    const int pos = order[j], key = keys[pos];
+    const int4 c = chan_of_key(la.km, key);
+    la.sm[base + j] = c.z + la.km.R * (c.y + la.km.T * c.x);
+    la.spos[base + j] = pos;
+    ChanRec q;
+    q.kd = la.kd[c.x];
+    q.kf = (float)q.kd;
+    q.pk = c.y | (c.z << 16);
+    la.crec[base + j] = q;
+    la.sf[base + j] = c.x;
+  }
+  __syncthreads();
+}
+
+// statistics of iteration k (stats_reduce_kernel's tree, threads 0-255 of every CTA, the same bits everywhere),
+// its record (CTA 0) and the time-budget flag; returns the relative magnitude change
+__device__ __forceinline__ double loop_stats(const LoopArgs& la, int k, int ntiles, double (*red)[256],
+                                             unsigned long long t0) {
+  if (threadIdx.x < 256) {
+    double acc[4] = {0, 0, 0, 0};
+    for (int i = threadIdx.x; i < ntiles; i += 256) {
+      acc[0] += la.stat_part[(size_t)i * 4 + 0];
+      acc[1] += la.stat_part[(size_t)i * 4 + 1];
+      acc[3] += la.stat_part[(size_t)i * 4 + 3];
+    }
+    const int nd = (la.B + 255) / 256;
+    for (int i = threadIdx.x; i < nd; i += 256) acc[2] += la.dpart[i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = acc[q];
+    named_sync(3, 256);
+    for (int sh = 128; sh > 0; sh >>= 1) {
+      if (threadIdx.x < sh)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + sh];
+      named_sync(3, 256);
+    }
+  }
+  __syncthreads();
+  const double st0 = red[0][0], st1 = red[1][0];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double* r = la.rec + (size_t)k * LOOP_REC;
+    r[0] = st0;
+    r[1] = st1;
+    r[2] = 0.5 * red[2][0];
+    r[3] = red[3][0];
+    const unsigned long long now = globaltimer();
+    r[4] = (double)(now - t0);
+    r[5] = 0;
+    if (la.budget_ns >= 0 && (long long)(now - t0) > la.budget_ns) {
+      la.state[2] = 1;
+      __threadfence();
+    }
+  }
+  __syncthreads();  // red[][] is rewritten later
+  return sqrt(st1) / fmax(sqrt(st0), 1e-12);
+}
+
 template <typename Real, bool EXACT>
 __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<Real> fa, AdjArgs<Real> aa) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int scan_sh[32];
-  // P3 / P5 scratch in the warp regions (no warp unit is in flight during those phases)
+  // sort / reduce / statistics scratch in the warp regions (no warp unit is in flight during those phases)
   double(*red)[256] = reinterpret_cast<double(*)[256]>(smem_raw);
   double(*grp_sh)[8] = reinterpret_cast<double(*)[8]>(smem_raw + 4 * 256 * sizeof(double));
   const Geo& g = fa.g;
@@ -2983,84 +3100,27 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
   const int nau = aa.t1 * aa.CH + (g.ntiles - aa.t1) * aa.CH2;
   unsigned char* wbase = smem_raw + (size_t)w * la.warp_bytes;
   const unsigned long long t0 = globaltimer();
-  int done = 0, reason = 0;
+  int done = 0, reason = 0, k = 0;
 #define LOOP_STAMP(i) \
   if (la.prof && blockIdx.x == 0 && threadIdx.x == 0) la.prof[(size_t)k * LOOP_PROF + (i)] = globaltimer() - t0
-  for (int k = 0; k < la.K; ++k) {
+  loop_sort(la, 0, scan_sh, smem_raw);
+  for (; k < la.K; ++k) {
     LOOP_STAMP(0);
     const Real* s_in = reinterpret_cast<const Real*>((k & 1) ? la.s_b : la.s_a);
     Real* s_out = reinterpret_cast<Real*>((k & 1) ? la.s_a : la.s_b);
-    if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[1] = 0;  // every warp is past its last adjoint fetch
-    // ---- P0: draw the batch and rank its keys (every CTA; keys are distinct), write this CTA's slice of the
-    // records in key order (the counting sort's order). Ranks come from a bitmap of the key space and a prefix
-    // count of its words when the bitmap fits in shared memory, else from pairwise comparisons.
-    {
-      int* keys = reinterpret_cast<int*>(smem_raw);
-      int* order = keys + LOOP_SORT_MAX;
-      unsigned* bm = reinterpret_cast<unsigned*>(order + LOOP_SORT_MAX);
-      int* pre = reinterpret_cast<int*>(bm + la.kwords);
-      const bool bitmap = la.kwords > 0;
-      if (bitmap)
-        for (int i = threadIdx.x; i < la.kwords; i += blockDim.x) bm[i] = 0;
-      __syncthreads();
-      for (int i = threadIdx.x; i < B; i += blockDim.x) {
-        const int key = key_of(la.km, loop_index(la, k, i));
-        keys[i] = key;
-        if (bitmap) atomicOr(bm + (key >> 5), 1u << (key & 31));
-      }
-      __syncthreads();
-      if (bitmap) {  // pre[w] = set bits in words < w
-        const int per = (la.kwords + blockDim.x - 1) / blockDim.x, w0 = threadIdx.x * per;
-        const int w1 = min(la.kwords, w0 + per);
-        int cnt = 0;
-        for (int q = w0; q < w1; ++q) cnt += __popc(bm[q]);
-        int total;
-        int run = block_excl_scan(cnt, scan_sh, total);
-        for (int q = w0; q < w1; ++q) {
-          pre[q] = run;
-          run += __popc(bm[q]);
-        }
-        __syncthreads();
-      }
-      const int j0 = (int)(((long long)B * blockIdx.x) / gridDim.x), j1 = (int)(((long long)B * (blockIdx.x + 1)) / gridDim.x);
-      for (int i = threadIdx.x; i < B; i += blockDim.x) {
-        const int ki = keys[i];
-        int r = 0;
-        if (bitmap) {
-          r = pre[ki >> 5] + __popc(bm[ki >> 5] & ((1u << (ki & 31)) - 1u));
-        } else {
-          for (int q = 0; q < B; ++q) r += keys[q] < ki;
-        }
-        if (r >= j0 && r < j1) order[r] = i;
-      }
-      __syncthreads();
-      for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-        const int pos = order[j], key = keys[pos];
-        const int4 c = chan_of_key(la.km, key);
-        la.sm[j] = c.z + la.km.R * (c.y + la.km.T * c.x);
-        la.spos[j] = pos;
-        ChanRec q;
-        q.kd = la.kd[c.x];
-        q.kf = (float)q.kd;
-        q.pk = c.y | (c.z << 16);
-        la.crec[j] = q;
-        la.sf[j] = c.x;
-      }
-    }
+    const size_t pbase = ((size_t)(k & 1) * gridDim.x + blockIdx.x) * B;  // this CTA's records of iteration k
+    // ---- forward(k) on this CTA's private records (sorted during iteration k-1: no barrier before)
+    for (int u = gw; u < nfu; u = next_unit(la.ctr, TW, L))
+      fwd_unit<Real, EXACT, true>(fa, u, wbase, 0, L, s_in, la.crec + pbase);
     LOOP_STAMP(1);
-    grid_sync(la.bar);
+    grid_sync(la.bar);  // B1
     LOOP_STAMP(2);
-    if (k > 0 && *(volatile int*)(la.state + 2)) {  // time budget spent (CTA 0's decision of iteration k-1)
+    if (k > 0 && *(volatile int*)(la.state + 2)) {  // time budget spent after iteration k-1 (CTA 0's clock)
       reason = 2;
       break;
     }
-    // ---- P1: forward
-    for (int u = gw; u < nfu; u = next_unit(la.ctr, TW, L)) fwd_unit<Real, EXACT, true>(fa, u, wbase, 0, L, s_in);
-    LOOP_STAMP(3);
-    grid_sync(la.bar);
-    LOOP_STAMP(4);
-    // ---- P2: level 1 of the forward reduce: tmp[seg][j] = sum over the segment's tiles (fixed order)
-    if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[0] = 0;  // every warp is past its last forward fetch
+    if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[1] = 0;  // every warp is past its adjoint fetches of k-1
+    // ---- level 1 of the forward reduce: tmp[seg][j] = sum over the segment's tiles (fixed order)
     {
       const int n = la.nseg * B;
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -3075,10 +3135,11 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
         la.tmp[(size_t)seg * B + j] = make_double2(sr, si);
       }
     }
-    LOOP_STAMP(5);
-    grid_sync(la.bar);
-    LOOP_STAMP(6);
-    // ---- P3: level 2 (y = p_f/(4pi) sum, rounded to Real as stored), residual records, dpart per 256 channels
+    LOOP_STAMP(3);
+    grid_sync(la.bar);  // B2
+    LOOP_STAMP(4);
+    if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[0] = 0;  // every warp is past its forward fetches of k
+    // ---- level 2 (y = p_f/(4pi) sum, rounded to Real as stored), residual records, dpart per 256 channels
     {
       const int half = threadIdx.x >> 8, ht = threadIdx.x & 255, halves = blockDim.x >> 8;
       const int ngrp = (B + 255) / 256;
@@ -3093,11 +3154,11 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
             sr += v.x;
             si += v.y;
           }
-          const int f = la.sf[j];
+          const int f = la.sf[pbase + j];
           const double pr = la.pulse[2 * f] / (4.0 * PI), pim = la.pulse[2 * f + 1] / (4.0 * PI);
           const Real yr = (Real)(pr * sr - pim * si), yi = (Real)(pr * si + pim * sr);
           double rr = (double)yr, ri = (double)yi;
-          const int m = la.sm[j];
+          const int m = la.sm[pbase + j];
           rr -= (double)ym[2 * (size_t)m];
           ri -= (double)ym[2 * (size_t)m + 1];
           e = rr * rr + ri * ri;
@@ -3119,58 +3180,24 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
         named_sync(1 + half, 256);
       }
     }
-    LOOP_STAMP(7);
-    grid_sync(la.bar);
-    LOOP_STAMP(8);
-    // ---- P4: adjoint + prox
-    for (int u = gw; u < nau; u = next_unit(la.ctr + 1, TW, L)) adj_unit<Real, true, EXACT>(aa, u, wbase, L, s_in, s_out);
-    LOOP_STAMP(9);
-    grid_sync(la.bar);
-    LOOP_STAMP(10);
-    // ---- P5: statistics (stats_reduce_kernel's order, threads 0-255 of every CTA), record, termination
-    if (threadIdx.x < 256) {
-      double acc[4] = {0, 0, 0, 0};
-      for (int i = threadIdx.x; i < g.ntiles; i += 256) {
-        acc[0] += la.stat_part[(size_t)i * 4 + 0];
-        acc[1] += la.stat_part[(size_t)i * 4 + 1];
-        acc[3] += la.stat_part[(size_t)i * 4 + 3];
-      }
-      const int nd = (B + 255) / 256;
-      for (int i = threadIdx.x; i < nd; i += 256) acc[2] += la.dpart[i];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = acc[q];
-      named_sync(3, 256);
-      for (int sh = 128; sh > 0; sh >>= 1) {
-        if (threadIdx.x < sh)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + sh];
-        named_sync(3, 256);
-      }
-    }
     __syncthreads();
-    const double st0 = red[0][0], st1 = red[1][0];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      double* r = la.rec + (size_t)k * LOOP_REC;
-      r[0] = st0;
-      r[1] = st1;
-      r[2] = 0.5 * red[2][0];
-      r[3] = red[3][0];
-      const unsigned long long now = globaltimer();
-      r[4] = (double)(now - t0);
-      r[5] = 0;
-      if (la.budget_ns >= 0 && (long long)(now - t0) > la.budget_ns) {
-        la.state[2] = 1;
-        __threadfence();
-      }
-    }
+    if (k + 1 < la.K) loop_sort(la, k + 1, scan_sh, smem_raw);  // the next iteration's records, meanwhile
+    LOOP_STAMP(5);
+    grid_sync(la.bar);  // B3
+    LOOP_STAMP(6);
+    // ---- adjoint(k) + prox
+    for (int u = gw; u < nau; u = next_unit(la.ctr + 1, TW, L))
+      adj_unit<Real, true, EXACT, true>(aa, u, wbase, L, s_in, s_out, la.crec + pbase);
+    LOOP_STAMP(7);
+    grid_sync(la.bar);  // B4
+    LOOP_STAMP(8);
+    const double change = loop_stats(la, k, g.ntiles, red, t0);
     done = k + 1;
-    LOOP_STAMP(11);
-    const double change = sqrt(st1) / fmax(sqrt(st0), 1e-12);
+    LOOP_STAMP(9);
     if (change < la.tol) {  // every CTA reaches the same decision from the same bits
       reason = 1;
       break;
     }
-    __syncthreads();  // red[][] is rewritten next iteration
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (reason == 0 && la.state[2]) reason = 2;  // the budget ran out on the last iteration of the launch
@@ -3568,6 +3595,8 @@ struct nf_plan {
   unsigned* d_loopbar = nullptr;  // persistent SPGM loop: grid barrier {arrivals, generation} (zero between launches)
   int loop_threads = 0;           // ... CTA size chosen on first use (0: not yet)
   unsigned long long* d_loop_prof = nullptr;  // ... phase time stamps (NFGPU_LOOP_PROFILE)
+  void* d_loop_priv = nullptr;  // spgm_loop_kernel: private records per CTA and tile epochs
+  size_t loop_priv_bytes = 0;
   void* d_tiny = nullptr;  // tiny_loop_kernel scratch: part, wch, ch, gpart, vbcnt, stat_part
   size_t tiny_bytes = 0;
   size_t loop_prof_elems = 0;
@@ -3616,6 +3645,7 @@ void free_plan(nf_plan* p) {
   cudaFree(p->d_loopbar);
   cudaFree(p->d_loop_prof);
   cudaFree(p->d_tiny);
+  cudaFree(p->d_loop_priv);
   cudaFree(p->d_epoch);
   cudaFree(p->d_comm_err);
   delete p;
@@ -4178,10 +4208,25 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   la.kd = p->d_kd;
   la.pulse = p->d_pulse;
   la.ymeas = ymeas;
-  la.sm = p->d_sm;
-  la.spos = p->d_spos;
-  la.sf = p->d_sf;
-  la.crec = p->d_crec;
+  {  // per-CTA private channel records [2][nsm][B]
+    const size_t n = (size_t)2 * nsm * B;
+    const size_t need = n * (sizeof(ChanRec) + 3 * sizeof(int));
+    if (need > p->loop_priv_bytes) {
+      cudaFree(p->d_loop_priv);
+      p->d_loop_priv = nullptr;
+      p->loop_priv_bytes = 0;
+      if (int rc = dalloc(p, (char**)&p->d_loop_priv, need)) return rc;
+      p->loop_priv_bytes = need;
+    }
+    char* b = (char*)p->d_loop_priv;
+    la.crec = (ChanRec*)b;
+    b += n * sizeof(ChanRec);
+    la.sm = (int*)b;
+    b += n * sizeof(int);
+    la.spos = (int*)b;
+    b += n * sizeof(int);
+    la.sf = (int*)b;
+  }
   la.tmp = p->d_tmp;
   la.dpart = p->d_dpart;
   la.stat_part = p->d_stat_part;
@@ -4195,19 +4240,7 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   la.s_b = s_b;
   la.warp_bytes = wb;
   la.kwords = bitmap ? (int)kwords : 0;
-  la.prof = nullptr;
-  if (std::getenv("NFGPU_LOOP_PROFILE")) {
-    const size_t need = (size_t)K * LOOP_PROF;
-    if (need > p->loop_prof_elems) {
-      cudaFree(p->d_loop_prof);
-  cudaFree(p->d_tiny);
-      p->d_loop_prof = nullptr;
-      p->loop_prof_elems = 0;
-      if (int rc = dalloc(p, &p->d_loop_prof, need * sizeof(unsigned long long))) return rc;
-      p->loop_prof_elems = need;
-    }
-    la.prof = p->d_loop_prof;
-  }
+  if (int rc = loop_profile_buffer(p, K, la)) return rc;
   FwdArgs<Real> fa = fwd_args<Real>(p, s_a, 0, B, true);
   AdjArgs<Real> aa = adj_args<Real>(p, nullptr, 0, s_a, s_b, eta_over_b, alpha, true);
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));

@@ -59,8 +59,8 @@ if os.environ.get("NFGPU_LOOP_PROFILE"):
         t = np.frombuffer(buf, dtype=np.uint64).reshape(K, 12).astype(np.float64)[K // 4:]
         tiny = not t[:, 6:].any()
         names = (["fwd", "bar0", "sums+adj+prox", "bar1", "stats"] if tiny else
-                 ["sort", "bar0", "fwd", "bar1", "red1", "bar2", "red2+resid", "bar3", "adj", "bar4", "stats"])
-        last = 5 if tiny else 11
+                 ["fwd", "bar1", "red1", "bar2", "red2+resid+next sort", "bar3", "adj", "bar4", "stats"])
+        last = 5 if tiny else 9
         d = np.diff(t[:, :last + 1], axis=1).mean(axis=0) / 1e3
         prof = {n: round(float(v), 2) for n, v in zip(names, d)}
         prof["next_iter_gap"] = round(float((t[1:, 0] - t[:-1, last]).mean() / 1e3), 2)
