@@ -3541,6 +3541,7 @@ struct nf_plan {
   // themselves: both (Medium loop 126.4 -> 121.5 us with the forward). Env NFGPU_WAVE_FIT / NFGPU_LOOP_WAVE_FIT.
   int wave_fit = 2;
   int loop_wave_fit = 3;
+  int fit_min_waves = 1;  // env NFGPU_FIT_MIN_WAVES
   double tail_waves = 1.0;                  // ... for about this many waves of warp slots (env NFGPU_TAIL_WAVES)
   double taper = 0.375;                     // chunk-major adjoint taper h: last chunk 1 − 2h of the first (env NFGPU_TAPER)
   double fwd_taper = 0.475;                 // ... forward (1/8 Large slab 0.3552 -> 0.3516 ms; env NFGPU_FWD_TAPER)
@@ -3697,7 +3698,7 @@ void wave_fit(const nf_plan* p, int order, int cmax, int& C, int& t1, int& C2) {
   if (order != 0 || t1 != p->g.ntiles || C2 != C) return;  // chunk-major or already split
   const long long slots = 148LL * 16, nt = p->g.ntiles, units = nt * C;
   if (units < slots / 2 || units > 4 * slots) return;
-  const long long target = (units + slots - 1) / slots * slots;
+  const long long target = std::max<long long>((units + slots - 1) / slots, p->fit_min_waves) * slots;
   const long long c = target / nt;
   if (c < 1 || c + 1 > cmax) return;
   t1 = (int)(nt * (c + 1) - target);
@@ -4352,6 +4353,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   if (const char* e = std::getenv("NFGPU_TAIL")) p->tail_split = std::atoi(e) != 0;
   if (const char* e = std::getenv("NFGPU_WAVE_FIT")) p->wave_fit = std::atoi(e);
   if (const char* e = std::getenv("NFGPU_LOOP_WAVE_FIT")) p->loop_wave_fit = std::atoi(e);
+  if (const char* e = std::getenv("NFGPU_FIT_MIN_WAVES")) p->fit_min_waves = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("NFGPU_TAIL_FACTOR")) p->tail_factor = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("NFGPU_TAIL_WAVES")) p->tail_waves = std::max(0.0, std::atof(e));
   if (const char* e = std::getenv("NFGPU_TAPER")) p->taper = std::min(0.49, std::max(0.0, std::atof(e)));

@@ -648,7 +648,10 @@ def _loop_batch(plan: DevicePlan, config: SolverConfig, scenario: ImagingScenari
         B = scenario.n_channels
         ok = routes_flat(np.arange(B))
     elif config.sampler == "table":
-        rows = np.asarray(config.index_table[: config.max_iters])
+        try:
+            rows = np.asarray(config.index_table[: config.max_iters])
+        except ValueError:  # ragged rows (batches of different sizes): the per-iteration path
+            return None
         if rows.dtype == object or rows.ndim != 2:
             return None
         B = rows.shape[1]
