@@ -38,6 +38,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -3634,6 +3636,23 @@ int dalloc(nf_plan* p, T** ptr, size_t bytes) {
   return NF_OK;
 }
 
+// Set a kernel's dynamic shared-memory limit (and the carveout) only when a launch needs more than was set
+// before on the current device (each cudaFuncSetAttribute call costs host time on every per-call launch).
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, int> g_attr_smem;
+cudaError_t ensure_smem(const void* kern, size_t bytes, bool carveout = false) {
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  int& cur = g_attr_smem[{kern, dev}];
+  if ((int)bytes <= cur) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && carveout)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) cur = (int)bytes;
+  return e;
+}
+
 void free_plan(nf_plan* p) {
   if (!p) return;
   void* ptrs[] = {p->d_ant,  p->d_kd,   p->d_kf,    p->d_pulse, p->d_tab,  p->d_D0,      p->d_pos_of_key,
@@ -3824,8 +3843,7 @@ template <typename Real>
 int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const size_t sm = fwd_smem(p);
   auto kern = p->exact ? fwd_kernel<Real, true> : fwd_kernel<Real, false>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+  CUDA_TRY(ensure_smem((const void*)kern, sm, true));
   for (int w0 = 0; w0 < p->B; w0 += p->fwd_chunk) {
     const int w1 = std::min(p->B, w0 + p->fwd_chunk);
     const int span = w1 - w0;
@@ -3899,7 +3917,7 @@ int launch_forward_tc(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const uint32_t smem = TcfLayout(npr, sa.nt + sa.nr, stream).bytes;
   auto kern = stream ? (p->exact ? fwd_tc_kernel<true, true> : fwd_tc_kernel<false, true>)
                      : (p->exact ? fwd_tc_kernel<true, false> : fwd_tc_kernel<false, false>);
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(ensure_smem((const void*)kern, smem));
   for (int fa = 0; fa < sa.nf; fa += (int)fwin) {
     const int fb = std::min(sa.nf, fa + (int)fwin);
     FwdArgs<float> a;
@@ -3948,8 +3966,7 @@ template <typename Real>
 int launch_forward_struct(nf_plan* p, const void* s, void* y, cudaStream_t st) {
   const size_t sm = struct_smem<Real, true>(p);
   auto kern = p->exact ? fwd_struct_kernel<Real, true> : fwd_struct_kernel<Real, false>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+  CUDA_TRY(ensure_smem((const void*)kern, sm, true));
   const StructArgs sa = struct_args(p);
   const int rows = sa.nf * sa.nt;
   const int win = std::max(1, p->fwd_chunk / sa.nr);  // rows per launch window (part buffer bound)
@@ -4005,7 +4022,7 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
       while (ns > 2 && TcLayout(npad, sa.nt + sa.nr, ns).bytes > TC_SMEM_MAX) --ns;
       const uint32_t smem = TcLayout(npad, sa.nt + sa.nr, ns).bytes;
       auto kern = p->exact ? adj_tc_kernel<PROX, true> : adj_tc_kernel<PROX, false>;
-      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(ensure_smem((const void*)kern, smem));
       kern<<<(unsigned)(p->g.ntiles * a.CH), TC_THREADS, smem, st>>>(a, sa, p->d_kd, p->d_bimg, npad, nch, fch, ns);
       CUDA_TRY(cudaGetLastError());
       p->launches += 3;
@@ -4022,16 +4039,12 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
     a.CH = std::min(struct_splits(p->struct_target, p->g.ntiles, sa.nf * sa.nt), p->adj_ch_cap);
     const size_t sm = struct_smem<Real, false>(p);
     auto kern = p->exact ? adj_struct_kernel<Real, PROX, true> : adj_struct_kernel<Real, PROX, false>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CUDA_TRY(
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    CUDA_TRY(ensure_smem((const void*)kern, sm, true));
     kern<<<(unsigned)(p->g.ntiles * a.CH), SW * 32, sm, st>>>(a, sa, p->d_kd);
   } else {
     const size_t sm = adj_smem(p);
     auto kern = p->exact ? adj_kernel<Real, PROX, true> : adj_kernel<Real, PROX, false>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CUDA_TRY(
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    CUDA_TRY(ensure_smem((const void*)kern, sm, true));
     const int units = a.t1 * a.CH + (p->g.ntiles - a.t1) * a.CH2;
     CUDA_TRY(launch_k(p->use_pdl, kern, dim3((units + ADJ_WARPS - 1) / ADJ_WARPS), dim3(ADJ_WARPS * 32), sm, st, a));
   }
@@ -4148,7 +4161,7 @@ int launch_tiny_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   if (int rc = loop_profile_buffer(p, K, la)) return rc;
   const size_t smem = (size_t)ta.chunk_max * (sizeof(double2) + sizeof(int4));
   auto kern = tiny_loop_kernel<Real>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(ensure_smem((const void*)kern, smem));
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
   CUDA_TRY(cudaMemsetAsync(ta.vbcnt, 0, b_cnt, st));
   void* args[] = {&la, &ta};
@@ -4181,7 +4194,7 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   const bool bitmap = (size_t)LOOP_SORT_MAX * 8 + kwords * 8 <= SMEM_DYN_MAX;
   const size_t sort_bytes = (size_t)LOOP_SORT_MAX * 8 + (bitmap ? kwords * 8 : 0);
   const size_t smem = std::max({(size_t)nw * wb, sort_bytes, (size_t)(4 * 256 + 16) * sizeof(double)});
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(ensure_smem((const void*)kern, smem));
   int dev = 0, nsm = 0, per_sm = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
