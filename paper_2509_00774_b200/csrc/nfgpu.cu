@@ -1052,8 +1052,11 @@ __device__ __forceinline__ void adj_epilogue(const AdjArgs<Real>& a, int tile, i
       const Real o_r = ur * sc, o_i = ui * sc;
       io[2 * v] = o_r;
       io[2 * v + 1] = o_i;
-      const double m0 = hypot((double)s_r, (double)s_i);
-      const double m1 = hypot((double)o_r, (double)o_i);
+      // |s|, |o| in fp64: for c64 inputs the squares cannot overflow or underflow, so sqrt is as exact as hypot
+      const double m0 = sizeof(Real) == 4 ? sqrt(fma((double)s_r, (double)s_r, (double)s_i * (double)s_i))
+                                          : hypot((double)s_r, (double)s_i);
+      const double m1 = sizeof(Real) == 4 ? sqrt(fma((double)o_r, (double)o_r, (double)o_i * (double)o_i))
+                                          : hypot((double)o_r, (double)o_i);
       st0 += m0 * m0;
       st1 += (m1 - m0) * (m1 - m0);
       st3 += m1;
@@ -2887,6 +2890,345 @@ __global__ void __launch_bounds__(1024) magchange_kernel(const Real* __restrict_
   }
 }
 
+// ------------------------------------------------------------------ CTA-tile ("ct") flat kernels
+//
+// For plans whose whole per-tile table (all T + R antennas: A·2·TILE Reals, 64 KB for BASELINE Medium in c64)
+// fits twice in shared memory, a CTA of CT_WARPS warps works on ONE tile at a time with every row of it
+// resident, and its warps split the tile's channels. Every CTA owns an equal contiguous range of the
+// tile-major (tile, sorted channel) pairs of the launch (one CTA per SM, balanced to one pair), cut into
+// pieces (tile, channel range). A piece's table rows arrive with one bulk copy (TMA) on an mbarrier,
+// double-buffered: the last warp done with piece i refills its buffer with piece i + 2. No warp stages tx
+// groups or receiver rows, and no warp waits for a straggler of another tile.
+// Each (tile, channel) value is computed by one warp with the flat kernel's arithmetic and transpose-reduce, so
+// part[tile][j] is bit-identical to fwd_kernel's and subsets stay bit-exact. (The adjoint stays on the warp-unit
+// kernel: a CTA-tile adjoint, whose warps' partial gradients are combined per piece, measured slower on Medium,
+// 63.5 vs 58.3 us under ncu.)
+constexpr int CT_WARPS = 16;
+
+template <typename Real>
+struct CtLayout {  // [mbarriers, counters | buffer 0 | buffer 1 | warp records ×CT_WARPS | warp transposes]
+  size_t tab_bytes, buf_bytes, off_buf, off_warp, warp_bytes, off_u, u_bytes, bytes;
+  __host__ __device__ explicit CtLayout(int A) {
+    tab_bytes = (size_t)A * TABW * sizeof(Real);
+    buf_bytes = tab_bytes + (size_t)d0_slots(A) * sizeof(double) + 2 * TILE * sizeof(Real);  // table | D0 | s
+    off_buf = 64;
+    off_warp = off_buf + 2 * buf_bytes;
+    warp_bytes = 34 * sizeof(R4<Real>) + 34 * sizeof(int2);
+    off_u = off_warp + (size_t)CT_WARPS * warp_bytes;
+    u_bytes = (size_t)CT_WARPS * TBR * 33 * sizeof(R2<Real>);  // per-warp transpose buffers
+    bytes = off_u + u_bytes;
+  }
+};
+
+struct CtArgs {
+  long long W;  // ntiles * span: tile-major (tile, sorted channel) pairs of the launch window
+  int span;     // channels of the window
+  int G;        // CTAs (one per SM; the persistent loop's grid)
+};
+// the CTA's range [r0, r1) of pairs: its first tile and piece count (the only 64-bit divisions, once per phase)
+struct CtRange {
+  long long r0, r1;
+  int t0, np;
+};
+__device__ __forceinline__ CtRange ct_range(const CtArgs& c, int b) {
+  CtRange r;
+  r.r0 = (long long)b * c.W / c.G;
+  r.r1 = (long long)(b + 1) * c.W / c.G;
+  r.t0 = (int)(r.r0 / c.span);
+  r.np = r.r1 > r.r0 ? (int)((r.r1 - 1) / c.span) - r.t0 + 1 : 0;
+  return r;
+}
+// piece i of the range: tile and window-relative channels [ja, jb)
+__device__ __forceinline__ void ct_piece(const CtArgs& c, const CtRange& r, int i, int& tile, int& ja, int& jb) {
+  tile = r.t0 + i;
+  const long long base = (long long)tile * c.span;
+  ja = (int)max(r.r0 - base, 0LL);
+  jb = (int)min(r.r1 - base, (long long)c.span);
+}
+// warp w's slice of the piece's channels
+__device__ __forceinline__ void ct_slice(int ja, int jb, int w, int& c0, int& c1) {
+  c0 = ja + (int)(((long long)(jb - ja) * w) / CT_WARPS);
+  c1 = ja + (int)(((long long)(jb - ja) * (w + 1)) / CT_WARPS);
+}
+
+// Fill buffer `buf` with tile's table rows (bulk copy, lane 0), its D0 row and its iterate values in the lane-quad
+// layout of ldv (plain loads by the 32 lanes). mbarrier `full` (33 arrivals: the expect_tx of lane 0 and every lane
+// after its stores) completes when all of it has landed.
+template <typename Real, bool LOOP>
+__device__ __forceinline__ void ct_produce(const Geo& g, const Real* __restrict__ tab, const double* __restrict__ D0,
+                                           const Real* __restrict__ sv, unsigned char* buf, uint64_t* full, int tile,
+                                           int L) {
+  const CtLayout<Real> lay(g.A);
+  double* d0 = reinterpret_cast<double*>(buf + lay.tab_bytes);
+  Real* ss = reinterpret_cast<Real*>(buf + lay.tab_bytes + (size_t)d0_slots(g.A) * sizeof(double));
+  if (L == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the old piece before the copy
+    mbar_expect(full, (uint32_t)lay.tab_bytes);
+    bulk_g2s(buf, tab + (size_t)tile * g.A * TABW, (uint32_t)lay.tab_bytes, full);
+  }
+  for (int i = L; i < g.A; i += 32) d0[i] = D0[(size_t)tile * g.A + i];
+  {
+    int tx, ty, tz;
+    tile_coords(g, tile, tx, ty, tz);
+    int x0, y, z;
+    lane_voxel(tx, ty, tz, L, x0, y, z);
+    constexpr int QD = 16 / (int)sizeof(Real);
+    const size_t n0 = ((size_t)z * g.ny + y) * g.nx + x0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const bool ok = x0 + v < g.nx && y < g.ny && z < g.nzs;
+      Real re = 0, im = 0;
+      if (ok) {
+        re = LOOP ? __ldcg(sv + 2 * (n0 + v)) : sv[2 * (n0 + v)];
+        im = LOOP ? __ldcg(sv + 2 * (n0 + v) + 1) : sv[2 * (n0 + v) + 1];
+      }
+      const int e = (v / QD) * 32 * QD + L * QD + v % QD;
+      ss[e] = re;
+      ss[TILE + e] = im;
+    }
+  }
+  mbar_arrive(full);
+}
+
+// Channel records of one batch of 32 (lane L <-> sorted position jb + L) as build_records, with the prefetch of
+// the NEXT batch at an explicit position (pf, pf_end): the next batch of this slice, or the first batch of the
+// warp's slice of the next piece.
+template <typename Real, bool EXACT>
+__device__ __forceinline__ unsigned ct_records(const Geo& g, const WarpSmem<Real>& ws, const ChanRec* __restrict__ crec,
+                                               const R2<Real>* __restrict__ wrec, int nb, int pf, int pf_end, int L,
+                                               int& carry, ChanRec& nxt, R2<Real>& nxtw) {
+  const ChanRec cr = nxt;
+  const R2<Real> w = nxtw;
+  if (pf + L < pf_end) {
+    nxt = crec[pf + L];
+    if (wrec) nxtw = wrec[pf + L];
+  }
+  int key = -1, toff = 0;
+  if (L < nb) {
+    const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = tx_group(g, t);
+    const double x = cr.kd * (ws.d0[t] + ws.d0[g.T + r]);
+    R4<Real> q;
+    if constexpr (std::is_same<Real, float>::value) {
+      if (EXACT) {
+        q.x = cr.kf;
+        q.y = (float)(x - rint(x));
+      } else {
+        q.x = (float)(2.0 * PI * cr.kd);
+        q.y = (float)(2.0 * PI * (x - rint(x)));
+      }
+    } else {
+      q.x = cr.kd;
+      q.y = (Real)(x - rint(x));
+    }
+    toff = (t - tg * g.Tg) * TABW;
+    if (wrec) {
+      q.z = w.x;
+      q.w = w.y;
+      q.y = with_low2(q.y, t - tg * g.Tg);
+    } else {
+      q.z = int_bits<Real>(toff);
+      q.w = 0;
+    }
+    ws.rec[L] = q;
+    key = r | (tg << 15);
+  }
+  int prev = __shfl_up_sync(FULL, key, 1);
+  if (L == 0) prev = carry;
+  const unsigned starts = __ballot_sync(FULL, L < nb && key != prev);
+  carry = __shfl_sync(FULL, key, nb - 1);
+  if (L < nb) {
+    const unsigned later = L < 31 ? (starts >> (L + 1)) << (L + 1) : 0u;
+    const int end = later ? __ffs(later) - 1 : nb;
+    ws.rect[L] = make_int2(toff, key | (end << 24));
+  }
+  __syncwarp();
+  return starts;
+}
+
+// One warp's slice [c0, c1) (absolute sorted positions) of a forward piece: fwd_unit's channel loop on resident rows.
+template <typename Real, bool EXACT>
+__device__ __forceinline__ void ct_fwd_slice(const Geo& g, const Real* __restrict__ tab_s, const Real* __restrict__ s_s,
+                                             const WarpSmem<Real>& ws, R2<Real>* tb, const ChanRec* __restrict__ crec,
+                                             int c0, int c1, int pn0, int pn1, R2<Real>* __restrict__ outl, int L,
+                                             ChanRec& nxt) {
+  constexpr int QD = 16 / (int)sizeof(Real);
+  R2<Real> nxtw;
+  nxtw.x = 0;
+  nxtw.y = 0;
+  QV<Real> dR, iR, shr, shi, nshr;
+  zero(dR);
+  zero(iR);
+  zero(shr);
+  zero(shi);
+  zero(nshr);
+  const Real* tsl = tab_s + L * QD;
+  int carry = -1;
+  for (int jb = c0; jb < c1; jb += 32) {
+    const int nb = min(32, c1 - jb);
+    const bool more = jb + 32 < c1;
+    const unsigned starts = ct_records<Real, EXACT>(g, ws, crec, nullptr, nb, more ? jb + 32 : pn0, more ? c1 : pn1, L,
+                                                    carry, nxt, nxtw);
+    for (int h0 = 0; h0 < nb; h0 += TBR) {
+      const int h1 = min(nb, h0 + TBR);
+      int c = h0;
+      while (c < h1) {
+        const int key = ws.rect[c].y;
+        const int e = min(key >> 24, h1);
+        if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c: rows straight from the resident table
+          const int rr = key & 0x7fff, tg = (key >> 15) & 0x1ff;
+          tsl = tab_s + (size_t)tg * g.Tg * TABW + L * QD;
+          const Real* rrow = tab_s + (size_t)(g.T + rr) * TABW + L * QD;
+          dR = ldv(rrow);
+          iR = ldv(rrow + TILE);
+          // the iterate from shared memory at every run start (not held in registers across the run)
+          scale_s(iR, ldv(s_s + L * QD), ldv(s_s + TILE + L * QD), shr, shi, nshr);
+        }
+        for (; c + 1 < e; c += 2) {
+          const R4<Real> q0 = ws.rec[c], q1 = ws.rec[c + 1];
+          const int o0 = bits_int(q0.z), o1 = bits_int(q1.z);
+          const QV<Real> dT0 = ldv(tsl + o0), iT0 = ldv(tsl + o0 + TILE);
+          const QV<Real> dT1 = ldv(tsl + o1), iT1 = ldv(tsl + o1 + TILE);
+          QV<Real> cs0, sn0, cs1, sn1;
+          phasorv<EXACT, NFGPU_FWD_CIS>(q0.x, q0.y, dT0, dR, cs0, sn0);
+          phasorv<EXACT, NFGPU_FWD_CIS>(q1.x, q1.y, dT1, dR, cs1, sn1);
+          const R2<Real> p0 = fwd_part(iT0, cs0, sn0, shr, shi, nshr);
+          const R2<Real> p1 = fwd_part(iT1, cs1, sn1, shr, shi, nshr);
+          tb[(c - h0) * 33 + L] = p0;
+          tb[(c + 1 - h0) * 33 + L] = p1;
+        }
+        if (c < e) {
+          const R4<Real> q = ws.rec[c];
+          const int off = bits_int(q.z);
+          const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
+          QV<Real> cs, sn;
+          phasorv<EXACT, NFGPU_FWD_CIS>(q.x, q.y, dT, dR, cs, sn);
+          tb[(c - h0) * 33 + L] = fwd_part(iT, cs, sn, shr, shi, nshr);
+          ++c;
+        }
+      }
+      __syncwarp();
+      constexpr int PER = 32 / TBR, SL = 32 / PER;
+      const int row = L % TBR, part = L / TBR;
+      R2<Real> S;
+      S.x = 0;
+      S.y = 0;
+#pragma unroll 8
+      for (int l = 0; l < SL; ++l) {
+        const R2<Real> t = tb[row * 33 + part * SL + l];
+        if constexpr (std::is_same<Real, float>::value) {
+          S = add2(S, t);
+        } else {
+          S.x += t.x;
+          S.y += t.y;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= TBR; o >>= 1) {
+        S.x += __shfl_down_sync(FULL, S.x, o);
+        S.y += __shfl_down_sync(FULL, S.y, o);
+      }
+      if (L < h1 - h0) outl[jb + h0] = S;
+      __syncwarp();
+    }
+  }
+}
+
+// the last of the CTA's warps to finish piece i on buffer b (counter in shared memory; it resets it)
+__device__ __forceinline__ bool ct_last(int* cnt, int L) {
+  __threadfence_block();
+  __syncwarp();
+  int last = 0;
+  if (L == 0) {
+    last = atomicAdd(cnt, 1) == CT_WARPS - 1;
+    if (last) *cnt = 0;
+  }
+  last = __shfl_sync(FULL, last, 0);
+  if (last) __threadfence_block();
+  return last != 0;
+}
+
+// The CTA's forward pieces (per-launch kernel and persistent loop). ph: per-thread mbarrier parities.
+template <typename Real, bool EXACT, bool LOOP>
+__device__ __forceinline__ void ct_forward(const FwdArgs<Real>& a, const CtArgs& c, unsigned char* smem,
+                                           const Real* __restrict__ sv, const ChanRec* __restrict__ crec,
+                                           unsigned& ph, bool pdl) {
+  const Geo& g = a.g;
+  const CtLayout<Real> lay(g.A);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  int* cnt = reinterpret_cast<int*>(smem + 16);
+  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+  const CtRange rg = ct_range(c, blockIdx.x);
+  const int np = rg.np;
+  int tile, ja, jb;
+  if (w == 0)
+    for (int q = 0; q < 2 && q < np; ++q) {
+      ct_piece(c, rg, q, tile, ja, jb);
+      ct_produce<Real, LOOP>(g, a.tab, a.D0, sv, smem + lay.off_buf + q * lay.buf_bytes, full + q, tile, L);
+    }
+  if (pdl) pdl_wait();
+  WarpSmem<Real> ws;
+  unsigned char* wr = smem + lay.off_warp + (size_t)w * lay.warp_bytes;
+  ws.rec = reinterpret_cast<R4<Real>*>(wr);
+  ws.rect = reinterpret_cast<int2*>(wr + 34 * sizeof(R4<Real>));
+  ws.tside = ws.rslot = nullptr;
+  R2<Real>* tb = reinterpret_cast<R2<Real>*>(smem + lay.off_u) + (size_t)w * TBR * 33;
+  for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
+  ChanRec nxt;
+  R2<Real> nxtw;
+  int c0 = 0, c1 = 0;
+  if (np > 0) {
+    ct_piece(c, rg, 0, tile, ja, jb);
+    ct_slice(ja, jb, w, c0, c1);
+    prefetch_first<Real>(crec, nullptr, a.w0 + c0, a.w0 + c1, L, nxt, nxtw);
+  }
+  for (int q = 0; q < np; ++q) {
+    const int b = q & 1;
+    ct_piece(c, rg, q, tile, ja, jb);
+    ct_slice(ja, jb, w, c0, c1);
+    int pn0 = 0, pn1 = 0;
+    if (q + 1 < np) {
+      int t2, ja2, jb2;
+      ct_piece(c, rg, q + 1, t2, ja2, jb2);
+      ct_slice(ja2, jb2, w, pn0, pn1);
+    }
+    unsigned char* buf = smem + lay.off_buf + b * lay.buf_bytes;
+    mbar_wait(full + b, (ph >> b) & 1u);
+    ph ^= 1u << b;
+    ws.d0 = reinterpret_cast<double*>(buf + lay.tab_bytes);
+    const Real* s_s = reinterpret_cast<const Real*>(buf + lay.tab_bytes + (size_t)d0_slots(g.A) * sizeof(double));
+    R2<Real>* outl = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * c.span - a.w0 + L;
+    if (c0 < c1)
+      ct_fwd_slice<Real, EXACT>(g, reinterpret_cast<const Real*>(buf), s_s, ws, tb, crec, a.w0 + c0, a.w0 + c1,
+                                a.w0 + pn0, a.w0 + pn1, outl, L, nxt);
+    else if (pn0 + L < pn1)
+      nxt = crec[a.w0 + pn0 + L];
+    if (ct_last(cnt + b, L) && q + 2 < np) {
+      ct_piece(c, rg, q + 2, tile, ja, jb);
+      ct_produce<Real, LOOP>(g, a.tab, a.D0, sv, buf, full + b, tile, L);
+    }
+  }
+}
+
+__device__ __forceinline__ void ct_init(unsigned char* smem) {
+  if (threadIdx.x == 0) {
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    mbar_init(full, 33);
+    mbar_init(full + 1, 33);
+    reinterpret_cast<int*>(smem + 16)[0] = 0;
+    reinterpret_cast<int*>(smem + 16)[1] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+template <typename Real, bool EXACT>
+__global__ void __launch_bounds__(CT_WARPS * 32, 1) fwd_ct_kernel(FwdArgs<Real> a, CtArgs c) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ct_init(smem_raw);
+  unsigned ph = 0;
+  ct_forward<Real, EXACT, false>(a, c, smem_raw, a.s, a.crec, ph, true);
+}
+
 // ------------------------------------------------------------------ persistent SPGM loop
 //
 // spgm_loop_kernel runs K SPGM iterations (solver.py:281-310) of a flat batch in ONE cooperative launch, one CTA
@@ -3085,8 +3427,8 @@ __device__ __forceinline__ double loop_stats(const LoopArgs& la, int k, int ntil
   return sqrt(st1) / fmax(sqrt(st0), 1e-12);
 }
 
-template <typename Real, bool EXACT>
-__global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<Real> fa, AdjArgs<Real> aa) {
+template <typename Real, bool EXACT, bool CT>
+__global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<Real> fa, AdjArgs<Real> aa, CtArgs ca) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int scan_sh[32];
   // sort / reduce / statistics scratch in the warp regions (no warp unit is in flight during those phases)
@@ -3112,8 +3454,15 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     Real* s_out = reinterpret_cast<Real*>((k & 1) ? la.s_a : la.s_b);
     const size_t pbase = ((size_t)(k & 1) * gridDim.x + blockIdx.x) * B;  // this CTA's records of iteration k
     // ---- forward(k) on this CTA's private records (sorted during iteration k-1: no barrier before)
-    for (int u = gw; u < nfu; u = next_unit(la.ctr, TW, L))
-      fwd_unit<Real, EXACT, true>(fa, u, wbase, 0, L, s_in, la.crec + pbase);
+    if constexpr (CT) {
+      // the other phases reuse this shared memory (sort, reduce and adjoint scratch): fresh mbarriers every time
+      ct_init(smem_raw);
+      unsigned ph = 0;
+      ct_forward<Real, EXACT, true>(fa, ca, smem_raw, s_in, la.crec + pbase, ph, false);
+    } else {
+      for (int u = gw; u < nfu; u = next_unit(la.ctr, TW, L))
+        fwd_unit<Real, EXACT, true>(fa, u, wbase, 0, L, s_in, la.crec + pbase);
+    }
     LOOP_STAMP(1);
     grid_sync(la.bar);  // B1
     LOOP_STAMP(2);
@@ -3208,10 +3557,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
   }
 }
 #undef LOOP_STAMP
-template __global__ void spgm_loop_kernel<float, false>(LoopArgs, FwdArgs<float>, AdjArgs<float>);
-template __global__ void spgm_loop_kernel<float, true>(LoopArgs, FwdArgs<float>, AdjArgs<float>);
-template __global__ void spgm_loop_kernel<double, true>(LoopArgs, FwdArgs<double>, AdjArgs<double>);
-template __global__ void spgm_loop_kernel<double, false>(LoopArgs, FwdArgs<double>, AdjArgs<double>);
+
 
 // ------------------------------------------------------------------ persistent loop for tiny problems
 //
@@ -3603,6 +3949,10 @@ struct nf_plan {
   void* d_tiny = nullptr;  // tiny_loop_kernel scratch: part, wch, ch, gpart, vbcnt, stat_part
   size_t tiny_bytes = 0;
   size_t loop_prof_elems = 0;
+  int nsm = 148;             // SMs of the plan's device: CTAs of the CTA-tile forward and the persistent loop
+  int ct_mode = 1;           // CTA-tile flat forward (use_ct): 0 off, 1 when the work is large enough, 2 whenever
+                             // the layout fits (tests); env NFGPU_CT
+  long long ct_min_pairs = 1024;  // ... fewest (tile, channel) pairs per CTA (env NFGPU_CT_MIN)
   bool comm_active = false;  // inside nf_forward_allreduce
   bool comm_fused = false;   // ... and the flat forward's last reduce already did the all-reduce
 };
@@ -3786,6 +4136,23 @@ int launch_reduce2(nf_plan* p, int span, int nseg, int w0, void* y, cudaStream_t
   return NF_OK;
 }
 
+// CTA-tile forward (ct_forward) for a flat window of n channels: the whole per-tile table fits twice in shared
+// memory and every CTA gets at least ct_min_pairs (tile, channel) pairs (at least one with NFGPU_CT=2)
+bool use_ct(const nf_plan* p, long long n) {
+  if (p->ct_mode == 0 || p->structured || n < 1) return false;
+  const size_t bytes = p->dtype == NF_C64 ? CtLayout<float>(p->g.A).bytes : CtLayout<double>(p->g.A).bytes;
+  if (bytes > 232448) return false;
+  if ((long long)p->g.ntiles * n < p->nsm) return false;
+  return p->ct_mode == 2 || (long long)p->g.ntiles * n >= p->ct_min_pairs * p->nsm;
+}
+CtArgs ct_args(const nf_plan* p, int span) {
+  CtArgs c;
+  c.W = (long long)p->g.ntiles * span;
+  c.span = span;
+  c.G = p->nsm;
+  return c;
+}
+
 // Forward launch arguments of one window [w0, w1) of the staged flat batch (launch_forward, spgm_loop)
 template <typename Real>
 FwdArgs<Real> fwd_args(const nf_plan* p, const void* s, int w0, int w1, bool loop = false) {
@@ -3848,9 +4215,16 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     const int w1 = std::min(p->B, w0 + p->fwd_chunk);
     const int span = w1 - w0;
     const FwdArgs<Real> a = fwd_args<Real>(p, s, w0, w1);
-    const long long units = (long long)a.t1 * a.Q + (long long)(p->g.ntiles - a.t1) * a.Q2;
-    CUDA_TRY(launch_k(p->use_pdl, kern, dim3((unsigned)((units + FWD_WARPS - 1) / FWD_WARPS)), dim3(FWD_WARPS * 32),
-                      sm, st, a));
+    if (use_ct(p, span)) {  // part[tile][j] is the same either way (bit-identical per-(tile, channel) values)
+      auto kct = p->exact ? fwd_ct_kernel<Real, true> : fwd_ct_kernel<Real, false>;
+      const size_t smc = CtLayout<Real>(p->g.A).bytes;
+      CUDA_TRY(ensure_smem((const void*)kct, smc));
+      CUDA_TRY(launch_k(p->use_pdl, kct, dim3(p->nsm), dim3(CT_WARPS * 32), smc, st, a, ct_args(p, span)));
+    } else {
+      const long long units = (long long)a.t1 * a.Q + (long long)(p->g.ntiles - a.t1) * a.Q2;
+      CUDA_TRY(launch_k(p->use_pdl, kern, dim3((unsigned)((units + FWD_WARPS - 1) / FWD_WARPS)),
+                        dim3(FWD_WARPS * 32), sm, st, a));
+    }
     // two-level reduce: ~sqrt(rows) segments so both levels have short serial sums. The segment count
     // depends on the plan only, never on the span, so a channel's summation tree is the same in every
     // batch: forward_apply(s, subset=sub) == forward_apply(s)[sub] bit for bit (forward.py:17-18).
@@ -4180,7 +4554,11 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   if ((!tiny_env || std::atoi(tiny_env) != 0) && (long long)B * p->nvox <= TINY_MAX_ENTRIES)
     return launch_tiny_loop<Real>(p, table, K, seed, iter0, B, ymeas, s_a, s_b, eta_over_b, alpha, tol, budget_ns,
                                   rec, state, st);
-  auto kern = p->exact ? spgm_loop_kernel<Real, true> : spgm_loop_kernel<Real, false>;
+  // the forward phase on the CTA-tile kernel (as nf_forward would run it; its values are bit-identical either way)
+  // when its layout fits next to 16 warp regions
+  bool ct = use_ct(p, B);
+  auto kern = ct ? (p->exact ? spgm_loop_kernel<Real, true, true> : spgm_loop_kernel<Real, false, true>)
+                 : (p->exact ? spgm_loop_kernel<Real, true, false> : spgm_loop_kernel<Real, false, false>);
   size_t wb = std::max(fwd_warp_bytes<Real>(p->g.Tg, p->g.A), warp_smem_bytes<Real>(p->g.Tg, p->g.A));
   wb = (wb + 15) & ~(size_t)15;
   cudaFuncAttributes fattr;
@@ -4193,7 +4571,12 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   const size_t kwords = ((size_t)p->KS + 31) / 32;
   const bool bitmap = (size_t)LOOP_SORT_MAX * 8 + kwords * 8 <= SMEM_DYN_MAX;
   const size_t sort_bytes = (size_t)LOOP_SORT_MAX * 8 + (bitmap ? kwords * 8 : 0);
-  const size_t smem = std::max({(size_t)nw * wb, sort_bytes, (size_t)(4 * 256 + 16) * sizeof(double)});
+  size_t smem = std::max({(size_t)nw * wb, sort_bytes, (size_t)(4 * 256 + 16) * sizeof(double)});
+  if (ct && (nw != 16 || CtLayout<Real>(p->g.A).bytes > SMEM_DYN_MAX)) {
+    ct = false;
+    kern = p->exact ? spgm_loop_kernel<Real, true, false> : spgm_loop_kernel<Real, false, false>;
+  }
+  if (ct) smem = std::max(smem, CtLayout<Real>(p->g.A).bytes);
   CUDA_TRY(ensure_smem((const void*)kern, smem));
   int dev = 0, nsm = 0, per_sm = 0;
   CUDA_TRY(cudaGetDevice(&dev));
@@ -4258,7 +4641,9 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   FwdArgs<Real> fa = fwd_args<Real>(p, s_a, 0, B, true);
   AdjArgs<Real> aa = adj_args<Real>(p, nullptr, 0, s_a, s_b, eta_over_b, alpha, true);
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
-  void* args[] = {&la, &fa, &aa};
+  CtArgs ca = ct_args(p, B);
+  ca.G = nsm;
+  void* args[] = {&la, &fa, &aa, &ca};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nsm), dim3(nw * 32), args, smem, st));
   p->loop_threads = nw * 32;
   p->launches += 1;
@@ -4437,6 +4822,14 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   }
   if (const char* e = std::getenv("NFGPU_TC_FWD")) p->tc_fwd = std::atoi(e) != 0;
   if (const char* e = std::getenv("NFGPU_PDL")) p->use_pdl = std::atoi(e) != 0;
+  if (const char* e = std::getenv("NFGPU_CT")) p->ct_mode = std::atoi(e);
+  if (const char* e = std::getenv("NFGPU_CT_MIN")) p->ct_min_pairs = std::max(1LL, std::atoll(e));
+  {
+    int dev = 0, nsm = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
+      p->nsm = nsm;
+  }
   if (p->use_tc) {
     const size_t npad_max = (size_t)((2 * n_tx + 15) / 16) * 16;
     ALLOC(p->d_bimg, (size_t)n_f * ((n_rx + TC_RCH - 1) / TC_RCH) * npad_max * (2 * TC_RCH) * 4 * 2);

@@ -414,3 +414,37 @@ def test_antenna_limits_raise_value_error():
     scn = _many_antenna_scenario(1100, 2, n_f=1, dims=(2, 2, 2))
     with pytest.raises(ValueError, match="transmitters"):
         forward_apply(np.zeros(scn.n_voxels), scn, dtype="c64")
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("case", ["medium", "ragged", "small"])
+def test_cta_tile_forward_is_bit_identical(case, dtype, rng, monkeypatch):
+    """The CTA-tile forward (fwd_ct_kernel: whole per-tile table resident in shared memory, one CTA per SM over an
+    equal range of (tile, channel) pairs) computes every (tile, channel) value with the warp-unit kernel's
+    arithmetic and transpose-reduce: forward values must be identical bit for bit (NFGPU_CT=2 forces it whenever
+    its layout fits; 0 forbids it), on full sets, subsets and a ragged grid."""
+    from paper_2509_00774_b200 import configs
+    from paper_2509_00774_b200.forward import forward_values
+
+    if case == "medium":
+        scn = configs.medium_scenario()
+        idxs = [np.sort(rng.choice(scn.n_channels, 512, replace=False)), np.arange(scn.n_channels)]
+    elif case == "small":
+        scn = configs.small_scenario()
+        idxs = [np.sort(rng.choice(scn.n_channels, 32, replace=False)), np.arange(scn.n_channels)]
+    else:
+        scn = ImagingScenario(
+            array=ArrayGeometry(((0.03, 0.01, 0.0), (-0.02, 0.04, 0.0), (0.0, -0.05, 0.0)),
+                                ((0.01, 0.0, 0.0), (-0.04, -0.01, 0.0))),
+            frequencies=FrequencyGrid(20e9, 30e9, 5),
+            voxels=VoxelGrid(center=Vec3(0.0, 0.0, 0.3), extent=(0.2, 0.07, 0.06), dims=(33, 11, 9)),
+        )
+        idxs = [np.arange(scn.n_channels), np.sort(rng.choice(scn.n_channels, 17, replace=False))]
+    s = rc(rng, scn.n_voxels)
+    out = {}
+    for mode in ("0", "2"):
+        monkeypatch.setenv("NFGPU_CT", mode)
+        plan = DevicePlan(scn, dtype=dtype, device="cuda:0", structured="never")
+        out[mode] = [forward_values(plan, s, idx) for idx in idxs]
+    for a, b in zip(out["0"], out["2"]):
+        assert np.array_equal(a, b)

@@ -22,10 +22,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="small")
 ap.add_argument("--iters", type=int, default=2000)
 ap.add_argument("--dtype", default=None)
+ap.add_argument("--batch", type=int, default=None)
 a = ap.parse_args()
 w = configs.WORKLOADS[a.workload]()
 scn = w.scenario
 dtype = a.dtype or w.dtype
+if a.batch:
+    import dataclasses
+    w = dataclasses.replace(w, batch=a.batch)
 rng = np.random.default_rng(0)
 y = rng.standard_normal(scn.n_channels) + 1j * rng.standard_normal(scn.n_channels)
 plan = DevicePlan(scn, dtype=dtype, device="cuda:0", max_batch=w.batch)
