@@ -20,7 +20,7 @@
  *   nf_adjoint_prox       replaces  solver._gradient + soft_threshold +
  *                                   relative_magnitude_change (one SPGM step)  solver.py:181-183, 228-251, 287-289
  *   nf_spgm_loop          replaces  solver._solve's iteration loop for flat batches    solver.py:259-318
- *                                   (K iterations per launch, device-side termination test)
+ *   nf_spgm_loop_chained            (K iterations per launch, device-side termination test)
  *   nf_sample_flat        replaces  host minibatch sampling (flat uniform w/o replacement; the
  *   nf_plan_set_iter                structured Cartesian sampler solver.py:206-225 stays on the host)
  *   nf_soft_threshold     replaces  solver.soft_threshold                      solver.py:228-241
@@ -141,6 +141,17 @@ int nf_sample_structured(nf_plan* plan, uint64_t seed, uint64_t iter, int n_f, i
 int nf_spgm_loop(nf_plan* plan, const int32_t* idx_table_dev, int iters, uint64_t seed, uint64_t iter0, int batch,
                  const void* ymeas_dev, void* s_a_dev, void* s_b_dev, double eta_over_b, double alpha, double tol,
                  double time_budget_s, double* records_dev, int* state_dev, void* stream);
+
+/* nf_spgm_loop for chained launches, so that a host can enqueue launch j + 1 before it reads launch j's state
+ * (its Python solver draws and uploads the next chunk's batches and builds the last chunk's records while the GPU
+ * runs): when prev_state_dev (device, the previous launch's state; NULL for the first) reports an early stop
+ * (reason != 0), this launch runs no iteration and reports {0, that reason}; and every launch ends with the latest
+ * iterate in s_a (an odd iteration count is copied back from s_b), so consecutive launches take the same
+ * buffers. prev_state_dev and state_dev must differ. */
+int nf_spgm_loop_chained(nf_plan* plan, const int32_t* idx_table_dev, int iters, uint64_t seed, uint64_t iter0,
+                         int batch, const void* ymeas_dev, void* s_a_dev, void* s_b_dev, double eta_over_b,
+                         double alpha, double tol, double time_budget_s, double* records_dev, int* state_dev,
+                         const int* prev_state_dev, void* stream);
 
 /* Set the plan's device iteration counter (stream-ordered). */
 int nf_plan_set_iter(nf_plan* plan, uint64_t iter, void* stream);

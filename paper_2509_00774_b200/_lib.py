@@ -40,6 +40,8 @@ SIGNATURES = {
     "nf_sample_structured": (_I, [_P, ctypes.c_uint64, ctypes.c_uint64, _I, _I, _I, _P, _P]),
     "nf_plan_set_iter": (_I, [_P, ctypes.c_uint64, _P]),
     "nf_spgm_loop": (_I, [_P, _P, _I, ctypes.c_uint64, ctypes.c_uint64, _I, _P, _P, _P, _D, _D, _D, _D, _P, _P, _P]),
+    "nf_spgm_loop_chained": (_I, [_P, _P, _I, ctypes.c_uint64, ctypes.c_uint64, _I, _P, _P, _P, _D, _D, _D, _D, _P, _P,
+                                  _P, _P]),
     "nf_soft_threshold": (_I, [_I, _P, _P, ctypes.c_int64, _D, _P]),
     "nf_magnitude_change": (_I, [_I, _P, _P, ctypes.c_int64, _P, _P]),
     "nf_comm_create": (_I, [_P, _I, _I, _P]),

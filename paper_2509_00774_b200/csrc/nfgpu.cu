@@ -3274,9 +3274,35 @@ struct LoopArgs {
   void* s_a;            // iteration k reads s_a (k even) or s_b (k odd) and writes the other
   void* s_b;
   size_t warp_bytes;
+  const int* prev_state;     // chained launches: the previous launch's state; it stopped early -> run nothing
+  int fold;                  // the latest iterate ends in s_a (an odd count copies s_b back; chained launches)
   unsigned long long* prof;  // diagnostics (NFGPU_LOOP_PROFILE): CTA 0's device clock at each phase boundary
+  int prof_cta;              // ... and (NFGPU_LOOP_PROFILE=2) every CTA's at the ends of its forward and adjoint
 };
 constexpr int LOOP_PROF = 12;
+constexpr int LOOP_PROF_CTA = 160;  // NFGPU_LOOP_PROFILE=2: also every CTA's forward and adjoint end (spgm_loop)
+
+// Chained persistent launches (nf_spgm_loop_chained): the host enqueues launch j + 1 before it has read launch j's
+// state. A launch whose predecessor stopped early (tolerance or budget) runs no iteration and forwards its reason.
+__device__ __forceinline__ bool loop_skip(const LoopArgs& la) {
+  if (!la.prev_state) return false;
+  const int prev = *(volatile const int*)(la.prev_state + 1);
+  if (prev != 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    la.state[0] = 0;
+    la.state[1] = prev;
+  }
+  return prev != 0;
+}
+// ... and every launch ends with the latest iterate in s_a: after an odd count (written to s_b) all CTAs copy it
+// back (every write to s_b happened before the last grid barrier, and nothing reads s_a any more)
+template <typename Real>
+__device__ __forceinline__ void loop_fold(const LoopArgs& la, int done, long long nvox) {
+  if (!la.fold || !(done & 1)) return;
+  const Real* src = reinterpret_cast<const Real*>(la.s_b);
+  Real* dst = reinterpret_cast<Real*>(la.s_a);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * nvox; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = __ldcg(src + i);
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -3447,6 +3473,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
   int done = 0, reason = 0, k = 0;
 #define LOOP_STAMP(i) \
   if (la.prof && blockIdx.x == 0 && threadIdx.x == 0) la.prof[(size_t)k * LOOP_PROF + (i)] = globaltimer() - t0
+  if (loop_skip(la)) return;
   loop_sort(la, 0, scan_sh, smem_raw);
   for (; k < la.K; ++k) {
     LOOP_STAMP(0);
@@ -3464,6 +3491,10 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
         fwd_unit<Real, EXACT, true>(fa, u, wbase, 0, L, s_in, la.crec + pbase);
     }
     LOOP_STAMP(1);
+    if (la.prof && la.prof_cta) {  // diagnostics: the whole CTA's end of the phase
+      __syncthreads();
+      if (threadIdx.x == 0) la.prof[(size_t)la.K * LOOP_PROF + ((size_t)k * 2) * LOOP_PROF_CTA + blockIdx.x] = globaltimer() - t0;
+    }
     grid_sync(la.bar);  // B1
     LOOP_STAMP(2);
     if (k > 0 && *(volatile int*)(la.state + 2)) {  // time budget spent after iteration k-1 (CTA 0's clock)
@@ -3540,6 +3571,10 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     for (int u = gw; u < nau; u = next_unit(la.ctr + 1, TW, L))
       adj_unit<Real, true, EXACT, true>(aa, u, wbase, L, s_in, s_out, la.crec + pbase);
     LOOP_STAMP(7);
+    if (la.prof && la.prof_cta) {  // diagnostics: the whole CTA's end of the phase
+      __syncthreads();
+      if (threadIdx.x == 0) la.prof[(size_t)la.K * LOOP_PROF + ((size_t)k * 2 + 1) * LOOP_PROF_CTA + blockIdx.x] = globaltimer() - t0;
+    }
     grid_sync(la.bar);  // B4
     LOOP_STAMP(8);
     const double change = loop_stats(la, k, g.ntiles, red, t0);
@@ -3555,6 +3590,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     la.state[0] = done;
     la.state[1] = reason;
   }
+  loop_fold<Real>(la, done, (long long)g.nx * g.ny * g.nzs);
 }
 #undef LOOP_STAMP
 
@@ -3654,6 +3690,7 @@ __global__ void __launch_bounds__(256, 1) tiny_loop_kernel(LoopArgs la, TinyArgs
   const Real* ym = reinterpret_cast<const Real*>(la.ymeas);
   const unsigned long long t0 = globaltimer();
   int done = 0, reason = 0;
+  if (loop_skip(la)) return;
 #define TINY_STAMP(i) \
   if (la.prof && blockIdx.x == 0 && threadIdx.x == 0) la.prof[(size_t)k * LOOP_PROF + (i)] = globaltimer() - t0
   for (int k = 0; k < la.K; ++k) {
@@ -3855,6 +3892,7 @@ __global__ void __launch_bounds__(256, 1) tiny_loop_kernel(LoopArgs la, TinyArgs
     la.state[0] = done;
     la.state[1] = reason;
   }
+  loop_fold<Real>(la, done, nvox);
 }
 template __global__ void tiny_loop_kernel<float>(LoopArgs, TinyArgs);
 template __global__ void tiny_loop_kernel<double>(LoopArgs, TinyArgs);
@@ -3949,6 +3987,8 @@ struct nf_plan {
   void* d_tiny = nullptr;  // tiny_loop_kernel scratch: part, wch, ch, gpart, vbcnt, stat_part
   size_t tiny_bytes = 0;
   size_t loop_prof_elems = 0;
+  const int* loop_prev = nullptr;  // nf_spgm_loop_chained: the previous launch's state (LoopArgs::prev_state)
+  int loop_fold = 0;               // ... and LoopArgs::fold
   int nsm = 148;             // SMs of the plan's device: CTAs of the CTA-tile forward and the persistent loop
   int ct_mode = 1;           // CTA-tile flat forward (use_ct): 0 off, 1 when the work is large enough, 2 whenever
                              // the layout fits (tests); env NFGPU_CT
@@ -4435,8 +4475,11 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
 // NFGPU_LOOP_PROFILE: phase time stamps of CTA 0 into a plan buffer (nf_loop_profile reads them back)
 int loop_profile_buffer(nf_plan* p, int K, LoopArgs& la) {
   la.prof = nullptr;
-  if (!std::getenv("NFGPU_LOOP_PROFILE")) return NF_OK;
-  const size_t need = (size_t)K * LOOP_PROF;
+  la.prof_cta = 0;
+  const char* env = std::getenv("NFGPU_LOOP_PROFILE");
+  if (!env) return NF_OK;
+  la.prof_cta = std::atoi(env) == 2;
+  const size_t need = (size_t)K * (LOOP_PROF + (la.prof_cta ? 2 * LOOP_PROF_CTA : 0));
   if (need > p->loop_prof_elems) {
     cudaFree(p->d_loop_prof);
     p->d_loop_prof = nullptr;
@@ -4532,6 +4575,8 @@ int launch_tiny_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   la.bar = p->d_loopbar;
   la.s_a = s_a;
   la.s_b = s_b;
+  la.prev_state = p->loop_prev;
+  la.fold = p->loop_fold;
   if (int rc = loop_profile_buffer(p, K, la)) return rc;
   const size_t smem = (size_t)ta.chunk_max * (sizeof(double2) + sizeof(int4));
   auto kern = tiny_loop_kernel<Real>;
@@ -4635,6 +4680,8 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   la.ctr = (int*)p->d_loopbar + 2;
   la.s_a = s_a;
   la.s_b = s_b;
+  la.prev_state = p->loop_prev;
+  la.fold = p->loop_fold;
   la.warp_bytes = wb;
   la.kwords = bitmap ? (int)kwords : 0;
   if (int rc = loop_profile_buffer(p, K, la)) return rc;
@@ -5166,11 +5213,26 @@ int nf_spgm_loop(nf_plan* p, const int32_t* idx_table, int iters, uint64_t seed,
                                   budget, records, state, st);
 }
 
+int nf_spgm_loop_chained(nf_plan* p, const int32_t* idx_table, int iters, uint64_t seed, uint64_t iter0, int batch,
+                         const void* ymeas, void* s_a, void* s_b, double eta_over_b, double alpha, double tol,
+                         double time_budget_s, double* records, int* state, const int* prev_state, void* stream) {
+  if (!p) return fail(NF_ERR_ARG, "null argument");
+  if (prev_state && prev_state == state) return fail(NF_ERR_ARG, "prev_state and state must not alias");
+  p->loop_prev = prev_state;
+  p->loop_fold = 1;
+  const int rc = nf_spgm_loop(p, idx_table, iters, seed, iter0, batch, ymeas, s_a, s_b, eta_over_b, alpha, tol,
+                              time_budget_s, records, state, stream);
+  p->loop_prev = nullptr;
+  p->loop_fold = 0;
+  return rc;
+}
+
 // diagnostics: copy the persistent loop's phase time stamps of its last launch (NFGPU_LOOP_PROFILE) to the host
 int nf_loop_profile(nf_plan* p, unsigned long long* host, int iters) {
   if (!p || !host) return fail(NF_ERR_ARG, "null argument");
-  if (!p->d_loop_prof || (size_t)iters * LOOP_PROF > p->loop_prof_elems) return fail(NF_ERR_STATE, "no loop profile");
-  CUDA_TRY(cudaMemcpy(host, p->d_loop_prof, (size_t)iters * LOOP_PROF * 8, cudaMemcpyDeviceToHost));
+  // iters: time stamps to copy (K * LOOP_PROF, plus K * 2 * LOOP_PROF_CTA with NFGPU_LOOP_PROFILE=2)
+  if (!p->d_loop_prof || (size_t)iters > p->loop_prof_elems) return fail(NF_ERR_STATE, "no loop profile");
+  CUDA_TRY(cudaMemcpy(host, p->d_loop_prof, (size_t)iters * 8, cudaMemcpyDeviceToHost));
   return NF_OK;
 }
 

@@ -307,18 +307,20 @@ class DevicePlan:
 
     def spgm_loop(self, table: torch.Tensor | None, iters: int, seed: int, iter0: int, batch: int,
                   ymeas: torch.Tensor, s_a: torch.Tensor, s_b: torch.Tensor, eta_over_b: float, alpha: float,
-                  tol: float, time_budget_s: float | None, records: torch.Tensor, state: torch.Tensor) -> None:
+                  tol: float, time_budget_s: float | None, records: torch.Tensor, state: torch.Tensor,
+                  prev_state: torch.Tensor | None = None, chained: bool = False) -> None:
         """nf_spgm_loop: ``iters`` flat-batch SPGM iterations in one persistent launch (table: device int32
-        [iters, batch] in subset order, or None for the device Feistel sampler)."""
-        _lib.check(
-            self.lib.nf_spgm_loop(
-                self._h, _ptr(table), int(iters), int(seed) & (2**64 - 1), int(iter0), int(batch), _ptr(ymeas),
+        [iters, batch] in subset order, or None for the device Feistel sampler). With ``prev_state`` (a tensor or
+        None) and ``chained`` the launch goes through nf_spgm_loop_chained: it runs nothing when the previous launch stopped
+        early, and it ends with the latest iterate in s_a."""
+        args = (self._h, _ptr(table), int(iters), int(seed) & (2**64 - 1), int(iter0), int(batch), _ptr(ymeas),
                 _ptr(s_a), _ptr(s_b), float(eta_over_b), float(alpha), float(tol),
-                -1.0 if time_budget_s is None else float(time_budget_s), _ptr(records), _ptr(state),
-                _stream(self.device),
-            ),
-            "nf_spgm_loop",
-        )
+                -1.0 if time_budget_s is None else float(time_budget_s), _ptr(records), _ptr(state))
+        if chained:
+            _lib.check(self.lib.nf_spgm_loop_chained(*args, _ptr(prev_state), _stream(self.device)),
+                       "nf_spgm_loop_chained")
+        else:
+            _lib.check(self.lib.nf_spgm_loop(*args, _stream(self.device)), "nf_spgm_loop")
         self.B = int(batch)
         self._idx = None
         self.staged_structured = False

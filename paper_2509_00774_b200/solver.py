@@ -350,6 +350,10 @@ class SPGMEngine:
         self._loop_pinned = None
         self._loop_tab = None
         self._loop_ev = None
+        # chained persistent launches (run_loop_chained): per-slot records, state and index-table staging
+        self._chain = [dict(rec=None, state=torch.zeros(4, dtype=torch.int32, device=dev), pinned=None, tab=None,
+                            ev=None, h_state=torch.zeros(4, dtype=torch.int32).pin_memory(), h_rec=None, done=None)
+                       for _ in range(2)]
 
     def _pinned_idx(self, n: int) -> tuple[torch.Tensor, int]:
         k = self._pinned_next
@@ -467,6 +471,56 @@ class SPGMEngine:
         if n % 2 == 1:
             self.s, self.s_next = self.s_next, self.s
         return n, reason
+
+    def run_loop_chained(self, slot: int, prev_slot: int | None, iters: int, table=None, seed: int = 0,
+                         iter0: int = 0, batch: int | None = None, tol: float = 0.0,
+                         time_budget_s: float | None = None) -> None:
+        """run_loop on slot ``slot``'s buffers through nf_spgm_loop_chained: if the launch on ``prev_slot``
+        stopped early this one runs no iteration, and ``self.s`` holds the latest iterate after every launch, so
+        the next launch can be enqueued before this one's state is read (chained_result)."""
+        if self.pg is not None:
+            raise RuntimeError("run_loop_chained is single-GPU")
+        dev = self.plan.device
+        c = self._chain[slot]
+        if table is not None:
+            arr = np.ascontiguousarray(np.asarray(table)[:iters], dtype=np.int32)
+            if c["ev"] is not None:  # the slot's previous H2D copy has completed before its staging is rewritten
+                c["ev"].synchronize()
+            if c["pinned"] is None or c["pinned"].numel() < arr.size:
+                c["pinned"] = torch.empty(max(arr.size, 4096), dtype=torch.int32).pin_memory()
+            if c["tab"] is None or c["tab"].numel() < arr.size:
+                c["tab"] = torch.empty(max(arr.size, 4096), dtype=torch.int32, device=dev)
+            c["pinned"].numpy()[: arr.size] = arr.reshape(-1)
+            c["tab"][: arr.size].copy_(c["pinned"][: arr.size], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(dev))
+            c["ev"] = ev
+            table = c["tab"][: arr.size]
+            batch = arr.shape[1]
+        if batch is None:
+            raise ValueError("run_loop_chained needs batch with the device sampler")
+        if c["rec"] is None or c["rec"].shape[0] < iters:
+            c["rec"] = torch.empty((max(iters, 64), 6), dtype=torch.float64, device=dev)
+        prev = None if prev_slot is None else self._chain[prev_slot]["state"]
+        self.plan.spgm_loop(table, iters, seed, iter0, batch, self.y, self.s, self.s_next, self.eta / batch,
+                            self.alpha, tol, time_budget_s, c["rec"], c["state"], prev_state=prev, chained=True)
+        # state and records to pinned host memory right behind the launch, so reading them (chained_result) waits
+        # for this launch only, not for the one enqueued after it
+        if c["h_rec"] is None or c["h_rec"].shape[0] < iters:
+            c["h_rec"] = torch.empty((max(iters, 64), 6), dtype=torch.float64).pin_memory()
+        c["h_state"].copy_(c["state"], non_blocking=True)
+        c["h_rec"][:iters].copy_(c["rec"][:iters], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(torch.cuda.current_stream(dev))
+        c["done"] = done
+
+    def chained_result(self, slot: int) -> tuple[int, int, np.ndarray]:
+        """(iterations run, reason, records [n, 6] on the host) of the chained launch on ``slot``: waits for that
+        launch (and its copies) only."""
+        c = self._chain[slot]
+        c["done"].synchronize()
+        n, reason = (int(v) for v in c["h_state"][:2])
+        return n, reason, c["h_rec"][:n].numpy()
 
     def _loop_table(self, n: int) -> torch.Tensor:
         if self._loop_ev is not None:
@@ -694,22 +748,32 @@ def _solve_persistent(eng: SPGMEngine, plan: DevicePlan, config: SolverConfig, s
     records: list[IterationRecord] = []
     termination = TERMINATION_MAX_ITERS
     done = 0
-    # chunks grow geometrically from LOOP_FIRST_CHUNK: the host draws only a few batches before the first
-    # launch, then each chunk's batches are drawn while the previous chunk runs
-    n = min(LOOP_FIRST_CHUNK, LOOP_CHUNK, config.max_iters)
-    table = draw(n)
-    while done < config.max_iters:
+    planned = 0  # iterations enqueued
+
+    def enqueue(slot, prev_slot, n):
+        nonlocal planned
         if config.sampler == "table":
-            table = np.asarray(config.index_table[done:done + n])
+            table = np.asarray(config.index_table[planned:planned + n])
+        else:
+            table = draw(n)
         budget = None
         if config.time_budget_s is not None:
             budget = max(0.0, config.time_budget_s - (time.perf_counter() - t_start))
-        rec, _ = eng.run_loop(n, table=table, seed=config.rng_seed, iter0=done + 1, batch=B, tol=config.tol,
-                              time_budget_s=budget)
-        n_next = min(2 * n, LOOP_CHUNK, config.max_iters - done - n)
-        table = draw(n_next) if n_next > 0 else None  # overlaps the launch on the GPU
-        k_run, reason = eng.loop_result()
-        r = rec[:k_run].cpu().numpy()
+        eng.run_loop_chained(slot, prev_slot, n, table=table, seed=config.rng_seed, iter0=planned + 1, batch=B,
+                             tol=config.tol, time_budget_s=budget)
+        planned += n
+
+    # Chunks grow geometrically from LOOP_FIRST_CHUNK. Chunk j + 1 is drawn and enqueued before chunk j's state is
+    # read (nf_spgm_loop_chained: it runs nothing if chunk j stopped early), so the host's sampling, record
+    # building and launch overlap the GPU, which runs the chunks back to back.
+    n = min(LOOP_FIRST_CHUNK, LOOP_CHUNK, config.max_iters)
+    enqueue(0, None, n)
+    slot = 0
+    while True:
+        n_next = min(2 * n, LOOP_CHUNK, config.max_iters - planned)
+        if n_next > 0:
+            enqueue(slot ^ 1, slot, n_next)
+        k_run, reason, r = eng.chained_result(slot)
         t_prev = 0.0
         for i in range(k_run):
             st0, st1 = float(r[i, 0]), float(r[i, 1])
@@ -723,6 +787,9 @@ def _solve_persistent(eng: SPGMEngine, plan: DevicePlan, config: SolverConfig, s
         if reason == 2 or (config.time_budget_s is not None and time.perf_counter() - t_start > config.time_budget_s):
             termination = TERMINATION_TIME_BUDGET
             break
+        if n_next <= 0:
+            break
+        slot ^= 1
         n = n_next
     vol = eng.volume()
     return SolveReport(volume=ReflectivityVolume(vol, scenario.voxels), iterations=done,

@@ -23,7 +23,7 @@ def header_symbols():
 
 def test_header_symbols_bound():
     syms = header_symbols()
-    assert len(syms) == 20
+    assert len(syms) == 21
     assert set(syms) == set(_lib.SIGNATURES)
 
 

@@ -203,3 +203,40 @@ def test_tiny_loop_terminations():
     rep = spgm_solve(y, scn, SolverConfig(eta=eta, alpha=1e-6, tol=1e-300, max_iters=10_000_000, flat_batch=32,
                                           time_budget_s=0.05))
     assert rep.termination == "time_budget" and 1 <= rep.iterations < 10_000_000
+
+
+@pytest.mark.parametrize("workload,dtype", [("small", "c128"), ("medium", "c64")])
+def test_chained_launches_match_one_launch(workload, dtype, monkeypatch):
+    """nf_spgm_loop_chained: launches enqueued back to back (odd and even chunk sizes, so the iterate is folded
+    back into s_a after odd counts) give the iterate and records of one launch over the same index table; a launch
+    whose predecessor stopped early runs no iteration and forwards the reason."""
+    w = configs.WORKLOADS[workload]()
+    scn = w.scenario
+    rng = np.random.default_rng(8)
+    y = rc(rng, scn.n_channels)
+    s0 = rc(rng, scn.n_voxels) * 0.01
+    a, b = _pair(scn, dtype, y, 1e-3, 1e-7, s0, max_batch=w.batch)
+    K = 12
+    table = np.stack([np.sort(rng.choice(scn.n_channels, w.batch, replace=False)) for _ in range(K)])
+    a.run_loop(K, table=table, tol=0.0)
+    assert a.loop_result() == (K, 0)
+    rec_a = a._loop_rec[:K, :4].clone()
+    sizes, at, slot, prev, recs = [3, 4, 5], 0, 0, None, []
+    for n in sizes:
+        b.run_loop_chained(slot, prev, n, table=table[at:at + n], tol=0.0)
+        prev, slot, at = slot, slot ^ 1, at + n
+        k_run, reason, rec = b.chained_result(prev)
+        assert (k_run, reason) == (n, 0)
+        recs.append(rec[:n, :4].copy())
+    assert torch.equal(a.s, b.s)
+    assert np.array_equal(np.concatenate(recs), rec_a.cpu().numpy())
+    # early stop: a tolerance every iteration meets stops the first launch after one iteration; the next runs none
+    c, _ = _pair(scn, dtype, y, 1e-3, 1e-7, s0, max_batch=w.batch)
+    c.run_loop_chained(0, None, 4, table=table[:4], tol=1e9)
+    c.run_loop_chained(1, 0, 4, table=table[4:8], tol=0.0)
+    assert c.chained_result(0)[:2] == (1, 1)
+    assert c.chained_result(1)[:2] == (0, 1)
+    a2, _ = _pair(scn, dtype, y, 1e-3, 1e-7, s0, max_batch=w.batch)
+    a2.run_loop(1, table=table[:1], tol=0.0)
+    a2.loop_result()
+    assert torch.equal(a2.s, c.s)
