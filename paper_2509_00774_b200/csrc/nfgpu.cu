@@ -3574,6 +3574,11 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     if (la.prof && la.prof_cta) {  // diagnostics: the whole CTA's end of the phase
       __syncthreads();
       if (threadIdx.x == 0) la.prof[(size_t)la.K * LOOP_PROF + ((size_t)k * 2 + 1) * LOOP_PROF_CTA + blockIdx.x] = globaltimer() - t0;
+      if (threadIdx.x == 0 && k == 0) {  // the SM of this CTA, in a row after the stamps
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        la.prof[(size_t)la.K * LOOP_PROF + (size_t)la.K * 2 * LOOP_PROF_CTA + blockIdx.x] = smid;
+      }
     }
     grid_sync(la.bar);  // B4
     LOOP_STAMP(8);
@@ -4479,7 +4484,7 @@ int loop_profile_buffer(nf_plan* p, int K, LoopArgs& la) {
   const char* env = std::getenv("NFGPU_LOOP_PROFILE");
   if (!env) return NF_OK;
   la.prof_cta = std::atoi(env) == 2;
-  const size_t need = (size_t)K * (LOOP_PROF + (la.prof_cta ? 2 * LOOP_PROF_CTA : 0));
+  const size_t need = (size_t)K * (LOOP_PROF + (la.prof_cta ? 2 * LOOP_PROF_CTA : 0)) + (la.prof_cta ? LOOP_PROF_CTA : 0);
   if (need > p->loop_prof_elems) {
     cudaFree(p->d_loop_prof);
     p->d_loop_prof = nullptr;

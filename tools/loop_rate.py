@@ -58,20 +58,23 @@ if os.environ.get("NFGPU_LOOP_PROFILE"):
     import ctypes
 
     per_cta = os.environ["NFGPU_LOOP_PROFILE"] == "2"
-    n = K * (12 + (2 * 160 if per_cta else 0))
+    n = K * (12 + (2 * 160 if per_cta else 0)) + (160 if per_cta else 0)
     buf = (ctypes.c_uint64 * n)()
     rc = plan.lib.nf_loop_profile(plan._h, buf, n)
     if rc == 0 and per_cta:  # every CTA's forward / adjoint end relative to CTA 0's phase start
         t0 = np.frombuffer(buf, dtype=np.uint64)[: K * 12].reshape(K, 12).astype(np.float64)
         nsm = torch.cuda.get_device_properties(0).multi_processor_count
-        c = np.frombuffer(buf, dtype=np.uint64)[K * 12:].reshape(K, 2, 160).astype(np.float64)[:, :, :nsm]
+        c = np.frombuffer(buf, dtype=np.uint64)[K * 12: K * 332].reshape(K, 2, 160).astype(np.float64)[:, :, :nsm]
+        smid = np.frombuffer(buf, dtype=np.uint64)[K * 332: K * 332 + nsm].astype(int)
         sl = slice(K // 4, K - 1)
         fe = (c[sl, 0, :] - t0[sl, 0:1]) / 1e3
         ae = (c[sl, 1, :] - t0[sl, 6:7]) / 1e3
         cta_prof = {"fwd_end_min": fe.min(1).mean(), "fwd_end_mean": fe.mean(), "fwd_end_max": fe.max(1).mean(),
                     "adj_end_min": ae.min(1).mean(), "adj_end_mean": ae.mean(), "adj_end_max": ae.max(1).mean(),
                     "adj_slowest_ctas": np.argsort(-ae.mean(0))[:8].tolist(),
-                    "adj_end_by_cta_q": np.percentile(ae.mean(0), [0, 25, 50, 75, 100]).round(2).tolist()}
+                    "adj_end_by_cta_q": np.percentile(ae.mean(0), [0, 25, 50, 75, 100]).round(2).tolist(),
+                    "adj_end_by_cta": ae.mean(0).round(2).tolist(), "fwd_end_by_cta": fe.mean(0).round(2).tolist(),
+                    "smid": smid.tolist()}
         print(json.dumps({k: (round(v, 2) if isinstance(v, float) else v) for k, v in cta_prof.items()}))
     if rc == 0:
         t = np.frombuffer(buf, dtype=np.uint64)[: K * 12].reshape(K, 12).astype(np.float64)[K // 4:]
