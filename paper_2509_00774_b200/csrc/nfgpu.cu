@@ -4588,6 +4588,8 @@ int launch_tiny_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   CUDA_TRY(ensure_smem((const void*)kern, smem));
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
   CUDA_TRY(cudaMemsetAsync(ta.vbcnt, 0, b_cnt, st));
+  if (std::getenv("NFGPU_VERBOSE"))
+    std::fprintf(stderr, "nf_spgm_loop: tiny_loop_kernel, %d CTAs x 256 threads, B=%d, K=%d\n", nsm, B, K);
   void* args[] = {&la, &ta};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nsm), dim3(256), args, smem, st));
   p->B = B;
@@ -4695,6 +4697,9 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
   CtArgs ca = ct_args(p, B);
   ca.G = nsm;
+  if (std::getenv("NFGPU_VERBOSE"))
+    std::fprintf(stderr, "nf_spgm_loop: spgm_loop_kernel (%s forward), %d CTAs x %d warps, %zu B shared, B=%d, K=%d\n",
+                 ct ? "CTA-tile" : "warp-unit", nsm, nw, smem, B, K);
   void* args[] = {&la, &fa, &aa, &ca};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nsm), dim3(nw * 32), args, smem, st));
   p->loop_threads = nw * 32;
