@@ -98,6 +98,20 @@ static_assert(TBR == 8 || TBR == 16, "TBR must be 8 or 16");
 constexpr int R_MAX = 32767;
 constexpr int TGROUPS_MAX = 511;
 constexpr unsigned FULL = 0xffffffffu;
+#ifdef NFGPU_DEBUG  // device bounds checks of the CTA-tile kernels (a debug build: tools/build_variants.sh)
+#define NF_CHECK(cond, ...)                              \
+  do {                                                   \
+    if (!(cond)) {                                       \
+      printf("NF_CHECK %s:%d: %s | ", __FILE__, __LINE__, #cond); \
+      printf(__VA_ARGS__);                               \
+      __trap();                                          \
+    }                                                    \
+  } while (0)
+#else
+#define NF_CHECK(cond, ...) \
+  do {                      \
+  } while (0)
+#endif
 
 // Programmatic dependent launch: kernels of the SPGM step are launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs are scheduled while its
@@ -2899,14 +2913,16 @@ __global__ void __launch_bounds__(1024) magchange_kernel(const Real* __restrict_
 // pieces (tile, channel range). A piece's table rows arrive with one bulk copy (TMA) on an mbarrier,
 // double-buffered: the last warp done with piece i refills its buffer with piece i + 2. No warp stages tx
 // groups or receiver rows, and no warp waits for a straggler of another tile.
-// Each (tile, channel) value is computed by one warp with the flat kernel's arithmetic and transpose-reduce, so
-// part[tile][j] is bit-identical to fwd_kernel's and subsets stay bit-exact. (The adjoint stays on the warp-unit
-// kernel: a CTA-tile adjoint, whose warps' partial gradients are combined per piece, measured slower on Medium,
-// 63.5 vs 58.3 us under ncu.)
+//   forward: each (tile, channel) value is computed by one warp with the flat kernel's arithmetic and
+//            transpose-reduce, so part[tile][j] is bit-identical to fwd_kernel's and subsets stay bit-exact.
+//   adjoint: the last warp done with a piece sums the warps' partial gradients in warp order (shared memory) and
+//            parks the piece's sum in global memory; after the last piece the CTA's warps run the pieces'
+//            epilogues side by side (a tile cut across CTAs sums its pieces in piece order, adj_epilogue), so no
+//            warp carries several epilogues' latency into the end of the phase.
 constexpr int CT_WARPS = 16;
 
 template <typename Real>
-struct CtLayout {  // [mbarriers, counters | buffer 0 | buffer 1 | warp records ×CT_WARPS | warp transposes]
+struct CtLayout {  // [mbarriers, counters | buffer 0 | buffer 1 | warp records ×CT_WARPS | union region]
   size_t tab_bytes, buf_bytes, off_buf, off_warp, warp_bytes, off_u, u_bytes, bytes;
   __host__ __device__ explicit CtLayout(int A) {
     tab_bytes = (size_t)A * TABW * sizeof(Real);
@@ -2915,7 +2931,9 @@ struct CtLayout {  // [mbarriers, counters | buffer 0 | buffer 1 | warp records 
     off_warp = off_buf + 2 * buf_bytes;
     warp_bytes = 34 * sizeof(R4<Real>) + 34 * sizeof(int2);
     off_u = off_warp + (size_t)CT_WARPS * warp_bytes;
-    u_bytes = (size_t)CT_WARPS * TBR * 33 * sizeof(R2<Real>);  // per-warp transpose buffers
+    const size_t tb = (size_t)CT_WARPS * TBR * 33 * sizeof(R2<Real>);  // forward: per-warp transpose buffers
+    const size_t gs = (size_t)2 * CT_WARPS * 2 * TILE * sizeof(Real);   // adjoint: warp partials [2][warps]
+    u_bytes = tb > gs ? tb : gs;
     bytes = off_u + u_bytes;
   }
 };
@@ -2938,6 +2956,8 @@ __device__ __forceinline__ CtRange ct_range(const CtArgs& c, int b) {
   r.np = r.r1 > r.r0 ? (int)((r.r1 - 1) / c.span) - r.t0 + 1 : 0;
   return r;
 }
+// the CTA whose range holds pair u
+__device__ __forceinline__ int ct_cta_of(const CtArgs& c, long long u) { return (int)(((u + 1) * c.G - 1) / c.W); }
 // piece i of the range: tile and window-relative channels [ja, jb)
 __device__ __forceinline__ void ct_piece(const CtArgs& c, const CtRange& r, int i, int& tile, int& ja, int& jb) {
   tile = r.t0 + i;
@@ -2951,41 +2971,46 @@ __device__ __forceinline__ void ct_slice(int ja, int jb, int w, int& c0, int& c1
   c1 = ja + (int)(((long long)(jb - ja) * (w + 1)) / CT_WARPS);
 }
 
-// Fill buffer `buf` with tile's table rows (bulk copy, lane 0), its D0 row and its iterate values in the lane-quad
-// layout of ldv (plain loads by the 32 lanes). mbarrier `full` (33 arrivals: the expect_tx of lane 0 and every lane
-// after its stores) completes when all of it has landed.
-template <typename Real, bool LOOP>
-__device__ __forceinline__ void ct_produce(const Geo& g, const Real* __restrict__ tab, const double* __restrict__ D0,
-                                           const Real* __restrict__ sv, unsigned char* buf, uint64_t* full, int tile,
-                                           int L) {
+// Fill buffer `buf` with tile's table rows (bulk copy, lane 0), its D0 row and (forward) its iterate values in the
+// lane-quad layout of ldv (plain loads by the 32 lanes). mbarrier `full` (33 arrivals: the expect_tx of lane 0 and
+// every lane after its stores) completes when all of it has landed.
+template <typename Real>
+__device__ __forceinline__ void ct_produce_table(const Geo& g, const Real* __restrict__ tab,
+                                                 const double* __restrict__ D0, unsigned char* buf, uint64_t* full,
+                                                 int tile, int L) {
   const CtLayout<Real> lay(g.A);
   double* d0 = reinterpret_cast<double*>(buf + lay.tab_bytes);
-  Real* ss = reinterpret_cast<Real*>(buf + lay.tab_bytes + (size_t)d0_slots(g.A) * sizeof(double));
   if (L == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the old piece before the copy
     mbar_expect(full, (uint32_t)lay.tab_bytes);
     bulk_g2s(buf, tab + (size_t)tile * g.A * TABW, (uint32_t)lay.tab_bytes, full);
   }
   for (int i = L; i < g.A; i += 32) d0[i] = D0[(size_t)tile * g.A + i];
-  {
-    int tx, ty, tz;
-    tile_coords(g, tile, tx, ty, tz);
-    int x0, y, z;
-    lane_voxel(tx, ty, tz, L, x0, y, z);
-    constexpr int QD = 16 / (int)sizeof(Real);
-    const size_t n0 = ((size_t)z * g.ny + y) * g.nx + x0;
+}
+template <typename Real, bool LOOP>
+__device__ __forceinline__ void ct_produce(const Geo& g, const Real* __restrict__ tab, const double* __restrict__ D0,
+                                           const Real* __restrict__ sv, unsigned char* buf, uint64_t* full, int tile,
+                                           int L) {
+  ct_produce_table<Real>(g, tab, D0, buf, full, tile, L);
+  const CtLayout<Real> lay(g.A);
+  Real* ss = reinterpret_cast<Real*>(buf + lay.tab_bytes + (size_t)d0_slots(g.A) * sizeof(double));
+  int tx, ty, tz;
+  tile_coords(g, tile, tx, ty, tz);
+  int x0, y, z;
+  lane_voxel(tx, ty, tz, L, x0, y, z);
+  constexpr int QD = 16 / (int)sizeof(Real);
+  const size_t n0 = ((size_t)z * g.ny + y) * g.nx + x0;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const bool ok = x0 + v < g.nx && y < g.ny && z < g.nzs;
-      Real re = 0, im = 0;
-      if (ok) {
-        re = LOOP ? __ldcg(sv + 2 * (n0 + v)) : sv[2 * (n0 + v)];
-        im = LOOP ? __ldcg(sv + 2 * (n0 + v) + 1) : sv[2 * (n0 + v) + 1];
-      }
-      const int e = (v / QD) * 32 * QD + L * QD + v % QD;
-      ss[e] = re;
-      ss[TILE + e] = im;
+  for (int v = 0; v < V; ++v) {
+    const bool ok = x0 + v < g.nx && y < g.ny && z < g.nzs;
+    Real re = 0, im = 0;
+    if (ok) {
+      re = LOOP ? __ldcg(sv + 2 * (n0 + v)) : sv[2 * (n0 + v)];
+      im = LOOP ? __ldcg(sv + 2 * (n0 + v) + 1) : sv[2 * (n0 + v) + 1];
     }
+    const int e = (v / QD) * 32 * QD + L * QD + v % QD;
+    ss[e] = re;
+    ss[TILE + e] = im;
   }
   mbar_arrive(full);
 }
@@ -3209,6 +3234,191 @@ __device__ __forceinline__ void ct_forward(const FwdArgs<Real>& a, const CtArgs&
   }
 }
 
+// One warp's slice of an adjoint piece: adj_unit's channel loop on resident rows; returns the flushed partial g.
+template <typename Real, bool EXACT>
+__device__ __forceinline__ void ct_adj_slice(const Geo& g, const Real* __restrict__ tab_s, const WarpSmem<Real>& ws,
+                                             const ChanRec* __restrict__ crec, const R2<Real>* __restrict__ wrec,
+                                             int c0, int c1, int pn0, int pn1, int L, ChanRec& nxt, R2<Real>& nxtw,
+                                             QV<Real>& gr, QV<Real>& gi) {
+  constexpr int QD = 16 / (int)sizeof(Real);
+  QV<Real> hr, hi, dR, iR;
+  zero(gr);
+  zero(gi);
+  zero(hr);
+  zero(hi);
+  zero(dR);
+  zero(iR);
+  const Real* tsl = tab_s + L * QD;
+  int carry = -1;
+  for (int jb = c0; jb < c1; jb += 32) {
+    const int nb = min(32, c1 - jb);
+    const bool more = jb + 32 < c1;
+    const unsigned starts = ct_records<Real, EXACT>(g, ws, crec, wrec, nb, more ? jb + 32 : pn0, more ? c1 : pn1, L,
+                                                    carry, nxt, nxtw);
+    int c = 0;
+    while (c < nb) {
+      const int key = ws.rect[c].y;
+      const int e = key >> 24;
+      if ((starts >> c) & 1u) {
+        const int rr = key & 0x7fff, tg = (key >> 15) & 0x1ff;
+        flush(iR, hr, hi, gr, gi);
+        tsl = tab_s + (size_t)tg * g.Tg * TABW + L * QD;
+        const Real* rrow = tab_s + (size_t)(g.T + rr) * TABW + L * QD;
+        dR = ldv(rrow);
+        iR = ldv(rrow + TILE);
+      }
+      R4<Real> q = ws.rec[c];
+      int off = low2(q.y) * TABW;
+#pragma unroll UNROLL
+      for (; c < e; ++c) {
+        const R4<Real> qn = ws.rec[c + 1];
+        const int offn = low2(qn.y) * TABW;
+        const QV<Real> dT = ldv(tsl + off), iT = ldv(tsl + off + TILE);
+        QV<Real> cs, sn;
+        phasorv<EXACT>(q.x, q.y, dT, dR, cs, sn);
+        adj_acc(iT, cs, sn, q.z, q.w, hr, hi);
+        q = qn;
+        off = offn;
+      }
+    }
+    __syncwarp();
+  }
+  flush(iR, hr, hi, gr, gi);
+}
+
+// The CTA's adjoint (+prox) pieces: slices as ct_forward; the last warp done with piece q combines the warps'
+// partials (warp order) into slot q of this CTA's part of `cpart` ([CTAs][pmax][32 lanes][2V] Reals); after the
+// last piece every piece's epilogue (adj_epilogue, chunk = its index among the CTAs sharing the tile) runs on its
+// own warp.
+template <typename Real, bool PROX, bool EXACT, bool LOOP>
+__device__ __forceinline__ void ct_adjoint(const AdjArgs<Real>& a, const CtArgs& c, unsigned char* smem,
+                                           const Real* __restrict__ s_in, Real* __restrict__ s_out,
+                                           const ChanRec* __restrict__ crec, Real* __restrict__ cpart, int pmax,
+                                           unsigned& ph, bool pdl) {
+  const Geo& g = a.g;
+  const CtLayout<Real> lay(g.A);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  int* cnt = reinterpret_cast<int*>(smem + 16);
+  const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+  const CtRange rg = ct_range(c, blockIdx.x);
+  const int np = rg.np;
+  int tile, ja, jb;
+  if (w == 0)
+    for (int q = 0; q < 2 && q < np; ++q) {
+      ct_piece(c, rg, q, tile, ja, jb);
+      ct_produce_table<Real>(g, a.tab, a.D0, smem + lay.off_buf + q * lay.buf_bytes, full + q, tile, L);
+      mbar_arrive(full + q);
+    }
+  WarpSmem<Real> ws;
+  unsigned char* wr = smem + lay.off_warp + (size_t)w * lay.warp_bytes;
+  ws.rec = reinterpret_cast<R4<Real>*>(wr);
+  ws.rect = reinterpret_cast<int2*>(wr + 34 * sizeof(R4<Real>));
+  ws.tside = ws.rslot = nullptr;
+  for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
+  using U16 = typename std::conditional<std::is_same<Real, float>::value, float4, double2>::type;
+  constexpr int NU = 2 * V * (int)sizeof(Real) / 16, PU = 16 / (int)sizeof(Real);
+  U16* gs = reinterpret_cast<U16*>(smem + lay.off_u);  // [2][CT_WARPS][NU][32] 16-byte quads
+  U16* cp = reinterpret_cast<U16*>(cpart) + (size_t)blockIdx.x * pmax * NU * 32;  // [pmax][NU][32]
+  ChanRec nxt;
+  R2<Real> nxtw;
+  int c0 = 0, c1 = 0;
+  if (np > 0) {
+    ct_piece(c, rg, 0, tile, ja, jb);
+    ct_slice(ja, jb, w, c0, c1);
+    prefetch_first<Real>(crec, nullptr, c0, c1, L, nxt, nxtw);
+  }
+  if (pdl) pdl_wait();
+  if (np > 0 && c0 + L < c1) nxtw = a.wrec[c0 + L];
+  for (int q = 0; q < np; ++q) {
+    const int b = q & 1;
+    ct_piece(c, rg, q, tile, ja, jb);
+    ct_slice(ja, jb, w, c0, c1);
+    int pn0 = 0, pn1 = 0;
+    if (q + 1 < np) {
+      int t2, ja2, jb2;
+      ct_piece(c, rg, q + 1, t2, ja2, jb2);
+      ct_slice(ja2, jb2, w, pn0, pn1);
+    }
+    unsigned char* buf = smem + lay.off_buf + b * lay.buf_bytes;
+    NF_CHECK(tile >= 0 && tile < g.ntiles && 0 <= c0 && c0 <= c1 && c1 <= c.span && pn1 <= c.span,
+             "adj piece q %d tile %d c0 %d c1 %d pn %d %d span %d\n", q, tile, c0, c1, pn0, pn1, c.span);
+    mbar_wait(full + b, (ph >> b) & 1u);
+    ph ^= 1u << b;
+    ws.d0 = reinterpret_cast<double*>(buf + lay.tab_bytes);
+    QV<Real> gr, gi;
+    if (c0 < c1) {
+      ct_adj_slice<Real, EXACT>(g, reinterpret_cast<const Real*>(buf), ws, crec, a.wrec, c0, c1, pn0, pn1, L, nxt,
+                                nxtw, gr, gi);
+    } else {
+      zero(gr);
+      zero(gi);
+      if (pn0 + L < pn1) {
+        nxt = crec[pn0 + L];
+        nxtw = a.wrec[pn0 + L];
+      }
+    }
+    {  // publish the warp's partial (interleaved re/im quads)
+      Real t[2 * V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        t[2 * v] = get(gr, v);
+        t[2 * v + 1] = get(gi, v);
+      }
+      U16* mine = gs + ((size_t)(b * CT_WARPS + w) * NU) * 32 + L;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) mine[u * 32] = *reinterpret_cast<const U16*>(t + u * PU);
+    }
+    if (ct_last(cnt + b, L)) {  // combine in warp order, park the piece's sum, refill the buffer
+      Real G[2 * V];
+#pragma unroll
+      for (int e = 0; e < 2 * V; ++e) G[e] = 0;
+      for (int ww = 0; ww < CT_WARPS; ++ww) {
+        const U16* src = gs + ((size_t)(b * CT_WARPS + ww) * NU) * 32 + L;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+          const U16 v4 = src[u * 32];
+          const Real* tv = reinterpret_cast<const Real*>(&v4);
+#pragma unroll
+          for (int k = 0; k < PU; ++k) G[u * PU + k] += tv[k];
+        }
+      }
+      NF_CHECK(q < pmax, "q %d pmax %d np %d b %d\n", q, pmax, np, (int)blockIdx.x);
+#pragma unroll
+      for (int u = 0; u < NU; ++u) cp[((size_t)q * NU + u) * 32 + L] = *reinterpret_cast<const U16*>(G + u * PU);
+      if (q + 2 < np) {
+        int t2, ja2, jb2;
+        ct_piece(c, rg, q + 2, t2, ja2, jb2);
+        ct_produce_table<Real>(g, a.tab, a.D0, buf, full + b, t2, L);
+        mbar_arrive(full + b);
+      }
+    }
+  }
+  __syncthreads();  // every piece's sum is parked (global stores by this CTA's warps)
+  for (int q = w; q < np; q += CT_WARPS) {
+    ct_piece(c, rg, q, tile, ja, jb);
+    Real Gr[V], Gi[V];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const U16 v4 = __ldcg(cp + ((size_t)q * NU + u) * 32 + L);
+      const Real* tv = reinterpret_cast<const Real*>(&v4);
+#pragma unroll
+      for (int k = 0; k < PU; ++k) {
+        const int e = u * PU + k;
+        if (e & 1)
+          Gi[e >> 1] = tv[k];
+        else
+          Gr[e >> 1] = tv[k];
+      }
+    }
+    const QV<Real> sgr = make_v(Gr), sgi = make_v(Gi);
+    const long long u0 = (long long)tile * c.span;
+    const int first = ct_cta_of(c, u0), lastc = ct_cta_of(c, u0 + c.span - 1);
+    NF_CHECK(tile >= 0 && tile < g.ntiles && first <= (int)blockIdx.x && (int)blockIdx.x <= lastc && lastc < c.G,
+             "tile %d first %d last %d b %d\n", tile, first, lastc, (int)blockIdx.x);
+    adj_epilogue<Real, PROX, LOOP>(a, tile, (int)blockIdx.x - first, lastc - first + 1, L, sgr, sgi, s_in, s_out);
+  }
+}
+
 __device__ __forceinline__ void ct_init(unsigned char* smem) {
   if (threadIdx.x == 0) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -3227,6 +3437,14 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 1) fwd_ct_kernel(FwdArgs<Real> 
   ct_init(smem_raw);
   unsigned ph = 0;
   ct_forward<Real, EXACT, false>(a, c, smem_raw, a.s, a.crec, ph, true);
+}
+
+template <typename Real, bool PROX, bool EXACT>
+__global__ void __launch_bounds__(CT_WARPS * 32, 1) adj_ct_kernel(AdjArgs<Real> a, CtArgs c, Real* cpart, int pmax) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ct_init(smem_raw);
+  unsigned ph = 0;
+  ct_adjoint<Real, PROX, EXACT, false>(a, c, smem_raw, a.s_in, a.s_out, a.crec, cpart, pmax, ph, true);
 }
 
 // ------------------------------------------------------------------ persistent SPGM loop
@@ -3274,6 +3492,8 @@ struct LoopArgs {
   void* s_a;            // iteration k reads s_a (k even) or s_b (k odd) and writes the other
   void* s_b;
   size_t warp_bytes;
+  void* ctpart;              // CTA-tile adjoint: parked piece sums [CTAs][ctpmax][32][2V]
+  int ctpmax;
   const int* prev_state;     // chained launches: the previous launch's state; it stopped early -> run nothing
   int fold;                  // the latest iterate ends in s_a (an odd count copies s_b back; chained launches)
   unsigned long long* prof;  // diagnostics (NFGPU_LOOP_PROFILE): CTA 0's device clock at each phase boundary
@@ -3453,8 +3673,9 @@ __device__ __forceinline__ double loop_stats(const LoopArgs& la, int k, int ntil
   return sqrt(st1) / fmax(sqrt(st0), 1e-12);
 }
 
-template <typename Real, bool EXACT, bool CT>
+template <typename Real, bool EXACT, int CTM>  // CTM: bit 0 CTA-tile forward, bit 1 CTA-tile adjoint
 __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<Real> fa, AdjArgs<Real> aa, CtArgs ca) {
+  constexpr bool CT = (CTM & 1) != 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int scan_sh[32];
   // sort / reduce / statistics scratch in the warp regions (no warp unit is in flight during those phases)
@@ -3568,8 +3789,15 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     grid_sync(la.bar);  // B3
     LOOP_STAMP(6);
     // ---- adjoint(k) + prox
-    for (int u = gw; u < nau; u = next_unit(la.ctr + 1, TW, L))
-      adj_unit<Real, true, EXACT, true>(aa, u, wbase, L, s_in, s_out, la.crec + pbase);
+    if constexpr ((CTM & 2) != 0) {
+      ct_init(smem_raw);  // the sort of P3 used this shared memory
+      unsigned ph = 0;
+      ct_adjoint<Real, true, EXACT, true>(aa, ca, smem_raw, s_in, s_out, la.crec + pbase,
+                                          reinterpret_cast<Real*>(la.ctpart), la.ctpmax, ph, false);
+    } else {
+      for (int u = gw; u < nau; u = next_unit(la.ctr + 1, TW, L))
+        adj_unit<Real, true, EXACT, true>(aa, u, wbase, L, s_in, s_out, la.crec + pbase);
+    }
     LOOP_STAMP(7);
     if (la.prof && la.prof_cta) {  // diagnostics: the whole CTA's end of the phase
       __syncthreads();
@@ -3998,6 +4226,9 @@ struct nf_plan {
   int ct_mode = 1;           // CTA-tile flat forward (use_ct): 0 off, 1 when the work is large enough, 2 whenever
                              // the layout fits (tests); env NFGPU_CT
   long long ct_min_pairs = 1024;  // ... fewest (tile, channel) pairs per CTA (env NFGPU_CT_MIN)
+  int ct_adj = 1;                 // CTA-tile adjoint too (when use_ct holds for the batch; env NFGPU_CT_ADJ)
+  void* d_ctpart = nullptr;       // ... its parked piece sums
+  size_t ctpart_bytes = 0;
   bool comm_active = false;  // inside nf_forward_allreduce
   bool comm_fused = false;   // ... and the flat forward's last reduce already did the all-reduce
 };
@@ -4061,6 +4292,7 @@ void free_plan(nf_plan* p) {
   cudaFree(p->d_loop_prof);
   cudaFree(p->d_tiny);
   cudaFree(p->d_loop_priv);
+  cudaFree(p->d_ctpart);
   cudaFree(p->d_epoch);
   cudaFree(p->d_comm_err);
   delete p;
@@ -4185,10 +4417,29 @@ int launch_reduce2(nf_plan* p, int span, int nseg, int w0, void* y, cudaStream_t
 // memory and every CTA gets at least ct_min_pairs (tile, channel) pairs (at least one with NFGPU_CT=2)
 bool use_ct(const nf_plan* p, long long n) {
   if (p->ct_mode == 0 || p->structured || n < 1) return false;
+  // (the margin keeps room for the persistent loop's static shared memory, so the loop runs what nf_forward and
+  // nf_adjoint_prox run: same bits)
   const size_t bytes = p->dtype == NF_C64 ? CtLayout<float>(p->g.A).bytes : CtLayout<double>(p->g.A).bytes;
-  if (bytes > 232448) return false;
+  if (bytes > 232448 - 4096) return false;
   if ((long long)p->g.ntiles * n < p->nsm) return false;
   return p->ct_mode == 2 || (long long)p->g.ntiles * n >= p->ct_min_pairs * p->nsm;
+}
+// ... and the CTA-tile adjoint (ct_adjoint) for a flat batch of B channels: a tile's pieces fit the chunk-partial
+// buffer (adj_epilogue), and the parked piece sums are allocated (pmax per CTA)
+bool use_ct_adj(const nf_plan* p, long long B) {
+  if (!p->ct_adj || !use_ct(p, B)) return false;
+  return (p->nsm + p->g.ntiles - 1) / p->g.ntiles + 1 <= p->adj_ch_cap;
+}
+int ct_pmax(const nf_plan* p) { return (p->g.ntiles + p->nsm - 1) / p->nsm + 2; }
+int ct_part_buffer(nf_plan* p) {
+  const size_t need = (size_t)p->nsm * ct_pmax(p) * TILE * 2 * real_size(p);
+  if (need <= p->ctpart_bytes) return NF_OK;
+  cudaFree(p->d_ctpart);
+  p->d_ctpart = nullptr;
+  p->ctpart_bytes = 0;
+  if (int rc = dalloc(p, (char**)&p->d_ctpart, need)) return rc;
+  p->ctpart_bytes = need;
+  return NF_OK;
 }
 CtArgs ct_args(const nf_plan* p, int span) {
   CtArgs c;
@@ -4460,6 +4711,13 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
     auto kern = p->exact ? adj_struct_kernel<Real, PROX, true> : adj_struct_kernel<Real, PROX, false>;
     CUDA_TRY(ensure_smem((const void*)kern, sm, true));
     kern<<<(unsigned)(p->g.ntiles * a.CH), SW * 32, sm, st>>>(a, sa, p->d_kd);
+  } else if (use_ct_adj(p, p->B)) {
+    if (int rc = ct_part_buffer(p)) return rc;
+    auto kct = p->exact ? adj_ct_kernel<Real, PROX, true> : adj_ct_kernel<Real, PROX, false>;
+    const size_t smc = CtLayout<Real>(p->g.A).bytes;
+    CUDA_TRY(ensure_smem((const void*)kct, smc));
+    CUDA_TRY(launch_k(p->use_pdl, kct, dim3(p->nsm), dim3(CT_WARPS * 32), smc, st, a, ct_args(p, p->B),
+                      (Real*)p->d_ctpart, ct_pmax(p)));
   } else {
     const size_t sm = adj_smem(p);
     auto kern = p->exact ? adj_kernel<Real, PROX, true> : adj_kernel<Real, PROX, false>;
@@ -4607,28 +4865,43 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
     return launch_tiny_loop<Real>(p, table, K, seed, iter0, B, ymeas, s_a, s_b, eta_over_b, alpha, tol, budget_ns,
                                   rec, state, st);
   // the forward phase on the CTA-tile kernel (as nf_forward would run it; its values are bit-identical either way)
-  // when its layout fits next to 16 warp regions
+  // when its layout fits next to 16 warp regions. The loop's batches are flat: the plan's structured flag (left by
+  // an earlier staged batch) must not steer the choice away from what nf_adjoint_prox runs on a flat batch.
+  p->structured = false;
   bool ct = use_ct(p, B);
-  auto kern = ct ? (p->exact ? spgm_loop_kernel<Real, true, true> : spgm_loop_kernel<Real, false, true>)
-                 : (p->exact ? spgm_loop_kernel<Real, true, false> : spgm_loop_kernel<Real, false, false>);
+  const bool cta = ct && use_ct_adj(p, B);
+  auto pick = [&](bool f, bool a) {
+    if (p->exact)
+      return a ? spgm_loop_kernel<Real, true, 3> : f ? spgm_loop_kernel<Real, true, 1> : spgm_loop_kernel<Real, true, 0>;
+    return a ? spgm_loop_kernel<Real, false, 3> : f ? spgm_loop_kernel<Real, false, 1> : spgm_loop_kernel<Real, false, 0>;
+  };
+  auto kern = pick(ct, cta);
   size_t wb = std::max(fwd_warp_bytes<Real>(p->g.Tg, p->g.A), warp_smem_bytes<Real>(p->g.Tg, p->g.A));
   wb = (wb + 15) & ~(size_t)15;
   cudaFuncAttributes fattr;
   CUDA_TRY(cudaFuncGetAttributes(&fattr, kern));
   const size_t SMEM_DYN_MAX = 232448 - fattr.sharedSizeBytes;  // 227 KB per block (opt-in) beside the static part
   int nw = 16;  // warps per CTA: 16, 12 or 8 (multiples of 4 keep the 256-thread groups of P3 / P5)
-  while (nw > 8 && (size_t)nw * wb > SMEM_DYN_MAX) nw -= 4;
-  if ((size_t)nw * wb > SMEM_DYN_MAX) return fail(NF_ERR_STATE, "persistent loop: shared memory layout does not fit");
+  if (!cta) {  // the warp-unit adjoint's regions (the CTA-tile kernels of both phases use CtLayout only)
+    while (nw > 8 && (size_t)nw * wb > SMEM_DYN_MAX) nw -= 4;
+    if ((size_t)nw * wb > SMEM_DYN_MAX)
+      return fail(NF_ERR_STATE, "persistent loop: shared memory layout does not fit");
+  }
   // P0 rank sort: keys + order (LOOP_SORT_MAX ints each), then the key bitmap and its word prefix counts
   const size_t kwords = ((size_t)p->KS + 31) / 32;
   const bool bitmap = (size_t)LOOP_SORT_MAX * 8 + kwords * 8 <= SMEM_DYN_MAX;
   const size_t sort_bytes = (size_t)LOOP_SORT_MAX * 8 + (bitmap ? kwords * 8 : 0);
-  size_t smem = std::max({(size_t)nw * wb, sort_bytes, (size_t)(4 * 256 + 16) * sizeof(double)});
-  if (ct && (nw != 16 || CtLayout<Real>(p->g.A).bytes > SMEM_DYN_MAX)) {
+  size_t smem = std::max(sort_bytes, (size_t)(4 * 256 + 16) * sizeof(double));
+  if (!cta) smem = std::max(smem, (size_t)nw * wb);
+  if (ct && !cta && nw != 16) {  // CTA-tile forward beside the warp-unit adjoint needs 16 warps (its values are the same)
     ct = false;
-    kern = p->exact ? spgm_loop_kernel<Real, true, false> : spgm_loop_kernel<Real, false, false>;
+    kern = pick(false, false);
   }
+  const bool ct_adjoint_on = cta;
   if (ct) smem = std::max(smem, CtLayout<Real>(p->g.A).bytes);
+  if (smem > SMEM_DYN_MAX) return fail(NF_ERR_STATE, "persistent loop: shared memory layout does not fit");
+  if (ct_adjoint_on)
+    if (int rc = ct_part_buffer(p)) return rc;
   CUDA_TRY(ensure_smem((const void*)kern, smem));
   int dev = 0, nsm = 0, per_sm = 0;
   CUDA_TRY(cudaGetDevice(&dev));
@@ -4697,9 +4970,13 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
   CtArgs ca = ct_args(p, B);
   ca.G = nsm;
+  la.ctpart = p->d_ctpart;
+  la.ctpmax = ct_pmax(p);
   if (std::getenv("NFGPU_VERBOSE"))
-    std::fprintf(stderr, "nf_spgm_loop: spgm_loop_kernel (%s forward), %d CTAs x %d warps, %zu B shared, B=%d, K=%d\n",
-                 ct ? "CTA-tile" : "warp-unit", nsm, nw, smem, B, K);
+    std::fprintf(stderr, "nf_spgm_loop: spgm_loop_kernel (%s forward, %s adjoint), %d CTAs x %d warps, %zu B shared, "
+                 "B=%d, K=%d, ctpart %p (%zu B, pmax %d)\n", ct ? "CTA-tile" : "warp-unit",
+                 ct_adjoint_on ? "CTA-tile" : "warp-unit", nsm, nw, smem, B, K, p->d_ctpart, p->ctpart_bytes,
+                 ct_pmax(p));
   void* args[] = {&la, &fa, &aa, &ca};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nsm), dim3(nw * 32), args, smem, st));
   p->loop_threads = nw * 32;
@@ -4881,6 +5158,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   if (const char* e = std::getenv("NFGPU_PDL")) p->use_pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("NFGPU_CT")) p->ct_mode = std::atoi(e);
   if (const char* e = std::getenv("NFGPU_CT_MIN")) p->ct_min_pairs = std::max(1LL, std::atoll(e));
+  if (const char* e = std::getenv("NFGPU_CT_ADJ")) p->ct_adj = std::atoi(e);
   {
     int dev = 0, nsm = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&

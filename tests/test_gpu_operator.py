@@ -448,3 +448,42 @@ def test_cta_tile_forward_is_bit_identical(case, dtype, rng, monkeypatch):
         out[mode] = [forward_values(plan, s, idx) for idx in idxs]
     for a, b in zip(out["0"], out["2"]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("case", ["medium", "ragged"])
+def test_cta_tile_adjoint_prox_matches_warp_unit(case, dtype, rng, monkeypatch):
+    """The CTA-tile adjoint + prox (adj_ct_kernel: warps split each piece's channels, the last one sums their
+    partial gradients in warp order, the pieces' epilogues run side by side at the end; tiles cut across CTAs sum
+    their pieces in piece order) against the warp-unit kernel: the same SPGM step to rounding, and the
+    statistics too (NFGPU_CT=2 forces the CTA-tile kernels whenever the layout fits, NFGPU_CT_ADJ=0 keeps the
+    adjoint on the warp-unit kernel)."""
+    from paper_2509_00774_b200 import configs
+    from paper_2509_00774_b200.solver import SPGMEngine
+
+    if case == "medium":
+        scn = configs.medium_scenario()
+        B = 512
+    else:
+        scn = ImagingScenario(
+            array=ArrayGeometry(((0.03, 0.01, 0.0), (-0.02, 0.04, 0.0), (0.0, -0.05, 0.0)),
+                                ((0.01, 0.0, 0.0), (-0.04, -0.01, 0.0))),
+            frequencies=FrequencyGrid(20e9, 30e9, 5),
+            voxels=VoxelGrid(center=Vec3(0.0, 0.0, 0.3), extent=(0.2, 0.07, 0.06), dims=(33, 11, 9)),
+        )
+        B = 23
+    s = rc(rng, scn.n_voxels)
+    y = rc(rng, scn.n_channels)
+    idx = np.sort(rng.choice(scn.n_channels, B, replace=False))
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("NFGPU_CT", "2")
+        monkeypatch.setenv("NFGPU_CT_ADJ", mode)
+        plan = DevicePlan(scn, dtype=dtype, device="cuda:0", structured="never")
+        eng = SPGMEngine(plan, y, eta=2e-3, alpha=0.05, initial=s)
+        eng.stage(idx)
+        eng.step_staged()
+        out[mode] = (eng.volume(), eng.stats.cpu().numpy())
+    tol = 1e-5 if dtype == "c64" else 1e-12
+    assert rel_l2(out["1"][0], out["0"][0]) <= tol
+    np.testing.assert_allclose(out["1"][1], out["0"][1], rtol=tol)
