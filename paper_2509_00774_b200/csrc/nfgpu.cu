@@ -3452,13 +3452,13 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 1) adj_ct_kernel(AdjArgs<Real> 
 // spgm_loop_kernel runs K SPGM iterations (solver.py:281-310) of a flat batch in ONE cooperative launch, one CTA
 // per SM: the device-side loop for latency-bound configurations (BASELINE Small: 12 launches of ~3 us each per
 // iteration otherwise). Per iteration, between grid barriers:
-//   P0  every CTA draws the batch (index table row k, or the Feistel sampler) and sorts its (key, position)
-//       keys by rank in shared memory (same order as the counting sort of nf_batch_prepare), then writes its
-//       slice of the sorted channel records
-//   P1  forward warp units (fwd_unit, the body of fwd_kernel) over the grid's warps -> part[tile][j]
+//   P0  one CTA draws the batch (index table row k, or the Feistel sampler), sorts its (key, position) keys by
+//       rank in shared memory (same order as the counting sort of nf_batch_prepare) and writes the sorted channel
+//       records of parity k & 1 -- during P3 of iteration k-1, beside CTA 0's level 2
+//   P1  forward: CTA-tile pieces (ct_forward) or warp units (fwd_unit, the body of fwd_kernel) -> part[tile][j]
 //   P2  level 1 of the forward reduce (fwd_reduce1_kernel's sums)
 //   P3  level 2 + residual records, per 256-channel group (fwd_reduce2_kernel + resid_kernel)
-//   P4  adjoint + prox warp units (adj_unit) -> s_out, per-tile statistics
+//   P4  adjoint + prox: CTA-tile pieces (ct_adjoint) or warp units (adj_unit) -> s_out, per-tile statistics
 //   P5  every CTA reduces the statistics (stats_reduce_kernel's tree), records them and tests the tolerance
 // Every value is computed by the same code in the same order as the per-launch path, so the iterates are
 // bit-identical to nf_batch_prepare + nf_forward + nf_adjoint_prox (tested). The time budget is checked on the
@@ -3474,7 +3474,7 @@ struct LoopArgs {
   const double* __restrict__ kd;
   const double* __restrict__ pulse;
   const void* ymeas;
-  int* sm;              // spgm_loop_kernel: per-CTA private records [2 parities][CTAs][B]
+  int* sm;              // spgm_loop_kernel: sorted records [2 parities][B]
   int* spos;
   int* sf;
   ChanRec* crec;
@@ -3571,9 +3571,9 @@ __device__ __forceinline__ int loop_index(const LoopArgs& la, int k, int i) {
   return (int)x;
 }
 
-// P0 of an iteration: draw its batch and rank the keys (every CTA; keys are distinct) in shared memory, then
-// write ALL B channel records in key order (the counting sort's order) to this CTA's private copy. Ranks come
-// from a bitmap of the key space and a prefix count of its words when the bitmap fits, else pairwise.
+// P0 of an iteration (one CTA): draw its batch and rank the keys (distinct) in shared memory, then write the B
+// channel records in key order (the counting sort's order) to the records of parity k & 1. Ranks come from a
+// bitmap of the key space and a prefix count of its words when the bitmap fits, else pairwise.
 __device__ __forceinline__ void loop_sort(const LoopArgs& la, int k, int* scan_sh, unsigned char* smem_raw) {
   const int B = la.B;
   int* keys = reinterpret_cast<int*>(smem_raw);
@@ -3614,7 +3614,7 @@ __device__ __forceinline__ void loop_sort(const LoopArgs& la, int k, int* scan_s
     order[r] = i;
   }
   __syncthreads();
-  const size_t base = ((size_t)(k & 1) * gridDim.x + blockIdx.x) * B;
+  const size_t base = (size_t)(k & 1) * B;
   for (int j = threadIdx.x; j < B; j += blockDim.x) {
     const int pos = order[j], key = keys[pos];
     const int4 c = chan_of_key(la.km, key);
@@ -3695,13 +3695,17 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
 #define LOOP_STAMP(i) \
   if (la.prof && blockIdx.x == 0 && threadIdx.x == 0) la.prof[(size_t)k * LOOP_PROF + (i)] = globaltimer() - t0
   if (loop_skip(la)) return;
-  loop_sort(la, 0, scan_sh, smem_raw);
+  // one CTA sorts each iteration's batch into the shared records of its parity (the last CTA: CTA 0 does level 2
+  // in P3); everybody reads them after the grid barriers that separate P3 from the phases that use them
+  const bool sorter = blockIdx.x == gridDim.x - 1;
+  if (sorter) loop_sort(la, 0, scan_sh, smem_raw);
+  grid_sync(la.bar);
   for (; k < la.K; ++k) {
     LOOP_STAMP(0);
     const Real* s_in = reinterpret_cast<const Real*>((k & 1) ? la.s_b : la.s_a);
     Real* s_out = reinterpret_cast<Real*>((k & 1) ? la.s_a : la.s_b);
-    const size_t pbase = ((size_t)(k & 1) * gridDim.x + blockIdx.x) * B;  // this CTA's records of iteration k
-    // ---- forward(k) on this CTA's private records (sorted during iteration k-1: no barrier before)
+    const size_t pbase = (size_t)(k & 1) * B;  // the records of iteration k
+    // ---- forward(k) on the records sorted during iteration k-1
     if constexpr (CT) {
       // the other phases reuse this shared memory (sort, reduce and adjoint scratch): fresh mbarriers every time
       ct_init(smem_raw);
@@ -3784,7 +3788,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
       }
     }
     __syncthreads();
-    if (k + 1 < la.K) loop_sort(la, k + 1, scan_sh, smem_raw);  // the next iteration's records, meanwhile
+    if (sorter && k + 1 < la.K) loop_sort(la, k + 1, scan_sh, smem_raw);  // the next iteration's records
     LOOP_STAMP(5);
     grid_sync(la.bar);  // B3
     LOOP_STAMP(6);
@@ -4215,7 +4219,7 @@ struct nf_plan {
   unsigned* d_loopbar = nullptr;  // persistent SPGM loop: grid barrier {arrivals, generation} (zero between launches)
   int loop_threads = 0;           // ... CTA size chosen on first use (0: not yet)
   unsigned long long* d_loop_prof = nullptr;  // ... phase time stamps (NFGPU_LOOP_PROFILE)
-  void* d_loop_priv = nullptr;  // spgm_loop_kernel: private records per CTA and tile epochs
+  void* d_loop_priv = nullptr;  // spgm_loop_kernel: sorted records of two iterations
   size_t loop_priv_bytes = 0;
   void* d_tiny = nullptr;  // tiny_loop_kernel scratch: part, wch, ch, gpart, vbcnt, stat_part
   size_t tiny_bytes = 0;
@@ -4930,8 +4934,8 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   la.kd = p->d_kd;
   la.pulse = p->d_pulse;
   la.ymeas = ymeas;
-  {  // per-CTA private channel records [2][nsm][B]
-    const size_t n = (size_t)2 * nsm * B;
+  {  // sorted channel records [2 parities][B]
+    const size_t n = (size_t)2 * B;
     const size_t need = n * (sizeof(ChanRec) + 3 * sizeof(int));
     if (need > p->loop_priv_bytes) {
       cudaFree(p->d_loop_priv);
