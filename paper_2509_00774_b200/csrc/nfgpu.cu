@@ -3459,7 +3459,9 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 1) adj_ct_kernel(AdjArgs<Real> 
 //   P2  level 1 of the forward reduce (fwd_reduce1_kernel's sums)
 //   P3  level 2 + residual records, per 256-channel group (fwd_reduce2_kernel + resid_kernel)
 //   P4  adjoint + prox: CTA-tile pieces (ct_adjoint) or warp units (adj_unit) -> s_out, per-tile statistics
-//   P5  every CTA reduces the statistics (stats_reduce_kernel's tree), records them and tests the tolerance
+//   P5  one CTA reduces the statistics (stats_reduce_kernel's tree) during the next iteration's level 1, records
+//       them and tests the tolerance; a stop takes effect after that level's barrier (the forward of the
+//       iteration after the last one is discarded), and the last iteration's statistics follow the loop
 // Every value is computed by the same code in the same order as the per-launch path, so the iterates are
 // bit-identical to nf_batch_prepare + nf_forward + nf_adjoint_prox (tested). The time budget is checked on the
 // device clock by CTA 0 and takes effect after the next barrier.
@@ -3633,7 +3635,7 @@ __device__ __forceinline__ void loop_sort(const LoopArgs& la, int k, int* scan_s
 // statistics of iteration k (stats_reduce_kernel's tree, threads 0-255 of every CTA, the same bits everywhere),
 // its record (CTA 0) and the time-budget flag; returns the relative magnitude change
 __device__ __forceinline__ double loop_stats(const LoopArgs& la, int k, int ntiles, double (*red)[256],
-                                             unsigned long long t0) {
+                                             unsigned long long t0, bool writer) {
   if (threadIdx.x < 256) {
     double acc[4] = {0, 0, 0, 0};
     for (int i = threadIdx.x; i < ntiles; i += 256) {
@@ -3655,7 +3657,7 @@ __device__ __forceinline__ double loop_stats(const LoopArgs& la, int k, int ntil
   }
   __syncthreads();
   const double st0 = red[0][0], st1 = red[1][0];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (writer && threadIdx.x == 0) {
     double* r = la.rec + (size_t)k * LOOP_REC;
     r[0] = st0;
     r[1] = st1;
@@ -3699,6 +3701,10 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
   // in P3); everybody reads them after the grid barriers that separate P3 from the phases that use them
   const bool sorter = blockIdx.x == gridDim.x - 1;
   if (sorter) loop_sort(la, 0, scan_sh, smem_raw);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // unit counters (a launch may have stopped between their resets)
+    la.ctr[0] = 0;
+    la.ctr[1] = 0;
+  }
   grid_sync(la.bar);
   for (; k < la.K; ++k) {
     LOOP_STAMP(0);
@@ -3722,9 +3728,10 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     }
     grid_sync(la.bar);  // B1
     LOOP_STAMP(2);
-    if (k > 0 && *(volatile int*)(la.state + 2)) {  // time budget spent after iteration k-1 (CTA 0's clock)
-      reason = 2;
-      break;
+    if (k > 0 && sorter) {  // statistics of iteration k-1 on one CTA, beside the others' level 1; its stop decision
+                            // (state[2]: 2 tolerance, 1 time budget) takes effect after the next barrier
+      const double change = loop_stats(la, k - 1, g.ntiles, red, t0, true);
+      if (threadIdx.x == 0 && change < la.tol) la.state[2] = 2;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[1] = 0;  // every warp is past its adjoint fetches of k-1
     // ---- level 1 of the forward reduce: tmp[seg][j] = sum over the segment's tiles (fixed order)
@@ -3745,6 +3752,14 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     LOOP_STAMP(3);
     grid_sync(la.bar);  // B2
     LOOP_STAMP(4);
+    if (k > 0) {  // iteration k-1 was the last (every CTA reads the same flag): k iterations ran
+      const int stop = *(volatile int*)(la.state + 2);
+      if (stop) {
+        done = k;
+        reason = stop == 2 ? 1 : 2;
+        break;
+      }
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[0] = 0;  // every warp is past its forward fetches of k
     // ---- level 2 (y = p_f/(4pi) sum, rounded to Real as stored), residual records, dpart per 256 channels
     {
@@ -3814,16 +3829,14 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     }
     grid_sync(la.bar);  // B4
     LOOP_STAMP(8);
-    const double change = loop_stats(la, k, g.ntiles, red, t0);
     done = k + 1;
-    LOOP_STAMP(9);
-    if (change < la.tol) {  // every CTA reaches the same decision from the same bits
-      reason = 1;
-      break;
-    }
+  }
+  if (k == la.K && blockIdx.x == 0) {  // every iteration ran: the statistics of the last one
+    const double change = loop_stats(la, la.K - 1, g.ntiles, red, t0, true);
+    if (change < la.tol) reason = 1;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (reason == 0 && la.state[2]) reason = 2;  // the budget ran out on the last iteration of the launch
+    if (reason == 0 && la.state[2] == 1) reason = 2;  // the budget ran out on the last iteration of the launch
     la.state[0] = done;
     la.state[1] = reason;
   }

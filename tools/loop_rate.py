@@ -80,8 +80,9 @@ if os.environ.get("NFGPU_LOOP_PROFILE"):
         t = np.frombuffer(buf, dtype=np.uint64)[: K * 12].reshape(K, 12).astype(np.float64)[K // 4:]
         tiny = not t[:, 6:].any()
         names = (["fwd", "bar0", "sums+adj+prox", "bar1", "stats"] if tiny else
-                 ["fwd", "bar1", "red1", "bar2", "red2+resid+next sort", "bar3", "adj", "bar4", "stats"])
-        last = 5 if tiny else 9
+                 ["fwd", "bar1", "red1 (+stats of k-1 on one CTA)", "bar2", "red2+resid (+next sort on one CTA)",
+                  "bar3", "adj", "bar4"])
+        last = 5 if tiny else 8
         d = np.diff(t[:, :last + 1], axis=1).mean(axis=0) / 1e3
         prof = {n: round(float(v), 2) for n, v in zip(names, d)}
         prof["next_iter_gap"] = round(float((t[1:, 0] - t[:-1, last]).mean() / 1e3), 2)
