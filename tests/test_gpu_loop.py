@@ -33,9 +33,14 @@ def _pair(scn, dtype, y, eta, alpha, s0=None, max_batch=None):
     return engs
 
 
+@pytest.mark.parametrize("ct", ["auto", "forced"])
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 @pytest.mark.parametrize("workload", ["small", "medium"])
-def test_loop_matches_per_launch_path_bitwise(workload, dtype, no_tiny):
+def test_loop_matches_per_launch_path_bitwise(workload, dtype, ct, no_tiny, monkeypatch):
+    """ct="forced" (NFGPU_CT=2) runs the CTA-tile forward and adjoint wherever their layout fits, Small included,
+    in both paths."""
+    if ct == "forced":
+        monkeypatch.setenv("NFGPU_CT", "2")
     w = configs.WORKLOADS[workload]()
     scn = w.scenario
     rng = np.random.default_rng(3)
