@@ -460,8 +460,11 @@ __global__ void build_table_kernel(Geo g, const double* __restrict__ ant, Real* 
 }
 
 // ------------------------------------------------------------------ batch prep
+// Sort key of a channel: (tx group, rx, tx in group, f) -- runs of one receiver within one tx group, whose tx rows a
+// warp stages -- or, for the CTA-tile kernels (all rows resident), rx-major (rx, tx group, tx in group, f): a
+// receiver's rows (and the forward's scaled iterate, the adjoint's partial sum) then change once per receiver.
 struct KeyMap {
-  int T, R, F, Tg;
+  int T, R, F, Tg, ng, rxmajor;
 };
 __device__ __forceinline__ int key_of(const KeyMap& k, int m) {
   const int TR = k.T * k.R;
@@ -470,15 +473,22 @@ __device__ __forceinline__ int key_of(const KeyMap& k, int m) {
   const int t = rem / k.R;
   const int r = rem - t * k.R;
   const int tg = t / k.Tg, tl = t - tg * k.Tg;
-  return ((tg * k.R + r) * k.Tg + tl) * k.F + f;
+  const int outer = k.rxmajor ? r * k.ng + tg : tg * k.R + r;
+  return (outer * k.Tg + tl) * k.F + f;
 }
 __device__ __forceinline__ int4 chan_of_key(const KeyMap& k, int key) {  // {f, t, r, tg}
   const int f = key % k.F;
   int q = key / k.F;
   const int tl = q % k.Tg;
   q /= k.Tg;
-  const int r = q % k.R;
-  const int tg = q / k.R;
+  int r, tg;
+  if (k.rxmajor) {
+    tg = q % k.ng;
+    r = q / k.ng;
+  } else {
+    r = q % k.R;
+    tg = q / k.R;
+  }
   return make_int4(f, tg * k.Tg + tl, r, tg);
 }
 
@@ -3087,7 +3097,7 @@ __device__ __forceinline__ void ct_fwd_slice(const Geo& g, const Real* __restric
   zero(shi);
   zero(nshr);
   const Real* tsl = tab_s + L * QD;
-  int carry = -1;
+  int carry = -1, cur_rr = -1;
   for (int jb = c0; jb < c1; jb += 32) {
     const int nb = min(32, c1 - jb);
     const bool more = jb + 32 < c1;
@@ -3102,11 +3112,14 @@ __device__ __forceinline__ void ct_fwd_slice(const Geo& g, const Real* __restric
         if ((starts >> c) & 1u) {  // a new (rx, tx-group) run begins at c: rows straight from the resident table
           const int rr = key & 0x7fff, tg = (key >> 15) & 0x1ff;
           tsl = tab_s + (size_t)tg * g.Tg * TABW + L * QD;
-          const Real* rrow = tab_s + (size_t)(g.T + rr) * TABW + L * QD;
-          dR = ldv(rrow);
-          iR = ldv(rrow + TILE);
-          // the iterate from shared memory at every run start (not held in registers across the run)
-          scale_s(iR, ldv(s_s + L * QD), ldv(s_s + TILE + L * QD), shr, shi, nshr);
+          if (rr != cur_rr) {  // a new receiver (rx-major batches: once per receiver, not per tx group)
+            cur_rr = rr;
+            const Real* rrow = tab_s + (size_t)(g.T + rr) * TABW + L * QD;
+            dR = ldv(rrow);
+            iR = ldv(rrow + TILE);
+            // the iterate from shared memory at every receiver start (not held in registers)
+            scale_s(iR, ldv(s_s + L * QD), ldv(s_s + TILE + L * QD), shr, shi, nshr);
+          }
         }
         for (; c + 1 < e; c += 2) {
           const R4<Real> q0 = ws.rec[c], q1 = ws.rec[c + 1];
@@ -3249,7 +3262,7 @@ __device__ __forceinline__ void ct_adj_slice(const Geo& g, const Real* __restric
   zero(dR);
   zero(iR);
   const Real* tsl = tab_s + L * QD;
-  int carry = -1;
+  int carry = -1, cur_rr = -1;
   for (int jb = c0; jb < c1; jb += 32) {
     const int nb = min(32, c1 - jb);
     const bool more = jb + 32 < c1;
@@ -3261,11 +3274,14 @@ __device__ __forceinline__ void ct_adj_slice(const Geo& g, const Real* __restric
       const int e = key >> 24;
       if ((starts >> c) & 1u) {
         const int rr = key & 0x7fff, tg = (key >> 15) & 0x1ff;
-        flush(iR, hr, hi, gr, gi);
         tsl = tab_s + (size_t)tg * g.Tg * TABW + L * QD;
-        const Real* rrow = tab_s + (size_t)(g.T + rr) * TABW + L * QD;
-        dR = ldv(rrow);
-        iR = ldv(rrow + TILE);
+        if (rr != cur_rr) {  // a new receiver: g += h/d_R, its rows (rx-major batches: once per receiver)
+          cur_rr = rr;
+          flush(iR, hr, hi, gr, gi);
+          const Real* rrow = tab_s + (size_t)(g.T + rr) * TABW + L * QD;
+          dR = ldv(rrow);
+          iR = ldv(rrow + TILE);
+        }
       }
       R4<Real> q = ws.rec[c];
       int off = low2(q.y) * TABW;
@@ -4186,7 +4202,9 @@ struct nf_plan {
   size_t dev_bytes = 0;
   int64_t launches = 0;
   int KS, ksblocks;
-  KeyMap km;
+  KeyMap km;     // batch order of the warp-unit kernels
+  KeyMap km_rx;  // ... of the CTA-tile kernels (rx-major; ct_rxmajor)
+  bool rxmajor = false;  // the staged flat batch is in rx-major order
   // device
   double* d_ant = nullptr;
   double* d_kd = nullptr;
@@ -4244,6 +4262,7 @@ struct nf_plan {
                              // the layout fits (tests); env NFGPU_CT
   long long ct_min_pairs = 1024;  // ... fewest (tile, channel) pairs per CTA (env NFGPU_CT_MIN)
   int ct_adj = 1;                 // CTA-tile adjoint too (when use_ct holds for the batch; env NFGPU_CT_ADJ)
+  int ct_rx = 1;                  // rx-major order for batches on the CTA-tile kernels (env NFGPU_CT_RXMAJOR)
   void* d_ctpart = nullptr;       // ... its parked piece sums
   size_t ctpart_bytes = 0;
   bool comm_active = false;  // inside nf_forward_allreduce
@@ -4457,6 +4476,10 @@ int ct_part_buffer(nf_plan* p) {
   if (int rc = dalloc(p, (char**)&p->d_ctpart, need)) return rc;
   p->ctpart_bytes = need;
   return NF_OK;
+}
+// rx-major batch order (KeyMap::rxmajor) when both phases of the batch run the CTA-tile kernels on one window
+bool ct_rxmajor(const nf_plan* p, int B) {
+  return p->ct_rx && B <= p->fwd_chunk && use_ct(p, B) && use_ct_adj(p, B);
 }
 CtArgs ct_args(const nf_plan* p, int span) {
   CtArgs c;
@@ -4933,7 +4956,7 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   p->B = B;
   p->structured = false;
   LoopArgs la;
-  la.km = p->km;
+  la.km = cta && ct_rxmajor(p, B) ? p->km_rx : p->km;  // the order nf_batch_prepare gives this batch
   la.M = p->M;
   la.B = B;
   la.K = K;
@@ -5074,7 +5097,8 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
                                   " bytes per block)");
     }
   }
-  p->km = KeyMap{g.T, g.R, g.F, g.Tg};
+  p->km = KeyMap{g.T, g.R, g.F, g.Tg, g.ng, 0};
+  p->km_rx = KeyMap{g.T, g.R, g.F, g.Tg, g.ng, 1};
   p->KS = g.ng * g.R * g.Tg * g.F;
   p->ksblocks = (p->KS + 1023) / 1024;
   p->fwd_gridx = g.ntiles;  // rows of the forward partial buffer (one per tile)
@@ -5176,6 +5200,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   if (const char* e = std::getenv("NFGPU_CT")) p->ct_mode = std::atoi(e);
   if (const char* e = std::getenv("NFGPU_CT_MIN")) p->ct_min_pairs = std::max(1LL, std::atoll(e));
   if (const char* e = std::getenv("NFGPU_CT_ADJ")) p->ct_adj = std::atoi(e);
+  if (const char* e = std::getenv("NFGPU_CT_RXMAJOR")) p->ct_rx = std::atoi(e);
   {
     int dev = 0, nsm = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -5246,15 +5271,18 @@ int nf_batch_prepare(nf_plan* p, const int32_t* idx, int B, void* stream) {
   if (B > p->max_batch) return fail(NF_ERR_ARG, "batch larger than the plan's max_batch");
   cudaStream_t st = (cudaStream_t)stream;
   const bool pdl = p->use_pdl;
-  CUDA_TRY(launch_k(pdl, mark_kernel, dim3((B + 255) / 256), dim3(256), 0, st, p->km, idx, B, p->d_pos_of_key));
+  p->structured = false;
+  const bool rx = ct_rxmajor(p, B);
+  const KeyMap km = rx ? p->km_rx : p->km;
+  CUDA_TRY(launch_k(pdl, mark_kernel, dim3((B + 255) / 256), dim3(256), 0, st, km, idx, B, p->d_pos_of_key));
   CUDA_TRY(launch_k(pdl, count_kernel, dim3(p->ksblocks), dim3(1024), 0, st, (const int*)p->d_pos_of_key, p->KS,
                     p->d_cnt));
   CUDA_TRY(launch_k(pdl, scan_kernel, dim3(1), dim3(1024), 0, st, p->d_cnt, p->ksblocks));
-  CUDA_TRY(launch_k(pdl, compact_kernel, dim3(p->ksblocks), dim3(1024), 0, st, p->km, p->d_pos_of_key, p->KS,
+  CUDA_TRY(launch_k(pdl, compact_kernel, dim3(p->ksblocks), dim3(1024), 0, st, km, p->d_pos_of_key, p->KS,
                     (const int*)p->d_cnt, p->d_sm, p->d_spos, p->d_crec, p->d_sf, (const double*)p->d_kd));
   p->launches += 4;
   p->B = B;
-  p->structured = false;
+  p->rxmajor = rx;
   return NF_OK;
 }
 
