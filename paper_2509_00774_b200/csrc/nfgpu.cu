@@ -2949,9 +2949,11 @@ struct CtLayout {  // [mbarriers, counters | buffer 0 | buffer 1 | warp records 
 };
 
 struct CtArgs {
-  long long W;  // ntiles * span: tile-major (tile, sorted channel) pairs of the launch window
-  int span;     // channels of the window
-  int G;        // CTAs (one per SM; the persistent loop's grid)
+  long long W;   // ntiles * span: tile-major (tile, sorted channel) pairs of the launch window
+  long long Wd;  // W + the pairs the LAST CTA's range is short of an equal share (the persistent loop's forward: that
+                 // CTA sorts the next batch first; forward values do not depend on the split). W everywhere else.
+  int span;      // channels of the window
+  int G;         // CTAs (one per SM; the persistent loop's grid)
 };
 // the CTA's range [r0, r1) of pairs: its first tile and piece count (the only 64-bit divisions, once per phase)
 struct CtRange {
@@ -2960,13 +2962,13 @@ struct CtRange {
 };
 __device__ __forceinline__ CtRange ct_range(const CtArgs& c, int b) {
   CtRange r;
-  r.r0 = (long long)b * c.W / c.G;
-  r.r1 = (long long)(b + 1) * c.W / c.G;
+  r.r0 = min((long long)b * c.Wd / c.G, c.W);
+  r.r1 = min((long long)(b + 1) * c.Wd / c.G, c.W);
   r.t0 = (int)(r.r0 / c.span);
   r.np = r.r1 > r.r0 ? (int)((r.r1 - 1) / c.span) - r.t0 + 1 : 0;
   return r;
 }
-// the CTA whose range holds pair u
+// the CTA whose range holds pair u (equal shares: Wd == W)
 __device__ __forceinline__ int ct_cta_of(const CtArgs& c, long long u) { return (int)(((u + 1) * c.G - 1) / c.W); }
 // piece i of the range: tile and window-relative channels [ja, jb)
 __device__ __forceinline__ void ct_piece(const CtArgs& c, const CtRange& r, int i, int& tile, int& ja, int& jb) {
@@ -3505,6 +3507,7 @@ struct LoopArgs {
   double* rec;          // [K][LOOP_REC]
   int* state;           // {iterations, reason: 0 max_iters / 1 tolerance / 2 time budget, stop flag}
   unsigned* bar;        // grid barrier {arrivals, generation}
+  int stage_ok;         // the reduce phase stages a CTA's partials [ntiles][channels per CTA] in shared memory
   int kwords;           // 32-bit words of the key-space bitmap of the P0 rank sort (0: pairwise ranks)
   int* ctr;             // work-unit counters {forward, adjoint}: warps fetch units past the first TW dynamically
   void* s_a;            // iteration k reads s_a (k even) or s_b (k odd) and writes the other
@@ -3650,7 +3653,7 @@ __device__ __forceinline__ void loop_sort(const LoopArgs& la, int k, int* scan_s
 
 // statistics of iteration k (stats_reduce_kernel's tree, threads 0-255 of every CTA, the same bits everywhere),
 // its record (CTA 0) and the time-budget flag; returns the relative magnitude change
-__device__ __forceinline__ double loop_stats(const LoopArgs& la, int k, int ntiles, double (*red)[256],
+__device__ __forceinline__ double loop_stats(const LoopArgs& la, int k, int ntiles, double (*red)[256], double* grp8,
                                              unsigned long long t0, bool writer) {
   if (threadIdx.x < 256) {
     double acc[4] = {0, 0, 0, 0};
@@ -3659,8 +3662,23 @@ __device__ __forceinline__ double loop_stats(const LoopArgs& la, int k, int ntil
       acc[1] += la.stat_part[(size_t)i * 4 + 1];
       acc[3] += la.stat_part[(size_t)i * 4 + 3];
     }
+    // resid_kernel's per-256-channel sums (lanes by xor tree, then the 8 warps in order) of iteration k's |y - y_meas|^2
+    const double* e2 = reinterpret_cast<const double*>(la.tmp) + (size_t)(k & 1) * la.B;
     const int nd = (la.B + 255) / 256;
-    for (int i = threadIdx.x; i < nd; i += 256) acc[2] += la.dpart[i];
+    for (int grp = 0; grp < nd; ++grp) {
+      const int j = grp * 256 + (int)threadIdx.x;
+      double e = j < la.B ? __ldcg(e2 + j) : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
+      if ((threadIdx.x & 31) == 0) grp8[threadIdx.x >> 5] = e;
+      named_sync(3, 256);
+      if ((int)threadIdx.x == (grp & 255)) {
+        double t = 0;
+        for (int i = 0; i < 8; ++i) t += grp8[i];
+        acc[2] += t;
+      }
+      named_sync(3, 256);
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = acc[q];
     named_sync(3, 256);
@@ -3692,7 +3710,8 @@ __device__ __forceinline__ double loop_stats(const LoopArgs& la, int k, int ntil
 }
 
 template <typename Real, bool EXACT, int CTM>  // CTM: bit 0 CTA-tile forward, bit 1 CTA-tile adjoint
-__global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<Real> fa, AdjArgs<Real> aa, CtArgs ca) {
+__global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<Real> fa, AdjArgs<Real> aa, CtArgs ca,
+                                                           CtArgs cf) {
   constexpr bool CT = (CTM & 1) != 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int scan_sh[32];
@@ -3728,11 +3747,14 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     Real* s_out = reinterpret_cast<Real*>((k & 1) ? la.s_a : la.s_b);
     const size_t pbase = (size_t)(k & 1) * B;  // the records of iteration k
     // ---- forward(k) on the records sorted during iteration k-1
+    // the sorting CTA first writes the next iteration's records (the other parity: last read by adjoint(k-1)); its
+    // forward share is shorter by about that time (cf.Wd; warp units are fetched dynamically anyway)
+    if (sorter && k + 1 < la.K) loop_sort(la, k + 1, scan_sh, smem_raw);
     if constexpr (CT) {
       // the other phases reuse this shared memory (sort, reduce and adjoint scratch): fresh mbarriers every time
       ct_init(smem_raw);
       unsigned ph = 0;
-      ct_forward<Real, EXACT, true>(fa, ca, smem_raw, s_in, la.crec + pbase, ph, false);
+      ct_forward<Real, EXACT, true>(fa, cf, smem_raw, s_in, la.crec + pbase, ph, false);
     } else {
       for (int u = gw; u < nfu; u = next_unit(la.ctr, TW, L))
         fwd_unit<Real, EXACT, true>(fa, u, wbase, 0, L, s_in, la.crec + pbase);
@@ -3744,30 +3766,95 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     }
     grid_sync(la.bar);  // B1
     LOOP_STAMP(2);
-    if (k > 0 && sorter) {  // statistics of iteration k-1 on one CTA, beside the others' level 1; its stop decision
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // every warp is past its forward fetches of k, adjoint fetches of k-1
+      la.ctr[0] = 0;
+      la.ctr[1] = 0;
+    }
+    if (sorter && k > 0) {  // statistics of iteration k-1 on one CTA, beside the others' reduce; its stop decision
                             // (state[2]: 2 tolerance, 1 time budget) takes effect after the next barrier
-      const double change = loop_stats(la, k - 1, g.ntiles, red, t0, true);
+      const double change = loop_stats(la, k - 1, g.ntiles, red, grp_sh[0], t0, true);
       if (threadIdx.x == 0 && change < la.tol) la.state[2] = 2;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[1] = 0;  // every warp is past its adjoint fetches of k-1
-    // ---- level 1 of the forward reduce: tmp[seg][j] = sum over the segment's tiles (fixed order)
-    {
-      const int n = la.nseg * B;
-      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int seg = i / B, j = i - seg * B;
+    // ---- the forward reduce and the residual records in one phase, per channel, on the other CTAs (JC consecutive
+    //      channels each): thread (seg, jj) sums the tiles of its segment in order (fwd_reduce1_kernel's sum), thread
+    //      jj then the segments in order (fwd_reduce2_kernel's), y = p_f/(4pi) sum rounded to Real as stored, the
+    //      residual record (resid_kernel) and |y - y_meas|^2 for the statistics (e2, parity k & 1, in la.tmp)
+    if (!sorter || gridDim.x == 1) {
+      const int nred = max(1, (int)gridDim.x - 1);
+      const int JC = (B + nred - 1) / nred;
+      const int j0 = blockIdx.x * JC, jn = min(JC, B - j0);
+      double2* seg_sh = reinterpret_cast<double2*>(smem_raw);  // [nseg][JC]
+      int f = 0, m = 0;
+      double pre = 0, pim = 0, ymr = 0, ymi = 0;
+      if ((int)threadIdx.x < jn) {  // the finishing threads' record loads go first
+        const Real* ym = reinterpret_cast<const Real*>(la.ymeas);
+        f = la.sf[pbase + j0 + threadIdx.x];
+        m = la.sm[pbase + j0 + threadIdx.x];
+        pre = la.pulse[2 * f];
+        pim = la.pulse[2 * f + 1];
+        ymr = (double)ym[2 * (size_t)m];
+        ymi = (double)ym[2 * (size_t)m + 1];
+      }
+      // the CTA's partials [ntiles][jn] first land in shared memory (every thread loads, one L2 latency) when they fit
+      R2<Real>* stage = reinterpret_cast<R2<Real>*>(seg_sh + (size_t)la.nseg * JC);
+      const bool staged = la.stage_ok != 0;
+      if (staged) {
+        const R2<Real>* src = reinterpret_cast<const R2<Real>*>(fa.part) + j0;
+        for (int it = threadIdx.x; it < g.ntiles * jn; it += blockDim.x) {
+          const int x = it / jn, jj = it - x * jn;
+          stage[it] = src[(size_t)x * B + jj];
+        }
+        __syncthreads();
+      }
+      for (int it = threadIdx.x; it < la.nseg * jn; it += blockDim.x) {
+        const int seg = it / jn, jj = it - seg * jn;
         const int x0 = (int)(((long long)g.ntiles * seg) / la.nseg), x1 = (int)(((long long)g.ntiles * (seg + 1)) / la.nseg);
         double sr = 0, si = 0;
-        for (int x = x0; x < x1; ++x) {
-          const R2<Real> v = reinterpret_cast<const R2<Real>*>(fa.part)[(size_t)x * B + j];
-          sr += (double)v.x;
-          si += (double)v.y;
+        if (staged) {
+#pragma unroll 4
+          for (int x = x0; x < x1; ++x) {
+            const R2<Real> v = stage[x * jn + jj];
+            sr += (double)v.x;
+            si += (double)v.y;
+          }
+        } else {
+          const R2<Real>* src = reinterpret_cast<const R2<Real>*>(fa.part) + j0 + jj;
+#pragma unroll 8
+          for (int x = x0; x < x1; ++x) {
+            const R2<Real> v = src[(size_t)x * B];
+            sr += (double)v.x;
+            si += (double)v.y;
+          }
         }
-        la.tmp[(size_t)seg * B + j] = make_double2(sr, si);
+        seg_sh[seg * JC + jj] = make_double2(sr, si);
+      }
+      __syncthreads();
+      if ((int)threadIdx.x < jn) {
+        const int j = j0 + threadIdx.x;
+        double sr = 0, si = 0;
+        for (int sgi = 0; sgi < la.nseg; ++sgi) {
+          const double2 v = seg_sh[sgi * JC + threadIdx.x];
+          sr += v.x;
+          si += v.y;
+        }
+        const double pr = pre / (4.0 * PI), pi_ = pim / (4.0 * PI);
+        const Real yr = (Real)(pr * sr - pi_ * si), yi = (Real)(pr * si + pi_ * sr);
+        double rr = (double)yr, ri = (double)yi;
+        rr -= ymr;
+        ri -= ymi;
+        const double qr = pre / (4.0 * PI), qi = -pim / (4.0 * PI);
+        R2<Real> wv;
+        wv.x = (Real)(qr * rr - qi * ri);
+        wv.y = (Real)(qr * ri + qi * rr);
+        const_cast<R2<Real>*>(aa.wrec)[j] = wv;
+        reinterpret_cast<double*>(la.tmp)[(size_t)(k & 1) * B + j] = rr * rr + ri * ri;
       }
     }
     LOOP_STAMP(3);
-    grid_sync(la.bar);  // B2
     LOOP_STAMP(4);
+    LOOP_STAMP(5);
+    grid_sync(la.bar);  // B3
+    LOOP_STAMP(6);
     if (k > 0) {  // iteration k-1 was the last (every CTA reads the same flag): k iterations ran
       const int stop = *(volatile int*)(la.state + 2);
       if (stop) {
@@ -3776,53 +3863,6 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
         break;
       }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) la.ctr[0] = 0;  // every warp is past its forward fetches of k
-    // ---- level 2 (y = p_f/(4pi) sum, rounded to Real as stored), residual records, dpart per 256 channels
-    {
-      const int half = threadIdx.x >> 8, ht = threadIdx.x & 255, halves = blockDim.x >> 8;
-      const int ngrp = (B + 255) / 256;
-      const Real* ym = reinterpret_cast<const Real*>(la.ymeas);
-      for (int grp = blockIdx.x * halves + half; half < halves && grp < ngrp; grp += gridDim.x * halves) {
-        const int j = grp * 256 + ht;
-        double e = 0;
-        if (j < B) {
-          double sr = 0, si = 0;
-          for (int sgi = 0; sgi < la.nseg; ++sgi) {
-            const double2 v = la.tmp[(size_t)sgi * B + j];
-            sr += v.x;
-            si += v.y;
-          }
-          const int f = la.sf[pbase + j];
-          const double pr = la.pulse[2 * f] / (4.0 * PI), pim = la.pulse[2 * f + 1] / (4.0 * PI);
-          const Real yr = (Real)(pr * sr - pim * si), yi = (Real)(pr * si + pim * sr);
-          double rr = (double)yr, ri = (double)yi;
-          const int m = la.sm[pbase + j];
-          rr -= (double)ym[2 * (size_t)m];
-          ri -= (double)ym[2 * (size_t)m + 1];
-          e = rr * rr + ri * ri;
-          const double qr = la.pulse[2 * f] / (4.0 * PI), qi = -la.pulse[2 * f + 1] / (4.0 * PI);
-          R2<Real> wv;
-          wv.x = (Real)(qr * rr - qi * ri);
-          wv.y = (Real)(qr * ri + qi * rr);
-          const_cast<R2<Real>*>(aa.wrec)[j] = wv;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
-        if ((ht & 31) == 0) grp_sh[half][ht >> 5] = e;
-        named_sync(1 + half, 256);
-        if (ht == 0) {
-          double t = 0;
-          for (int i = 0; i < 8; ++i) t += grp_sh[half][i];
-          la.dpart[grp] = t;
-        }
-        named_sync(1 + half, 256);
-      }
-    }
-    __syncthreads();
-    if (sorter && k + 1 < la.K) loop_sort(la, k + 1, scan_sh, smem_raw);  // the next iteration's records
-    LOOP_STAMP(5);
-    grid_sync(la.bar);  // B3
-    LOOP_STAMP(6);
     // ---- adjoint(k) + prox
     if constexpr ((CTM & 2) != 0) {
       ct_init(smem_raw);  // the sort of P3 used this shared memory
@@ -3848,7 +3888,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     done = k + 1;
   }
   if (k == la.K && blockIdx.x == 0) {  // every iteration ran: the statistics of the last one
-    const double change = loop_stats(la, la.K - 1, g.ntiles, red, t0, true);
+    const double change = loop_stats(la, la.K - 1, g.ntiles, red, grp_sh[0], t0, true);
     if (change < la.tol) reason = 1;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -4193,6 +4233,7 @@ struct nf_plan {
   // themselves: both (Medium loop 126.4 -> 121.5 us with the forward). Env NFGPU_WAVE_FIT / NFGPU_LOOP_WAVE_FIT.
   int wave_fit = 2;
   int loop_wave_fit = 3;
+  double loop_sort_disc = 12.0;  // % of an equal forward share the loop's sorting CTA is spared (NFGPU_SORT_DISC)
   int fit_min_waves = 1;  // env NFGPU_FIT_MIN_WAVES
   double tail_waves = 1.0;                  // ... for about this many waves of warp slots (env NFGPU_TAIL_WAVES)
   double taper = 0.375;                     // chunk-major adjoint taper h: last chunk 1 − 2h of the first (env NFGPU_TAPER)
@@ -4484,6 +4525,7 @@ bool ct_rxmajor(const nf_plan* p, int B) {
 CtArgs ct_args(const nf_plan* p, int span) {
   CtArgs c;
   c.W = (long long)p->g.ntiles * span;
+  c.Wd = c.W;
   c.span = span;
   c.G = p->nsm;
   return c;
@@ -4939,6 +4981,19 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   }
   const bool ct_adjoint_on = cta;
   if (ct) smem = std::max(smem, CtLayout<Real>(p->g.A).bytes);
+  bool stage_ok = false;
+  {  // the reduce phase's segment sums [nseg][channels per CTA], and the CTA's partials [ntiles][channels per CTA]
+    // staged behind them when that stays within the layout the other phases need anyway (or 64 KB)
+    const int nred = std::max(1, p->nsm - 1);
+    const size_t jc = (size_t)(B + nred - 1) / nred;
+    const size_t seg_bytes = (size_t)p->fwd_nseg * jc * sizeof(double2);
+    smem = std::max(smem, seg_bytes);
+    const size_t staged = seg_bytes + (size_t)p->g.ntiles * jc * 2 * sizeof(Real);
+    if (staged <= std::max(smem, (size_t)65536) && staged <= SMEM_DYN_MAX) {
+      stage_ok = true;
+      smem = std::max(smem, staged);
+    }
+  }
   if (smem > SMEM_DYN_MAX) return fail(NF_ERR_STATE, "persistent loop: shared memory layout does not fit");
   if (ct_adjoint_on)
     if (int rc = ct_part_buffer(p)) return rc;
@@ -5004,6 +5059,7 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   la.fold = p->loop_fold;
   la.warp_bytes = wb;
   la.kwords = bitmap ? (int)kwords : 0;
+  la.stage_ok = stage_ok ? 1 : 0;
   if (int rc = loop_profile_buffer(p, K, la)) return rc;
   FwdArgs<Real> fa = fwd_args<Real>(p, s_a, 0, B, true);
   AdjArgs<Real> aa = adj_args<Real>(p, nullptr, 0, s_a, s_b, eta_over_b, alpha, true);
@@ -5017,7 +5073,9 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
                  "B=%d, K=%d, ctpart %p (%zu B, pmax %d)\n", ct ? "CTA-tile" : "warp-unit",
                  ct_adjoint_on ? "CTA-tile" : "warp-unit", nsm, nw, smem, B, K, p->d_ctpart, p->ctpart_bytes,
                  ct_pmax(p));
-  void* args[] = {&la, &fa, &aa, &ca};
+  CtArgs cf = ca;  // forward ranges: the sorting CTA (the last) gets loop_sort_disc % less than an equal share
+  cf.Wd = ca.W + (long long)((double)ca.W / nsm * p->loop_sort_disc / 100.0);
+  void* args[] = {&la, &fa, &aa, &ca, &cf};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nsm), dim3(nw * 32), args, smem, st));
   p->loop_threads = nw * 32;
   p->launches += 1;
@@ -5126,6 +5184,7 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   if (const char* e = std::getenv("NFGPU_TAIL")) p->tail_split = std::atoi(e) != 0;
   if (const char* e = std::getenv("NFGPU_WAVE_FIT")) p->wave_fit = std::atoi(e);
   if (const char* e = std::getenv("NFGPU_LOOP_WAVE_FIT")) p->loop_wave_fit = std::atoi(e);
+  if (const char* e = std::getenv("NFGPU_SORT_DISC")) p->loop_sort_disc = std::max(0.0, std::min(90.0, std::atof(e)));
   if (const char* e = std::getenv("NFGPU_FIT_MIN_WAVES")) p->fit_min_waves = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("NFGPU_TAIL_FACTOR")) p->tail_factor = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("NFGPU_TAIL_WAVES")) p->tail_waves = std::max(0.0, std::atof(e));

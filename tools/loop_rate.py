@@ -80,7 +80,7 @@ if os.environ.get("NFGPU_LOOP_PROFILE"):
         t = np.frombuffer(buf, dtype=np.uint64)[: K * 12].reshape(K, 12).astype(np.float64)[K // 4:]
         tiny = not t[:, 6:].any()
         names = (["fwd", "bar0", "sums+adj+prox", "bar1", "stats"] if tiny else
-                 ["fwd", "bar1", "red1 (+stats of k-1 on one CTA)", "bar2", "red2+resid (+next sort on one CTA)",
+                 ["fwd (next sort first on one CTA)", "bar1", "reduce+resid (stats of k-1 on one CTA)", "-", "-",
                   "bar3", "adj", "bar4"])
         last = 5 if tiny else 8
         d = np.diff(t[:, :last + 1], axis=1).mean(axis=0) / 1e3
