@@ -2948,28 +2948,38 @@ struct CtLayout {  // [mbarriers, counters | buffer 0 | buffer 1 | warp records 
   }
 };
 
+constexpr int CT_GMAX = 160;  // CTAs a CtArgs can describe (148 SMs on a B200)
 struct CtArgs {
-  long long W;   // ntiles * span: tile-major (tile, sorted channel) pairs of the launch window
-  long long Wd;  // W + the pairs the LAST CTA's range is short of an equal share (the persistent loop's forward: that
-                 // CTA sorts the next batch first; forward values do not depend on the split). W everywhere else.
-  int span;      // channels of the window
-  int G;         // CTAs (one per SM; the persistent loop's grid)
+  long long W;  // ntiles * span: tile-major (tile, sorted channel) pairs of the launch window (< 2^31)
+  int span;     // channels of the window
+  int G;        // CTAs (one per SM; the persistent loop's grid)
+  // CTA b owns pairs [bnd[b], bnd[b + 1]) (bnd[0] = 0, bnd[G] = W; empty ranges only at the end). Equal ranges leave
+  // the CTAs whose range cuts one more tile behind the others (a piece has a fixed cost: table wait, record start-up,
+  // partial combine), so ct_args places the cuts to minimise the largest pairs + cost * pieces instead. Forward values
+  // do not depend on the cuts; the adjoint's chunk sums do, and nf_adjoint_prox and the persistent loop build the
+  // same CtArgs.
+  int bnd[CT_GMAX + 1];
 };
-// the CTA's range [r0, r1) of pairs: its first tile and piece count (the only 64-bit divisions, once per phase)
+// the CTA's range [r0, r1) of pairs: its first tile and piece count
 struct CtRange {
   long long r0, r1;
   int t0, np;
 };
 __device__ __forceinline__ CtRange ct_range(const CtArgs& c, int b) {
   CtRange r;
-  r.r0 = min((long long)b * c.Wd / c.G, c.W);
-  r.r1 = min((long long)(b + 1) * c.Wd / c.G, c.W);
+  r.r0 = c.bnd[b];
+  r.r1 = c.bnd[b + 1];
   r.t0 = (int)(r.r0 / c.span);
   r.np = r.r1 > r.r0 ? (int)((r.r1 - 1) / c.span) - r.t0 + 1 : 0;
   return r;
 }
-// the CTA whose range holds pair u (equal shares: Wd == W)
-__device__ __forceinline__ int ct_cta_of(const CtArgs& c, long long u) { return (int)(((u + 1) * c.G - 1) / c.W); }
+// the first and last of the CTAs whose ranges share `tile`, from CTA b, one of them
+__device__ __forceinline__ void ct_sharers(const CtArgs& c, int tile, int b, int& first, int& last) {
+  const long long u0 = (long long)tile * c.span, u1 = u0 + c.span;
+  first = last = b;
+  while (first > 0 && c.bnd[first] > u0) --first;
+  while (last + 1 < c.G && c.bnd[last + 1] < u1) ++last;
+}
 // piece i of the range: tile and window-relative channels [ja, jb)
 __device__ __forceinline__ void ct_piece(const CtArgs& c, const CtRange& r, int i, int& tile, int& ja, int& jb) {
   tile = r.t0 + i;
@@ -3429,8 +3439,8 @@ __device__ __forceinline__ void ct_adjoint(const AdjArgs<Real>& a, const CtArgs&
       }
     }
     const QV<Real> sgr = make_v(Gr), sgi = make_v(Gi);
-    const long long u0 = (long long)tile * c.span;
-    const int first = ct_cta_of(c, u0), lastc = ct_cta_of(c, u0 + c.span - 1);
+    int first, lastc;
+    ct_sharers(c, tile, (int)blockIdx.x, first, lastc);
     NF_CHECK(tile >= 0 && tile < g.ntiles && first <= (int)blockIdx.x && (int)blockIdx.x <= lastc && lastc < c.G,
              "tile %d first %d last %d b %d\n", tile, first, lastc, (int)blockIdx.x);
     adj_epilogue<Real, PROX, LOOP>(a, tile, (int)blockIdx.x - first, lastc - first + 1, L, sgr, sgi, s_in, s_out);
@@ -3748,7 +3758,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     const size_t pbase = (size_t)(k & 1) * B;  // the records of iteration k
     // ---- forward(k) on the records sorted during iteration k-1
     // the sorting CTA first writes the next iteration's records (the other parity: last read by adjoint(k-1)); its
-    // forward share is shorter by about that time (cf.Wd; warp units are fetched dynamically anyway)
+    // forward range is shorter by about that time (cf, ct_args kind 2; warp units are fetched dynamically anyway)
     if (sorter && k + 1 < la.K) loop_sort(la, k + 1, scan_sh, smem_raw);
     if constexpr (CT) {
       // the other phases reuse this shared memory (sort, reduce and adjoint scratch): fresh mbarriers every time
@@ -4233,6 +4243,14 @@ struct nf_plan {
   // themselves: both (Medium loop 126.4 -> 121.5 us with the forward). Env NFGPU_WAVE_FIT / NFGPU_LOOP_WAVE_FIT.
   int wave_fit = 2;
   int loop_wave_fit = 3;
+  double ct_cost_fwd = 80, ct_cost_adj = 150;  // fixed cost of a CTA-tile piece, in (tile, channel) pairs (ct_args;
+                                               // env NFGPU_CT_COST_FWD / NFGPU_CT_COST_ADJ, 0: equal ranges)
+  struct CtCache {
+    int span = -1, G = 0;
+    double cost = -1, disc = -1;
+    CtArgs args;
+  };
+  mutable CtCache ct_cache[3];
   double loop_sort_disc = 12.0;  // % of an equal forward share the loop's sorting CTA is spared (NFGPU_SORT_DISC)
   int fit_min_waves = 1;  // env NFGPU_FIT_MIN_WAVES
   double tail_waves = 1.0;                  // ... for about this many waves of warp slots (env NFGPU_TAIL_WAVES)
@@ -4498,7 +4516,7 @@ bool use_ct(const nf_plan* p, long long n) {
   // nf_adjoint_prox run: same bits)
   const size_t bytes = p->dtype == NF_C64 ? CtLayout<float>(p->g.A).bytes : CtLayout<double>(p->g.A).bytes;
   if (bytes > 232448 - 4096) return false;
-  if ((long long)p->g.ntiles * n < p->nsm) return false;
+  if ((long long)p->g.ntiles * n < p->nsm || (long long)p->g.ntiles * n > INT32_MAX || p->nsm > CT_GMAX) return false;
   return p->ct_mode == 2 || (long long)p->g.ntiles * n >= p->ct_min_pairs * p->nsm;
 }
 // ... and the CTA-tile adjoint (ct_adjoint) for a flat batch of B channels: a tile's pieces fit the chunk-partial
@@ -4522,12 +4540,68 @@ int ct_part_buffer(nf_plan* p) {
 bool ct_rxmajor(const nf_plan* p, int B) {
   return p->ct_rx && B <= p->fwd_chunk && use_ct(p, B) && use_ct_adj(p, B);
 }
-CtArgs ct_args(const nf_plan* p, int span) {
+// CtArgs of a window of `span` channels on G CTAs. kind 0: per-launch forward, 1: adjoint, 2: the persistent loop's
+// forward (its last CTA sorts the next batch first and gets `loop_sort_disc` % less). The cuts equalise
+// pairs + cost * pieces (cost in pairs; p->ct_cost_fwd / ct_cost_adj, 0: equal ranges) by bisection on the budget of a
+// greedy walk; cached per kind (a plan's batches mostly repeat one span).
+CtArgs ct_args(const nf_plan* p, int span, int kind, int G) {
+  nf_plan::CtCache& cc = p->ct_cache[kind];
+  const double cost = kind == 1 ? p->ct_cost_adj : p->ct_cost_fwd, disc = kind == 2 ? p->loop_sort_disc / 100.0 : 0.0;
+  if (cc.span == span && cc.G == G && cc.cost == cost && cc.disc == disc) return cc.args;
   CtArgs c;
   c.W = (long long)p->g.ntiles * span;
-  c.Wd = c.W;
   c.span = span;
-  c.G = p->nsm;
+  c.G = G;
+  for (int i = 0; i <= CT_GMAX; ++i) c.bnd[i] = (int)std::min<long long>(c.W, (long long)std::min(i, G) * c.W / G);
+  const int pmax = ct_pmax(p), shmax = p->adj_ch_cap;
+  std::vector<long long> bnd(G + 1, 0);
+  // greedy walk with budget C per CTA: every piece costs `cost`, a piece is started only with room for `minp` pairs
+  const double minp = CT_WARPS;
+  auto walk = [&](double C) {
+    long long u = 0;
+    for (int i = 0; i < G; ++i) {
+      bnd[i] = u;
+      double budget = i == G - 1 ? C * (1.0 - disc) : C;
+      while (u < c.W && budget >= cost + minp) {
+        const long long rem = span - u % span;
+        const long long take = std::min<long long>(rem, (long long)(budget - cost));
+        u += take;
+        budget -= cost + (double)take;
+        if (take < rem) break;
+      }
+    }
+    bnd[G] = u;
+    return u >= c.W;
+  };
+  bool ok = G > 1 && (cost > 0 || disc > 0) && c.W / G > 4 * (long long)(cost + minp);
+  if (ok) {
+    double lo = (double)c.W / G, hi = 2.0 * ((double)c.W / G + cost * (pmax + 1)) / (1.0 - disc);
+    ok = walk(hi);
+    for (int it = 0; ok && it < 50 && hi - lo > 0.5; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (walk(mid)) hi = mid; else lo = mid;
+    }
+    if (ok) {
+      walk(hi);
+      bnd[G] = c.W;
+      std::vector<int> share(p->g.ntiles, 0);
+      for (int i = 0; ok && i < G; ++i) {  // within the parked-sum slots and the chunk-partial buffer
+        const long long a = bnd[i], b = bnd[i + 1];
+        if (b <= a) continue;  // the last CTAs may be left without pairs
+        const int t0 = (int)(a / span), t1 = (int)((b - 1) / span);
+        if (t1 - t0 + 1 > pmax) ok = false;
+        for (int t = t0; t <= t1; ++t)
+          if (++share[t] > shmax) ok = false;
+      }
+    }
+    if (ok)
+      for (int i = 1; i <= G; ++i) c.bnd[i] = (int)bnd[i];
+  }
+  cc.span = span;
+  cc.G = G;
+  cc.cost = cost;
+  cc.disc = disc;
+  cc.args = c;
   return c;
 }
 
@@ -4597,7 +4671,7 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
       auto kct = p->exact ? fwd_ct_kernel<Real, true> : fwd_ct_kernel<Real, false>;
       const size_t smc = CtLayout<Real>(p->g.A).bytes;
       CUDA_TRY(ensure_smem((const void*)kct, smc));
-      CUDA_TRY(launch_k(p->use_pdl, kct, dim3(p->nsm), dim3(CT_WARPS * 32), smc, st, a, ct_args(p, span)));
+      CUDA_TRY(launch_k(p->use_pdl, kct, dim3(p->nsm), dim3(CT_WARPS * 32), smc, st, a, ct_args(p, span, 0, p->nsm)));
     } else {
       const long long units = (long long)a.t1 * a.Q + (long long)(p->g.ntiles - a.t1) * a.Q2;
       CUDA_TRY(launch_k(p->use_pdl, kern, dim3((unsigned)((units + FWD_WARPS - 1) / FWD_WARPS)),
@@ -4798,7 +4872,7 @@ int launch_adjoint(nf_plan* p, const void* r, const void* ymeas, void* gout, dou
     auto kct = p->exact ? adj_ct_kernel<Real, PROX, true> : adj_ct_kernel<Real, PROX, false>;
     const size_t smc = CtLayout<Real>(p->g.A).bytes;
     CUDA_TRY(ensure_smem((const void*)kct, smc));
-    CUDA_TRY(launch_k(p->use_pdl, kct, dim3(p->nsm), dim3(CT_WARPS * 32), smc, st, a, ct_args(p, p->B),
+    CUDA_TRY(launch_k(p->use_pdl, kct, dim3(p->nsm), dim3(CT_WARPS * 32), smc, st, a, ct_args(p, p->B, 1, p->nsm),
                       (Real*)p->d_ctpart, ct_pmax(p)));
   } else {
     const size_t sm = adj_smem(p);
@@ -5064,8 +5138,7 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   FwdArgs<Real> fa = fwd_args<Real>(p, s_a, 0, B, true);
   AdjArgs<Real> aa = adj_args<Real>(p, nullptr, 0, s_a, s_b, eta_over_b, alpha, true);
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
-  CtArgs ca = ct_args(p, B);
-  ca.G = nsm;
+  CtArgs ca = ct_args(p, B, 1, nsm);
   la.ctpart = p->d_ctpart;
   la.ctpmax = ct_pmax(p);
   if (std::getenv("NFGPU_VERBOSE"))
@@ -5073,8 +5146,7 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
                  "B=%d, K=%d, ctpart %p (%zu B, pmax %d)\n", ct ? "CTA-tile" : "warp-unit",
                  ct_adjoint_on ? "CTA-tile" : "warp-unit", nsm, nw, smem, B, K, p->d_ctpart, p->ctpart_bytes,
                  ct_pmax(p));
-  CtArgs cf = ca;  // forward ranges: the sorting CTA (the last) gets loop_sort_disc % less than an equal share
-  cf.Wd = ca.W + (long long)((double)ca.W / nsm * p->loop_sort_disc / 100.0);
+  CtArgs cf = ct_args(p, B, 2, nsm);  // forward ranges: the sorting CTA (the last) gets loop_sort_disc % less
   void* args[] = {&la, &fa, &aa, &ca, &cf};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nsm), dim3(nw * 32), args, smem, st));
   p->loop_threads = nw * 32;
@@ -5184,6 +5256,8 @@ int nf_plan_create(const double* tx_xyz, int n_tx, const double* rx_xyz, int n_r
   if (const char* e = std::getenv("NFGPU_TAIL")) p->tail_split = std::atoi(e) != 0;
   if (const char* e = std::getenv("NFGPU_WAVE_FIT")) p->wave_fit = std::atoi(e);
   if (const char* e = std::getenv("NFGPU_LOOP_WAVE_FIT")) p->loop_wave_fit = std::atoi(e);
+  if (const char* e = std::getenv("NFGPU_CT_COST_FWD")) p->ct_cost_fwd = std::max(0.0, std::atof(e));
+  if (const char* e = std::getenv("NFGPU_CT_COST_ADJ")) p->ct_cost_adj = std::max(0.0, std::atof(e));
   if (const char* e = std::getenv("NFGPU_SORT_DISC")) p->loop_sort_disc = std::max(0.0, std::min(90.0, std::atof(e)));
   if (const char* e = std::getenv("NFGPU_FIT_MIN_WAVES")) p->fit_min_waves = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("NFGPU_TAIL_FACTOR")) p->tail_factor = std::max(1, std::atoi(e));
