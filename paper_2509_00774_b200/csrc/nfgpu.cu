@@ -3507,6 +3507,8 @@ struct LoopArgs {
   int* sm;              // spgm_loop_kernel: sorted records [2 parities][B]
   int* spos;
   int* sf;
+  double2* yrec;        // [2 parities][B][2]: {p_f, y_meas[m_j]} of sorted position j
+  int ymeas_f64;        // y_meas is complex128
   ChanRec* crec;
   double2* tmp;
   double* dpart;
@@ -3516,7 +3518,7 @@ struct LoopArgs {
   double eta_over_b, alpha;  // tiny_loop_kernel's prox (spgm_loop_kernel takes them from its AdjArgs)
   double* rec;          // [K][LOOP_REC]
   int* state;           // {iterations, reason: 0 max_iters / 1 tolerance / 2 time budget, stop flag}
-  unsigned* bar;        // grid barrier {arrivals, generation}
+  unsigned* bar;        // grid barrier arrival counter (grid_sync)
   int stage_ok;         // the reduce phase stages a CTA's partials [ntiles][channels per CTA] in shared memory
   int kwords;           // 32-bit words of the key-space bitmap of the P0 rank sort (0: pairwise ranks)
   int* ctr;             // work-unit counters {forward, adjoint}: warps fetch units past the first TW dynamically
@@ -3560,25 +3562,21 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// sense-reversing grid barrier (all CTAs co-resident: cooperative launch). Thread 0 arrives with an acq_rel
-// atomic (its release is cumulative over the CTA's writes ordered before it by __syncthreads), the last arrival
-// publishes the next generation with a release store, the others poll it with acquire loads.
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* a, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
-  return old;
+// grid barrier (all CTAs co-resident: cooperative launch) on one monotonic arrival counter, zeroed by the host before
+// every launch: thread 0 arrives with a release reduction (cumulative over the CTA's writes ordered before it by
+// __syncthreads) and polls the counter with acquire loads until the n-th barrier's G arrivals are in. Every CTA
+// counts its own barriers (`nbar`), so a barrier costs the reduction's trip to L2 and one poll, with no generation
+// word to read first and no last arrival to publish it.
+__device__ __forceinline__ void red_release_add_u32(unsigned* a, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& nbar) {
   __syncthreads();
+  ++nbar;
   if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire_u32(bar + 1);
-    if (atom_add_acq_rel(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;  // ordered before the release below; nobody touches it until the new generation is seen
-      st_release_u32(bar + 1, gen + 1);
-    } else {
-      int spins = 0;
-      while (ld_acquire_u32(bar + 1) == gen)
-        if (++spins > 64) __nanosleep(32);
+    red_release_add_u32(bar, 1u);
+    const unsigned target = nbar * gridDim.x;
+    while ((int)(ld_acquire_u32(bar) - target) < 0) {
     }
   }
   __syncthreads();
@@ -3657,6 +3655,18 @@ __device__ __forceinline__ void loop_sort(const LoopArgs& la, int k, int* scan_s
     q.pk = c.y | (c.z << 16);
     la.crec[base + j] = q;
     la.sf[base + j] = c.x;
+    // what the residual record of position j needs (the reduce phase then has no dependent loads)
+    const int m = c.z + la.km.R * (c.y + la.km.T * c.x);
+    double yr, yi;
+    if (la.ymeas_f64) {
+      yr = reinterpret_cast<const double*>(la.ymeas)[2 * (size_t)m];
+      yi = reinterpret_cast<const double*>(la.ymeas)[2 * (size_t)m + 1];
+    } else {
+      yr = (double)reinterpret_cast<const float*>(la.ymeas)[2 * (size_t)m];
+      yi = (double)reinterpret_cast<const float*>(la.ymeas)[2 * (size_t)m + 1];
+    }
+    la.yrec[2 * (base + j)] = make_double2(la.pulse[2 * c.x], la.pulse[2 * c.x + 1]);
+    la.yrec[2 * (base + j) + 1] = make_double2(yr, yi);
   }
   __syncthreads();
 }
@@ -3738,6 +3748,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
   const int nau = aa.t1 * aa.CH + (g.ntiles - aa.t1) * aa.CH2;
   unsigned char* wbase = smem_raw + (size_t)w * la.warp_bytes;
   const unsigned long long t0 = globaltimer();
+  unsigned nbar = 0;  // grid barriers passed (grid_sync)
   int done = 0, reason = 0, k = 0;
 #define LOOP_STAMP(i) \
   if (la.prof && blockIdx.x == 0 && threadIdx.x == 0) la.prof[(size_t)k * LOOP_PROF + (i)] = globaltimer() - t0
@@ -3750,7 +3761,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     la.ctr[0] = 0;
     la.ctr[1] = 0;
   }
-  grid_sync(la.bar);
+  grid_sync(la.bar, nbar);
   for (; k < la.K; ++k) {
     LOOP_STAMP(0);
     const Real* s_in = reinterpret_cast<const Real*>((k & 1) ? la.s_b : la.s_a);
@@ -3774,7 +3785,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
       __syncthreads();
       if (threadIdx.x == 0) la.prof[(size_t)la.K * LOOP_PROF + ((size_t)k * 2) * LOOP_PROF_CTA + blockIdx.x] = globaltimer() - t0;
     }
-    grid_sync(la.bar);  // B1
+    grid_sync(la.bar, nbar);  // B1
     LOOP_STAMP(2);
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // every warp is past its forward fetches of k, adjoint fetches of k-1
       la.ctr[0] = 0;
@@ -3794,16 +3805,13 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
       const int JC = (B + nred - 1) / nred;
       const int j0 = blockIdx.x * JC, jn = min(JC, B - j0);
       double2* seg_sh = reinterpret_cast<double2*>(smem_raw);  // [nseg][JC]
-      int f = 0, m = 0;
       double pre = 0, pim = 0, ymr = 0, ymi = 0;
       if ((int)threadIdx.x < jn) {  // the finishing threads' record loads go first
-        const Real* ym = reinterpret_cast<const Real*>(la.ymeas);
-        f = la.sf[pbase + j0 + threadIdx.x];
-        m = la.sm[pbase + j0 + threadIdx.x];
-        pre = la.pulse[2 * f];
-        pim = la.pulse[2 * f + 1];
-        ymr = (double)ym[2 * (size_t)m];
-        ymi = (double)ym[2 * (size_t)m + 1];
+        const double2 pf = la.yrec[2 * (pbase + j0 + threadIdx.x)], ym = la.yrec[2 * (pbase + j0 + threadIdx.x) + 1];
+        pre = pf.x;
+        pim = pf.y;
+        ymr = ym.x;
+        ymi = ym.y;
       }
       // the CTA's partials [ntiles][jn] first land in shared memory (every thread loads, one L2 latency) when they fit
       R2<Real>* stage = reinterpret_cast<R2<Real>*>(seg_sh + (size_t)la.nseg * JC);
@@ -3863,7 +3871,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
     LOOP_STAMP(3);
     LOOP_STAMP(4);
     LOOP_STAMP(5);
-    grid_sync(la.bar);  // B3
+    grid_sync(la.bar, nbar);  // B3
     LOOP_STAMP(6);
     if (k > 0) {  // iteration k-1 was the last (every CTA reads the same flag): k iterations ran
       const int stop = *(volatile int*)(la.state + 2);
@@ -3893,7 +3901,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
         la.prof[(size_t)la.K * LOOP_PROF + (size_t)la.K * 2 * LOOP_PROF_CTA + blockIdx.x] = smid;
       }
     }
-    grid_sync(la.bar);  // B4
+    grid_sync(la.bar, nbar);  // B4
     LOOP_STAMP(8);
     done = k + 1;
   }
@@ -4005,6 +4013,7 @@ __global__ void __launch_bounds__(256, 1) tiny_loop_kernel(LoopArgs la, TinyArgs
   const long long nvox = (long long)ta.nx * ta.ny * ta.nzs;
   const Real* ym = reinterpret_cast<const Real*>(la.ymeas);
   const unsigned long long t0 = globaltimer();
+  unsigned nbar = 0;  // grid barriers passed (grid_sync)
   int done = 0, reason = 0;
   if (loop_skip(la)) return;
 #define TINY_STAMP(i) \
@@ -4041,7 +4050,7 @@ __global__ void __launch_bounds__(256, 1) tiny_loop_kernel(LoopArgs la, TinyArgs
       if (threadIdx.x < jc && j < B) ta.part[(size_t)vb * B + j] = v[0];
     }
     TINY_STAMP(1);
-    grid_sync(la.bar);
+    grid_sync(la.bar, nbar);
     TINY_STAMP(2);
     if (k > 0 && *(volatile int*)(la.state + 2)) {
       reason = 2;
@@ -4140,7 +4149,7 @@ __global__ void __launch_bounds__(256, 1) tiny_loop_kernel(LoopArgs la, TinyArgs
       __syncthreads();
     }
     TINY_STAMP(3);
-    grid_sync(la.bar);
+    grid_sync(la.bar, nbar);
     TINY_STAMP(4);
     // ---- PD: statistics (fixed order, every CTA), record, termination
     if (nvb <= 256 && B <= 1024) {  // one warp: lane-strided sums, then a shuffle tree (no block barriers)
@@ -4306,7 +4315,7 @@ struct nf_plan {
   void* comm_peer[PEER_MAX] = {};
   unsigned long long* d_epoch = nullptr;
   int* d_comm_err = nullptr;
-  unsigned* d_loopbar = nullptr;  // persistent SPGM loop: grid barrier {arrivals, generation} (zero between launches)
+  unsigned* d_loopbar = nullptr;  // persistent SPGM loop: grid barrier arrival counter (zeroed before every launch), unit counters
   int loop_threads = 0;           // ... CTA size chosen on first use (0: not yet)
   unsigned long long* d_loop_prof = nullptr;  // ... phase time stamps (NFGPU_LOOP_PROFILE)
   void* d_loop_priv = nullptr;  // spgm_loop_kernel: sorted records of two iterations
@@ -5001,6 +5010,7 @@ int launch_tiny_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   auto kern = tiny_loop_kernel<Real>;
   CUDA_TRY(ensure_smem((const void*)kern, smem));
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
+  CUDA_TRY(cudaMemsetAsync(p->d_loopbar, 0, sizeof(unsigned), st));  // the grid barrier's arrival counter
   CUDA_TRY(cudaMemsetAsync(ta.vbcnt, 0, b_cnt, st));
   if (std::getenv("NFGPU_VERBOSE"))
     std::fprintf(stderr, "nf_spgm_loop: tiny_loop_kernel, %d CTAs x 256 threads, B=%d, K=%d\n", nsm, B, K);
@@ -5099,9 +5109,10 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   la.kd = p->d_kd;
   la.pulse = p->d_pulse;
   la.ymeas = ymeas;
+  la.ymeas_f64 = std::is_same<Real, double>::value ? 1 : 0;
   {  // sorted channel records [2 parities][B]
     const size_t n = (size_t)2 * B;
-    const size_t need = n * (sizeof(ChanRec) + 3 * sizeof(int));
+    const size_t need = n * (sizeof(ChanRec) + 3 * sizeof(int) + 2 * sizeof(double2)) + 16;
     if (need > p->loop_priv_bytes) {
       cudaFree(p->d_loop_priv);
       p->d_loop_priv = nullptr;
@@ -5110,6 +5121,8 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
       p->loop_priv_bytes = need;
     }
     char* b = (char*)p->d_loop_priv;
+    la.yrec = (double2*)b;
+    b += n * 2 * sizeof(double2);
     la.crec = (ChanRec*)b;
     b += n * sizeof(ChanRec);
     la.sm = (int*)b;
@@ -5138,6 +5151,7 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   FwdArgs<Real> fa = fwd_args<Real>(p, s_a, 0, B, true);
   AdjArgs<Real> aa = adj_args<Real>(p, nullptr, 0, s_a, s_b, eta_over_b, alpha, true);
   CUDA_TRY(cudaMemsetAsync(state, 0, 3 * sizeof(int), st));
+  CUDA_TRY(cudaMemsetAsync(p->d_loopbar, 0, sizeof(unsigned), st));  // the grid barrier's arrival counter
   CtArgs ca = ct_args(p, B, 1, nsm);
   la.ctpart = p->d_ctpart;
   la.ctpmax = ct_pmax(p);
