@@ -2953,6 +2953,7 @@ struct CtArgs {
   long long W;  // ntiles * span: tile-major (tile, sorted channel) pairs of the launch window (< 2^31)
   int span;     // channels of the window
   int G;        // CTAs (one per SM; the persistent loop's grid)
+  int ns;       // forward: pieces whose iterate values fit the staging area behind the layout (ct_stage_bytes)
   // CTA b owns pairs [bnd[b], bnd[b + 1]) (bnd[0] = 0, bnd[G] = W; empty ranges only at the end). Equal ranges leave
   // the CTAs whose range cuts one more tile behind the others (a piece has a fixed cost: table wait, record start-up,
   // partial combine), so ct_args places the cuts to minimise the largest pairs + cost * pieces instead. Forward values
@@ -2962,15 +2963,15 @@ struct CtArgs {
 };
 // the CTA's range [r0, r1) of pairs: its first tile and piece count
 struct CtRange {
-  long long r0, r1;
+  int r0, r1;
   int t0, np;
 };
 __device__ __forceinline__ CtRange ct_range(const CtArgs& c, int b) {
   CtRange r;
   r.r0 = c.bnd[b];
   r.r1 = c.bnd[b + 1];
-  r.t0 = (int)(r.r0 / c.span);
-  r.np = r.r1 > r.r0 ? (int)((r.r1 - 1) / c.span) - r.t0 + 1 : 0;
+  r.t0 = (int)((unsigned)r.r0 / (unsigned)c.span);
+  r.np = r.r1 > r.r0 ? (int)((unsigned)(r.r1 - 1) / (unsigned)c.span) - r.t0 + 1 : 0;
   return r;
 }
 // the first and last of the CTAs whose ranges share `tile`, from CTA b, one of them
@@ -2983,14 +2984,14 @@ __device__ __forceinline__ void ct_sharers(const CtArgs& c, int tile, int b, int
 // piece i of the range: tile and window-relative channels [ja, jb)
 __device__ __forceinline__ void ct_piece(const CtArgs& c, const CtRange& r, int i, int& tile, int& ja, int& jb) {
   tile = r.t0 + i;
-  const long long base = (long long)tile * c.span;
-  ja = (int)max(r.r0 - base, 0LL);
-  jb = (int)min(r.r1 - base, (long long)c.span);
+  const int base = tile * c.span;  // W < 2^31
+  ja = max(r.r0 - base, 0);
+  jb = min(r.r1 - base, c.span);
 }
 // warp w's slice of the piece's channels
 __device__ __forceinline__ void ct_slice(int ja, int jb, int w, int& c0, int& c1) {
-  c0 = ja + (int)(((long long)(jb - ja) * w) / CT_WARPS);
-  c1 = ja + (int)(((long long)(jb - ja) * (w + 1)) / CT_WARPS);
+  c0 = ja + (int)(((unsigned)(jb - ja) * (unsigned)w) / CT_WARPS);  // spans stay far below 2^27
+  c1 = ja + (int)(((unsigned)(jb - ja) * (unsigned)(w + 1)) / CT_WARPS);
 }
 
 // Fill buffer `buf` with tile's table rows (bulk copy, lane 0), its D0 row and (forward) its iterate values in the
@@ -3002,20 +3003,22 @@ __device__ __forceinline__ void ct_produce_table(const Geo& g, const Real* __res
                                                  int tile, int L) {
   const CtLayout<Real> lay(g.A);
   double* d0 = reinterpret_cast<double*>(buf + lay.tab_bytes);
+  // (an even antenna count keeps the tile's D0 row 16-byte aligned and sized: it rides a second bulk copy, and the
+  // producing warp waits for no load)
+  const bool d0_bulk = (g.A & 1) == 0;
   if (L == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the old piece before the copy
-    mbar_expect(full, (uint32_t)lay.tab_bytes);
+    const uint32_t d0_bytes = d0_bulk ? (uint32_t)g.A * (uint32_t)sizeof(double) : 0u;
+    mbar_expect(full, (uint32_t)lay.tab_bytes + d0_bytes);
     bulk_g2s(buf, tab + (size_t)tile * g.A * TABW, (uint32_t)lay.tab_bytes, full);
+    if (d0_bulk) bulk_g2s(d0, D0 + (size_t)tile * g.A, d0_bytes, full);
   }
-  for (int i = L; i < g.A; i += 32) d0[i] = D0[(size_t)tile * g.A + i];
+  if (!d0_bulk)
+    for (int i = L; i < g.A; i += 32) d0[i] = D0[(size_t)tile * g.A + i];
 }
+// the iterate values of `tile` in the lane-quad layout of ldv, into ss[2 * TILE]
 template <typename Real, bool LOOP>
-__device__ __forceinline__ void ct_produce(const Geo& g, const Real* __restrict__ tab, const double* __restrict__ D0,
-                                           const Real* __restrict__ sv, unsigned char* buf, uint64_t* full, int tile,
-                                           int L) {
-  ct_produce_table<Real>(g, tab, D0, buf, full, tile, L);
-  const CtLayout<Real> lay(g.A);
-  Real* ss = reinterpret_cast<Real*>(buf + lay.tab_bytes + (size_t)d0_slots(g.A) * sizeof(double));
+__device__ __forceinline__ void ct_stage_s(const Geo& g, const Real* __restrict__ sv, Real* ss, int tile, int L) {
   int tx, ty, tz;
   tile_coords(g, tile, tx, ty, tz);
   int x0, y, z;
@@ -3033,6 +3036,17 @@ __device__ __forceinline__ void ct_produce(const Geo& g, const Real* __restrict_
     const int e = (v / QD) * 32 * QD + L * QD + v % QD;
     ss[e] = re;
     ss[TILE + e] = im;
+  }
+}
+template <typename Real, bool LOOP>
+__device__ __forceinline__ void ct_produce(const Geo& g, const Real* __restrict__ tab, const double* __restrict__ D0,
+                                           const Real* __restrict__ sv, unsigned char* buf, uint64_t* full, int tile,
+                                           int L, bool with_s) {
+  ct_produce_table<Real>(g, tab, D0, buf, full, tile, L);
+  if (with_s) {
+    const CtLayout<Real> lay(g.A);
+    ct_stage_s<Real, LOOP>(g, sv, reinterpret_cast<Real*>(buf + lay.tab_bytes + (size_t)d0_slots(g.A) * sizeof(double)),
+                           tile, L);
   }
   mbar_arrive(full);
 }
@@ -3210,11 +3224,22 @@ __device__ __forceinline__ void ct_forward(const FwdArgs<Real>& a, const CtArgs&
   const CtRange rg = ct_range(c, blockIdx.x);
   const int np = rg.np;
   int tile, ja, jb;
+  // When the staging area behind the layout holds every piece's iterate values (c.ns pieces), the warps load them
+  // side by side now and a table refill is two bulk copies: the warp that issues it waits for no load.
+  const bool sst = np <= c.ns;
+  Real* ss_all = reinterpret_cast<Real*>(smem + lay.bytes);
   if (w == 0)
     for (int q = 0; q < 2 && q < np; ++q) {
       ct_piece(c, rg, q, tile, ja, jb);
-      ct_produce<Real, LOOP>(g, a.tab, a.D0, sv, smem + lay.off_buf + q * lay.buf_bytes, full + q, tile, L);
+      ct_produce<Real, LOOP>(g, a.tab, a.D0, sv, smem + lay.off_buf + q * lay.buf_bytes, full + q, tile, L, !sst);
     }
+  if (sst) {
+    for (int q = w; q < np; q += CT_WARPS) {
+      ct_piece(c, rg, q, tile, ja, jb);
+      ct_stage_s<Real, LOOP>(g, sv, ss_all + (size_t)q * 2 * TILE, tile, L);
+    }
+    __syncthreads();
+  }
   if (pdl) pdl_wait();
   WarpSmem<Real> ws;
   unsigned char* wr = smem + lay.off_warp + (size_t)w * lay.warp_bytes;
@@ -3245,7 +3270,8 @@ __device__ __forceinline__ void ct_forward(const FwdArgs<Real>& a, const CtArgs&
     mbar_wait(full + b, (ph >> b) & 1u);
     ph ^= 1u << b;
     ws.d0 = reinterpret_cast<double*>(buf + lay.tab_bytes);
-    const Real* s_s = reinterpret_cast<const Real*>(buf + lay.tab_bytes + (size_t)d0_slots(g.A) * sizeof(double));
+    const Real* s_s = sst ? ss_all + (size_t)q * 2 * TILE
+                          : reinterpret_cast<const Real*>(buf + lay.tab_bytes + (size_t)d0_slots(g.A) * sizeof(double));
     R2<Real>* outl = reinterpret_cast<R2<Real>*>(a.part) + (size_t)tile * c.span - a.w0 + L;
     if (c0 < c1)
       ct_fwd_slice<Real, EXACT>(g, reinterpret_cast<const Real*>(buf), s_s, ws, tb, crec, a.w0 + c0, a.w0 + c1,
@@ -3254,7 +3280,7 @@ __device__ __forceinline__ void ct_forward(const FwdArgs<Real>& a, const CtArgs&
       nxt = crec[a.w0 + pn0 + L];
     if (ct_last(cnt + b, L) && q + 2 < np) {
       ct_piece(c, rg, q + 2, tile, ja, jb);
-      ct_produce<Real, LOOP>(g, a.tab, a.D0, sv, buf, full + b, tile, L);
+      ct_produce<Real, LOOP>(g, a.tab, a.D0, sv, buf, full + b, tile, L, !sst);
     }
   }
 }
@@ -4535,6 +4561,16 @@ bool use_ct_adj(const nf_plan* p, long long B) {
   return (p->nsm + p->g.ntiles - 1) / p->g.ntiles + 1 <= p->adj_ch_cap;
 }
 int ct_pmax(const nf_plan* p) { return (p->g.ntiles + p->nsm - 1) / p->nsm + 2; }
+// forward: the pieces whose iterate values (2 * TILE Reals each) fit behind the layout, and the layout with them
+int ct_stage_pieces(const nf_plan* p) {
+  const size_t lay = p->dtype == NF_C64 ? CtLayout<float>(p->g.A).bytes : CtLayout<double>(p->g.A).bytes;
+  const size_t per = 2 * (size_t)TILE * real_size(p), room = 232448 - 4096 > lay ? 232448 - 4096 - lay : 0;
+  return (int)std::min<size_t>(ct_pmax(p), room / per);
+}
+size_t ct_fwd_smem(const nf_plan* p) {
+  const size_t lay = p->dtype == NF_C64 ? CtLayout<float>(p->g.A).bytes : CtLayout<double>(p->g.A).bytes;
+  return lay + (size_t)ct_stage_pieces(p) * 2 * TILE * real_size(p);
+}
 int ct_part_buffer(nf_plan* p) {
   const size_t need = (size_t)p->nsm * ct_pmax(p) * TILE * 2 * real_size(p);
   if (need <= p->ctpart_bytes) return NF_OK;
@@ -4561,6 +4597,7 @@ CtArgs ct_args(const nf_plan* p, int span, int kind, int G) {
   c.W = (long long)p->g.ntiles * span;
   c.span = span;
   c.G = G;
+  c.ns = kind == 1 ? 0 : ct_stage_pieces(p);
   for (int i = 0; i <= CT_GMAX; ++i) c.bnd[i] = (int)std::min<long long>(c.W, (long long)std::min(i, G) * c.W / G);
   const int pmax = ct_pmax(p), shmax = p->adj_ch_cap;
   std::vector<long long> bnd(G + 1, 0);
@@ -4678,7 +4715,7 @@ int launch_forward(nf_plan* p, const void* s, void* y, cudaStream_t st) {
     const FwdArgs<Real> a = fwd_args<Real>(p, s, w0, w1);
     if (use_ct(p, span)) {  // part[tile][j] is the same either way (bit-identical per-(tile, channel) values)
       auto kct = p->exact ? fwd_ct_kernel<Real, true> : fwd_ct_kernel<Real, false>;
-      const size_t smc = CtLayout<Real>(p->g.A).bytes;
+      const size_t smc = ct_fwd_smem(p);
       CUDA_TRY(ensure_smem((const void*)kct, smc));
       CUDA_TRY(launch_k(p->use_pdl, kct, dim3(p->nsm), dim3(CT_WARPS * 32), smc, st, a, ct_args(p, span, 0, p->nsm)));
     } else {
@@ -5064,7 +5101,7 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
     kern = pick(false, false);
   }
   const bool ct_adjoint_on = cta;
-  if (ct) smem = std::max(smem, CtLayout<Real>(p->g.A).bytes);
+  if (ct) smem = std::max(smem, ct_fwd_smem(p));
   bool stage_ok = false;
   {  // the reduce phase's segment sums [nseg][channels per CTA], and the CTA's partials [ntiles][channels per CTA]
     // staged behind them when that stays within the layout the other phases need anyway (or 64 KB)
