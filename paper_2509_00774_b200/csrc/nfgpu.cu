@@ -3844,15 +3844,31 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
       const bool staged = la.stage_ok != 0;
       if (staged) {
         const R2<Real>* src = reinterpret_cast<const R2<Real>*>(fa.part) + j0;
-        for (int it = threadIdx.x; it < g.ntiles * jn; it += blockDim.x) {
-          const int x = it / jn, jj = it - x * jn;
-          stage[it] = src[(size_t)x * B + jj];
+        const int total = g.ntiles * jn;
+        for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {  // 8 loads in flight per thread
+          R2<Real> v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int it = base + u * blockDim.x;
+            if (it < total) {
+              const int x = (int)((unsigned)it / (unsigned)jn), jj = it - x * jn;
+              v[u] = src[(size_t)x * B + jj];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int it = base + u * blockDim.x;
+            if (it < total) stage[it] = v[u];
+          }
         }
         __syncthreads();
       }
+      LOOP_STAMP(3);
       for (int it = threadIdx.x; it < la.nseg * jn; it += blockDim.x) {
         const int seg = it / jn, jj = it - seg * jn;
-        const int x0 = (int)(((long long)g.ntiles * seg) / la.nseg), x1 = (int)(((long long)g.ntiles * (seg + 1)) / la.nseg);
+        // (tiles * segments < 2^31: the same quotients as the 64-bit form of fwd_reduce1_kernel)
+        const int x0 = (int)((unsigned)(g.ntiles * seg) / (unsigned)la.nseg);
+        const int x1 = (int)((unsigned)(g.ntiles * (seg + 1)) / (unsigned)la.nseg);
         double sr = 0, si = 0;
         if (staged) {
 #pragma unroll 4
@@ -3873,6 +3889,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
         seg_sh[seg * JC + jj] = make_double2(sr, si);
       }
       __syncthreads();
+      LOOP_STAMP(4);
       if ((int)threadIdx.x < jn) {
         const int j = j0 + threadIdx.x;
         double sr = 0, si = 0;
@@ -3881,7 +3898,7 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
           sr += v.x;
           si += v.y;
         }
-        const double pr = pre / (4.0 * PI), pi_ = pim / (4.0 * PI);
+        const double pr = pre / (4.0 * PI), pi_ = pim / (4.0 * PI);  // (the quotients the per-launch kernels form)
         const Real yr = (Real)(pr * sr - pi_ * si), yi = (Real)(pr * si + pi_ * sr);
         double rr = (double)yr, ri = (double)yi;
         rr -= ymr;
@@ -3894,8 +3911,6 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
         reinterpret_cast<double*>(la.tmp)[(size_t)(k & 1) * B + j] = rr * rr + ri * ri;
       }
     }
-    LOOP_STAMP(3);
-    LOOP_STAMP(4);
     LOOP_STAMP(5);
     grid_sync(la.bar, nbar);  // B3
     LOOP_STAMP(6);

@@ -80,7 +80,7 @@ if os.environ.get("NFGPU_LOOP_PROFILE"):
         t = np.frombuffer(buf, dtype=np.uint64)[: K * 12].reshape(K, 12).astype(np.float64)[K // 4:]
         tiny = not t[:, 6:].any()
         names = (["fwd", "bar0", "sums+adj+prox", "bar1", "stats"] if tiny else
-                 ["fwd (next sort first on one CTA)", "bar1", "reduce+resid (stats of k-1 on one CTA)", "-", "-",
+                 ["fwd (next sort first on one CTA)", "bar1", "reduce: partials to shared (stats of k-1 on one CTA)", "reduce: segment sums", "reduce: level 2 + residual records",
                   "bar3", "adj", "bar4"])
         last = 5 if tiny else 8
         d = np.diff(t[:, :last + 1], axis=1).mean(axis=0) / 1e3
