@@ -1,3 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_loop.py -x -q 2>&1 | tail -2
-NFGPU_LOOP_PROFILE=1 timeout 120 python tools/loop_rate.py --workload medium --iters 400 2>&1 | tail -1 | grep -oE '"profile_us.*next_iter_gap": [0-9.]+'
-timeout 120 python tools/loop_rate.py --workload medium --iters 2000 2>&1 | tail -1 | grep -oE '"loop_us_per_iter": [0-9.]+|"graph_us_per_iter": [0-9.]+' | paste - -
+ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv --log-file gpurun_out/r02_launches_all.csv python bench.py --steps 20 --warmup 3 --no-extras --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo "launch list rc $?"
+wc -l gpurun_out/r02_launches_all.csv
