@@ -3505,20 +3505,20 @@ __global__ void __launch_bounds__(CT_WARPS * 32, 1) adj_ct_kernel(AdjArgs<Real> 
 //
 // spgm_loop_kernel runs K SPGM iterations (solver.py:281-310) of a flat batch in ONE cooperative launch, one CTA
 // per SM: the device-side loop for latency-bound configurations (BASELINE Small: 12 launches of ~3 us each per
-// iteration otherwise). Per iteration, between grid barriers:
-//   P0  one CTA draws the batch (index table row k, or the Feistel sampler), sorts its (key, position) keys by
-//       rank in shared memory (same order as the counting sort of nf_batch_prepare) and writes the sorted channel
-//       records of parity k & 1 -- during P3 of iteration k-1, beside CTA 0's level 2
-//   P1  forward: CTA-tile pieces (ct_forward) or warp units (fwd_unit, the body of fwd_kernel) -> part[tile][j]
-//   P2  level 1 of the forward reduce (fwd_reduce1_kernel's sums)
-//   P3  level 2 + residual records, per 256-channel group (fwd_reduce2_kernel + resid_kernel)
-//   P4  adjoint + prox: CTA-tile pieces (ct_adjoint) or warp units (adj_unit) -> s_out, per-tile statistics
-//   P5  one CTA reduces the statistics (stats_reduce_kernel's tree) during the next iteration's level 1, records
-//       them and tests the tolerance; a stop takes effect after that level's barrier (the forward of the
-//       iteration after the last one is discarded), and the last iteration's statistics follow the loop
+// iteration otherwise). Per iteration, three phases between three grid barriers:
+//   P1  forward(k): CTA-tile pieces (ct_forward) or warp units (fwd_unit, the body of fwd_kernel) -> part[tile][j].
+//       One CTA (the last, "sorter") first draws iteration k+1's batch (index table row, or the Feistel sampler), sorts
+//       its (key, position) keys by rank in shared memory (same order as the counting sort of nf_batch_prepare) and
+//       writes the sorted channel records of parity (k+1) & 1, with {p_f, y_meas[m_j]} per sorted position
+//   P2  both levels of the forward reduce and the residual records in one phase, per channel, on the other CTAs
+//       (fwd_reduce1_kernel's, fwd_reduce2_kernel's and resid_kernel's sums in their order); the sorter reduces the
+//       statistics of iteration k-1 (stats_reduce_kernel's tree), records them and tests the tolerance: a stop takes
+//       effect after this phase's barrier (the forward and reduce of the iteration after the last one are
+//       discarded), and the last iteration's statistics follow the loop
+//   P3  adjoint(k) + prox: CTA-tile pieces (ct_adjoint) or warp units (adj_unit) -> s_out, per-tile statistics
 // Every value is computed by the same code in the same order as the per-launch path, so the iterates are
 // bit-identical to nf_batch_prepare + nf_forward + nf_adjoint_prox (tested). The time budget is checked on the
-// device clock by CTA 0 and takes effect after the next barrier.
+// device clock by the CTA that records the statistics and takes effect after the next barrier.
 constexpr int LOOP_SORT_MAX = 4096;  // batches sorted in shared memory
 constexpr int LOOP_REC = 6;          // per iteration: the 4 statistics, device time (ns since launch), spare
 
