@@ -33,7 +33,7 @@ def _pair(scn, dtype, y, eta, alpha, s0=None, max_batch=None):
     return engs
 
 
-@pytest.mark.parametrize("ct", ["auto", "forced"])
+@pytest.mark.parametrize("ct", ["auto", "forced", "forward-only", "equal-ranges"])
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 @pytest.mark.parametrize("workload", ["small", "medium"])
 def test_loop_matches_per_launch_path_bitwise(workload, dtype, ct, no_tiny, monkeypatch):
@@ -41,6 +41,13 @@ def test_loop_matches_per_launch_path_bitwise(workload, dtype, ct, no_tiny, monk
     in both paths."""
     if ct == "forced":
         monkeypatch.setenv("NFGPU_CT", "2")
+    elif ct == "forward-only":  # CTA-tile forward beside the warp-unit adjoint
+        monkeypatch.setenv("NFGPU_CT", "2")
+        monkeypatch.setenv("NFGPU_CT_ADJ", "0")
+    elif ct == "equal-ranges":  # no cost-balanced cuts (ct_args)
+        monkeypatch.setenv("NFGPU_CT", "2")
+        monkeypatch.setenv("NFGPU_CT_COST_FWD", "0")
+        monkeypatch.setenv("NFGPU_CT_COST_ADJ", "0")
     w = configs.WORKLOADS[workload]()
     scn = w.scenario
     rng = np.random.default_rng(3)

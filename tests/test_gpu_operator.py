@@ -416,8 +416,19 @@ def test_antenna_limits_raise_value_error():
         forward_apply(np.zeros(scn.n_voxels), scn, dtype="c64")
 
 
+
+def _tight_scenario():
+    """4 + 4 antennas: in c128 the CTA-tile layout leaves no room behind it for staged iterate values (the refilling
+    warp loads them into the buffer instead), and the even antenna count takes the bulk-copied D0 row."""
+    return ImagingScenario(
+        array=ArrayGeometry(((0.03, 0.01, 0.0), (-0.02, 0.04, 0.0), (0.0, -0.05, 0.0), (0.05, 0.05, 0.0)),
+                            ((0.01, 0.0, 0.0), (-0.04, -0.01, 0.0), (0.02, -0.03, 0.0), (-0.01, 0.03, 0.0))),
+        frequencies=FrequencyGrid(20e9, 30e9, 6),
+        voxels=VoxelGrid(center=Vec3(0.0, 0.0, 0.3), extent=(0.2, 0.1, 0.08), dims=(40, 18, 11)),
+    )
+
 @pytest.mark.parametrize("dtype", DTYPES)
-@pytest.mark.parametrize("case", ["medium", "ragged", "small"])
+@pytest.mark.parametrize("case", ["medium", "ragged", "small", "tight"])
 def test_cta_tile_forward_is_bit_identical(case, dtype, rng, monkeypatch):
     """The CTA-tile forward (fwd_ct_kernel: whole per-tile table resident in shared memory, one CTA per SM over an
     equal range of (tile, channel) pairs) computes every (tile, channel) value with the warp-unit kernel's
@@ -432,6 +443,9 @@ def test_cta_tile_forward_is_bit_identical(case, dtype, rng, monkeypatch):
     elif case == "small":
         scn = configs.small_scenario()
         idxs = [np.sort(rng.choice(scn.n_channels, 32, replace=False)), np.arange(scn.n_channels)]
+    elif case == "tight":
+        scn = _tight_scenario()
+        idxs = [np.arange(scn.n_channels), np.sort(rng.choice(scn.n_channels, 41, replace=False))]
     else:
         scn = ImagingScenario(
             array=ArrayGeometry(((0.03, 0.01, 0.0), (-0.02, 0.04, 0.0), (0.0, -0.05, 0.0)),
@@ -448,11 +462,18 @@ def test_cta_tile_forward_is_bit_identical(case, dtype, rng, monkeypatch):
         out[mode] = [forward_values(plan, s, idx) for idx in idxs]
     for a, b in zip(out["0"], out["2"]):
         assert np.array_equal(a, b)
+    # ... whatever the CTA ranges' cuts (equal ranges, the default piece cost, a large one)
+    for cost in ("0", "400"):
+        monkeypatch.setenv("NFGPU_CT_COST_FWD", cost)
+        plan = DevicePlan(scn, dtype=dtype, device="cuda:0", structured="never")
+        for idx, b in zip(idxs, out["2"]):
+            assert np.array_equal(forward_values(plan, s, idx), b)
 
 
+@pytest.mark.parametrize("cost", [None, "0", "400"])
 @pytest.mark.parametrize("dtype", DTYPES)
-@pytest.mark.parametrize("case", ["medium", "ragged"])
-def test_cta_tile_adjoint_prox_matches_warp_unit(case, dtype, rng, monkeypatch):
+@pytest.mark.parametrize("case", ["medium", "ragged", "tight"])
+def test_cta_tile_adjoint_prox_matches_warp_unit(case, dtype, cost, rng, monkeypatch):
     """The CTA-tile adjoint + prox (adj_ct_kernel: warps split each piece's channels, the last one sums their
     partial gradients in warp order, the pieces' epilogues run side by side at the end; tiles cut across CTAs sum
     their pieces in piece order) against the warp-unit kernel: the same SPGM step to rounding, and the
@@ -461,9 +482,14 @@ def test_cta_tile_adjoint_prox_matches_warp_unit(case, dtype, rng, monkeypatch):
     from paper_2509_00774_b200 import configs
     from paper_2509_00774_b200.solver import SPGMEngine
 
+    if cost is not None:  # the CTA ranges' cuts (ct_args): equal ranges, or a large piece cost; default otherwise
+        monkeypatch.setenv("NFGPU_CT_COST_ADJ", cost)
     if case == "medium":
         scn = configs.medium_scenario()
         B = 512
+    elif case == "tight":
+        scn = _tight_scenario()
+        B = 57
     else:
         scn = ImagingScenario(
             array=ArrayGeometry(((0.03, 0.01, 0.0), (-0.02, 0.04, 0.0), (0.0, -0.05, 0.0)),
