@@ -2918,11 +2918,11 @@ __global__ void __launch_bounds__(1024) magchange_kernel(const Real* __restrict_
 //
 // For plans whose whole per-tile table (all T + R antennas: A·2·TILE Reals, 64 KB for BASELINE Medium in c64)
 // fits twice in shared memory, a CTA of CT_WARPS warps works on ONE tile at a time with every row of it
-// resident, and its warps split the tile's channels. Every CTA owns an equal contiguous range of the
-// tile-major (tile, sorted channel) pairs of the launch (one CTA per SM, balanced to one pair), cut into
-// pieces (tile, channel range). A piece's table rows arrive with one bulk copy (TMA) on an mbarrier,
-// double-buffered: the last warp done with piece i refills its buffer with piece i + 2. No warp stages tx
-// groups or receiver rows, and no warp waits for a straggler of another tile.
+// resident, and its warps split the tile's channels. Every CTA owns a contiguous range of the tile-major
+// (tile, sorted channel) pairs of the launch (one CTA per SM; the cuts equalise pairs + cost x pieces, ct_args),
+// cut into pieces (tile, channel range). A piece's table rows and D0 row arrive with two bulk copies (TMA) on an
+// mbarrier, double-buffered: the last warp done with piece i refills its buffer with piece i + 2. No warp
+// stages tx groups or receiver rows, and no warp waits for a straggler of another tile.
 //   forward: each (tile, channel) value is computed by one warp with the flat kernel's arithmetic and
 //            transpose-reduce, so part[tile][j] is bit-identical to fwd_kernel's and subsets stay bit-exact.
 //   adjoint: the last warp done with a piece sums the warps' partial gradients in warp order (shared memory) and
