@@ -3545,7 +3545,7 @@ struct LoopArgs {
   double* rec;          // [K][LOOP_REC]
   int* state;           // {iterations, reason: 0 max_iters / 1 tolerance / 2 time budget, stop flag}
   unsigned* bar;        // grid barrier arrival counter (grid_sync)
-  int stage_ok;         // the reduce phase stages a CTA's partials [ntiles][channels per CTA] in shared memory
+  int stage_tiles;      // the reduce phase stages a CTA's partials in shared memory, this many tiles at a time (0: no)
   int kwords;           // 32-bit words of the key-space bitmap of the P0 rank sort (0: pairwise ranks)
   int* ctr;             // work-unit counters {forward, adjoint}: warps fetch units past the first TW dynamically
   void* s_a;            // iteration k reads s_a (k even) or s_b (k odd) and writes the other
@@ -3839,54 +3839,67 @@ __global__ void __launch_bounds__(512, 1) spgm_loop_kernel(LoopArgs la, FwdArgs<
         ymr = ym.x;
         ymi = ym.y;
       }
-      // the CTA's partials [ntiles][jn] first land in shared memory (every thread loads, one L2 latency) when they fit
+      // The CTA's partials [tiles][jn] go through shared memory in chunks of la.stage_tiles tiles (asynchronous
+      // copies, so the loads in flight are not bounded by registers; BASELINE Medium: one chunk); thread (seg, jj)
+      // adds its segment's tiles of the chunk in order to its running sum, kept in seg_sh between chunks.
       R2<Real>* stage = reinterpret_cast<R2<Real>*>(seg_sh + (size_t)la.nseg * JC);
-      const bool staged = la.stage_ok != 0;
-      if (staged) {
+      const int cap = la.stage_tiles;
+      const int nitems = la.nseg * jn;
+      if (cap > 0) {
         const R2<Real>* src = reinterpret_cast<const R2<Real>*>(fa.part) + j0;
-        const int total = g.ntiles * jn;
-        for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {  // 8 loads in flight per thread
-          R2<Real> v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int it = base + u * blockDim.x;
-            if (it < total) {
-              const int x = (int)((unsigned)it / (unsigned)jn), jj = it - x * jn;
-              v[u] = src[(size_t)x * B + jj];
+        for (int xa = 0; xa < g.ntiles; xa += cap) {
+          const int xb = min(g.ntiles, xa + cap);
+          const int total = (xb - xa) * jn;
+          for (int it = threadIdx.x; it < total; it += blockDim.x) {
+            const int x = (int)((unsigned)it / (unsigned)jn), jj = it - x * jn;
+            const unsigned d = (unsigned)__cvta_generic_to_shared(stage + it);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src + (size_t)(xa + x) * B + jj),
+                         "n"((int)sizeof(R2<Real>))
+                         : "memory");
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          __syncthreads();
+          if (xa == 0) LOOP_STAMP(3);
+          for (int it = threadIdx.x; it < nitems; it += blockDim.x) {
+            const int seg = (int)((unsigned)it / (unsigned)jn), jj = it - seg * jn;
+            // (tiles * segments < 2^31: the same quotients as the 64-bit form of fwd_reduce1_kernel)
+            const int x0 = (int)((unsigned)(g.ntiles * seg) / (unsigned)la.nseg);
+            const int x1 = (int)((unsigned)(g.ntiles * (seg + 1)) / (unsigned)la.nseg);
+            const int lo = max(x0, xa), hi = min(x1, xb);
+            if (lo >= hi && !(xa == 0 && x0 >= x1)) continue;
+            double sr = 0, si = 0;
+            if (lo > x0) {
+              const double2 acc = seg_sh[seg * JC + jj];
+              sr = acc.x;
+              si = acc.y;
             }
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int it = base + u * blockDim.x;
-            if (it < total) stage[it] = v[u];
-          }
-        }
-        __syncthreads();
-      }
-      LOOP_STAMP(3);
-      for (int it = threadIdx.x; it < la.nseg * jn; it += blockDim.x) {
-        const int seg = it / jn, jj = it - seg * jn;
-        // (tiles * segments < 2^31: the same quotients as the 64-bit form of fwd_reduce1_kernel)
-        const int x0 = (int)((unsigned)(g.ntiles * seg) / (unsigned)la.nseg);
-        const int x1 = (int)((unsigned)(g.ntiles * (seg + 1)) / (unsigned)la.nseg);
-        double sr = 0, si = 0;
-        if (staged) {
 #pragma unroll 4
-          for (int x = x0; x < x1; ++x) {
-            const R2<Real> v = stage[x * jn + jj];
-            sr += (double)v.x;
-            si += (double)v.y;
+            for (int x = lo; x < hi; ++x) {
+              const R2<Real> v = stage[(x - xa) * jn + jj];
+              sr += (double)v.x;
+              si += (double)v.y;
+            }
+            seg_sh[seg * JC + jj] = make_double2(sr, si);
           }
-        } else {
+          __syncthreads();
+        }
+      } else {
+        LOOP_STAMP(3);
+        for (int it = threadIdx.x; it < nitems; it += blockDim.x) {
+          const int seg = it / jn, jj = it - seg * jn;
+          const int x0 = (int)((unsigned)(g.ntiles * seg) / (unsigned)la.nseg);
+          const int x1 = (int)((unsigned)(g.ntiles * (seg + 1)) / (unsigned)la.nseg);
           const R2<Real>* src = reinterpret_cast<const R2<Real>*>(fa.part) + j0 + jj;
+          double sr = 0, si = 0;
 #pragma unroll 8
           for (int x = x0; x < x1; ++x) {
             const R2<Real> v = src[(size_t)x * B];
             sr += (double)v.x;
             si += (double)v.y;
           }
+          seg_sh[seg * JC + jj] = make_double2(sr, si);
         }
-        seg_sh[seg * JC + jj] = make_double2(sr, si);
       }
       __syncthreads();
       LOOP_STAMP(4);
@@ -5117,18 +5130,17 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   }
   const bool ct_adjoint_on = cta;
   if (ct) smem = std::max(smem, ct_fwd_smem(p));
-  bool stage_ok = false;
-  {  // the reduce phase's segment sums [nseg][channels per CTA], and the CTA's partials [ntiles][channels per CTA]
-    // staged behind them when that stays within the layout the other phases need anyway (or 64 KB)
+  int stage_tiles = 0;
+  {  // the reduce phase's segment sums [nseg][channels per CTA], and behind them the staging buffer for the CTA's
+    // partials [tiles per chunk][channels per CTA]: within the layout the other phases need anyway (or 64 KB)
     const int nred = std::max(1, p->nsm - 1);
     const size_t jc = (size_t)(B + nred - 1) / nred;
     const size_t seg_bytes = (size_t)p->fwd_nseg * jc * sizeof(double2);
     smem = std::max(smem, seg_bytes);
-    const size_t staged = seg_bytes + (size_t)p->g.ntiles * jc * 2 * sizeof(Real);
-    if (staged <= std::max(smem, (size_t)65536) && staged <= SMEM_DYN_MAX) {
-      stage_ok = true;
-      smem = std::max(smem, staged);
-    }
+    const size_t budget = std::min(std::max(smem, (size_t)65536), SMEM_DYN_MAX), per_tile = jc * 2 * sizeof(Real);
+    if (budget > seg_bytes) stage_tiles = (int)std::min<size_t>(p->g.ntiles, (budget - seg_bytes) / per_tile);
+    if (stage_tiles < 16 && stage_tiles < p->g.ntiles) stage_tiles = 0;
+    if (stage_tiles > 0) smem = std::max(smem, seg_bytes + (size_t)stage_tiles * per_tile);
   }
   if (smem > SMEM_DYN_MAX) return fail(NF_ERR_STATE, "persistent loop: shared memory layout does not fit");
   if (ct_adjoint_on)
@@ -5198,7 +5210,7 @@ int launch_spgm_loop(nf_plan* p, const int32_t* table, int K, uint64_t seed, uin
   la.fold = p->loop_fold;
   la.warp_bytes = wb;
   la.kwords = bitmap ? (int)kwords : 0;
-  la.stage_ok = stage_ok ? 1 : 0;
+  la.stage_tiles = stage_tiles;
   if (int rc = loop_profile_buffer(p, K, la)) return rc;
   FwdArgs<Real> fa = fwd_args<Real>(p, s_a, 0, B, true);
   AdjArgs<Real> aa = adj_args<Real>(p, nullptr, 0, s_a, s_b, eta_over_b, alpha, true);
