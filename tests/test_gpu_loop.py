@@ -71,6 +71,37 @@ def test_loop_matches_per_launch_path_bitwise(workload, dtype, ct, no_tiny, monk
 
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_loop_many_tiles_large_batch_bitwise(dtype):
+    """2048 tiles and |B| = 4096: a CTA's partials [tiles][28 channels] do not fit in shared memory at once, so the
+    loop's reduce phase stages them in chunks of tiles and keeps its running segment sums between chunks; the
+    iterates must still equal the per-launch path's bit for bit."""
+    from paper_2509_00774_b200 import ArrayGeometry, FrequencyGrid, ImagingScenario, Vec3, VoxelGrid
+
+    rng = np.random.default_rng(9)
+    tx = rng.uniform(-0.1, 0.1, size=(4, 2))
+    rx = rng.uniform(-0.1, 0.1, size=(4, 2))
+    scn = ImagingScenario(
+        array=ArrayGeometry(tuple(Vec3(a, b, 0.0) for a, b in tx), tuple(Vec3(a, b, 0.0) for a, b in rx)),
+        frequencies=FrequencyGrid(57e9, 64e9, 512),
+        voxels=VoxelGrid(center=Vec3(0.0, 0.0, 0.4), extent=(0.3, 0.3, 0.2), dims=(128, 64, 64)),
+    )
+    B, K = 4096, 3
+    y = rc(rng, scn.n_channels)
+    s0 = rc(rng, scn.n_voxels) * 0.01
+    a, b = _pair(scn, dtype, y, 1e-3, 1e-7, s0, max_batch=B)
+    table = np.stack([np.sort(rng.choice(scn.n_channels, B, replace=False)) for _ in range(K)])
+    stats = []
+    for k in range(K):
+        a.stage(table[k])
+        a.step_staged()
+        stats.append(a.stats.clone())
+    b.run_loop(K, table=table, tol=0.0)
+    assert b.loop_result() == (K, 0)
+    assert torch.equal(a.s, b.s)
+    assert torch.equal(torch.stack(stats), b._loop_rec[:K, :4])
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_loop_device_sampler_matches_per_launch(dtype, no_tiny):
     w = configs.WORKLOADS["small"]()
     scn = w.scenario
