@@ -3066,7 +3066,9 @@ __device__ __forceinline__ unsigned ct_records(const Geo& g, const WarpSmem<Real
   }
   int key = -1, toff = 0;
   if (L < nb) {
-    const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = tx_group(g, t);
+    // forward (no wrec): every tx row is resident and the record carries the row's full offset, so a run is a
+    // receiver (tx group 0 for all: fewer, longer runs); the adjoint packs the tx index within its group into the phase
+    const int t = pk_t(cr.pk), r = pk_r(cr.pk), tg = wrec ? tx_group(g, t) : 0;
     const double x = cr.kd * (ws.d0[t] + ws.d0[g.T + r]);
     R4<Real> q;
     if constexpr (std::is_same<Real, float>::value) {
