@@ -2930,6 +2930,8 @@ __global__ void __launch_bounds__(1024) magchange_kernel(const Real* __restrict_
 //            epilogues side by side (a tile cut across CTAs sums its pieces in piece order, adj_epilogue), so no
 //            warp carries several epilogues' latency into the end of the phase.
 constexpr int CT_WARPS = 16;
+constexpr int CT_TBR = 16;    // forward transpose depth of the CTA-tile kernel (lane sums in the order of TBR = 8)
+constexpr int CT_UNROLL = 4;  // adjoint channel loop (runs are long here)
 constexpr int CT_TGA = 16;  // adjoint: transmitters per run group (their index rides in 4 low mantissa bits of the record)
 
 template <typename Real>
@@ -2942,7 +2944,7 @@ struct CtLayout {  // [mbarriers, counters | buffer 0 | buffer 1 | warp records 
     off_warp = off_buf + 2 * buf_bytes;
     warp_bytes = 34 * sizeof(R4<Real>) + 34 * sizeof(int2);
     off_u = off_warp + (size_t)CT_WARPS * warp_bytes;
-    const size_t tb = (size_t)CT_WARPS * TBR * 33 * sizeof(R2<Real>);  // forward: per-warp transpose buffers
+    const size_t tb = (size_t)CT_WARPS * CT_TBR * 33 * sizeof(R2<Real>);  // forward: per-warp transpose buffers
     const size_t gs = (size_t)2 * CT_WARPS * 2 * TILE * sizeof(Real);   // adjoint: warp partials [2][warps]
     u_bytes = tb > gs ? tb : gs;
     bytes = off_u + u_bytes;
@@ -3135,8 +3137,8 @@ __device__ __forceinline__ void ct_fwd_slice(const Geo& g, const Real* __restric
     const bool more = jb + 32 < c1;
     const unsigned starts = ct_records<Real, EXACT>(g, ws, crec, nullptr, nb, more ? jb + 32 : pn0, more ? c1 : pn1, L,
                                                     carry, nxt, nxtw);
-    for (int h0 = 0; h0 < nb; h0 += TBR) {
-      const int h1 = min(nb, h0 + TBR);
+    for (int h0 = 0; h0 < nb; h0 += CT_TBR) {
+      const int h1 = min(nb, h0 + CT_TBR);
       int c = h0;
       while (c < h1) {
         const int key = ws.rect[c].y;
@@ -3177,26 +3179,34 @@ __device__ __forceinline__ void ct_fwd_slice(const Geo& g, const Real* __restric
         }
       }
       __syncwarp();
-      constexpr int PER = 32 / TBR, SL = 32 / PER;
-      const int row = L % TBR, part = L / TBR;
-      R2<Real> S;
-      S.x = 0;
-      S.y = 0;
+      // 16 rows, two lanes per row. The flat kernels (TBR = 8) sum a channel's 32 lane values as four sequential
+      // 8-sums S0..S3 combined (S0 + S2) + (S1 + S3); lane (row, h) forms S_h and S_{h+2} here, their sum, and one
+      // shuffle adds the halves: the same operations in the same order, so the same bits.
+      static_assert(TBR == 8 && CT_TBR == 16, "the CTA-tile transpose reproduces the TBR = 8 summation order");
+      const int row = L % CT_TBR, h = L / CT_TBR;
+      R2<Real> S, Sb;
+      S.x = S.y = Sb.x = Sb.y = 0;
 #pragma unroll 8
-      for (int l = 0; l < SL; ++l) {
-        const R2<Real> t = tb[row * 33 + part * SL + l];
+      for (int l = 0; l < 8; ++l) {
+        const R2<Real> ta = tb[row * 33 + h * 8 + l], tc = tb[row * 33 + (h + 2) * 8 + l];
         if constexpr (std::is_same<Real, float>::value) {
-          S = add2(S, t);
+          S = add2(S, ta);
+          Sb = add2(Sb, tc);
         } else {
-          S.x += t.x;
-          S.y += t.y;
+          S.x += ta.x;
+          S.y += ta.y;
+          Sb.x += tc.x;
+          Sb.y += tc.y;
         }
       }
-#pragma unroll
-      for (int o = 16; o >= TBR; o >>= 1) {
-        S.x += __shfl_down_sync(FULL, S.x, o);
-        S.y += __shfl_down_sync(FULL, S.y, o);
+      if constexpr (std::is_same<Real, float>::value) {
+        S = add2(S, Sb);
+      } else {
+        S.x += Sb.x;
+        S.y += Sb.y;
       }
+      S.x += __shfl_down_sync(FULL, S.x, 16);
+      S.y += __shfl_down_sync(FULL, S.y, 16);
       if (L < h1 - h0) outl[jb + h0] = S;
       __syncwarp();
     }
@@ -3252,7 +3262,7 @@ __device__ __forceinline__ void ct_forward(const FwdArgs<Real>& a, const CtArgs&
   ws.rec = reinterpret_cast<R4<Real>*>(wr);
   ws.rect = reinterpret_cast<int2*>(wr + 34 * sizeof(R4<Real>));
   ws.tside = ws.rslot = nullptr;
-  R2<Real>* tb = reinterpret_cast<R2<Real>*>(smem + lay.off_u) + (size_t)w * TBR * 33;
+  R2<Real>* tb = reinterpret_cast<R2<Real>*>(smem + lay.off_u) + (size_t)w * CT_TBR * 33;
   for (int i = L; i < 34; i += 32) ws.rect[i] = make_int2(0, -1);
   ChanRec nxt;
   R2<Real> nxtw;
@@ -3329,7 +3339,7 @@ __device__ __forceinline__ void ct_adj_slice(const Geo& g, const Real* __restric
       }
       R4<Real> q = ws.rec[c];
       int off = (low2(q.y) | (low2(q.z) << 2)) * TABW;
-#pragma unroll UNROLL
+#pragma unroll CT_UNROLL
       for (; c < e; ++c) {
         const R4<Real> qn = ws.rec[c + 1];
         const int offn = (low2(qn.y) | (low2(qn.z) << 2)) * TABW;
