@@ -2931,7 +2931,10 @@ __global__ void __launch_bounds__(1024) magchange_kernel(const Real* __restrict_
 //            warp carries several epilogues' latency into the end of the phase.
 constexpr int CT_WARPS = 16;
 constexpr int CT_TBR = 16;    // forward transpose depth of the CTA-tile kernel (lane sums in the order of TBR = 8)
-constexpr int CT_UNROLL = 4;  // adjoint channel loop (runs are long here)
+#ifndef NFGPU_CT_UNROLL
+#define NFGPU_CT_UNROLL 4
+#endif
+constexpr int CT_UNROLL = NFGPU_CT_UNROLL;  // adjoint channel loop (runs are long here)
 constexpr int CT_TGA = 16;  // adjoint: transmitters per run group (their index rides in 4 low mantissa bits of the record)
 
 template <typename Real>
