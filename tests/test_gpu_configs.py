@@ -40,9 +40,6 @@ def _adjoint_at(geo, r, idx, vox, step=131072):
 def test_microbenchmark_grids_spot_check(grid, dtype, structured):
     """One full-M forward and one full-M adjoint (M = 64 x 64 x 256 = 1,048,576) with N(0,1) complex
     inputs, checked at 12 rows and 8 voxels against the direct formula."""
-    if dtype == "c128" and not structured and grid == "192x192x96":
-        pytest.skip("flat c128 at 192x192x96 is 2 x 3.7e12 fp64 entries (~30 s): covered by 128^3 and the "
-                    "structured c128 kernels on this grid")
     scn = configs.micro_scenario(grid)
     geo = O.geom_from_scenario(scn)
     rng = np.random.default_rng(13)
